@@ -1,0 +1,78 @@
+/* C-ABI of the B200-native SIP-Helmholtz apply (libsipg.so).
+ *
+ * Replaces the reference's Python operator hot path
+ *   HelmholtzOperator.lhs_eval(x) -> y      (reference pkg/src/dgsipg/sipg.py:558-602,
+ *                                            alias __call__ at sipg.py:605)
+ * whose plan is built by HelmholtzOperator.__init__ (sipg.py:234-281).  The plan
+ * descriptor below carries the flattened setup products of that constructor:
+ * element classes (sipg.py:302-349), DoF offsets (sipg.py:269-273), geometric
+ * factors (mesh.py:331-432), face couplings with transfers, shared-trace rules and
+ * penalties (sipg.py:351-554).  It is produced by the Python plan builder
+ * (paper_2504_03573_b200/plan.py) and is opaque to callers of sipg_apply.
+ *
+ * Ownership: the caller owns x / y (device buffers for sipg_apply, host buffers
+ * for sipg_apply_host); the plan owns its device tables.  One stream per plan;
+ * not re-entrant (like the reference).  All functions return 0 on
+ * success or a negative SIPG_ERR_* code; sipg_last_error() describes the last
+ * failure on the calling thread.  There is no CPU fallback: without a CUDA
+ * device sipg_plan_create fails with SIPG_ERR_NO_DEVICE.
+ */
+#ifndef SIPG_H
+#define SIPG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIPG_ERR_ARG (-1)
+#define SIPG_ERR_CUDA (-2)
+#define SIPG_ERR_NO_DEVICE (-3)
+#define SIPG_ERR_UNSUPPORTED (-4)
+
+typedef struct sipg_plan sipg_plan;
+
+typedef struct sipg_plan_desc {
+  int32_t abi_version;      /* must equal the library's SIPG_ABI_VERSION */
+  int32_t record_bytes;     /* sizeof(face record) = 128 */
+  int32_t dim;              /* 2 or 3 */
+  int32_t n_classes;        /* element classes (shape, n_modes, n_quad, geometry) */
+  int64_t n_elements;
+  int64_t n_dofs;
+  int64_t n_records;        /* one per (element, local face) */
+  int64_t n_tables, n_elem_geom, n_face_geom;
+  double lambda;            /* reaction coefficient (HelmholtzParams.lambda_, sipg.py:64-74) */
+  const int32_t* class_desc;   /* n_classes x 64 */
+  const int32_t* class_elems;  /* n_elements: element ids grouped by class */
+  const int32_t* elem_class;   /* n_elements */
+  const int32_t* elem_pos;     /* n_elements: position within its class */
+  const int64_t* dof_off;      /* n_elements + 1: element-major DoF offsets (sipg.py:269-273) */
+  const void* face_records;    /* n_records x 128 bytes */
+  const double* tables;        /* 1-D basis / derivative / transfer tables */
+  const double* elem_geom;     /* per-element metric (regular) or per-point (deformed) */
+  const double* face_geom;     /* per-face-point swj and G.n where not constant */
+} sipg_plan_desc;
+
+/* Build the device-resident plan (uploads all tables). */
+int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);
+
+/* y = (lambda M + L_SIP) x with x, y device pointers of n_dofs doubles, enqueued on
+ * `stream` (a cudaStream_t, NULL = legacy default stream).  Replaces lhs_eval. */
+int sipg_apply(sipg_plan* plan, const double* x_dev, double* y_dev, void* stream);
+
+/* Same, from host buffers: H2D copy of x, apply, D2H copy of y, stream sync. */
+int sipg_apply_host(sipg_plan* plan, const double* x_host, double* y_host, void* stream);
+
+int sipg_plan_destroy(sipg_plan* plan);
+const char* sipg_last_error(void);
+
+/* Introspection: kernel launches issued so far / per apply; layout constants. */
+int64_t sipg_plan_launches(const sipg_plan* plan);
+int sipg_plan_kernels_per_apply(const sipg_plan* plan);
+int sipg_abi_layout(int32_t* out, int32_t n);
+int sipg_supported(int32_t shape, int32_t n_modes, int32_t n_quad);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIPG_H */

@@ -1,0 +1,146 @@
+"""ctypes binding of libsipg.so (the C-ABI declared in include/sipg.h).
+
+The library is built in-tree by `paper_2504_03573_b200.build.build_native()`
+(nvcc, sm_100a).  There is no fallback: if the library is missing or no CUDA
+device is present, constructing an operator raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+from . import layout as L
+
+LIB_PATH = Path(__file__).resolve().parent / "libsipg.so"
+
+EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
+           "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
+           "sipg_abi_layout", "sipg_supported"]
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("record_bytes", ctypes.c_int32),
+        ("dim", ctypes.c_int32), ("n_classes", ctypes.c_int32),
+        ("n_elements", ctypes.c_int64), ("n_dofs", ctypes.c_int64), ("n_records", ctypes.c_int64),
+        ("n_tables", ctypes.c_int64), ("n_elem_geom", ctypes.c_int64), ("n_face_geom", ctypes.c_int64),
+        ("lam", ctypes.c_double),
+        ("class_desc", ctypes.c_void_p), ("class_elems", ctypes.c_void_p),
+        ("elem_class", ctypes.c_void_p), ("elem_pos", ctypes.c_void_p), ("dof_off", ctypes.c_void_p),
+        ("face_records", ctypes.c_void_p), ("tables", ctypes.c_void_p),
+        ("elem_geom", ctypes.c_void_p), ("face_geom", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libsipg.so (once).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc sm_100a)")
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.sipg_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)]
+    lib.sipg_plan_create.restype = ctypes.c_int
+    lib.sipg_apply.argtypes = [vp, vp, vp, vp]
+    lib.sipg_apply.restype = ctypes.c_int
+    lib.sipg_apply_host.argtypes = [vp, vp, vp, vp]
+    lib.sipg_apply_host.restype = ctypes.c_int
+    lib.sipg_plan_destroy.argtypes = [vp]
+    lib.sipg_plan_destroy.restype = ctypes.c_int
+    lib.sipg_last_error.argtypes = []
+    lib.sipg_last_error.restype = ctypes.c_char_p
+    lib.sipg_plan_launches.argtypes = [vp]
+    lib.sipg_plan_launches.restype = i64
+    lib.sipg_plan_kernels_per_apply.argtypes = [vp]
+    lib.sipg_plan_kernels_per_apply.restype = ctypes.c_int
+    lib.sipg_abi_layout.argtypes = [ctypes.POINTER(i32), i32]
+    lib.sipg_abi_layout.restype = ctypes.c_int
+    lib.sipg_supported.argtypes = [i32, i32, i32]
+    lib.sipg_supported.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().sipg_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise RuntimeError(f"{what} failed ({rc}): {last_error()}")
+
+
+def abi_layout() -> list:
+    lib = load()
+    buf = (ctypes.c_int32 * 16)()
+    n = lib.sipg_abi_layout(buf, 16)
+    return list(buf[:n])
+
+
+class NativePlan:
+    """Owns a sipg_plan* built from a PlanBuilder."""
+
+    def __init__(self, pb):
+        lib = load()
+        self._keep = [
+            np.ascontiguousarray(pb.class_desc, dtype=np.int32),
+            np.ascontiguousarray(pb.class_elems, dtype=np.int32),
+            np.ascontiguousarray(pb.elem_class, dtype=np.int32),
+            np.ascontiguousarray(pb.elem_pos, dtype=np.int32),
+            np.ascontiguousarray(pb.dof_off, dtype=np.int64),
+            np.ascontiguousarray(pb.recs),
+            np.ascontiguousarray(pb.tables, dtype=np.float64),
+            np.ascontiguousarray(pb.egeo, dtype=np.float64),
+            np.ascontiguousarray(pb.fgeo, dtype=np.float64),
+        ]
+        cd, ce, ec, ep, do, rc, tb, eg, fg = self._keep
+        d = PlanDesc()
+        d.abi_version, d.record_bytes = L.ABI_VERSION, L.FACE_REC.itemsize
+        d.dim, d.n_classes = pb.dim, cd.shape[0]
+        d.n_elements, d.n_dofs, d.n_records = ec.size, pb.n_dofs, rc.size
+        d.n_tables, d.n_elem_geom, d.n_face_geom = tb.size, eg.size, fg.size
+        d.lam = pb.lam
+        for name, arr in zip(["class_desc", "class_elems", "elem_class", "elem_pos", "dof_off",
+                              "face_records", "tables", "elem_geom", "face_geom"], self._keep):
+            setattr(d, name, arr.ctypes.data)
+        h = ctypes.c_void_p()
+        check(lib.sipg_plan_create(ctypes.byref(d), ctypes.byref(h)), "sipg_plan_create")
+        self._lib = lib
+        self.handle = h
+        self.n_dofs = pb.n_dofs
+        self._keep = None          # tables now live on the device
+
+    def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        check(self._lib.sipg_apply(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                   ctypes.c_void_p(stream)), "sipg_apply")
+
+    def apply_host(self, x: np.ndarray, y: np.ndarray, stream: int = 0) -> None:
+        check(self._lib.sipg_apply_host(self.handle, x.ctypes.data, y.ctypes.data,
+                                        ctypes.c_void_p(stream)), "sipg_apply_host")
+
+    @property
+    def launches(self) -> int:
+        return int(self._lib.sipg_plan_launches(self.handle))
+
+    @property
+    def kernels_per_apply(self) -> int:
+        return int(self._lib.sipg_plan_kernels_per_apply(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.sipg_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

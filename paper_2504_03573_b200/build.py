@@ -1,0 +1,61 @@
+"""In-tree build of libsipg.so for sm_100a (nvcc, one object per element
+shape compiled in parallel, then linked).  Used by __graft_entry__.build()."""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "libsipg.so"
+BUILD = PKG / "build"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I", str(PKG.parent / "include")]
+SOURCES = ["sipg_capi.cu", "sipg_quad.cu", "sipg_tri.cu", "sipg_hex.cu"]
+
+
+def _nvcc():
+    nv = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(nv).exists():
+        raise RuntimeError("nvcc not found")
+    return nv
+
+
+def _stale(obj: Path, deps) -> bool:
+    return not obj.exists() or any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
+
+
+def build_native(force: bool = False, verbose: bool = True, extra_flags=()) -> Path:
+    nv = _nvcc()
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "sipg.h"]
+    objs, jobs = [], []
+    for src in SOURCES:
+        s = CSRC / src
+        o = BUILD / (Path(src).stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            jobs.append([nv, *ARCH, *FLAGS, *extra_flags, "-c", str(s), "-o", str(o)])
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            for cmd, res in zip(jobs, ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs)):
+                if res.returncode != 0:
+                    raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+                if verbose:
+                    print("built", cmd[-1])
+    if force or jobs or _stale(OUT, objs):
+        cmd = [nv, *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-lcudart"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"link failed: {res.stdout}\n{res.stderr}")
+        if verbose:
+            print("linked", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    build_native()

@@ -1,0 +1,196 @@
+// C-ABI of libsipg.so (declared in include/sipg.h).  Plain pointers and sizes:
+// no torch types cross this boundary.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+#include "sipg_plan.h"
+#include "../../include/sipg.h"
+#include "sipg_registry.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(SIPG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));  \
+  } while (0)
+
+const std::vector<KernelEntry>& kernel_table() {
+  static const std::vector<KernelEntry> t = [] {
+    std::vector<KernelEntry> v;
+    sipg_register_quad(v);
+    sipg_register_tri(v);
+    sipg_register_hex(v);
+    return v;
+  }();
+  return t;
+}
+
+const KernelEntry* find_kernel(int shape, int n, int q, int geom) {
+  for (const auto& k : kernel_table())
+    if (k.shape == shape && k.n == n && k.q == q && k.geom == geom) return &k;
+  return nullptr;
+}
+
+template <typename T>
+int upload(const T* host, int64_t count, T** dev) {
+  *dev = nullptr;
+  if (count <= 0) return 0;
+  CK(cudaMalloc((void**)dev, sizeof(T) * count));
+  CK(cudaMemcpy(*dev, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+}  // namespace
+
+struct sipg_plan {
+  DevPlan dp;
+  int n_cls;
+  int64_t n_dofs;
+  std::vector<int32_t> cd_host;
+  std::vector<const KernelEntry*> kern;
+  void* bufs[9];
+  double* x_stage = nullptr;
+  double* y_stage = nullptr;
+  int64_t launches = 0;
+};
+
+extern "C" {
+
+const char* sipg_last_error(void) { return g_err.c_str(); }
+
+int sipg_abi_layout(int32_t* out, int32_t n) {
+  const int32_t v[] = {SIPG_ABI_VERSION, (int32_t)sizeof(FaceRec), CD_WORDS, CD_TAX, TR_GSTART,
+                       F_OTHER_NEG, (int32_t)offsetof(FaceRec, tau), (int32_t)offsetof(FaceRec, gs)};
+  const int m = (int)(sizeof(v) / sizeof(v[0]));
+  for (int i = 0; i < n && i < m; ++i) out[i] = v[i];
+  return m;
+}
+
+int sipg_supported(int32_t shape, int32_t n_modes, int32_t n_quad) {
+  return find_kernel(shape, n_modes, n_quad, GEOM_REGULAR) != nullptr;
+}
+
+int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
+  if (!d || !out) return fail(SIPG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (d->abi_version != SIPG_ABI_VERSION)
+    return fail(SIPG_ERR_ARG, "ABI version mismatch: plan built for " + std::to_string(d->abi_version) +
+                                  ", library is " + std::to_string(SIPG_ABI_VERSION));
+  if (d->record_bytes != (int32_t)sizeof(FaceRec)) return fail(SIPG_ERR_ARG, "face record size mismatch");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SIPG_ERR_NO_DEVICE, "no CUDA device available (the SIP apply has no CPU fallback)");
+  sipg_plan* p = new sipg_plan();
+  memset(p->bufs, 0, sizeof(p->bufs));
+  p->n_cls = d->n_classes;
+  p->n_dofs = d->n_dofs;
+  p->cd_host.assign(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD_WORDS);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD_WORDS;
+    const int shape = cd[CD_SHAPE], n = cd[CD_N], q = cd[CD_Q0], geom = cd[CD_GEOM];
+    bool uniform = true;
+    const int dim = shape == SHAPE_HEX ? 3 : 2;
+    for (int a = 1; a < dim; ++a) uniform = uniform && cd[CD_Q0 + a] == q;
+    const KernelEntry* k = uniform ? find_kernel(shape, n, q, geom) : nullptr;
+    if (!k) {
+      delete p;
+      return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a kernel for shape=" + std::to_string(shape) +
+                                            " n_modes=" + std::to_string(n) + " n_quad=" + std::to_string(q));
+    }
+    p->kern.push_back(k);
+  }
+  int rc = 0;
+  int32_t *cd_d, *ce_d, *ec_d, *ep_d;
+  int64_t* dof_d;
+  FaceRec* rec_d;
+  double *tab_d, *eg_d, *fg_d;
+  if ((rc = upload(d->class_desc, (int64_t)d->n_classes * CD_WORDS, &cd_d)) ||
+      (rc = upload(d->class_elems, d->n_elements, &ce_d)) ||
+      (rc = upload(d->elem_class, d->n_elements, &ec_d)) ||
+      (rc = upload(d->elem_pos, d->n_elements, &ep_d)) ||
+      (rc = upload(d->dof_off, d->n_elements + 1, &dof_d)) ||
+      (rc = upload((const FaceRec*)d->face_records, d->n_records, &rec_d)) ||
+      (rc = upload(d->tables, d->n_tables, &tab_d)) || (rc = upload(d->elem_geom, d->n_elem_geom, &eg_d)) ||
+      (rc = upload(d->face_geom, d->n_face_geom, &fg_d))) {
+    delete p;
+    return rc;
+  }
+  void* b[9] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d};
+  memcpy(p->bufs, b, sizeof(b));
+  p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes};
+  for (const KernelEntry* k : p->kern) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)k->smem);
+    if (e != cudaSuccess) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = p;
+  return 0;
+}
+
+int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
+  if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int c = 0; c < p->n_cls; ++c) {
+    const int32_t* cd = p->cd_host.data() + c * CD_WORDS;
+    const int count = cd[CD_COUNT];
+    if (count == 0) continue;
+    const KernelEntry* k = p->kern[c];
+    k->fn<<<count, k->threads, k->smem, s>>>(p->dp, c, x_dev, y_dev);
+    ++p->launches;
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* stream) {
+  if (!p || !x_host || !y_host) return fail(SIPG_ERR_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * (size_t)p->n_dofs;
+  if (!p->x_stage) {
+    CK(cudaMalloc((void**)&p->x_stage, bytes));
+    CK(cudaMalloc((void**)&p->y_stage, bytes));
+  }
+  CK(cudaMemcpyAsync(p->x_stage, x_host, bytes, cudaMemcpyHostToDevice, s));
+  int rc = sipg_apply(p, p->x_stage, p->y_stage, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(y_host, p->y_stage, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int64_t sipg_plan_launches(const sipg_plan* p) { return p ? p->launches : -1; }
+
+int sipg_plan_kernels_per_apply(const sipg_plan* p) {
+  if (!p) return -1;
+  int k = 0;
+  for (int c = 0; c < p->n_cls; ++c)
+    if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0) ++k;
+  return k;
+}
+
+int sipg_plan_destroy(sipg_plan* p) {
+  if (!p) return 0;
+  for (void* b : p->bufs)
+    if (b) cudaFree(b);
+  if (p->x_stage) cudaFree(p->x_stage);
+  if (p->y_stage) cudaFree(p->y_stage);
+  delete p;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""The SIP-Helmholtz operator: drop-in for the reference's
+`dgsipg.sipg.HelmholtzOperator` hot path (reference sipg.py:219-605).
+
+Same constructor signature and public surface (`n_dofs`, `dof_slice`,
+`certificates`, `timers`, `lhs_eval`, `__call__`, `report`); `lhs_eval` runs
+the sm_100a kernels in libsipg.so through the C-ABI.  Inputs may be numpy
+arrays (copied host->device->host, like the reference returns a new array) or
+CUDA torch tensors (zero-copy, enqueued on the current stream, returns a new
+CUDA tensor).  There is no CPU path.
+
+Extra keyword arguments (not in the reference):
+  tau_rule     "reference": tau = C max(n-1,1)^2 / h (sipg.py:351-360);
+               "baseline":  tau = max(n_L, n_R)^2 / h (BASELINE.json "(P+1)^2/h").
+  shared_rule  "patched" (default): Gauss-Legendre shared-trace rule on faces
+               touching a non-GLL side (the reference produces NaN there,
+               SURVEY.md §8c P2); "reference": higher side's kind.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .plan import PlanBuilder
+from .polylib import BasisKind
+
+__all__ = ["HelmholtzParams", "HelmholtzOperator"]
+
+
+@dataclass(frozen=True)
+class HelmholtzParams:
+    """Reaction coefficient and penalty constant (reference sipg.py:64-74)."""
+    lambda_: float = 1.0
+    tau_constant: float = 10.0
+
+
+class HelmholtzOperator:
+    """Matrix-free SIPG Helmholtz operator y = (lambda M + L_SIP) x on B200."""
+
+    def __init__(self, mesh, order_map, *, basis_kind=BasisKind.LAGRANGE, rule_kinds=None,
+                 params: HelmholtzParams = HelmholtzParams(), strategy: str = "p2p",
+                 batch_width: int = 4, face_absorb: str = "auto", force_interp: bool = False,
+                 p_geom: int = 1, tau_rule: str = "reference", shared_rule: str = "patched"):
+        if strategy not in ("p2p", "p2p_forced", "shared_trace"):
+            raise ValueError(f"unknown strategy {strategy!r}")
+        if face_absorb not in ("auto", "trace_iproduct"):
+            raise ValueError(f"unknown face_absorb {face_absorb!r}")
+        if tau_rule not in ("reference", "baseline"):
+            raise ValueError(f"unknown tau_rule {tau_rule!r}")
+        self.mesh, self.order_map, self.params = mesh, order_map, params
+        self.strategy, self.face_absorb, self.force_interp = strategy, face_absorb, force_interp
+        self.batch_width = max(1, int(batch_width))   # GPU batches by class; accepted for API parity
+        self.p_geom = p_geom
+        self.timers = {"setup": 0.0, "total": 0.0, "applies": 0}
+        t0 = time.perf_counter()
+        self.plan = PlanBuilder(mesh, order_map, basis_kind=basis_kind, rule_kinds=rule_kinds,
+                                lambda_=params.lambda_, tau_constant=params.tau_constant,
+                                strategy=strategy, face_absorb=face_absorb, force_interp=force_interp,
+                                p_geom=p_geom, tau_rule=tau_rule, shared_rule=shared_rule).build()
+        self.n_dofs = self.plan.n_dofs
+        self._dof_off = self.plan.dof_off
+        self.certificates = self.plan.certificates
+        self.native = _native.NativePlan(self.plan)
+        self.timers["setup"] = time.perf_counter() - t0
+
+    def dof_slice(self, e: int) -> slice:
+        return slice(int(self._dof_off[e]), int(self._dof_off[e + 1]))
+
+    def lhs_eval(self, x):
+        """Action of the SIPG operator on a global coefficient vector
+        (reference sipg.py:558-602)."""
+        t0 = time.perf_counter()
+        if _is_cuda_tensor(x):
+            import torch
+            if x.dtype != torch.float64 or x.shape != (self.n_dofs,):
+                raise ValueError(f"expected a float64 vector of length {self.n_dofs}")
+            x = x.contiguous()
+            y = torch.empty_like(x)
+            self.native.apply_device(x.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        else:
+            x = np.ascontiguousarray(np.asarray(x, dtype=float))
+            if x.shape != (self.n_dofs,):
+                raise ValueError(f"expected a vector of length {self.n_dofs}")
+            y = np.empty(self.n_dofs)
+            self.native.apply_host(x, y)
+        self.timers["total"] += time.perf_counter() - t0
+        self.timers["applies"] += 1
+        return y
+
+    __call__ = lhs_eval
+
+    def apply_into(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        """Raw device-pointer apply (no allocation), for benchmarks and solvers."""
+        self.native.apply_device(x_ptr, y_ptr, stream)
+
+    def report(self) -> str:
+        """Certificate report for non-conforming interfaces (reference trace.py:109-130)."""
+        lines = ["# interface  left(P,Q)  right(P,Q)  strategy  cond1  cond2  required  actual  symmetric"]
+        itf = self.mesh.interfaces
+        for iid, (sym, c1, c2, req, act), strat in self.certificates:
+            (le, _), (re_, _) = itf[iid].left, itf[iid].right
+            nm, nq = self.order_map.n_modes, self.order_map.n_quad
+            lines.append("%d  P%dQ%d  P%dQ%d  %s  %s  %s  %d  %d  %s" % (
+                iid, nm[le], nq[le], nm[re_], nq[re_], strat, "yes" if c1 else "no",
+                "yes" if c2 else "no", req, act, "yes" if sym else "no"))
+        return "\n".join(lines) + "\n"
+
+
+def _is_cuda_tensor(x) -> bool:
+    mod = type(x).__module__
+    return mod.startswith("torch") and getattr(x, "is_cuda", False)
