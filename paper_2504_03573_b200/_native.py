@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsipg.so"
 
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
-           "sipg_abi_layout", "sipg_supported"]
+           "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info"]
 
 
 class PlanDesc(ctypes.Structure):
@@ -65,6 +65,10 @@ def load() -> ctypes.CDLL:
     lib.sipg_abi_layout.restype = ctypes.c_int
     lib.sipg_supported.argtypes = [i32, i32, i32]
     lib.sipg_supported.restype = ctypes.c_int
+    lib.sipg_apply_class.argtypes = [vp, i32, vp, vp, vp]
+    lib.sipg_apply_class.restype = ctypes.c_int
+    lib.sipg_plan_class_info.argtypes = [vp, i32, ctypes.POINTER(i32)]
+    lib.sipg_plan_class_info.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -116,6 +120,7 @@ class NativePlan:
         self._lib = lib
         self.handle = h
         self.n_dofs = pb.n_dofs
+        self.n_classes = int(cd.shape[0])
         self._keep = None          # tables now live on the device
 
     def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
@@ -125,6 +130,19 @@ class NativePlan:
     def apply_host(self, x: np.ndarray, y: np.ndarray, stream: int = 0) -> None:
         check(self._lib.sipg_apply_host(self.handle, x.ctypes.data, y.ctypes.data,
                                         ctypes.c_void_p(stream)), "sipg_apply_host")
+
+    def apply_host_ptr(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        check(self._lib.sipg_apply_host(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                        ctypes.c_void_p(stream)), "sipg_apply_host")
+
+    def apply_class(self, cls: int, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        check(self._lib.sipg_apply_class(self.handle, cls, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                         ctypes.c_void_p(stream)), "sipg_apply_class")
+
+    def class_info(self, cls: int):
+        buf = (ctypes.c_int32 * 5)()
+        check(self._lib.sipg_plan_class_info(self.handle, cls, buf), "sipg_plan_class_info")
+        return dict(zip(("shape", "n", "q", "geom", "count"), list(buf)))
 
     @property
     def launches(self) -> int:

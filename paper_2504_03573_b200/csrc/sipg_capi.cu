@@ -157,6 +157,24 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
   return 0;
 }
 
+int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
+  if (!p || !x_dev || !y_dev || cls < 0 || cls >= p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+  const int count = p->cd_host[cls * CD_WORDS + CD_COUNT];
+  if (count == 0) return 0;
+  const KernelEntry* k = p->kern[cls];
+  k->fn<<<count, k->threads, k->smem, (cudaStream_t)stream>>>(p->dp, cls, x_dev, y_dev);
+  ++p->launches;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out5) {
+  if (!p || cls < 0 || cls >= p->n_cls || !out5) return fail(SIPG_ERR_ARG, "bad argument");
+  const int32_t* cd = p->cd_host.data() + cls * CD_WORDS;
+  out5[0] = cd[CD_SHAPE]; out5[1] = cd[CD_N]; out5[2] = cd[CD_Q0]; out5[3] = cd[CD_GEOM]; out5[4] = cd[CD_COUNT];
+  return 0;
+}
+
 int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* stream) {
   if (!p || !x_host || !y_host) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
