@@ -63,8 +63,8 @@ int sipg_apply(sipg_plan* plan, const double* x_dev, double* y_dev, void* stream
 /* One element class only (instrumentation: per-kernel timing).  Classes are
  * independent, so applying every class once equals sipg_apply. */
 int sipg_apply_class(sipg_plan* plan, int32_t cls, const double* x_dev, double* y_dev, void* stream);
-/* (shape, n_modes, n_quad, geometry mode, element count) of a class. */
-int sipg_plan_class_info(const sipg_plan* plan, int32_t cls, int32_t* out5);
+/* (shape, n_modes, n_quad, geometry mode, element count, kernel kind) of a class. */
+int sipg_plan_class_info(const sipg_plan* plan, int32_t cls, int32_t* out6);
 
 /* Same, from host buffers: H2D copy of x, apply, D2H copy of y, stream sync. */
 int sipg_apply_host(sipg_plan* plan, const double* x_host, double* y_host, void* stream);

@@ -140,9 +140,9 @@ class NativePlan:
                                          ctypes.c_void_p(stream)), "sipg_apply_class")
 
     def class_info(self, cls: int):
-        buf = (ctypes.c_int32 * 5)()
+        buf = (ctypes.c_int32 * 6)()
         check(self._lib.sipg_plan_class_info(self.handle, cls, buf), "sipg_plan_class_info")
-        return dict(zip(("shape", "n", "q", "geom", "count"), list(buf)))
+        return dict(zip(("shape", "n", "q", "geom", "count", "kernel"), list(buf)))
 
     @property
     def launches(self) -> int:

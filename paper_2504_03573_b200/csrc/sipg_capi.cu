@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 #include <string>
 #include <vector>
 #include "sipg_plan.h"
@@ -37,10 +38,30 @@ const std::vector<KernelEntry>& kernel_table() {
   return t;
 }
 
-const KernelEntry* find_kernel(int shape, int n, int q, int geom) {
+const KernelEntry* find_kernel(int shape, int n, int q, int geom, int kind = 0) {
   for (const auto& k : kernel_table())
-    if (k.shape == shape && k.n == n && k.q == q && k.geom == geom) return &k;
+    if (k.shape == shape && k.n == n && k.q == q && k.geom == geom && k.kind == kind) return &k;
   return nullptr;
+}
+
+// Does every face of every element of class c take the register-column fast
+// path (boundary or conforming same-class neighbour, identity transfer,
+// constant geometry, no tangential neighbour metric)?  Mirrors k_hex's test.
+bool class_all_fast(const sipg_plan_desc* d, int c) {
+  const int32_t* cd = d->class_desc + c * CD_WORDS;
+  const FaceRec* recs = (const FaceRec*)d->face_records;
+  const int n = cd[CD_N], q = cd[CD_Q0];
+  for (int64_t r = cd[CD_REC_OFF]; r < cd[CD_REC_OFF] + (int64_t)cd[CD_COUNT] * cd[CD_NFACES]; ++r) {
+    const FaceRec& f = recs[r];
+    if (f.type == FT_BOUNDARY && !(f.flags & F_SELF_PW)) continue;
+    if (f.type != FT_DIRECT || !(f.flags & F_OTHER_ID) || (f.flags & (F_SELF_PW | F_OTHER_PW))) return false;
+    const int32_t* co = d->class_desc + d->elem_class[f.nbr] * CD_WORDS;
+    const int ao = f.nbr_face >> 1;
+    const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
+    if (co[CD_SHAPE] != SHAPE_HEX || co[CD_N] != n || co[CD_Q0] != q || f.go[b0] != 0.0 || f.go[b1] != 0.0)
+      return false;
+  }
+  return true;
 }
 
 template <typename T>
@@ -103,7 +124,21 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     bool uniform = true;
     const int dim = shape == SHAPE_HEX ? 3 : 2;
     for (int a = 1; a < dim; ++a) uniform = uniform && cd[CD_Q0 + a] == q;
-    const KernelEntry* k = uniform ? find_kernel(shape, n, q, geom) : nullptr;
+    const KernelEntry* k = nullptr;
+    if (uniform && shape == SHAPE_HEX && geom == GEOM_REGULAR && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7 &&
+        !getenv("SIPG_GENERIC_KERNELS")) {
+      k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? 1 : 2);
+      if (k) {
+        const int* ax = cd + CD_TAX;
+        cudaError_t e = k->upload(d->tables + ax[TX_V], d->tables + ax[TX_D], d->tables + ax[TX_W],
+                                  d->tables + ax[TX_DVEND]);
+        if (e != cudaSuccess) {
+          delete p;
+          return fail(SIPG_ERR_CUDA, std::string("constant table upload: ") + cudaGetErrorString(e));
+        }
+      }
+    }
+    if (!k && uniform) k = find_kernel(shape, n, q, geom);
     if (!k) {
       delete p;
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a kernel for shape=" + std::to_string(shape) +
@@ -131,6 +166,7 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   memcpy(p->bufs, b, sizeof(b));
   p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes};
   for (const KernelEntry* k : p->kern) {
+    if (k->smem == 0) continue;
     cudaError_t e = cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)k->smem);
     if (e != cudaSuccess) {
@@ -168,10 +204,11 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
   return 0;
 }
 
-int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out5) {
-  if (!p || cls < 0 || cls >= p->n_cls || !out5) return fail(SIPG_ERR_ARG, "bad argument");
+int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
+  if (!p || cls < 0 || cls >= p->n_cls || !out6) return fail(SIPG_ERR_ARG, "bad argument");
   const int32_t* cd = p->cd_host.data() + cls * CD_WORDS;
-  out5[0] = cd[CD_SHAPE]; out5[1] = cd[CD_N]; out5[2] = cd[CD_Q0]; out5[3] = cd[CD_GEOM]; out5[4] = cd[CD_COUNT];
+  out6[0] = cd[CD_SHAPE]; out6[1] = cd[CD_N]; out6[2] = cd[CD_Q0]; out6[3] = cd[CD_GEOM]; out6[4] = cd[CD_COUNT];
+  out6[5] = p->kern[cls]->kind;
   return 0;
 }
 

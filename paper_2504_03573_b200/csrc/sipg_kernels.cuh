@@ -523,6 +523,126 @@ __device__ __forceinline__ void fold_face(double* P0, double* Pk, const double* 
   }
 }
 
+// Flux of one face on the own face grid (any coupling type).  `us` holds the
+// own u, du_k at the own face points (stride FP, filled and synced by the
+// caller); the result fbf holds (fv, fd Gn_k) on the own face grid (stride NS).
+// Scratch layout of fscr: uo, xo, xs, ff (4*FP each), tmp (4*QMAX^2), nscr.
+template <int SHAPE, int N, int Q>
+__device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, const int f,
+                                          const double* __restrict__ x, double* __restrict__ us,
+                                          double* __restrict__ fbf, double* __restrict__ fscr,
+                                          const int tid, const int nt) {
+  using C = Cfg<SHAPE, N, Q>;
+  constexpr int D = C::D, NS = C::NS, FP = C::FP;
+  const double* T = P.tab;
+  const int fd = D - 1;
+  double* uo = fscr;
+  double* xo = uo + 4 * FP;
+  double* xs = xo + 4 * FP;
+  double* ff = xs + 4 * FP;
+  double* tmp = ff + 4 * FP;
+  double* nscr = tmp + 4 * QMAX * QMAX;
+  int no = 0;
+  int qo0 = 0, qo1 = 1;
+  if (r.type != FT_BOUNDARY) {
+    __syncthreads();
+    no = eval_face_from_coeffs(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt);
+    const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
+    const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
+    qo0 = cdo[CD_Q0 + fto.run0];
+    qo1 = fto.run1 >= 0 ? cdo[CD_Q0 + fto.run1] : 1;
+  }
+  __syncthreads();
+  const double tau = r.tau;
+  if (r.type != FT_SHARED) {
+    // flux on the own face grid
+    if (r.type == FT_DIRECT) {
+      // g_o on the other grid, then (u_o, g_o) -> own grid
+      for (int p = tid; p < no; p += nt) {
+        double gn[3];
+        other_gn(P, r, D, p, no, gn);
+        double g = 0.0;
+        for (int k = 0; k < D; ++k) g = fma(gn[k], uo[(1 + k) * FP + p], g);
+        uo[FP + p] = g;      // field 1 now holds g_o (du_0 no longer needed)
+      }
+      __syncthreads();
+      if (!(r.flags & F_OTHER_ID)) {
+        const int q0s = (SHAPE == SHAPE_TRI || D == 2) ? NS : Q;
+        const int q1s = D == 3 ? Q : 1;
+        xfer_fwd(uo, FP, qo0, qo1, xo, FP, q0s, q1s, T + r.to0, D == 3 ? T + r.to1 : nullptr,
+                 (r.flags & F_OTHER_SWAP) != 0, 2, tmp, fd, tid, nt);
+      } else {
+        for (int p = tid; p < NS; p += nt) { xo[p] = uo[p]; xo[FP + p] = uo[FP + p]; }
+        __syncthreads();
+      }
+    }
+    for (int p = tid; p < NS; p += nt) {
+      double gn[3];
+      const double swj = self_geom(P, r, SHAPE, f, D, p, NS, gn);
+      double gs = 0.0;
+      for (int k = 0; k < D; ++k) gs = fma(gn[k], us[(1 + k) * FP + p], gs);
+      double jump, avg;
+      if (r.type == FT_BOUNDARY) {
+        jump = 2.0 * us[p];
+        avg = gs;
+      } else {
+        jump = us[p] - xo[p];
+        avg = 0.5 * (gs - xo[FP + p]);
+      }
+      const double fv = (tau * jump - avg) * swj;
+      const double fdd = -0.5 * jump * swj;
+      fbf[p] = fv;
+      for (int k = 0; k < D; ++k) fbf[(1 + k) * NS + p] = fdd * gn[k];
+    }
+    __syncthreads();
+    return;
+  }
+  // ---- shared trace: flux on the trace grid
+  const int m0 = r.nt0, m1 = r.nt1, nflux = m0 * m1;
+  const bool same_self = (r.flags & F_SELF_ID) != 0;
+  if (!same_self) {
+    const int q0s = D == 3 ? Q : NS;
+    const int q1s = D == 3 ? Q : 1;
+    xfer_fwd(us, FP, q0s, q1s, xs, FP, m0, m1, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
+             (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
+  }
+  const double* vs = same_self ? us : xs;
+  if (!(r.flags & F_OTHER_ID)) {
+    xfer_fwd(uo, FP, qo0, qo1, xo, FP, m0, m1, T + r.to0, D == 3 ? T + r.to1 : nullptr,
+             (r.flags & F_OTHER_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
+  }
+  const double* vo = (r.flags & F_OTHER_ID) ? uo : xo;
+  for (int t = tid; t < nflux; t += nt) {
+    double gns[3], gno[3];
+    const double swj = self_geom(P, r, SHAPE, f, D, t, nflux, gns);
+    other_gn(P, r, D, t, nflux, gno);
+    double gs = 0.0, go = 0.0;
+    for (int k = 0; k < D; ++k) {
+      gs = fma(gns[k], vs[(1 + k) * FP + t], gs);
+      go = fma(gno[k], vo[(1 + k) * FP + t], go);
+    }
+    const double jump = vs[t] - vo[t];
+    const double avg = 0.5 * (gs - go);
+    const double fv = (tau * jump - avg) * swj;
+    const double fdd = -0.5 * jump * swj;
+    ff[t] = fv;
+    for (int k = 0; k < D; ++k) ff[(1 + k) * FP + t] = fdd * gns[k];
+  }
+  __syncthreads();
+  if (same_self) {
+    for (int i = tid; i < (1 + D) * NS; i += nt) {
+      const int fl = i / NS, p = i - fl * NS;
+      fbf[i] = ff[fl * FP + p];
+    }
+    __syncthreads();
+  } else {
+    const int q0s = D == 3 ? Q : NS;
+    const int q1s = D == 3 ? Q : 1;
+    xfer_bwd(ff, FP, m0, m1, fbf, NS, q0s, q1s, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
+             (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
+  }
+}
+
 template <int SHAPE, int N, int Q, int GEOM>
 __global__ void __launch_bounds__(Cfg<SHAPE, N, Q>::NT)
 k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
@@ -631,116 +751,12 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
   // ---- 3-4. faces: flux on each face, stored on the own face grid in fb
   const int rbase = cd[CD_REC_OFF] + i_el * C::NF;
   double* us = fs;              // 4 fields x FP, own face grid
-  double* uo = us + 4 * FP;     // other face grid
-  double* xo = uo + 4 * FP;     // other -> flux grid
-  double* xs = xo + 4 * FP;     // self -> flux grid
-  double* ff = xs + 4 * FP;     // flux fields on flux grid
-  double* tmp = ff + 4 * FP;    // transfer temporaries (4 x QMAX^2)
-  double* nscr = tmp + 4 * QMAX * QMAX;
-  const int fd = D - 1;
   for (int f = 0; f < C::NF; ++f) {
     const FaceRec r = P.recs[rbase + f];
-    double* fbf = fb + f * (1 + D) * NS;
     restrict_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, us, tid, nt);
-    int no = 0;
-    int qo0 = 0, qo1 = 1;
-    if (r.type != FT_BOUNDARY) {
-      __syncthreads();
-      no = eval_face_from_coeffs(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt);
-      const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
-      const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
-      qo0 = cdo[CD_Q0 + fto.run0];
-      qo1 = fto.run1 >= 0 ? cdo[CD_Q0 + fto.run1] : 1;
-    }
     __syncthreads();
-    const double tau = r.tau;
-    if (r.type != FT_SHARED) {
-      // flux on the own face grid
-      if (r.type == FT_DIRECT) {
-        // g_o on the other grid, then (u_o, g_o) -> own grid
-        for (int p = tid; p < no; p += nt) {
-          double gn[3];
-          other_gn(P, r, D, p, no, gn);
-          double g = 0.0;
-          for (int k = 0; k < D; ++k) g = fma(gn[k], uo[(1 + k) * FP + p], g);
-          uo[FP + p] = g;      // field 1 now holds g_o (du_0 no longer needed)
-        }
-        __syncthreads();
-        if (!(r.flags & F_OTHER_ID)) {
-          const int q0s = (SHAPE == SHAPE_TRI || D == 2) ? NS : Q;
-          const int q1s = D == 3 ? Q : 1;
-          xfer_fwd(uo, FP, qo0, qo1, xo, FP, q0s, q1s, T + r.to0, D == 3 ? T + r.to1 : nullptr,
-                   (r.flags & F_OTHER_SWAP) != 0, 2, tmp, fd, tid, nt);
-        } else {
-          for (int p = tid; p < NS; p += nt) { xo[p] = uo[p]; xo[FP + p] = uo[FP + p]; }
-          __syncthreads();
-        }
-      }
-      for (int p = tid; p < NS; p += nt) {
-        double gn[3];
-        const double swj = self_geom(P, r, SHAPE, f, D, p, NS, gn);
-        double gs = 0.0;
-        for (int k = 0; k < D; ++k) gs = fma(gn[k], us[(1 + k) * FP + p], gs);
-        double jump, avg;
-        if (r.type == FT_BOUNDARY) {
-          jump = 2.0 * us[p];
-          avg = gs;
-        } else {
-          jump = us[p] - xo[p];
-          avg = 0.5 * (gs - xo[FP + p]);
-        }
-        const double fv = (tau * jump - avg) * swj;
-        const double fdd = -0.5 * jump * swj;
-        fbf[p] = fv;
-        for (int k = 0; k < D; ++k) fbf[(1 + k) * NS + p] = fdd * gn[k];
-      }
-      __syncthreads();
-      continue;
-    }
-    // ---- shared trace: flux on the trace grid
-    const int m0 = r.nt0, m1 = r.nt1, nflux = m0 * m1;
-    const bool same_self = (r.flags & F_SELF_ID) != 0;
-    if (!same_self) {
-      const int q0s = D == 3 ? Q : NS;
-      const int q1s = D == 3 ? Q : 1;
-      xfer_fwd(us, FP, q0s, q1s, xs, FP, m0, m1, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
-               (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
-    }
-    const double* vs = same_self ? us : xs;
-    if (!(r.flags & F_OTHER_ID)) {
-      xfer_fwd(uo, FP, qo0, qo1, xo, FP, m0, m1, T + r.to0, D == 3 ? T + r.to1 : nullptr,
-               (r.flags & F_OTHER_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
-    }
-    const double* vo = (r.flags & F_OTHER_ID) ? uo : xo;
-    for (int t = tid; t < nflux; t += nt) {
-      double gns[3], gno[3];
-      const double swj = self_geom(P, r, SHAPE, f, D, t, nflux, gns);
-      other_gn(P, r, D, t, nflux, gno);
-      double gs = 0.0, go = 0.0;
-      for (int k = 0; k < D; ++k) {
-        gs = fma(gns[k], vs[(1 + k) * FP + t], gs);
-        go = fma(gno[k], vo[(1 + k) * FP + t], go);
-      }
-      const double jump = vs[t] - vo[t];
-      const double avg = 0.5 * (gs - go);
-      const double fv = (tau * jump - avg) * swj;
-      const double fdd = -0.5 * jump * swj;
-      ff[t] = fv;
-      for (int k = 0; k < D; ++k) ff[(1 + k) * FP + t] = fdd * gns[k];
-    }
+    generic_face<SHAPE, N, Q>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt);
     __syncthreads();
-    if (same_self) {
-      for (int i = tid; i < (1 + D) * NS; i += nt) {
-        const int fl = i / NS, p = i - fl * NS;
-        fbf[i] = ff[fl * FP + p];
-      }
-      __syncthreads();
-    } else {
-      const int q0s = D == 3 ? Q : NS;
-      const int q1s = D == 3 ? Q : 1;
-      xfer_bwd(ff, FP, m0, m1, fbf, NS, q0s, q1s, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
-               (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
-    }
   }
 
   // ---- volume point arrays: u -> P0 = lam jw u, du -> P_k = (jw G G^T du)_k

@@ -5,18 +5,24 @@
 #include "sipg_plan.h"
 
 using KernelFn = void (*)(const DevPlan, const int, const double*, double*);
+using UploadFn = cudaError_t (*)(const double* V, const double* D, const double* W, const double* dVend);
 
+// kind: 0 = generic smem kernel (any basis / rule / geometry),
+//       1 = register-column hex kernel, conforming + boundary faces only,
+//       2 = register-column hex kernel with the generic face path
 struct KernelEntry {
-  int shape, n, q, geom;
+  int shape, n, q, geom, kind;
   KernelFn fn;
   int threads;
-  size_t smem;
+  size_t smem;          // dynamic shared memory bytes
+  UploadFn upload;      // constant-table upload (kinds 1, 2)
 };
 
 void sipg_register_quad(std::vector<KernelEntry>& v);
 void sipg_register_tri(std::vector<KernelEntry>& v);
 void sipg_register_hex(std::vector<KernelEntry>& v);
 
+#include <cuda_runtime.h>
 #ifdef __CUDACC__
 template <int SHAPE, int N, int Q, int GEOM>
 KernelEntry sipg_entry();
@@ -24,10 +30,16 @@ KernelEntry sipg_entry();
   template <int SHAPE, int N, int Q, int GEOM>                                               \
   KernelEntry sipg_entry() {                                                                 \
     using C = sipg::Cfg<SHAPE, N, Q>;                                                        \
-    return KernelEntry{SHAPE, N, Q, GEOM, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,          \
-                       sizeof(double) * (size_t)C::TOTAL};                                   \
+    return KernelEntry{SHAPE, N, Q, GEOM, 0, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,       \
+                       sizeof(double) * (size_t)C::TOTAL, nullptr};                          \
   }
 #define SIPG_ENTRIES_NQ(S, N)                                                                \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_REGULAR>());                                      \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_POINTWISE>())
+#define SIPG_HEX_FAST(N)                                                                     \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1, &sipg::k_hex<N, N + 1, false>,  \
+                          (N + 1) * (N + 1), 0, &sipg::hex_fast_upload<N, N + 1>});             \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex<N, N + 1, true>,   \
+                          (N + 1) * (N + 1), sizeof(double) * sipg::HexFast<N, N + 1>::GSZ,      \
+                          &sipg::hex_fast_upload<N, N + 1>})
 #endif
