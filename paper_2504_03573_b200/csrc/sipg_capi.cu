@@ -50,16 +50,11 @@ const KernelEntry* find_kernel(int shape, int n, int q, int geom, int kind = 0) 
 bool class_all_fast(const sipg_plan_desc* d, int c) {
   const int32_t* cd = d->class_desc + c * CD_WORDS;
   const FaceRec* recs = (const FaceRec*)d->face_records;
-  const int n = cd[CD_N], q = cd[CD_Q0];
   for (int64_t r = cd[CD_REC_OFF]; r < cd[CD_REC_OFF] + (int64_t)cd[CD_COUNT] * cd[CD_NFACES]; ++r) {
     const FaceRec& f = recs[r];
     if (f.type == FT_BOUNDARY && !(f.flags & F_SELF_PW)) continue;
-    if (f.type != FT_DIRECT || !(f.flags & F_OTHER_ID) || (f.flags & (F_SELF_PW | F_OTHER_PW))) return false;
-    const int32_t* co = d->class_desc + d->elem_class[f.nbr] * CD_WORDS;
-    const int ao = f.nbr_face >> 1;
-    const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
-    if (co[CD_SHAPE] != SHAPE_HEX || co[CD_N] != n || co[CD_Q0] != q || f.go[b0] != 0.0 || f.go[b1] != 0.0)
-      return false;
+    if (f.type == FT_DIRECT && (f.flags & F_FAST_HEX)) continue;
+    return false;
   }
   return true;
 }

@@ -3,15 +3,19 @@
 // (j,k) owns the Q points (i, j, k) along axis 0 in registers, so the axis-0
 // contractions of BwdTrans / PhysDeriv / PhysDeriv^T / IProduct are in-register
 // and only the axis-1/2 contractions go through (bank-padded) shared memory.
-// 1-D tables live in __constant__ memory per (N, Q) instantiation and are
-// read as immediate operands of DFMA.
+// 1-D tables live in __constant__ memory per (N, Q) instantiation and are read
+// as uniform operands of DFMA.
 //
-// Faces: conforming same-class neighbours and boundary faces take the batched
-// fast path (all six faces' neighbour traces evaluated together from the
-// neighbours' coefficients, flux computed by the thread owning each face point
-// and added straight into its register point arrays — no scatter, no
-// atomics).  Any other coupling (shared trace, p2p, orientation transfers,
-// pointwise geometry) goes through generic_face().
+// Data movement: the element's and its six neighbours' coefficients are
+// fetched with cp.async at kernel entry (the neighbour copies complete behind
+// BwdTrans/PhysDeriv).  Faces flagged F_FAST_HEX (conforming same-class
+// neighbour, identity grid, constant metric) and constant-metric boundary faces
+// are evaluated together: the neighbour trace (u, du_normal) on the shared face
+// grid from its coefficients (boundary-mode plane + normal-derivative plane, two
+// sum-factorised 2-D passes), the flux at every face point, and the lift folded
+// into the owning thread's register point arrays (no scatter, no atomics).  Any
+// other coupling (shared trace, p2p, orientation transfers, pointwise metric)
+// goes through generic_face() in dynamic shared memory (GEN instantiations).
 #pragma once
 #include "sipg_kernels.cuh"
 
@@ -22,34 +26,53 @@ template <int N, int Q> __constant__ double hxD[Q * Q];     // collocation deriv
 template <int N, int Q> __constant__ double hxW[Q];         // GLL weights
 template <int N, int Q> __constant__ double hxDVE[2 * N];   // psi_i'(-1), psi_i'(+1)
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(PENDING) : "memory"); }
+
 template <int N, int Q>
 struct HexFast {
   static constexpr int NT = Q * Q;
-  static constexpr int SJ = Q + 1;            // padded row stride (bank spread)
+  static constexpr int SJ = (Q & 1) ? Q : Q + 1;   // odd row stride: conflict-free strided lines
   static constexpr int SI = Q * SJ;
   static constexpr int BUF = Q * SI;
-  static constexpr int FSC = 12 * N * N + 12 * Q * N + 12 * Q * Q;   // fast-face scratch
-  static constexpr int SCR = 4 * BUF > FSC ? 4 * BUF : FSC;            // B0..B3 as one array
-  // generic-face scratch (dynamic smem): us (4 FP), fscr (4*4 FP + 4 QMAX^2 + nscr), fb (6*4*Q*Q)
+  static constexpr int RS = (N & 1) ? N : N + 1;   // own-coefficient row stride
+  static constexpr int N3 = N * N * N;
+  // neighbour region: 6 coefficient blocks; later stage-1 output + face flux buffers
+  static constexpr int NBR = 6 * N3 > 12 * Q * N + 16 * Q * Q ? 6 * N3 : 12 * Q * N + 16 * Q * Q;
+  // scratch: 3 padded Q^3 buffers; later planes (12 N^2) + stage-2 output (12 Q^2)
+  static constexpr int SCR = 3 * BUF > 12 * N * N + 12 * Q * Q ? 3 * BUF : 12 * N * N + 12 * Q * Q;
+  // generic-face scratch (dynamic smem): us (4 FP), fscr, fb (6*4*Q*Q)
   static constexpr int FP = QMAX * QMAX;
-  static constexpr int GSZ = 4 * FP + 16 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX + 6 * 4 * Q * Q;
+  static constexpr int GFB = 4 * FP + 16 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX;
+  static constexpr int GSZ = GFB + 6 * 4 * Q * Q;
+  // dynamic shared memory layout (doubles): C | NB | S | generic scratch
+  static constexpr int CSZ = N * N * RS;
+  static constexpr int O_NB = CSZ;
+  static constexpr int O_S = O_NB + NBR;
+  static constexpr int O_G = O_S + SCR;
+  static size_t smem_bytes(bool gen) { return sizeof(double) * (size_t)(O_G + (gen ? GSZ : 0)); }
 };
 
-// face f of a hex: fixed axis f>>1, side (f&1 ? +1 : -1), run axes ascending
 __device__ __forceinline__ int hex_stride(int axis, int n) { return axis == 0 ? n * n : (axis == 1 ? n : 1); }
 
 template <int N, int Q, bool GEN>
 __global__ void __launch_bounds__(Q * Q)
 k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   using H = HexFast<N, Q>;
-  constexpr int NT = H::NT, SJ = H::SJ, SI = H::SI, BUF = H::BUF;
-  __shared__ double S[H::SCR];
+  constexpr int NT = H::NT, SJ = H::SJ, SI = H::SI, BUF = H::BUF, RS = H::RS, N3 = H::N3, QQ = Q * Q;
+  extern __shared__ double dsm[];
+  double* C = dsm;
+  double* NB = dsm + H::O_NB;
+  double* S = dsm + H::O_S;
+  double* gsm = dsm + H::O_G;
   __shared__ double sW[Q];
   __shared__ FaceRec srec[6];
-  __shared__ int sfast[6];            // 1 fast conforming, 2 boundary, 0 generic
-  __shared__ int snbr[6];
-  __shared__ int64_t snoff[6];
-  extern __shared__ double gsm[];
+  __shared__ int sk[6];               // 1 fast conforming, 2 boundary, 0 generic
   double* B0 = S;
   double* B1 = S + BUF;
   double* B2 = S + 2 * BUF;
@@ -58,60 +81,60 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   const int* cd = P.cd + cls * CD_WORDS;
   const int iel = blockIdx.x;
   const int e = P.class_elems[cd[CD_ELEM_OFF] + iel];
-  const double* xe = x + P.dof_off[e];
+  const int64_t dof0 = P.dof_off[e];
   const int rbase = cd[CD_REC_OFF] + iel * 6;
 
-  // ---- records, weights, coefficients
+  // ---- async fetch: records + own coefficients (group 0), neighbour blocks (group 1)
   for (int i = t; i < 6 * 16; i += NT)
-    reinterpret_cast<double*>(srec)[i] = __ldg(reinterpret_cast<const double*>(P.recs + rbase) + i);
-  if (t < Q) sW[t] = hxW<N, Q>[t];
-  for (int idx = t; idx < N * N * N; idx += NT) {
-    const int a = idx / (N * N), r = idx - a * N * N, b = r / N, c = r - b * N;
-    B0[a * SI + b * SJ + c] = __ldg(xe + idx);
+    cp_async8(reinterpret_cast<double*>(srec) + i, reinterpret_cast<const double*>(P.recs + rbase) + i);
+  if (ta < N && tb < N) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) cp_async8(C + (ta * N + tb) * RS + c, x + dof0 + (ta * N + tb) * N + c);
   }
+  cp_async_commit();
+  if (t < Q) sW[t] = hxW<N, Q>[t];
+  cp_async_wait<0>();
   __syncthreads();
   if (t < 6) {
-    const FaceRec& r = srec[t];
-    int kind = 0;
-    if (r.type == FT_BOUNDARY && !(r.flags & F_SELF_PW)) {
-      kind = 2;
-    } else if (r.type == FT_DIRECT && (r.flags & F_OTHER_ID) && !(r.flags & (F_SELF_PW | F_OTHER_PW))) {
-      const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
-      const int fo = r.nbr_face;
-      const int b0 = (fo >> 1) == 0 ? 1 : 0, b1 = (fo >> 1) == 2 ? 1 : 2;
-      if (cdo[CD_SHAPE] == SHAPE_HEX && cdo[CD_N] == N && cdo[CD_Q0] == Q && r.go[b0] == 0.0 && r.go[b1] == 0.0)
-        kind = 1;
-    }
-    sfast[t] = kind;
-    snbr[t] = r.nbr;
-    snoff[t] = r.nbr >= 0 ? P.dof_off[r.nbr] : 0;
+    const int fl = srec[t].flags, ty = srec[t].type;
+    sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
   }
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    if (srec[f].type == FT_DIRECT && (srec[f].flags & F_FAST_HEX)) {
+      const double* xo = x + srec[f].nbr_dof;
+      for (int i = t; i < N3; i += NT) cp_async8(NB + f * N3 + i, xo + i);
+    }
+  }
+  cp_async_commit();
 
   // ---- BwdTrans: axis 2 (thread (a,b)), axis 1 (thread (a,k)), axis 0 (thread (j,k))
   if (ta < N && tb < N) {
-    double v[N];
+    double v[N], o[Q];
 #pragma unroll
-    for (int c = 0; c < N; ++c) v[c] = B0[ta * SI + tb * SJ + c];
+    for (int c = 0; c < N; ++c) v[c] = C[(ta * N + tb) * RS + c];
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {
-      double acc = 0.0;
+    for (int k = 0; k < Q; ++k) o[k] = 0.0;
 #pragma unroll
-      for (int c = 0; c < N; ++c) acc = fma(hxV<N, Q>[k * N + c], v[c], acc);
-      B1[ta * SI + tb * SJ + k] = acc;
-    }
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int k = 0; k < Q; ++k) o[k] = fma(hxV<N, Q>[k * N + c], v[c], o[k]);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) B1[ta * SI + tb * SJ + k] = o[k];
   }
   __syncthreads();
   if (ta < N) {
-    double v[N];
+    double v[N], o[Q];
 #pragma unroll
     for (int b = 0; b < N; ++b) v[b] = B1[ta * SI + b * SJ + tb];
 #pragma unroll
-    for (int j = 0; j < Q; ++j) {
-      double acc = 0.0;
+    for (int j = 0; j < Q; ++j) o[j] = 0.0;
 #pragma unroll
-      for (int b = 0; b < N; ++b) acc = fma(hxV<N, Q>[j * N + b], v[b], acc);
-      B2[ta * SI + j * SJ + tb] = acc;
-    }
+    for (int b = 0; b < N; ++b)
+#pragma unroll
+      for (int j = 0; j < Q; ++j) o[j] = fma(hxV<N, Q>[j * N + b], v[b], o[j]);
+#pragma unroll
+    for (int j = 0; j < Q; ++j) B2[ta * SI + j * SJ + tb] = o[j];
   }
   __syncthreads();
   double u[Q], d0[Q], d1[Q], d2[Q];
@@ -120,22 +143,22 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 #pragma unroll
     for (int a = 0; a < N; ++a) v[a] = B2[a * SI + ta * SJ + tb];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-      double acc = 0.0;
+    for (int i = 0; i < Q; ++i) u[i] = 0.0;
 #pragma unroll
-      for (int a = 0; a < N; ++a) acc = fma(hxV<N, Q>[i * N + a], v[a], acc);
-      u[i] = acc;
-    }
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int i = 0; i < Q; ++i) u[i] = fma(hxV<N, Q>[i * N + a], v[a], u[i]);
   }
   // ---- PhysDeriv: axis 0 in registers; axes 1, 2 through shared memory
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    double acc = 0.0;
-#pragma unroll
-    for (int m = 0; m < Q; ++m) acc = fma(hxD<N, Q>[i * Q + m], u[m], acc);
-    d0[i] = acc;
+    d0[i] = 0.0;
     B0[i * SI + ta * SJ + tb] = u[i];
   }
+#pragma unroll
+  for (int m = 0; m < Q; ++m)
+#pragma unroll
+    for (int i = 0; i < Q; ++i) d0[i] = fma(hxD<N, Q>[i * Q + m], u[m], d0[i]);
   __syncthreads();
   {
     double v[Q], w[Q];
@@ -146,89 +169,98 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     }
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
-      double a1 = 0.0, a2 = 0.0;
+      d1[r] = 0.0;
+      d2[r] = 0.0;
+    }
 #pragma unroll
-      for (int m = 0; m < Q; ++m) {
-        a1 = fma(hxD<N, Q>[r * Q + m], v[m], a1);
-        a2 = fma(hxD<N, Q>[r * Q + m], w[m], a2);
+    for (int m = 0; m < Q; ++m)
+#pragma unroll
+      for (int r = 0; r < Q; ++r) {
+        d1[r] = fma(hxD<N, Q>[r * Q + m], v[m], d1[r]);
+        d2[r] = fma(hxD<N, Q>[r * Q + m], w[m], d2[r]);
       }
-      B1[ta * SI + r * SJ + tb] = a1;
-      B2[ta * SI + tb * SJ + r] = a2;
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+      B1[ta * SI + r * SJ + tb] = d1[r];
+      B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
+  cp_async_wait<0>();
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     d1[i] = B1[i * SI + ta * SJ + tb];
     d2[i] = B2[i * SI + ta * SJ + tb];
   }
-  __syncthreads();   // S is face scratch from here on
+  __syncthreads();   // S reused from here on
 
-  // ---- faces.  Fast path: neighbour (u, du_normal) on the shared face grid
-  // straight from the neighbours' coefficients, all fast faces at once.
-  // planes: NPu/NPd [f][i0][i1] (N*N each), stage 1 T[f][pl][p0][i1], stage 2 U[f][pl][p0][p1]
-  double* NP = S;                              // 6*2*N*N
-  double* T1 = NP + 12 * N * N;                // 6*2*Q*N
-  double* U2 = T1 + 12 * Q * N;                // 6*2*Q*Q
-  static_assert(12 * N * N + 12 * Q * N + 12 * Q * Q <= H::SCR, "face scratch");
-  for (int it = t; it < 6 * N * N; it += NT) {
-    const int f = it / (N * N), r = it - f * N * N;
-    if (sfast[f] != 1) continue;
-    const int i0 = r / N, i1 = r - i0 * N;
-    const int fo = srec[f].nbr_face, ao = fo >> 1, so = fo & 1;
-    const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
-    const double* xo = x + snoff[f];
-    const int base = i0 * hex_stride(b0, N) + i1 * hex_stride(b1, N);
-    const int sa = hex_stride(ao, N);
-    double pd = 0.0;
+  // ---- fast faces: neighbour (u, du_normal) on the face grid from its coefficients
+  double* NP = S;                      // [f][pl][i0][i1], 12 N^2
+  double* U2 = S + 12 * N * N;         // [f][pl][p0][p1], 12 Q^2
+  double* T1 = NB;                     // [f][pl][p0][i1], 12 Q N (neighbour blocks dead by then)
+  double* OWN = NB + 12 * Q * N;       // faces 2..5: own (u, g_s) [f-2][2][QQ]
+  double* FVD = OWN + 8 * QQ;          // faces 2..5: (fv, fd) [f-2][2][QQ]
+  if (t < N * N) {
+    const int i0 = t / N, i1 = t - (t / N) * N;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double dv = so ? hxDVE<N, Q>[N + i] : hxDVE<N, Q>[i];
-      pd = fma(dv, __ldg(xo + base + i * sa), pd);
+    for (int f = 0; f < 6; ++f) {
+      if (sk[f] != 1) continue;
+      const int fo = srec[f].nbr_face, ao = fo >> 1;
+      const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
+      const double* c = NB + f * N3 + i0 * hex_stride(b0, N) + i1 * hex_stride(b1, N);
+      const int sa = hex_stride(ao, N);
+      double pd = 0.0;
+      if (fo & 1) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[N + i], c[i * sa], pd);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[i], c[i * sa], pd);
+      }
+      NP[(2 * f) * N * N + t] = c[(fo & 1) ? (N - 1) * sa : 0];   // modified-modal boundary mode
+      NP[(2 * f + 1) * N * N + t] = pd;
     }
-    NP[(2 * f) * N * N + r] = __ldg(xo + base + (so ? (N - 1) * sa : 0));   // modified-modal boundary mode
-    NP[(2 * f + 1) * N * N + r] = pd;
   }
   __syncthreads();
-  for (int it = t; it < 12 * N; it += NT) {      // stage 1: contract i0 -> p0, line over i0 at fixed i1
-    const int fp = it / N, i1 = it - fp * N;
-    if (sfast[fp >> 1] != 1) continue;
-    double v[N];
+  for (int it = t; it < 12 * N; it += NT) {      // stage 1: contract i0 -> p0 (line over i0 at fixed i1)
+    const int fp = it / N, i1 = it - (it / N) * N;
+    if (sk[fp >> 1] != 1) continue;
+    double v[N], o[Q];
 #pragma unroll
     for (int i0 = 0; i0 < N; ++i0) v[i0] = NP[fp * N * N + i0 * N + i1];
 #pragma unroll
-    for (int p0 = 0; p0 < Q; ++p0) {
-      double acc = 0.0;
+    for (int p0 = 0; p0 < Q; ++p0) o[p0] = 0.0;
 #pragma unroll
-      for (int i0 = 0; i0 < N; ++i0) acc = fma(hxV<N, Q>[p0 * N + i0], v[i0], acc);
-      T1[fp * Q * N + p0 * N + i1] = acc;
-    }
+    for (int i0 = 0; i0 < N; ++i0)
+#pragma unroll
+      for (int p0 = 0; p0 < Q; ++p0) o[p0] = fma(hxV<N, Q>[p0 * N + i0], v[i0], o[p0]);
+#pragma unroll
+    for (int p0 = 0; p0 < Q; ++p0) T1[fp * Q * N + p0 * N + i1] = o[p0];
   }
   __syncthreads();
   for (int it = t; it < 12 * Q; it += NT) {      // stage 2: contract i1 -> p1
-    const int fp = it / Q, p0 = it - fp * Q;
-    if (sfast[fp >> 1] != 1) continue;
-    double v[N];
+    const int fp = it / Q, p0 = it - (it / Q) * Q;
+    if (sk[fp >> 1] != 1) continue;
+    double v[N], o[Q];
 #pragma unroll
     for (int i1 = 0; i1 < N; ++i1) v[i1] = T1[fp * Q * N + p0 * N + i1];
 #pragma unroll
-    for (int p1 = 0; p1 < Q; ++p1) {
-      double acc = 0.0;
+    for (int p1 = 0; p1 < Q; ++p1) o[p1] = 0.0;
 #pragma unroll
-      for (int i1 = 0; i1 < N; ++i1) acc = fma(hxV<N, Q>[p1 * N + i1], v[i1], acc);
-      U2[fp * Q * Q + p0 * Q + p1] = acc;
-    }
+    for (int i1 = 0; i1 < N; ++i1)
+#pragma unroll
+      for (int p1 = 0; p1 < Q; ++p1) o[p1] = fma(hxV<N, Q>[p1 * N + i1], v[i1], o[p1]);
+#pragma unroll
+    for (int p1 = 0; p1 < Q; ++p1) U2[fp * QQ + p0 * Q + p1] = o[p1];
   }
-  // generic faces (dynamic shared memory; GEN instantiations only)
-  double* gfb = gsm + 4 * H::FP + 16 * H::FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX;
+  // ---- generic faces (dynamic shared memory; GEN instantiations only)
+  double* gfb = gsm + H::GFB;
   if (GEN) {
     __syncthreads();
     for (int f = 0; f < 6; ++f) {
-      if (sfast[f] != 0) continue;
-      // own u, du_k on face f's grid (owners write), then the generic flux
+      if (sk[f] != 0) continue;
       const int a = f >> 1, hi = f & 1;
       double* us = gsm;
-      // point (p0, p1) of face f: a=0 -> (j,k); a=1 -> (i,k); a=2 -> (i,j)
       if (a == 0) {
         const int i = hi ? Q - 1 : 0;
         const int p = ta * Q + tb;
@@ -242,13 +274,73 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
         }
       }
       __syncthreads();
-      generic_face<SHAPE_HEX, N, Q>(P, srec[f], f, x, us, gfb + f * 4 * Q * Q, gsm + 4 * H::FP, t, NT);
+      generic_face<SHAPE_HEX, N, Q>(P, srec[f], f, x, us, gfb + f * 4 * QQ, gsm + 4 * H::FP, t, NT);
       __syncthreads();
     }
   }
+  // ---- faces 2..5: owners publish own (u, g_s); the flux is computed cooperatively
+#pragma unroll
+  for (int f = 2; f < 6; ++f) {
+    const int a = f >> 1, hi = f & 1;
+    const bool own = a == 1 ? (ta == (hi ? Q - 1 : 0)) : (tb == (hi ? Q - 1 : 0));
+    if (sk[f] == 0 || !own) continue;
+    const double g0 = srec[f].gs[0], g1 = srec[f].gs[1], g2 = srec[f].gs[2];
+    const int q1 = a == 1 ? tb : ta;
+    double* o = OWN + (f - 2) * 2 * QQ;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      o[i * Q + q1] = u[i];
+      o[QQ + i * Q + q1] = g0 * d0[i] + g1 * d1[i] + g2 * d2[i];
+    }
+  }
+  __syncthreads();
+  for (int it = t; it < 4 * QQ; it += NT) {
+    const int f = 2 + it / QQ, p = it - (it / QQ) * QQ;
+    const int kind = sk[f];
+    if (kind == 0) continue;
+    const FaceRec& r = srec[f];
+    const int p0 = p / Q, p1 = p - (p / Q) * Q;
+    const double* o = OWN + (f - 2) * 2 * QQ;
+    const double swj = r.sJ * sW[p0] * sW[p1];
+    const double us = o[p], gs = o[QQ + p];
+    double jump, avg;
+    if (kind == 2) {
+      jump = 2.0 * us;
+      avg = gs;
+    } else {
+      jump = us - U2[(2 * f) * QQ + p];
+      avg = 0.5 * (gs - r.go[r.nbr_face >> 1] * U2[(2 * f + 1) * QQ + p]);
+    }
+    FVD[(f - 2) * 2 * QQ + p] = (r.tau * jump - avg) * swj;
+    FVD[(f - 2) * 2 * QQ + QQ + p] = -0.5 * jump * swj;
+  }
+  // ---- faces 0/1 (points i = 0 and i = Q-1 of every thread): flux in registers
+  double fv01[2], fd01[2];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int i = f ? Q - 1 : 0;
+    const int kind = sk[f];
+    fv01[f] = 0.0;
+    fd01[f] = 0.0;
+    if (kind == 0) continue;
+    const FaceRec& r = srec[f];
+    const int p = ta * Q + tb;
+    const double swj = r.sJ * sW[ta] * sW[tb];
+    const double gs = r.gs[0] * d0[i] + r.gs[1] * d1[i] + r.gs[2] * d2[i];
+    double jump, avg;
+    if (kind == 2) {
+      jump = 2.0 * u[i];
+      avg = gs;
+    } else {
+      jump = u[i] - U2[(2 * f) * QQ + p];
+      avg = 0.5 * (gs - r.go[r.nbr_face >> 1] * U2[(2 * f + 1) * QQ + p]);
+    }
+    fv01[f] = (r.tau * jump - avg) * swj;
+    fd01[f] = -0.5 * jump * swj;
+  }
   __syncthreads();
 
-  // ---- flux at the face points owned by this thread + volume metric, per point
+  // ---- volume metric + lift of the face fluxes, per owned point
   const double lam = P.lam;
   const double* eg = P.egeo + cd[CD_EGEO_OFF] + (int64_t)iel * cd[CD_EGEO_STRIDE];
   const double J = eg[0];
@@ -256,51 +348,51 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   const double wjk = sW[ta] * sW[tb];
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;     // face contributions to P0..P3
-    const double ui = u[i], g0 = d0[i], g1 = d1[i], g2 = d2[i];
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
       const int a = f >> 1, hi = f & 1;
-      const int own = a == 0 ? (i == (hi ? Q - 1 : 0)) : (a == 1 ? (ta == (hi ? Q - 1 : 0)) : (tb == (hi ? Q - 1 : 0)));
+      bool own;
+      int p;
+      if (a == 0) {
+        own = i == (hi ? Q - 1 : 0);
+        p = ta * Q + tb;
+      } else if (a == 1) {
+        own = ta == (hi ? Q - 1 : 0);
+        p = i * Q + tb;
+      } else {
+        own = tb == (hi ? Q - 1 : 0);
+        p = i * Q + ta;
+      }
       if (!own) continue;
-      const int p0 = a == 0 ? ta : i, p1 = a == 2 ? ta : tb;
-      const int kind = sfast[f];
+      const int kind = sk[f];
       if (kind == 0) {
         if (GEN) {
-          const double* fbf = gfb + f * 4 * Q * Q;
-          const int p = p0 * Q + p1;
-          c0 += fbf[p]; c1 += fbf[Q * Q + p]; c2 += fbf[2 * Q * Q + p]; c3 += fbf[3 * Q * Q + p];
+          const double* fbf = gfb + f * 4 * QQ;
+          c0 += fbf[p]; c1 += fbf[QQ + p]; c2 += fbf[2 * QQ + p]; c3 += fbf[3 * QQ + p];
         }
         continue;
       }
-      const FaceRec& r = srec[f];
-      const double swj = r.sJ * sW[p0] * sW[p1];
-      const double gs = r.gs[0] * g0 + r.gs[1] * g1 + r.gs[2] * g2;
-      double jump, avg;
-      if (kind == 2) {
-        jump = 2.0 * ui;
-        avg = gs;
+      double fv, fd;
+      if (a == 0) {
+        fv = fv01[hi];
+        fd = fd01[hi];
       } else {
-        const int ao = r.nbr_face >> 1;
-        const double uo = U2[(2 * f) * Q * Q + p0 * Q + p1];
-        const double go = r.go[ao] * U2[(2 * f + 1) * Q * Q + p0 * Q + p1];
-        jump = ui - uo;
-        avg = 0.5 * (gs - go);
+        fv = FVD[(f - 2) * 2 * QQ + p];
+        fd = FVD[(f - 2) * 2 * QQ + QQ + p];
       }
-      const double fv = (r.tau * jump - avg) * swj;
-      const double fd = -0.5 * jump * swj;
       c0 += fv;
-      c1 += fd * r.gs[0];
-      c2 += fd * r.gs[1];
-      c3 += fd * r.gs[2];
+      c1 = fma(fd, srec[f].gs[0], c1);
+      c2 = fma(fd, srec[f].gs[1], c2);
+      c3 = fma(fd, srec[f].gs[2], c3);
     }
     const double jw = J * hxW<N, Q>[i] * wjk;
+    const double ui = u[i], g0 = d0[i], g1 = d1[i], g2 = d2[i];
     u[i] = lam * jw * ui + c0;
     d0[i] = jw * (K0 * g0 + K1 * g1 + K2 * g2) + c1;
     d1[i] = jw * (K1 * g0 + K3 * g1 + K4 * g2) + c2;
     d2[i] = jw * (K2 * g0 + K4 * g1 + K5 * g2) + c3;
   }
-  __syncthreads();   // face scratch (S) is reused below
 
   // ---- R = P0 + D0^T P1 (registers) + D1^T P2 + D2^T P3 (shared memory)
 #pragma unroll
@@ -309,12 +401,9 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     B2[i * SI + ta * SJ + tb] = d2[i];
   }
 #pragma unroll
-  for (int i = 0; i < Q; ++i) {
-    double acc = u[i];
+  for (int m = 0; m < Q; ++m)
 #pragma unroll
-    for (int m = 0; m < Q; ++m) acc = fma(hxD<N, Q>[m * Q + i], d0[m], acc);
-    u[i] = acc;
-  }
+    for (int i = 0; i < Q; ++i) u[i] = fma(hxD<N, Q>[m * Q + i], d0[m], u[i]);
   __syncthreads();
   {
     double v[Q], w[Q];
@@ -325,53 +414,65 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     }
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
-      double a1 = 0.0, a2 = 0.0;
+      d1[r] = 0.0;
+      d2[r] = 0.0;
+    }
 #pragma unroll
-      for (int m = 0; m < Q; ++m) {
-        a1 = fma(hxD<N, Q>[m * Q + r], v[m], a1);
-        a2 = fma(hxD<N, Q>[m * Q + r], w[m], a2);
+    for (int m = 0; m < Q; ++m)
+#pragma unroll
+      for (int r = 0; r < Q; ++r) {
+        d1[r] = fma(hxD<N, Q>[m * Q + r], v[m], d1[r]);
+        d2[r] = fma(hxD<N, Q>[m * Q + r], w[m], d2[r]);
       }
-      B1[ta * SI + r * SJ + tb] = a1;
-      B2[ta * SI + tb * SJ + r] = a2;
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+      B1[ta * SI + r * SJ + tb] = d1[r];
+      B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
   __syncthreads();
   // ---- IProduct: axis 0 in registers (thread (j,k)), then axes 1 and 2
 #pragma unroll
   for (int i = 0; i < Q; ++i) u[i] += B1[i * SI + ta * SJ + tb] + B2[i * SI + ta * SJ + tb];
+  {
+    double o[N];
 #pragma unroll
-  for (int a = 0; a < N; ++a) {
-    double acc = 0.0;
+    for (int a = 0; a < N; ++a) o[a] = 0.0;
 #pragma unroll
-    for (int i = 0; i < Q; ++i) acc = fma(hxV<N, Q>[i * N + a], u[i], acc);
-    B0[a * SI + ta * SJ + tb] = acc;
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+      for (int a = 0; a < N; ++a) o[a] = fma(hxV<N, Q>[i * N + a], u[i], o[a]);
+#pragma unroll
+    for (int a = 0; a < N; ++a) B0[a * SI + ta * SJ + tb] = o[a];
   }
   __syncthreads();
   if (ta < N) {                                     // thread (a, k): contract j -> b
-    double v[Q];
+    double v[Q], o[N];
 #pragma unroll
     for (int j = 0; j < Q; ++j) v[j] = B0[ta * SI + j * SJ + tb];
 #pragma unroll
-    for (int b = 0; b < N; ++b) {
-      double acc = 0.0;
+    for (int b = 0; b < N; ++b) o[b] = 0.0;
 #pragma unroll
-      for (int j = 0; j < Q; ++j) acc = fma(hxV<N, Q>[j * N + b], v[j], acc);
-      B1[ta * SI + b * SJ + tb] = acc;
-    }
+    for (int j = 0; j < Q; ++j)
+#pragma unroll
+      for (int b = 0; b < N; ++b) o[b] = fma(hxV<N, Q>[j * N + b], v[j], o[b]);
+#pragma unroll
+    for (int b = 0; b < N; ++b) B1[ta * SI + b * SJ + tb] = o[b];
   }
   __syncthreads();
   if (ta < N && tb < N) {                           // thread (a, b): contract k -> c, write y
-    double v[Q];
+    double v[Q], o[N];
 #pragma unroll
     for (int k = 0; k < Q; ++k) v[k] = B1[ta * SI + tb * SJ + k];
-    double* ye = y + P.dof_off[e] + (ta * N + tb) * N;
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double acc = 0.0;
+    for (int c = 0; c < N; ++c) o[c] = 0.0;
 #pragma unroll
-      for (int k = 0; k < Q; ++k) acc = fma(hxV<N, Q>[k * N + c], v[k], acc);
-      ye[c] = acc;
-    }
+    for (int k = 0; k < Q; ++k)
+#pragma unroll
+      for (int c = 0; c < N; ++c) o[c] = fma(hxV<N, Q>[k * N + c], v[k], o[c]);
+    double* ye = y + dof0 + (ta * N + tb) * N;
+#pragma unroll
+    for (int c = 0; c < N; ++c) ye[c] = o[c];
   }
 }
 

@@ -3,7 +3,7 @@
 #pragma once
 #include <stdint.h>
 
-#define SIPG_ABI_VERSION 3
+#define SIPG_ABI_VERSION 4
 
 enum { SHAPE_QUAD = 0, SHAPE_TRI = 1, SHAPE_HEX = 2 };
 enum { GEOM_REGULAR = 0, GEOM_POINTWISE = 1 };
@@ -24,11 +24,13 @@ enum {
 enum { FT_BOUNDARY = 0, FT_DIRECT = 1, FT_SHARED = 2 };
 enum {
   F_SELF_PW = 1, F_OTHER_PW = 2, F_OTHER_ID = 4, F_OTHER_SWAP = 8,
-  F_SELF_ID = 16, F_SELF_SWAP = 32, F_SELF_NEG = 64, F_OTHER_NEG = 128
+  F_SELF_ID = 16, F_SELF_SWAP = 32, F_SELF_NEG = 64, F_OTHER_NEG = 128,
+  F_FAST_HEX = 256   // conforming same-class hex neighbour, identity grid, constant metric, normal-only
 };
 
 struct FaceRec {            // 128 bytes, numpy dtype layout.FACE_REC
-  int32_t type, flags, nbr, nbr_face, nbr_rec, nt0, nt1, to0, to1, ts0, ts1, wt0, wt1, geo, pad0, pad1;
+  int32_t type, flags, nbr, nbr_face, nbr_rec, nt0, nt1, to0, to1, ts0, ts1, wt0, wt1, geo;
+  int64_t nbr_dof;          // dof offset of the neighbour (-1 on boundary faces)
   double tau, sJ, gs[3], go[3];
 };
 static_assert(sizeof(FaceRec) == 128, "FaceRec layout");

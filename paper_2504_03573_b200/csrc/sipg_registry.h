@@ -38,8 +38,9 @@ KernelEntry sipg_entry();
   v.push_back(sipg_entry<S, N, N + 1, GEOM_POINTWISE>())
 #define SIPG_HEX_FAST(N)                                                                     \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1, &sipg::k_hex<N, N + 1, false>,  \
-                          (N + 1) * (N + 1), 0, &sipg::hex_fast_upload<N, N + 1>});             \
+                          (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(false),         \
+                          &sipg::hex_fast_upload<N, N + 1>});                                   \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex<N, N + 1, true>,   \
-                          (N + 1) * (N + 1), sizeof(double) * sipg::HexFast<N, N + 1>::GSZ,      \
+                          (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(true),          \
                           &sipg::hex_fast_upload<N, N + 1>})
 #endif

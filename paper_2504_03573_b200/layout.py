@@ -4,7 +4,7 @@
 """
 import numpy as np
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 SHAPE_QUAD, SHAPE_TRI, SHAPE_HEX = 0, 1, 2
 SHAPE_ID = {"quad": SHAPE_QUAD, "tri": SHAPE_TRI, "hex": SHAPE_HEX}
@@ -35,12 +35,14 @@ F_SELF_ID = 16      # own face grid -> flux grid is the identity
 F_SELF_SWAP = 32
 F_SELF_NEG = 64     # triangle chain: self face parameter at flux point = -t
 F_OTHER_NEG = 128
+F_FAST_HEX = 256    # conforming same-class hex neighbour, identity grid, constant metric,
+                    # normal-only neighbour metric: register-column fast path
 
 FACE_REC = np.dtype([
     ("type", "<i4"), ("flags", "<i4"), ("nbr", "<i4"), ("nbr_face", "<i4"),
     ("nbr_rec", "<i4"), ("nt0", "<i4"), ("nt1", "<i4"), ("to0", "<i4"),
     ("to1", "<i4"), ("ts0", "<i4"), ("ts1", "<i4"), ("wt0", "<i4"),
-    ("wt1", "<i4"), ("geo", "<i4"), ("pad0", "<i4"), ("pad1", "<i4"),
+    ("wt1", "<i4"), ("geo", "<i4"), ("nbr_dof", "<i8"),
     ("tau", "<f8"), ("sJ", "<f8"), ("gs", "<f8", (3,)), ("go", "<f8", (3,)),
 ])
 assert FACE_REC.itemsize == 128

@@ -562,6 +562,13 @@ class PlanBuilder:
                     oc = self.f_const[eo, fo]
                     recs["go"][r, :d] = self.f_gxn[eo, fo, :d]
                     recs["flags"][r[~oc]] |= L.F_OTHER_PW
+                    if (d == 3 and ident and el == er and cl.kind.value == "modified_modal"
+                            and all(c_.axis[a]["gll"] for c_ in (cl,) for a in range(3))):
+                        ao = fo // 2
+                        tang = [b for b in range(3) if b != ao]
+                        ok = (oc & self.f_const[ee, ff_] & (self.f_gxn[eo, fo, tang[0]] == 0.0)
+                              & (self.f_gxn[eo, fo, tang[1]] == 0.0))
+                        recs["flags"][r[ok]] |= L.F_FAST_HEX
                 continue
             self._shared_bucket(cl, fl, cr, fr, code, le, re_, rl, rr)
         self._finish()
@@ -648,5 +655,7 @@ class PlanBuilder:
                 recs["geo"][r[j]] = self._add_fgeo(np.concatenate([swj[j], gs.T.reshape(-1), go.T.reshape(-1)]))
 
     def _finish(self):
+        nb = self.recs["nbr"]
+        self.recs["nbr_dof"] = np.where(nb >= 0, self.dof_off[np.maximum(nb, 0)], -1)
         self.fgeo = np.concatenate(self._fgeo) if self._fgeo else np.zeros(1)
         self.tables = self.pool.array()
