@@ -76,6 +76,7 @@ struct sipg_plan {
   int64_t n_dofs;
   std::vector<int32_t> cd_host;
   std::vector<const KernelEntry*> kern;
+  std::vector<int> grid;                 // CTAs per class launch (persistent kernels: SMs x occupancy)
   void* bufs[9];
   double* x_stage = nullptr;
   double* y_stage = nullptr;
@@ -169,6 +170,24 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
       return fail(SIPG_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     }
   }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int c = 0; c < p->n_cls; ++c) {
+    const KernelEntry* k = p->kern[c];
+    const int count = p->cd_host[c * CD_WORDS + CD_COUNT];
+    int g = count;
+    if (k->kind != 0) {
+      int per_sm = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k->fn, k->threads, k->smem);
+      if (e != cudaSuccess || per_sm <= 0) {
+        sipg_plan_destroy(p);
+        return fail(SIPG_ERR_CUDA, "occupancy query failed for a persistent kernel");
+      }
+      g = count < per_sm * sms ? count : per_sm * sms;
+    }
+    p->grid.push_back(g);
+  }
   *out = p;
   return 0;
 }
@@ -181,7 +200,7 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
     const int count = cd[CD_COUNT];
     if (count == 0) continue;
     const KernelEntry* k = p->kern[c];
-    k->fn<<<count, k->threads, k->smem, s>>>(p->dp, c, x_dev, y_dev);
+    k->fn<<<p->grid[c], k->threads, k->smem, s>>>(p->dp, c, x_dev, y_dev);
     ++p->launches;
   }
   CK(cudaGetLastError());
@@ -193,7 +212,7 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
   const int count = p->cd_host[cls * CD_WORDS + CD_COUNT];
   if (count == 0) return 0;
   const KernelEntry* k = p->kern[cls];
-  k->fn<<<count, k->threads, k->smem, (cudaStream_t)stream>>>(p->dp, cls, x_dev, y_dev);
+  k->fn<<<p->grid[cls], k->threads, k->smem, (cudaStream_t)stream>>>(p->dp, cls, x_dev, y_dev);
   ++p->launches;
   CK(cudaGetLastError());
   return 0;

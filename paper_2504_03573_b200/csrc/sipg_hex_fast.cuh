@@ -34,25 +34,70 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int PENDING>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(PENDING) : "memory"); }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  unsigned long long state;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state) : "r"(smem_u32(bar)), "r"(bytes) : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Copy n doubles at 8-byte-aligned global src into a shared region laid out so
+// that the 16-byte-aligned body can go through one TMA bulk copy; the (at most
+// one) unaligned head and tail doubles are plain loads.  Returns the offset of
+// element 0 inside `region` (region must be 16-byte aligned, n + 2 doubles).
+// Returns the bulk byte count through *bytes (to be expected on `bar`).
+__device__ __forceinline__ int bulk_block(double* region, const double* src, int n, uint64_t* bar,
+                                          unsigned* bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const int o = (a & 15) ? 1 : 0;
+  const uintptr_t b0 = (a + 15) & ~uintptr_t(15);
+  const uintptr_t e = a + 8 * (uintptr_t)n;
+  const uintptr_t b1 = e & ~uintptr_t(15);
+  if (o) region[0 + o] = __ldg(src);
+  if (e != b1) region[o + n - 1] = __ldg(src + n - 1);
+  const unsigned nb = b1 > b0 ? (unsigned)(b1 - b0) : 0u;
+  if (nb) bulk_g2s(region + o + (int)((b0 - a) >> 3), reinterpret_cast<const void*>(b0), nb, bar);
+  *bytes = nb;
+  return o;
+}
+
 template <int N, int Q>
 struct HexFast {
   static constexpr int NT = Q * Q;
   static constexpr int SJ = (Q & 1) ? Q : Q + 1;   // odd row stride: conflict-free strided lines
   static constexpr int SI = Q * SJ;
   static constexpr int BUF = Q * SI;
-  static constexpr int RS = (N & 1) ? N : N + 1;   // own-coefficient row stride
   static constexpr int N3 = N * N * N;
+  static constexpr int BLK = (N3 + 2 + 1) & ~1;    // one coefficient block (+ alignment slack), even
   // neighbour region: 6 coefficient blocks; later stage-1 output + face flux buffers
-  static constexpr int NBR = 6 * N3 > 12 * Q * N + 16 * Q * Q ? 6 * N3 : 12 * Q * N + 16 * Q * Q;
+  static constexpr int NBR = 6 * BLK > 12 * Q * N + 16 * Q * Q ? 6 * BLK : 12 * Q * N + 16 * Q * Q;
   // scratch: 3 padded Q^3 buffers; later planes (12 N^2) + stage-2 output (12 Q^2)
-  static constexpr int SCR = 3 * BUF > 12 * N * N + 12 * Q * Q ? 3 * BUF : 12 * N * N + 12 * Q * Q;
+  static constexpr int SCR0 = 3 * BUF > 12 * N * N + 12 * Q * Q ? 3 * BUF : 12 * N * N + 12 * Q * Q;
+  static constexpr int SCR = (SCR0 + 1) & ~1;
   // generic-face scratch (dynamic smem): us (4 FP), fscr, fb (6*4*Q*Q)
   static constexpr int FP = QMAX * QMAX;
   static constexpr int GFB = 4 * FP + 16 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX;
   static constexpr int GSZ = GFB + 6 * 4 * Q * Q;
-  // dynamic shared memory layout (doubles): C | NB | S | generic scratch
-  static constexpr int CSZ = N * N * RS;
-  static constexpr int O_NB = CSZ;
+  // dynamic shared memory (doubles, 16-byte aligned regions):
+  //   REC[2] (6 records = 96 doubles each) | CO[2] own coefficients | NB | S | generic scratch
+  static constexpr int O_REC = 0;
+  static constexpr int O_CO = 2 * 96;
+  static constexpr int O_NB = O_CO + 2 * BLK;
   static constexpr int O_S = O_NB + NBR;
   static constexpr int O_G = O_S + SCR;
   static size_t smem_bytes(bool gen) { return sizeof(double) * (size_t)(O_G + (gen ? GSZ : 0)); }
@@ -60,59 +105,82 @@ struct HexFast {
 
 __device__ __forceinline__ int hex_stride(int axis, int n) { return axis == 0 ? n * n : (axis == 1 ? n : 1); }
 
+// Persistent: CTA b processes elements b, b + gridDim.x, ... of the class.  The
+// next element's face records and coefficients stream in (TMA bulk copies on an
+// mbarrier) while the current one computes; the neighbours' coefficients
+// stream in behind BwdTrans / PhysDeriv.
 template <int N, int Q, bool GEN>
 __global__ void __launch_bounds__(Q * Q)
 k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   using H = HexFast<N, Q>;
-  constexpr int NT = H::NT, SJ = H::SJ, SI = H::SI, BUF = H::BUF, RS = H::RS, N3 = H::N3, QQ = Q * Q;
-  extern __shared__ double dsm[];
-  double* C = dsm;
+  constexpr int NT = H::NT, SJ = H::SJ, SI = H::SI, BUF = H::BUF, N3 = H::N3, QQ = Q * Q;
+  extern __shared__ __align__(16) double dsm[];
   double* NB = dsm + H::O_NB;
   double* S = dsm + H::O_S;
   double* gsm = dsm + H::O_G;
   __shared__ double sW[Q];
-  __shared__ FaceRec srec[6];
   __shared__ int sk[6];               // 1 fast conforming, 2 boundary, 0 generic
+  __shared__ int soff[8];             // block offsets (own coefficients per stage, neighbours)
+  __shared__ __align__(8) uint64_t mbar[3];   // records+own [stage 0, 1], neighbours
   double* B0 = S;
   double* B1 = S + BUF;
   double* B2 = S + 2 * BUF;
   const int t = threadIdx.x;
   const int ta = t / Q, tb = t - (t / Q) * Q;
   const int* cd = P.cd + cls * CD_WORDS;
-  const int iel = blockIdx.x;
-  const int e = P.class_elems[cd[CD_ELEM_OFF] + iel];
-  const int64_t dof0 = P.dof_off[e];
-  const int rbase = cd[CD_REC_OFF] + iel * 6;
-
-  // ---- async fetch: records + own coefficients (group 0), neighbour blocks (group 1)
-  for (int i = t; i < 6 * 16; i += NT)
-    cp_async8(reinterpret_cast<double*>(srec) + i, reinterpret_cast<const double*>(P.recs + rbase) + i);
-  if (ta < N && tb < N) {
-#pragma unroll
-    for (int c = 0; c < N; ++c) cp_async8(C + (ta * N + tb) * RS + c, x + dof0 + (ta * N + tb) * N + c);
+  const int count = cd[CD_COUNT];
+  const int* elist = P.class_elems + cd[CD_ELEM_OFF];
+  const double lam = P.lam;
+  if (t == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
+    fence_proxy_async();
   }
-  cp_async_commit();
   if (t < Q) sW[t] = hxW<N, Q>[t];
-  cp_async_wait<0>();
   __syncthreads();
+  // issue records + own coefficients of element `iel` into stage `st`
+  auto issue_own = [&](int iel, int st) {
+    const FaceRec* rsrc = P.recs + cd[CD_REC_OFF] + (int64_t)iel * 6;
+    bulk_g2s(dsm + H::O_REC + st * 96, rsrc, 6 * sizeof(FaceRec), &mbar[st]);
+    unsigned nb;
+    soff[st] = bulk_block(dsm + H::O_CO + st * H::BLK, x + P.dof_off[elist[iel]], N3, &mbar[st], &nb);
+    mbar_expect_tx(&mbar[st], 6 * sizeof(FaceRec) + nb);
+  };
+  if (t == 0 && blockIdx.x < count) issue_own(blockIdx.x, 0);
+
+  int k = 0;
+  for (int iel = blockIdx.x; iel < count; iel += gridDim.x, ++k) {
+  const int st = k & 1;
+  if (t == 0 && iel + (int)gridDim.x < count) issue_own(iel + gridDim.x, st ^ 1);
+  mbar_wait(&mbar[st], (k >> 1) & 1);
+  __syncthreads();
+  const FaceRec* srec = reinterpret_cast<const FaceRec*>(dsm + H::O_REC + st * 96);
+  const double* C = dsm + H::O_CO + st * H::BLK + soff[st];
+  const int e = elist[iel];
+  const int64_t dof0 = P.dof_off[e];
   if (t < 6) {
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
   }
+  if (t == 0) {
+    unsigned total = 0;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    if (srec[f].type == FT_DIRECT && (srec[f].flags & F_FAST_HEX)) {
-      const double* xo = x + srec[f].nbr_dof;
-      for (int i = t; i < N3; i += NT) cp_async8(NB + f * N3 + i, xo + i);
+    for (int f = 0; f < 6; ++f) {
+      if (srec[f].type == FT_DIRECT && (srec[f].flags & F_FAST_HEX)) {
+        unsigned nb;
+        soff[2 + f] = bulk_block(NB + f * H::BLK, x + srec[f].nbr_dof, N3, &mbar[2], &nb);
+        total += nb;
+      }
     }
+    mbar_expect_tx(&mbar[2], total);
   }
-  cp_async_commit();
 
   // ---- BwdTrans: axis 2 (thread (a,b)), axis 1 (thread (a,k)), axis 0 (thread (j,k))
   if (ta < N && tb < N) {
     double v[N], o[Q];
 #pragma unroll
-    for (int c = 0; c < N; ++c) v[c] = C[(ta * N + tb) * RS + c];
+    for (int c = 0; c < N; ++c) v[c] = C[(ta * N + tb) * N + c];
 #pragma unroll
     for (int k = 0; k < Q; ++k) o[k] = 0.0;
 #pragma unroll
@@ -185,7 +253,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
-  cp_async_wait<0>();
+  mbar_wait(&mbar[2], k & 1);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
@@ -207,7 +275,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       if (sk[f] != 1) continue;
       const int fo = srec[f].nbr_face, ao = fo >> 1;
       const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
-      const double* c = NB + f * N3 + i0 * hex_stride(b0, N) + i1 * hex_stride(b1, N);
+      const double* c = NB + f * H::BLK + soff[2 + f] + i0 * hex_stride(b0, N) + i1 * hex_stride(b1, N);
       const int sa = hex_stride(ao, N);
       double pd = 0.0;
       if (fo & 1) {
@@ -341,7 +409,6 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   __syncthreads();
 
   // ---- volume metric + lift of the face fluxes, per owned point
-  const double lam = P.lam;
   const double* eg = P.egeo + cd[CD_EGEO_OFF] + (int64_t)iel * cd[CD_EGEO_STRIDE];
   const double J = eg[0];
   const double K0 = eg[1], K1 = eg[2], K2 = eg[3], K3 = eg[4], K4 = eg[5], K5 = eg[6];
@@ -474,6 +541,9 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 #pragma unroll
     for (int c = 0; c < N; ++c) ye[c] = o[c];
   }
+  fence_proxy_async();   // generic accesses of this element before the next TMA writes
+  __syncthreads();
+  }  // element loop
 }
 
 // Upload the constant tables of one (N, Q) instantiation (from the plan's pool).
