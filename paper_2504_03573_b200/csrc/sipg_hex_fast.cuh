@@ -68,8 +68,10 @@ __device__ __forceinline__ int bulk_block(double* region, const double* src, int
   const uintptr_t b0 = (a + 15) & ~uintptr_t(15);
   const uintptr_t e = a + 8 * (uintptr_t)n;
   const uintptr_t b1 = e & ~uintptr_t(15);
-  if (o) region[0 + o] = __ldg(src);
-  if (e != b1) region[o + n - 1] = __ldg(src + n - 1);
+  // unaligned head / tail doubles: 8-byte cp.async (asynchronous; the issuing
+  // thread completes them with cp_async_wait<0>() before the consumers' barrier)
+  if (o) cp_async8(region + o, src);
+  if (e != b1) cp_async8(region + o + n - 1, src + n - 1);
   const unsigned nb = b1 > b0 ? (unsigned)(b1 - b0) : 0u;
   if (nb) bulk_g2s(region + o + (int)((b0 - a) >> 3), reinterpret_cast<const void*>(b0), nb, bar);
   *bytes = nb;
@@ -146,13 +148,18 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     unsigned nb;
     soff[st] = bulk_block(dsm + H::O_CO + st * H::BLK, x + P.dof_off[elist[iel]], N3, &mbar[st], &nb);
     mbar_expect_tx(&mbar[st], 6 * sizeof(FaceRec) + nb);
+    cp_async_commit();
   };
   if (t == 0 && blockIdx.x < count) issue_own(blockIdx.x, 0);
 
   int k = 0;
   for (int iel = blockIdx.x; iel < count; iel += gridDim.x, ++k) {
   const int st = k & 1;
-  if (t == 0 && iel + (int)gridDim.x < count) issue_own(iel + gridDim.x, st ^ 1);
+  const bool more = iel + (int)gridDim.x < count;
+  if (t == 0 && more) issue_own(iel + gridDim.x, st ^ 1);
+  if (t == 0) {
+    if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+  }
   mbar_wait(&mbar[st], (k >> 1) & 1);
   __syncthreads();
   const FaceRec* srec = reinterpret_cast<const FaceRec*>(dsm + H::O_REC + st * 96);
@@ -163,7 +170,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
   }
-  if (t == 0) {
+  if (t == 32) {                       // neighbour blocks: another warp than the prefetch issuer
     unsigned total = 0;
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
@@ -174,6 +181,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       }
     }
     mbar_expect_tx(&mbar[2], total);
+    cp_async_commit();
   }
 
   // ---- BwdTrans: axis 2 (thread (a,b)), axis 1 (thread (a,k)), axis 0 (thread (j,k))
@@ -253,6 +261,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
+  if (t == 32) cp_async_wait<0>();
   mbar_wait(&mbar[2], k & 1);
   __syncthreads();
 #pragma unroll

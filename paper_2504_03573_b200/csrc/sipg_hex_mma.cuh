@@ -49,18 +49,23 @@ __device__ __forceinline__ void mma_axis(const double* __restrict__ in, double* 
                                          const int lane, const int tile0) {
   const int kq = lane & 3, n = lane >> 2;
   const int r = lane >> 2, c = 2 * (lane & 3);
+  double b0[NTL], b1[NTL], c0[NTL], c1[NTL];
 #pragma unroll
   for (int tt = 0; tt < NTL; ++tt) {
-    const int tile = tile0 + tt;
-    double c0 = 0.0, c1 = 0.0;
-    if (ACC) {
-      c0 = out[tidx<AX>(r, tile, c)];
-      c1 = out[tidx<AX>(r, tile, c + 1)];
-    }
-    dmma(c0, c1, A.a0, in[tidx<AX>(kq, tile, n)]);
-    dmma(c0, c1, A.a1, in[tidx<AX>(4 + kq, tile, n)]);
-    out[tidx<AX>(r, tile, c)] = c0;
-    out[tidx<AX>(r, tile, c + 1)] = c1;
+    b0[tt] = in[tidx<AX>(kq, tile0 + tt, n)];
+    b1[tt] = in[tidx<AX>(4 + kq, tile0 + tt, n)];
+    c0[tt] = ACC ? out[tidx<AX>(r, tile0 + tt, c)] : 0.0;
+    c1[tt] = ACC ? out[tidx<AX>(r, tile0 + tt, c + 1)] : 0.0;
+  }
+#pragma unroll
+  for (int tt = 0; tt < NTL; ++tt) {
+    dmma(c0[tt], c1[tt], A.a0, b0[tt]);
+    dmma(c0[tt], c1[tt], A.a1, b1[tt]);
+  }
+#pragma unroll
+  for (int tt = 0; tt < NTL; ++tt) {
+    out[tidx<AX>(r, tile0 + tt, c)] = c0[tt];
+    out[tidx<AX>(r, tile0 + tt, c + 1)] = c1[tt];
   }
 }
 
@@ -142,13 +147,18 @@ k_hex_mma(const DevPlan P, const int cls, const double* __restrict__ x, double* 
     unsigned nb;
     soff[st] = bulk_block(dsm + H::O_X + st * H::BLK, x + P.dof_off[elist[iel]], N3, &mbar[st], &nb);
     mbar_expect_tx(&mbar[st], 6 * sizeof(FaceRec) + nb);
+    cp_async_commit();
   };
   if (t == 0 && blockIdx.x < count) issue_own(blockIdx.x, 0);
 
   int kk = 0;
   for (int iel = blockIdx.x; iel < count; iel += gridDim.x, ++kk) {
     const int st = kk & 1;
-    if (t == 0 && iel + (int)gridDim.x < count) issue_own(iel + gridDim.x, st ^ 1);
+    const bool more = iel + (int)gridDim.x < count;
+    if (t == 0 && more) issue_own(iel + gridDim.x, st ^ 1);
+    if (t == 0) {                        // head/tail doubles of this element (issued by thread 0)
+      if (more) cp_async_wait<1>(); else cp_async_wait<0>();
+    }
     mbar_wait(&mbar[st], (kk >> 1) & 1);
     __syncthreads();
     const FaceRec* srec = reinterpret_cast<const FaceRec*>(dsm + H::O_REC + st * 96);
@@ -170,6 +180,7 @@ k_hex_mma(const DevPlan P, const int cls, const double* __restrict__ x, double* 
         }
       }
       mbar_expect_tx(&mbar[2], total);
+      cp_async_commit();
     }
 
     // ---- BwdTrans.  Axis 2 straight from the raw coefficient block (zero padded on the fly)
@@ -197,6 +208,7 @@ k_hex_mma(const DevPlan P, const int cls, const double* __restrict__ x, double* 
     mma_axis<0, false, 2>(U, G0, AD, lane, warp * 2);
     mma_axis<1, false, 2>(U, G1, AD, lane, warp * 2);
     mma_axis<2, false, 2>(U, G2, AD, lane, warp * 2);
+    if (t == 32) cp_async_wait<0>();     // neighbour head/tail doubles (issued by thread 32)
     mbar_wait(&mbar[2], kk & 1);
     __syncthreads();
 
