@@ -2,6 +2,7 @@
 #include "sipg_kernels.cuh"
 #include "sipg_hex_fast.cuh"
 #include "sipg_hex_mma.cuh"
+#include "sipg_hex_warp.cuh"
 #include "sipg_registry.h"
 SIPG_DEFINE_ENTRY
 void sipg_register_hex(std::vector<KernelEntry>& v) {

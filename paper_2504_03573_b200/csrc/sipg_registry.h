@@ -43,10 +43,12 @@ KernelEntry sipg_entry();
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex<N, N + 1, true>,   \
                           (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(true),          \
                           &sipg::hex_fast_upload<N, N + 1>})
-// fp64 tensor-core (DMMA) hex kernel, Q <= 8
+// fp64 tensor-core (DMMA) hex kernels, Q <= 8: warp-per-element (all faces fast) and CTA-per-element
 #define SIPG_HEX_MMA(N)                                                                      \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1, &sipg::k_hex_mma<N, N + 1, false>, \
-                          128, sipg::HexMma<N, N + 1>::smem_bytes(false),                        \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1,                              \
+                          &sipg::k_hexw<N, N + 1, sipg::HexWarpSlice<N, N + 1>::W>,           \
+                          32 * sipg::HexWarpSlice<N, N + 1>::W,                               \
+                          sipg::HexWarp<N, N + 1, sipg::HexWarpSlice<N, N + 1>::W>::smem_bytes(), \
                           &sipg::hex_mma_upload<N, N + 1>});                                    \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex_mma<N, N + 1, true>,  \
                           128, sipg::HexMma<N, N + 1>::smem_bytes(true),                         \
