@@ -123,7 +123,12 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     const KernelEntry* k = nullptr;
     if (uniform && shape == SHAPE_HEX && geom == GEOM_REGULAR && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7 &&
         !getenv("SIPG_GENERIC_KERNELS")) {
-      k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? 1 : 2);
+      // SIPG_HEX_FAST_KERNEL: instrumentation override of the all-fast-faces kernel
+      // (1 warp-per-element DMMA, 3 CTA-per-element DMMA, 4 DFMA register-column [default, fastest measured])
+      const char* ov = getenv("SIPG_HEX_FAST_KERNEL");
+      const int fast_kind = ov ? atoi(ov) : 4;
+      k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? fast_kind : 2);
+      if (!k) k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? 1 : 2);
       if (k) {
         const int* ax = cd + CD_TAX;
         cudaError_t e = k->upload(d->tables + ax[TX_V], d->tables + ax[TX_D], d->tables + ax[TX_W],
@@ -160,7 +165,8 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   }
   void* b[9] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d};
   memcpy(p->bufs, b, sizeof(b));
-  p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes};
+  p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes,
+                  getenv("SIPG_DEBUG") ? atoi(getenv("SIPG_DEBUG")) : 0, 0};
   for (const KernelEntry* k : p->kern) {
     if (k->smem == 0) continue;
     cudaError_t e = cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -167,13 +167,13 @@ k_hexw(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
     if (lane < 6) {
       const FaceRec& r = srec[lane];
       const bool fast = r.type == FT_DIRECT && (r.flags & F_FAST_HEX);
-      sk[lane] = fast ? 1 : ((r.type == FT_BOUNDARY && !(r.flags & F_SELF_PW)) ? 2 : 0);
+      sk[lane] = (P.debug & 1) ? 0 : (fast ? 1 : ((r.type == FT_BOUNDARY && !(r.flags & F_SELF_PW)) ? 2 : 0));
     }
     if (lane >= 1 && lane <= 6) {     // one neighbour block per lane
       const int f = lane - 1;
       const FaceRec& r = srec[f];
       unsigned nb = 0;
-      if (r.type == FT_DIRECT && (r.flags & F_FAST_HEX))
+      if (r.type == FT_DIRECT && (r.flags & F_FAST_HEX) && !(P.debug & 1))
         soff[2 + f] = bulk_block(NB + f * H::FBLK, x + r.nbr_dof, N3, &mbar[2], &nb);
       mbar_expect_tx(&mbar[2], nb);
       cp_async_commit();

@@ -48,4 +48,6 @@ struct DevPlan {
   double lam;
   int32_t dim;
   int32_t n_cls;
+  int32_t debug;               // instrumentation bits (SIPG_DEBUG env): 1 = skip face work (timing only)
+  int32_t pad;
 };

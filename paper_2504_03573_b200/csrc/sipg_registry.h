@@ -52,5 +52,11 @@ KernelEntry sipg_entry();
                           &sipg::hex_mma_upload<N, N + 1>});                                    \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex_mma<N, N + 1, true>,  \
                           128, sipg::HexMma<N, N + 1>::smem_bytes(true),                         \
-                          &sipg::hex_mma_upload<N, N + 1>})
+                          &sipg::hex_mma_upload<N, N + 1>});                                    \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 3, &sipg::k_hex_mma<N, N + 1, false>, \
+                          128, sipg::HexMma<N, N + 1>::smem_bytes(false),                        \
+                          &sipg::hex_mma_upload<N, N + 1>});                                    \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 4, &sipg::k_hex<N, N + 1, false>,     \
+                          (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(false),         \
+                          &sipg::hex_fast_upload<N, N + 1>})
 #endif
