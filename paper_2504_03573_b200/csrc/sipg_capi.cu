@@ -96,7 +96,7 @@ int sipg_abi_layout(int32_t* out, int32_t n) {
 }
 
 int sipg_supported(int32_t shape, int32_t n_modes, int32_t n_quad) {
-  return find_kernel(shape, n_modes, n_quad, GEOM_REGULAR) != nullptr;
+  return find_kernel(shape, n_modes, n_quad, GEOM_REGULAR, shape == SHAPE_HEX ? 0 : 5) != nullptr;
 }
 
 int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
@@ -139,7 +139,7 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
         }
       }
     }
-    if (!k && uniform) k = find_kernel(shape, n, q, geom);
+    if (!k && uniform) k = find_kernel(shape, n, q, geom, shape == SHAPE_HEX ? 0 : 5);
     if (!k) {
       delete p;
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a kernel for shape=" + std::to_string(shape) +

@@ -27,6 +27,10 @@ constexpr int NMAX = 10;   // largest supported modes per direction
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
+// A "team" works on one element: a whole CTA or a single warp.
+struct CtaTeam { static __device__ __forceinline__ void sync() { __syncthreads(); } };
+struct WarpTeam { static __device__ __forceinline__ void sync() { __syncwarp(); } };
+
 // ---------------------------------------------------------------------------
 // compile-time tensor contraction on shared memory.
 // in: dims (S0,S1,S2) row-major, contract axis AX (size K) with M:
@@ -91,6 +95,7 @@ __device__ __forceinline__ void tri_chain(int f, double p, double& c00, double& 
 // neighbour trace evaluation from coefficients, on the neighbour's own face grid.
 // out[0*FP + p] = u, out[(1+k)*FP + p] = du/deta_k (neighbour axes).  Returns the
 // number of face points.  Runtime sizes: only used for the face part.
+template <class TM = CtaTeam>
 static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, const double* __restrict__ x,
                                      double* __restrict__ out, int FP, double* __restrict__ scr,
                                      int tid, int nt) {
@@ -119,7 +124,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
         }
         tg[g] = a; dtg[g] = b;
       }
-      __syncthreads();
+      TM::sync();
       const double* A = T + cd[TR_A];
       const double* dA = T + cd[TR_DA];
       for (int p = tid; p < q; p += nt) {
@@ -132,7 +137,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
         }
         out[p] = u; out[FP + p] = d0; out[2 * FP + p] = d1;
       }
-      __syncthreads();
+      TM::sync();
       return q;
     }
     // eta1 = side: direction-1 row at the endpoint, direction-2 tables at the GL points
@@ -159,7 +164,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
       }
       out[p] = u; out[FP + p] = d0; out[2 * FP + p] = d1;
     }
-    __syncthreads();
+    TM::sync();
     return q;
   }
   const int d = shape == SHAPE_HEX ? 3 : 2;
@@ -185,7 +190,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
       }
       pv[i] = s; pd[i] = t;
     }
-    __syncthreads();
+    TM::sync();
     for (int p = tid; p < q0; p += nt) {
       double u = 0.0, du = 0.0, dn = 0.0;
       for (int i = 0; i < n; ++i) {
@@ -198,7 +203,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
       out[(1 + b0) * FP + p] = du;
       out[(1 + a) * FP + p] = dn;
     }
-    __syncthreads();
+    TM::sync();
     return q0;
   }
   const int b1 = ft.run1;
@@ -222,7 +227,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
     }
     pv[i] = s; pd[i] = t;
   }
-  __syncthreads();
+  TM::sync();
   for (int i = tid; i < q0 * n; i += nt) {
     const int p0 = i / n, i1 = i - p0 * n;
     double s = 0.0, t = 0.0, r = 0.0;
@@ -234,7 +239,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
     }
     tv[i] = s; td[i] = t; tp[i] = r;
   }
-  __syncthreads();
+  TM::sync();
   for (int i = tid; i < q0 * q1; i += nt) {
     const int p0 = i / q1, p1 = i - p0 * q1;
     double u = 0.0, d1 = 0.0, d0 = 0.0, dn = 0.0;
@@ -250,13 +255,14 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
     out[(1 + b1) * FP + i] = d1;
     out[(1 + a) * FP + i] = dn;
   }
-  __syncthreads();
+  TM::sync();
   return q0 * q1;
 }
 
 // ---------------------------------------------------------------------------
 // transfers between face grids: per flux axis 1-D matrices (pool), optional swap.
 // forward: in (n0 x n1) -> out (m0 x m1); T0: m0 x n_sig0, T1: m1 x n_sig1.
+template <class TM = CtaTeam>
 static __device__ void xfer_fwd(const double* __restrict__ in, int FPin, int n0, int n1,
                          double* __restrict__ out, int FPout, int m0, int m1,
                          const double* __restrict__ T0, const double* __restrict__ T1, bool swap,
@@ -268,7 +274,7 @@ static __device__ void xfer_fwd(const double* __restrict__ in, int FPin, int n0,
       for (int k = 0; k < n0; ++k) s = fma(ldg(T0 + t * n0 + k), in[fl * FPin + k], s);
       out[fl * FPout + t] = s;
     }
-    __syncthreads();
+    TM::sync();
     return;
   }
   if (!swap) {
@@ -279,7 +285,7 @@ static __device__ void xfer_fwd(const double* __restrict__ in, int FPin, int n0,
       for (int k = 0; k < n1; ++k) s = fma(ldg(T1 + t1 * n1 + k), in[fl * FPin + s0 * n1 + k], s);
       tmp[fl * QMAX * QMAX + s0 * m1 + t1] = s;
     }
-    __syncthreads();
+    TM::sync();
     for (int i = tid; i < nf * m0 * m1; i += nt) {
       const int fl = i / (m0 * m1), r = i - fl * m0 * m1, t0 = r / m1, t1 = r - t0 * m1;
       double s = 0.0;
@@ -294,7 +300,7 @@ static __device__ void xfer_fwd(const double* __restrict__ in, int FPin, int n0,
       for (int k = 0; k < n0; ++k) s = fma(ldg(T1 + t1 * n0 + k), in[fl * FPin + k * n1 + s1], s);
       tmp[fl * QMAX * QMAX + t1 * n1 + s1] = s;
     }
-    __syncthreads();
+    TM::sync();
     for (int i = tid; i < nf * m0 * m1; i += nt) {
       const int fl = i / (m0 * m1), r = i - fl * m0 * m1, t0 = r / m1, t1 = r - t0 * m1;
       double s = 0.0;
@@ -302,10 +308,11 @@ static __device__ void xfer_fwd(const double* __restrict__ in, int FPin, int n0,
       out[fl * FPout + r] = s;
     }
   }
-  __syncthreads();
+  TM::sync();
 }
 
 // transpose: in (m0 x m1) on the flux grid -> out (n0 x n1) on the source grid
+template <class TM = CtaTeam>
 static __device__ void xfer_bwd(const double* __restrict__ in, int FPin, int m0, int m1,
                          double* __restrict__ out, int FPout, int n0, int n1,
                          const double* __restrict__ T0, const double* __restrict__ T1, bool swap,
@@ -317,7 +324,7 @@ static __device__ void xfer_bwd(const double* __restrict__ in, int FPin, int m0,
       for (int t = 0; t < m0; ++t) s = fma(ldg(T0 + t * n0 + s0), in[fl * FPin + t], s);
       out[fl * FPout + s0] = s;
     }
-    __syncthreads();
+    TM::sync();
     return;
   }
   if (!swap) {
@@ -328,7 +335,7 @@ static __device__ void xfer_bwd(const double* __restrict__ in, int FPin, int m0,
       for (int t1 = 0; t1 < m1; ++t1) s = fma(ldg(T1 + t1 * n1 + s1), in[fl * FPin + t0 * m1 + t1], s);
       tmp[fl * QMAX * QMAX + t0 * n1 + s1] = s;
     }
-    __syncthreads();
+    TM::sync();
     for (int i = tid; i < nf * n0 * n1; i += nt) {
       const int fl = i / (n0 * n1), r = i - fl * n0 * n1, s0 = r / n1, s1 = r - s0 * n1;
       double s = 0.0;
@@ -343,7 +350,7 @@ static __device__ void xfer_bwd(const double* __restrict__ in, int FPin, int m0,
       for (int t0 = 0; t0 < m0; ++t0) s = fma(ldg(T0 + t0 * n1 + s1), in[fl * FPin + t0 * m1 + t1], s);
       tmp[fl * QMAX * QMAX + t1 * n1 + s1] = s;
     }
-    __syncthreads();
+    TM::sync();
     for (int i = tid; i < nf * n0 * n1; i += nt) {
       const int fl = i / (n0 * n1), r = i - fl * n0 * n1, s0 = r / n1, s1 = r - s0 * n1;
       double s = 0.0;
@@ -351,7 +358,7 @@ static __device__ void xfer_bwd(const double* __restrict__ in, int FPin, int m0,
       out[fl * FPout + r] = s;
     }
   }
-  __syncthreads();
+  TM::sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -439,21 +446,23 @@ struct Cfg {
   static constexpr int NS = D == 3 ? Q * Q : Q;              // own face points
   static constexpr int FP = D == 3 ? QMAX * QMAX : QMAX;     // face-field stride
   static constexpr int NT = D == 3 ? 128 : 64;
-  // shared memory layout (doubles)
-  static constexpr int o_c = 0;
-  static constexpr int o_u = o_c + ((NC + 1) & ~1);
-  static constexpr int o_du = o_u + NP;
-  static constexpr int o_t1 = o_du + D * NP;
-  static constexpr int o_t2 = o_t1 + NP;
-  static constexpr int o_tab = o_t2 + NP;
   static constexpr int TABSZ = SHAPE == SHAPE_TRI
-      ? (2 * Q * (N + 1) + 3 * Q * Q + 2 * Q + Q * NC + NC + 4 * Q + 2 * Q)
+      ? (2 * Q * (N + 1) + 3 * Q * Q + 2 * Q + Q * NC + NC + 4 * Q + 2 * Q + (N + 2) + NC)
       : D * (Q * N + Q * Q + Q + 2 * Q);
-  static constexpr int o_fb = o_tab + ((TABSZ + 1) & ~1);
-  static constexpr int o_fs = o_fb + NF * (1 + D) * NS;
-  // face scratch: us(4FP) uo(4FP) xo(4FP) xs(4FP) ff(4FP) tmp(4 QMAX^2) nbr(2NMAX^2+3QMAX NMAX)
-  static constexpr int FSZ = 5 * 4 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX;
-  static constexpr int TOTAL = o_fs + FSZ;
+  static constexpr int TABP = (TABSZ + 1) & ~1;
+  // element scratch layout (doubles)
+  static constexpr int e_c = 0;
+  static constexpr int e_u = e_c + ((NC + 1) & ~1);
+  static constexpr int e_du = e_u + NP;
+  static constexpr int e_t1 = e_du + D * NP;
+  static constexpr int e_t2 = e_t1 + NP;
+  static constexpr int e_fb = e_t2 + NP;
+  static constexpr int e_fs = e_fb + NF * (1 + D) * NS;
+  // face scratch: us(4FP) uo(4FP) xo(4FP) xs(4FP) ff(4FP) tmp(4 QMAX^2, 3-D) nbr
+  static constexpr int FSZ = D == 3 ? 5 * 4 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX
+                                    : 5 * 4 * FP + 2 * (NMAX + 2);
+  static constexpr int ESZ = (e_fs + FSZ + 1) & ~1;
+  static constexpr int TOTAL = TABP + ESZ;
 };
 
 // own face values (u and du_k) on the own face grid from the volume arrays
@@ -527,7 +536,7 @@ __device__ __forceinline__ void fold_face(double* P0, double* Pk, const double* 
 // own u, du_k at the own face points (stride FP, filled and synced by the
 // caller); the result fbf holds (fv, fd Gn_k) on the own face grid (stride NS).
 // Scratch layout of fscr: uo, xo, xs, ff (4*FP each), tmp (4*QMAX^2), nscr.
-template <int SHAPE, int N, int Q>
+template <int SHAPE, int N, int Q, class TM = CtaTeam>
 __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, const int f,
                                           const double* __restrict__ x, double* __restrict__ us,
                                           double* __restrict__ fbf, double* __restrict__ fscr,
@@ -541,18 +550,18 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
   double* xs = xo + 4 * FP;
   double* ff = xs + 4 * FP;
   double* tmp = ff + 4 * FP;
-  double* nscr = tmp + 4 * QMAX * QMAX;
+  double* nscr = tmp + (D == 3 ? 4 * QMAX * QMAX : 0);
   int no = 0;
   int qo0 = 0, qo1 = 1;
   if (r.type != FT_BOUNDARY) {
-    __syncthreads();
-    no = eval_face_from_coeffs(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt);
+    TM::sync();
+    no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt);
     const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
     const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
     qo0 = cdo[CD_Q0 + fto.run0];
     qo1 = fto.run1 >= 0 ? cdo[CD_Q0 + fto.run1] : 1;
   }
-  __syncthreads();
+  TM::sync();
   const double tau = r.tau;
   if (r.type != FT_SHARED) {
     // flux on the own face grid
@@ -565,15 +574,15 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
         for (int k = 0; k < D; ++k) g = fma(gn[k], uo[(1 + k) * FP + p], g);
         uo[FP + p] = g;      // field 1 now holds g_o (du_0 no longer needed)
       }
-      __syncthreads();
+      TM::sync();
       if (!(r.flags & F_OTHER_ID)) {
         const int q0s = (SHAPE == SHAPE_TRI || D == 2) ? NS : Q;
         const int q1s = D == 3 ? Q : 1;
-        xfer_fwd(uo, FP, qo0, qo1, xo, FP, q0s, q1s, T + r.to0, D == 3 ? T + r.to1 : nullptr,
+        xfer_fwd<TM>(uo, FP, qo0, qo1, xo, FP, q0s, q1s, T + r.to0, D == 3 ? T + r.to1 : nullptr,
                  (r.flags & F_OTHER_SWAP) != 0, 2, tmp, fd, tid, nt);
       } else {
         for (int p = tid; p < NS; p += nt) { xo[p] = uo[p]; xo[FP + p] = uo[FP + p]; }
-        __syncthreads();
+        TM::sync();
       }
     }
     for (int p = tid; p < NS; p += nt) {
@@ -594,7 +603,7 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
       fbf[p] = fv;
       for (int k = 0; k < D; ++k) fbf[(1 + k) * NS + p] = fdd * gn[k];
     }
-    __syncthreads();
+    TM::sync();
     return;
   }
   // ---- shared trace: flux on the trace grid
@@ -603,12 +612,12 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
   if (!same_self) {
     const int q0s = D == 3 ? Q : NS;
     const int q1s = D == 3 ? Q : 1;
-    xfer_fwd(us, FP, q0s, q1s, xs, FP, m0, m1, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
+    xfer_fwd<TM>(us, FP, q0s, q1s, xs, FP, m0, m1, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
              (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
   }
   const double* vs = same_self ? us : xs;
   if (!(r.flags & F_OTHER_ID)) {
-    xfer_fwd(uo, FP, qo0, qo1, xo, FP, m0, m1, T + r.to0, D == 3 ? T + r.to1 : nullptr,
+    xfer_fwd<TM>(uo, FP, qo0, qo1, xo, FP, m0, m1, T + r.to0, D == 3 ? T + r.to1 : nullptr,
              (r.flags & F_OTHER_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
   }
   const double* vo = (r.flags & F_OTHER_ID) ? uo : xo;
@@ -628,47 +637,30 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
     ff[t] = fv;
     for (int k = 0; k < D; ++k) ff[(1 + k) * FP + t] = fdd * gns[k];
   }
-  __syncthreads();
+  TM::sync();
   if (same_self) {
     for (int i = tid; i < (1 + D) * NS; i += nt) {
       const int fl = i / NS, p = i - fl * NS;
       fbf[i] = ff[fl * FP + p];
     }
-    __syncthreads();
+    TM::sync();
   } else {
     const int q0s = D == 3 ? Q : NS;
     const int q1s = D == 3 ? Q : 1;
-    xfer_bwd(ff, FP, m0, m1, fbf, NS, q0s, q1s, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
+    xfer_bwd<TM>(ff, FP, m0, m1, fbf, NS, q0s, q1s, T + r.ts0, D == 3 ? T + r.ts1 : nullptr,
              (r.flags & F_SELF_SWAP) != 0, 1 + D, tmp, fd, tid, nt);
   }
 }
 
-template <int SHAPE, int N, int Q, int GEOM>
-__global__ void __launch_bounds__(Cfg<SHAPE, N, Q>::NT)
-k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
+// Stage the class's 1-D tables into shared memory (layout: see apply_elem).
+template <int SHAPE, int N, int Q>
+__device__ __forceinline__ void stage_tables(const DevPlan& P, const int* cd, double* tb, int tid, int nt) {
   using C = Cfg<SHAPE, N, Q>;
-  constexpr int D = C::D, NP = C::NP, NS = C::NS, FP = C::FP, NC = C::NC;
-  extern __shared__ double sm[];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int* cd = P.cd + cls * CD_WORDS;
-  const int i_el = blockIdx.x;
-  const int e = P.class_elems[cd[CD_ELEM_OFF] + i_el];
-  const int64_t dof0 = P.dof_off[e];
+  constexpr int D = C::D, NC = C::NC;
   const double* T = P.tab;
-  const int gllmask = cd[CD_GLLMASK];
-
-  double* c = sm + C::o_c;
-  double* u = sm + C::o_u;
-  double* du = sm + C::o_du;
-  double* t1 = sm + C::o_t1;
-  double* t2 = sm + C::o_t2;
-  double* tb = sm + C::o_tab;
-  double* fb = sm + C::o_fb;
-  double* fs = sm + C::o_fs;
-
-  // ---- stage tables and coefficients
   double *V = tb, *Dm, *W, *Lt;
-  double *A = nullptr, *dA = nullptr, *Bt = nullptr, *gidd = nullptr, *refw = nullptr, *eta0 = nullptr, *eta1 = nullptr;
+  double *A = nullptr, *dA = nullptr, *Bt = nullptr, *gidd = nullptr, *refw = nullptr, *eta0 = nullptr,
+         *eta1 = nullptr, *gst = nullptr, *gmo = nullptr;
   if (SHAPE != SHAPE_TRI) {
     Dm = V + D * Q * N;
     W = Dm + D * Q * Q;
@@ -692,6 +684,8 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
     refw = Lt + 4 * Q;            // Q*Q
     eta0 = refw + Q * Q;          // Q
     eta1 = eta0 + Q;              // Q
+    gst = eta1 + Q;               // group starts (NG + 1)
+    gmo = gst + NG + 1;           // modes ordered by group (NC)
     for (int i = tid; i < Q * NG; i += nt) { A[i] = ldg(T + cd[TR_A] + i); dA[i] = ldg(T + cd[TR_DA] + i); }
     for (int i = tid; i < Q * Q; i += nt) {
       Dm[i] = ldg(T + cd[TR_D0] + i);
@@ -704,30 +698,76 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
     }
     for (int i = tid; i < Q * NC; i += nt) Bt[i] = ldg(T + cd[TR_B] + i);
     for (int i = tid; i < 2 * Q; i += nt) { Lt[i] = ldg(T + cd[TR_L0] + i); Lt[2 * Q + i] = ldg(T + cd[TR_L1] + i); }
+    for (int i = tid; i < NG + 1; i += nt) gst[i] = ldg(T + cd[TR_GSTART] + i);
+    for (int i = tid; i < NC; i += nt) gmo[i] = ldg(T + cd[TR_GID] + i);
     for (int g = tid; g < NG; g += nt) {
       const int j0 = (int)ldg(T + cd[TR_GSTART] + g), j1 = (int)ldg(T + cd[TR_GSTART] + g + 1);
       for (int j = j0; j < j1; ++j) gidd[(int)ldg(T + cd[TR_GID] + j)] = (double)g;
     }
   }
+}
+
+// One element: volume terms, faces, lift, transposed pass; written to y once.
+// `es` is the element's scratch (Cfg layout without the table region), `tb`
+// the staged tables; the team (CTA or warp) is tid / nt with TM::sync().
+template <int SHAPE, int N, int Q, int GEOM, class TM>
+__device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, const int i_el,
+                                           const double* __restrict__ x, double* __restrict__ y,
+                                           double* es, const double* tb, const int tid, const int nt) {
+  using C = Cfg<SHAPE, N, Q>;
+  constexpr int D = C::D, NP = C::NP, NS = C::NS, FP = C::FP, NC = C::NC;
+  const int e = P.class_elems[cd[CD_ELEM_OFF] + i_el];
+  const int64_t dof0 = P.dof_off[e];
+  const int gllmask = cd[CD_GLLMASK];
+  double* c = es + C::e_c;
+  double* u = es + C::e_u;
+  double* du = es + C::e_du;
+  double* t1 = es + C::e_t1;
+  double* t2 = es + C::e_t2;
+  double* fb = es + C::e_fb;
+  double* fs = es + C::e_fs;
+  // table pointers (layout of stage_tables)
+  const double *V = tb, *Dm, *W, *Lt;
+  const double *A = nullptr, *dA = nullptr, *Bt = nullptr, *gidd = nullptr, *refw = nullptr, *eta0 = nullptr,
+               *eta1 = nullptr, *gst = nullptr, *gmo = nullptr;
+  if (SHAPE != SHAPE_TRI) {
+    Dm = V + D * Q * N;
+    W = Dm + D * Q * Q;
+    Lt = W + D * Q;
+  } else {
+    constexpr int NG = N + 1;
+    A = tb;
+    dA = A + Q * NG;
+    Dm = dA + Q * NG;
+    W = Dm + 2 * Q * Q;
+    Bt = W + 2 * Q;
+    gidd = Bt + Q * NC;
+    Lt = gidd + NC;
+    refw = Lt + 4 * Q;
+    eta0 = refw + Q * Q;
+    eta1 = eta0 + Q;
+    gst = eta1 + Q;
+    gmo = gst + NG + 1;
+  }
   for (int i = tid; i < NC; i += nt) c[i] = ldg(x + dof0 + i);
-  __syncthreads();
+  TM::sync();
 
   // ---- 1-2. BwdTrans and PhysDeriv
   if (SHAPE == SHAPE_HEX) {
     contract<N, N, N, 0, Q, false, false>(c, t1, V, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, N, N, 1, Q, false, false>(t1, t2, V + Q * N, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, N, 2, Q, false, false>(t2, u, V + 2 * Q * N, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, Q, 0, Q, false, false>(u, du, Dm, tid, nt);
     contract<Q, Q, Q, 1, Q, false, false>(u, du + NP, Dm + Q * Q, tid, nt);
     contract<Q, Q, Q, 2, Q, false, false>(u, du + 2 * NP, Dm + 2 * Q * Q, tid, nt);
   } else if (SHAPE == SHAPE_QUAD) {
     contract<N, N, 1, 0, Q, false, false>(c, t1, V, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, N, 1, 1, Q, false, false>(t1, u, V + Q * N, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 0, Q, false, false>(u, du, Dm, tid, nt);
     contract<Q, Q, 1, 1, Q, false, false>(u, du + NP, Dm + Q * Q, tid, nt);
   } else {
@@ -736,17 +776,20 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
     for (int i = tid; i < NG * Q; i += nt) {
       const int g = i / Q, b = i - g * Q;
       double s = 0.0;
-      for (int m = 0; m < NC; ++m)
-        if ((int)gidd[m] == g) s = fma(Bt[b * NC + m], c[m], s);
+      const int j0 = (int)gst[g], j1 = (int)gst[g + 1];
+      for (int j = j0; j < j1; ++j) {
+        const int m = (int)gmo[j];
+        s = fma(Bt[b * NC + m], c[m], s);
+      }
       t1[i] = s;
     }
-    __syncthreads();
+    TM::sync();
     contract<NG, Q, 1, 0, Q, false, false>(t1, u, A, tid, nt);    // u[a][b] = sum_g A[a][g] t1[g][b]
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 0, Q, false, false>(u, du, Dm, tid, nt);
     contract<Q, Q, 1, 1, Q, false, false>(u, du + NP, Dm + Q * Q, tid, nt);
   }
-  __syncthreads();
+  TM::sync();
 
   // ---- 3-4. faces: flux on each face, stored on the own face grid in fb
   const int rbase = cd[CD_REC_OFF] + i_el * C::NF;
@@ -754,9 +797,9 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
   for (int f = 0; f < C::NF; ++f) {
     const FaceRec r = P.recs[rbase + f];
     restrict_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, us, tid, nt);
-    __syncthreads();
-    generic_face<SHAPE, N, Q>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt);
-    __syncthreads();
+    TM::sync();
+    generic_face<SHAPE, N, Q, TM>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt);
+    TM::sync();
   }
 
   // ---- volume point arrays: u -> P0 = lam jw u, du -> P_k = (jw G G^T du)_k
@@ -808,41 +851,41 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
       u[p] = lam * jw * uv;
     }
   }
-  __syncthreads();
+  TM::sync();
   // ---- 5. fold face fluxes (faces sequentially: they share edge points)
   for (int f = 0; f < C::NF; ++f) {
     fold_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, fb + f * (1 + D) * NS, tid, nt);
-    __syncthreads();
+    TM::sync();
   }
   // ---- 6. R = P0 + sum_k D_k^T P_k, then IProduct
   if (SHAPE == SHAPE_HEX) {
     contract<Q, Q, Q, 0, Q, true, true>(du, u, Dm, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, Q, 1, Q, true, true>(du + NP, u, Dm + Q * Q, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, Q, 2, Q, true, true>(du + 2 * NP, u, Dm + 2 * Q * Q, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, Q, 0, N, true, false>(u, t1, V, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<N, Q, Q, 1, N, true, false>(t1, t2, V + Q * N, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<N, N, Q, 2, N, true, false>(t2, c, V + 2 * Q * N, tid, nt);
   } else if (SHAPE == SHAPE_QUAD) {
     contract<Q, Q, 1, 0, Q, true, true>(du, u, Dm, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 1, Q, true, true>(du + NP, u, Dm + Q * Q, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 0, N, true, false>(u, t1, V, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<N, Q, 1, 1, N, true, false>(t1, c, V + Q * N, tid, nt);
   } else {
     constexpr int NG = N + 1;
     contract<Q, Q, 1, 0, Q, true, true>(du, u, Dm, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 1, Q, true, true>(du + NP, u, Dm + Q * Q, tid, nt);
-    __syncthreads();
+    TM::sync();
     contract<Q, Q, 1, 0, NG, true, false>(u, t1, A, tid, nt);    // s[g][b] = sum_a A[a][g] R[a][b]
-    __syncthreads();
+    TM::sync();
     for (int m = tid; m < NC; m += nt) {
       const int g = (int)gidd[m];
       double s = 0.0;
@@ -850,8 +893,36 @@ k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __
       c[m] = s;
     }
   }
-  __syncthreads();
+  TM::sync();
   for (int i = tid; i < NC; i += nt) y[dof0 + i] = c[i];
+  TM::sync();
+}
+
+template <int SHAPE, int N, int Q, int GEOM>
+__global__ void __launch_bounds__(Cfg<SHAPE, N, Q>::NT)
+k_apply(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
+  using C = Cfg<SHAPE, N, Q>;
+  extern __shared__ double sm[];
+  const int* cd = P.cd + cls * CD_WORDS;
+  stage_tables<SHAPE, N, Q>(P, cd, sm, threadIdx.x, blockDim.x);
+  apply_elem<SHAPE, N, Q, GEOM, CtaTeam>(P, cd, blockIdx.x, x, y, sm + C::TABP, sm, threadIdx.x, blockDim.x);
+}
+
+// Warp-per-element variant (2-D shapes): WPC independent warps per CTA share the
+// staged tables; each warp walks the class's elements with stride gridDim.x*WPC.
+template <int SHAPE, int N, int Q, int GEOM, int WPC>
+__global__ void __launch_bounds__(32 * WPC)
+k_apply_w(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
+  using C = Cfg<SHAPE, N, Q>;
+  extern __shared__ double sm[];
+  const int* cd = P.cd + cls * CD_WORDS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  stage_tables<SHAPE, N, Q>(P, cd, sm, threadIdx.x, blockDim.x);
+  __syncthreads();
+  double* es = sm + C::TABP + warp * C::ESZ;
+  const int count = cd[CD_COUNT];
+  for (int i_el = blockIdx.x * WPC + warp; i_el < count; i_el += gridDim.x * WPC)
+    apply_elem<SHAPE, N, Q, GEOM, WarpTeam>(P, cd, i_el, x, y, es, sm, lane, 32);
 }
 
 }  // namespace sipg

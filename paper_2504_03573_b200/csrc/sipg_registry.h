@@ -7,7 +7,8 @@
 using KernelFn = void (*)(const DevPlan, const int, const double*, double*);
 using UploadFn = cudaError_t (*)(const double* V, const double* D, const double* W, const double* dVend);
 
-// kind: 0 = generic smem kernel (any basis / rule / geometry),
+// kind: 0 = generic smem kernel, one CTA per element (any basis / rule / geometry),
+//       5 = the same element routine, one warp per element (2-D shapes, persistent),
 //       1 = register-column hex kernel, conforming + boundary faces only,
 //       2 = register-column hex kernel with the generic face path
 struct KernelEntry {
@@ -30,8 +31,11 @@ KernelEntry sipg_entry();
   template <int SHAPE, int N, int Q, int GEOM>                                               \
   KernelEntry sipg_entry() {                                                                 \
     using C = sipg::Cfg<SHAPE, N, Q>;                                                        \
-    return KernelEntry{SHAPE, N, Q, GEOM, 0, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,       \
-                       sizeof(double) * (size_t)C::TOTAL, nullptr};                          \
+    if (SHAPE == SHAPE_HEX)                                                                  \
+      return KernelEntry{SHAPE, N, Q, GEOM, 0, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,     \
+                         sizeof(double) * (size_t)C::TOTAL, nullptr};                        \
+    return KernelEntry{SHAPE, N, Q, GEOM, 5, &sipg::k_apply_w<SHAPE, N, Q, GEOM, 8>, 256,    \
+                       sizeof(double) * (size_t)(C::TABP + 8 * C::ESZ), nullptr};            \
   }
 #define SIPG_ENTRIES_NQ(S, N)                                                                \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_REGULAR>());                                      \
