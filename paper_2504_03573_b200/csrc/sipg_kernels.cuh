@@ -27,6 +27,16 @@ constexpr int NMAX = 10;   // largest supported modes per direction
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
+__device__ __forceinline__ void cp_async8_(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// coefficient read that works for global (read-only path) and staged shared data
+__device__ __forceinline__ double c_at(const double* p) { return __isShared(p) ? *p : __ldg(p); }
+
 // A "team" works on one element: a whole CTA or a single warp.
 struct CtaTeam { static __device__ __forceinline__ void sync() { __syncthreads(); } };
 struct WarpTeam { static __device__ __forceinline__ void sync() { __syncwarp(); } };
@@ -98,10 +108,10 @@ __device__ __forceinline__ void tri_chain(int f, double p, double& c00, double& 
 template <class TM = CtaTeam>
 static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, const double* __restrict__ x,
                                      double* __restrict__ out, int FP, double* __restrict__ scr,
-                                     int tid, int nt) {
+                                     int tid, int nt, const double* staged = nullptr) {
   const int* cd = P.cd + P.elem_class[e] * CD_WORDS;
   const int shape = cd[CD_SHAPE], n = cd[CD_N];
-  const double* c = x + P.dof_off[e];
+  const double* c = staged ? staged : x + P.dof_off[e];
   const double* T = P.tab;
   const FaceTopo ft = face_topo(shape, f);
   if (shape == SHAPE_TRI) {
@@ -118,7 +128,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
         const int j0 = (int)ldg(gst + g), j1 = (int)ldg(gst + g + 1);
         for (int j = j0; j < j1; ++j) {
           const int m = (int)ldg(gmo + j);
-          const double cm = ldg(c + m);
+          const double cm = c_at(c + m);
           a = fma(ldg(T + cd[TR_BM1] + m), cm, a);
           b = fma(ldg(T + cd[TR_DBM1] + m), cm, b);
         }
@@ -154,7 +164,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
         double s = 0.0, ds = 0.0;
         for (int j = j0; j < j1; ++j) {
           const int m = (int)ldg(gmo + j);
-          const double cm = ldg(c + m);
+          const double cm = c_at(c + m);
           s = fma(ldg(B + p * nc + m), cm, s);
           ds = fma(ldg(dB + p * nc + m), cm, ds);
         }
@@ -184,7 +194,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
     for (int i = tid; i < n; i += nt) {
       double s = 0.0, t = 0.0;
       for (int k = 0; k < n; ++k) {
-        const double cv = ldg(c + k * sa + i * sb);
+        const double cv = c_at(c + k * sa + i * sb);
         s = fma(ldg(vend + k), cv, s);
         t = fma(ldg(dvend + k), cv, t);
       }
@@ -221,7 +231,7 @@ static __device__ int eval_face_from_coeffs(const DevPlan& P, int e, int f, cons
     const int i0 = i / n, i1 = i - i0 * n;
     double s = 0.0, t = 0.0;
     for (int k = 0; k < n; ++k) {
-      const double cv = ldg(c + k * sa + i0 * s0 + i1 * s1);
+      const double cv = c_at(c + k * sa + i0 * s0 + i1 * s1);
       s = fma(ldg(vend + k), cv, s);
       t = fma(ldg(dvend + k), cv, t);
     }
@@ -461,7 +471,10 @@ struct Cfg {
   // face scratch: us(4FP) uo(4FP) xo(4FP) xs(4FP) ff(4FP) tmp(4 QMAX^2, 3-D) nbr
   static constexpr int FSZ = D == 3 ? 5 * 4 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX
                                     : 5 * 4 * FP + 2 * (NMAX + 2);
-  static constexpr int ESZ = (e_fs + FSZ + 1) & ~1;
+  static constexpr int NBK = NMAX * NMAX + 2;                 // staged neighbour block (2-D)
+  static constexpr int e_rec = (e_fs + FSZ + 1) & ~1;          // NF face records (16 doubles each)
+  static constexpr int e_nb = e_rec + NF * 16;
+  static constexpr int ESZ = e_nb + (D == 2 ? NF * NBK : 0);
   static constexpr int TOTAL = TABP + ESZ;
 };
 
@@ -540,7 +553,7 @@ template <int SHAPE, int N, int Q, class TM = CtaTeam>
 __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, const int f,
                                           const double* __restrict__ x, double* __restrict__ us,
                                           double* __restrict__ fbf, double* __restrict__ fscr,
-                                          const int tid, const int nt) {
+                                          const int tid, const int nt, const double* staged = nullptr) {
   using C = Cfg<SHAPE, N, Q>;
   constexpr int D = C::D, NS = C::NS, FP = C::FP;
   const double* T = P.tab;
@@ -555,7 +568,7 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
   int qo0 = 0, qo1 = 1;
   if (r.type != FT_BOUNDARY) {
     TM::sync();
-    no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt);
+    no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt, staged);
     const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
     const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
     qo0 = cdo[CD_Q0 + fto.run0];
@@ -749,7 +762,27 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
     gst = eta1 + Q;
     gmo = gst + NG + 1;
   }
+  // 2-D: records and neighbour coefficient blocks fetched asynchronously up front
+  FaceRec* srec = reinterpret_cast<FaceRec*>(es + C::e_rec);
+  double* snb = es + C::e_nb;
+  const int rbase = cd[CD_REC_OFF] + i_el * C::NF;
+  if (D == 2) {
+    for (int i = tid; i < C::NF * 16; i += nt)
+      cp_async8_(reinterpret_cast<double*>(srec) + i, reinterpret_cast<const double*>(P.recs + rbase) + i);
+    cp_async_commit_();
+  }
   for (int i = tid; i < NC; i += nt) c[i] = ldg(x + dof0 + i);
+  if (D == 2) {
+    cp_async_wait_all_();
+    TM::sync();
+    for (int f = 0; f < C::NF; ++f) {
+      if (srec[f].type == FT_BOUNDARY) continue;
+      const int no = P.cd[P.elem_class[srec[f].nbr] * CD_WORDS + CD_NC];
+      const double* src = x + srec[f].nbr_dof;
+      for (int i = tid; i < no; i += nt) cp_async8_(snb + f * C::NBK + i, src + i);
+    }
+    cp_async_commit_();
+  }
   TM::sync();
 
   // ---- 1-2. BwdTrans and PhysDeriv
@@ -792,13 +825,15 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
   TM::sync();
 
   // ---- 3-4. faces: flux on each face, stored on the own face grid in fb
-  const int rbase = cd[CD_REC_OFF] + i_el * C::NF;
   double* us = fs;              // 4 fields x FP, own face grid
+  if (D == 2) cp_async_wait_all_();
+  TM::sync();
   for (int f = 0; f < C::NF; ++f) {
-    const FaceRec r = P.recs[rbase + f];
+    const FaceRec r = D == 2 ? srec[f] : P.recs[rbase + f];
     restrict_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, us, tid, nt);
     TM::sync();
-    generic_face<SHAPE, N, Q, TM>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt);
+    generic_face<SHAPE, N, Q, TM>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt,
+                                  D == 2 ? snb + f * C::NBK : nullptr);
     TM::sync();
   }
 
