@@ -194,19 +194,46 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    case = build_workload(args.config, args.nx, args.seed + rank, rank, world)
-    t0 = time.perf_counter()
-    op = HelmholtzOperator(case.mesh, case.order_map, **OP_KW)
-    setup_s = time.perf_counter() - t0
-    n = op.n_dofs
-    x_host = case.draw_x(n)
+    dop = None
+    if world == 1:
+        case = build_workload(args.config, args.nx, args.seed)
+        t0 = time.perf_counter()
+        op = HelmholtzOperator(case.mesh, case.order_map, **OP_KW)
+        setup_s = time.perf_counter() - t0
+        n = op.n_dofs
+        n_elements = case.mesh.n_elements
+        x_host = case.draw_x(n)
+        n_owned = n
+    else:
+        # weak scaling: `world` copies of the config box stacked in x, one slab per rank
+        from paper_2504_03573_b200.distributed import DistributedHelmholtz
+        from paper_2504_03573_b200.partition import stack_box_config
+        m, om, rng = stack_box_config(args.config, world, nx=args.nx, seed=args.seed)
+        t0 = time.perf_counter()
+        dop = DistributedHelmholtz(m, om, rank, world, dist, **OP_KW)
+        setup_s = time.perf_counter() - t0
+        op = dop.op
+        n = op.n_dofs
+        n_elements = int(dop.lp.owned_mask.sum())
+        from paper_2504_03573_b200.partition import _dof_offsets
+        x_glob = rng.uniform(-1.0, 1.0, int(_dof_offsets(om, m)[-1]))
+        x_host = np.zeros(n)
+        x_host[dop.owned] = x_glob[dop.lp.dof_lo:dop.lp.dof_hi]
+        n_owned = dop.lp.dof_hi - dop.lp.dof_lo
     x = torch.from_numpy(x_host).cuda()
-    y = torch.empty_like(x)
+    y = torch.zeros_like(x)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def apply_once():
+        if dop is None:
+            op.apply_into(x.data_ptr(), y.data_ptr(), sp)
+        else:
+            dop.apply(x, y, sp)
+
     for _ in range(args.warmup):
-        op.apply_into(x.data_ptr(), y.data_ptr(), sp)
+        apply_once()
     torch.cuda.synchronize()
 
     # per-class kernel time (dominant kernel = largest share)
@@ -234,7 +261,7 @@ def main():
         for s in range(args.steps):
             flush.zero_()
             evs[s][0].record(stream)
-            op.apply_into(x.data_ptr(), y.data_ptr(), sp)
+            apply_once()
             evs[s][1].record(stream)
         torch.cuda.synchronize()
     step_ms = np.array([a.elapsed_time(b) for a, b in evs])
@@ -246,17 +273,35 @@ def main():
         total_ms = float(t.item())
         dist.barrier()
     ms = total_ms / args.steps
-    value = world * n / (ms * 1e-3) / 1e9
+    n_total = n_owned
+    if dist is not None:
+        t = torch.tensor([n_owned], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        n_total = int(t.item())
+    value = n_total / (ms * 1e-3) / 1e9
 
-    # e2e through the C-ABI host entry point from pinned host memory
+    # e2e: the same apply from pinned host memory, H2D of x and D2H of y inside the
+    # timed region.  One GPU: the C-ABI host entry point sipg_apply_host; N GPUs:
+    # owned slice H2D, distributed apply (halo exchange included), owned y D2H.
     xp = torch.from_numpy(x_host).pin_memory()
     yp = torch.empty(n, dtype=torch.float64).pin_memory()
-    op.native.apply_host_ptr(xp.data_ptr(), yp.data_ptr(), sp)
+    own = slice(0, n) if dop is None else dop.owned
+
+    def e2e_once():
+        if dop is None:
+            op.native.apply_host_ptr(xp.data_ptr(), yp.data_ptr(), sp)
+        else:
+            x[own].copy_(xp[own], non_blocking=True)
+            apply_once()
+            yp[own].copy_(y[own], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+    e2e_once()
     e2e_ms = []
     for _ in range(args.e2e_steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        op.native.apply_host_ptr(xp.data_ptr(), yp.data_ptr(), sp)
+        e2e_once()
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(a.elapsed_time(b))
@@ -265,7 +310,7 @@ def main():
         t = torch.tensor([e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
-    check = float(np.abs(yp.numpy() - y.cpu().numpy()).max())
+    check = float(np.abs(yp.numpy()[own] - y.cpu().numpy()[own]).max())
 
     if rank == 0:
         rows = roofline.per_class(op.plan)
@@ -289,10 +334,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "description": configs.DESCRIPTION.get(args.config),
-                       "n_dofs_per_gpu": n, "elements_per_gpu": case.mesh.n_elements,
+                       "n_dofs_per_gpu": n_owned, "elements_per_gpu": n_elements, "n_dofs_total": n_total,
                        "classes": ncls, "seed": args.seed,
                        "l2": "L2 flushed (256 MB write) before every timed step",
-                       "parallelism": f"{world} replicas (one cfg per GPU)" if world > 1 else "single GPU"},
+                       "parallelism": (f"x-slab dp{world}: {world} config boxes stacked in x, one slab + "
+                                       "ghost layer per GPU, NCCL halo exchange overlapped with interior "
+                                       "elements") if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": ach_gbs, "peak": peak, "unit": "GB/s",
                          "frac": ach_gbs / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
@@ -306,8 +353,8 @@ def main():
             "apply_totals": {"algorithmic_bytes": b_alg, "algorithmic_flops": f_alg,
                              "hbm_frac": b_alg / (ms * 1e-3) / 1e9 / peak,
                              "fp64_frac": f_alg / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
-            "e2e": {"value": world * n / (e2e * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": e2e,
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+            "e2e": {"value": n_total / (e2e * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": e2e,
+                    "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * n_owned,
                     "path": "sipg_apply_host (pinned host x -> H2D -> apply -> D2H -> host y)",
                     "max_abs_diff_vs_device_y": check},
             "gpu_launches": int(launches),

@@ -60,6 +60,11 @@ int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);
  * `stream` (a cudaStream_t, NULL = legacy default stream).  Replaces lhs_eval. */
 int sipg_apply(sipg_plan* plan, const double* x_dev, double* y_dev, void* stream);
 
+/* Only the element classes of one launch role (0: elements whose neighbours are
+ * all local, 1: elements touching a ghost element, i.e. after the halo
+ * exchange; -1: both).  Multi-GPU slabs: role 0, exchange, role 1. */
+int sipg_apply_role(sipg_plan* plan, int32_t role, const double* x_dev, double* y_dev, void* stream);
+
 /* One element class only (instrumentation: per-kernel timing).  Classes are
  * independent, so applying every class once equals sipg_apply. */
 int sipg_apply_class(sipg_plan* plan, int32_t cls, const double* x_dev, double* y_dev, void* stream);

@@ -18,7 +18,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libsipg.so"
 
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
-           "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info"]
+           "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
+           "sipg_apply_role"]
 
 
 class PlanDesc(ctypes.Structure):
@@ -65,6 +66,8 @@ def load() -> ctypes.CDLL:
     lib.sipg_abi_layout.restype = ctypes.c_int
     lib.sipg_supported.argtypes = [i32, i32, i32]
     lib.sipg_supported.restype = ctypes.c_int
+    lib.sipg_apply_role.argtypes = [vp, i32, vp, vp, vp]
+    lib.sipg_apply_role.restype = ctypes.c_int
     lib.sipg_apply_class.argtypes = [vp, i32, vp, vp, vp]
     lib.sipg_apply_class.restype = ctypes.c_int
     lib.sipg_plan_class_info.argtypes = [vp, i32, ctypes.POINTER(i32)]
@@ -130,6 +133,10 @@ class NativePlan:
     def apply_host(self, x: np.ndarray, y: np.ndarray, stream: int = 0) -> None:
         check(self._lib.sipg_apply_host(self.handle, x.ctypes.data, y.ctypes.data,
                                         ctypes.c_void_p(stream)), "sipg_apply_host")
+
+    def apply_role(self, role: int, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        check(self._lib.sipg_apply_role(self.handle, role, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                        ctypes.c_void_p(stream)), "sipg_apply_role")
 
     def apply_host_ptr(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
         check(self._lib.sipg_apply_host(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),

@@ -198,19 +198,23 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   return 0;
 }
 
-int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
+int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   for (int c = 0; c < p->n_cls; ++c) {
     const int32_t* cd = p->cd_host.data() + c * CD_WORDS;
     const int count = cd[CD_COUNT];
-    if (count == 0) continue;
+    if (count == 0 || cd[CD_ROLE] == 2 || (role >= 0 && cd[CD_ROLE] != role)) continue;
     const KernelEntry* k = p->kern[c];
     k->fn<<<p->grid[c], k->threads, k->smem, s>>>(p->dp, c, x_dev, y_dev);
     ++p->launches;
   }
   CK(cudaGetLastError());
   return 0;
+}
+
+int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
+  return sipg_apply_role(p, -1, x_dev, y_dev, stream);
 }
 
 int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
@@ -254,7 +258,7 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   if (!p) return -1;
   int k = 0;
   for (int c = 0; c < p->n_cls; ++c)
-    if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0) ++k;
+    if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->cd_host[c * CD_WORDS + CD_ROLE] != 2) ++k;
   return k;
 }
 

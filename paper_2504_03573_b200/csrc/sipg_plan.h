@@ -13,7 +13,8 @@ enum { GEOM_REGULAR = 0, GEOM_POINTWISE = 1 };
 enum {
   CD_SHAPE = 0, CD_N, CD_Q0, CD_Q1, CD_Q2, CD_NC, CD_NPHYS, CD_NFACES,
   CD_GEOM, CD_COUNT, CD_ELEM_OFF, CD_REC_OFF, CD_EGEO_OFF, CD_EGEO_STRIDE, CD_GLLMASK, CD_KIND,
-  CD_TAX = 16
+  CD_TAX = 16,
+  CD_ROLE = 63   // launch role: 0 first, 1 after the halo exchange, 2 ghost (never launched)
 };
 enum { TX_V = 0, TX_DV, TX_D, TX_W, TX_VEND, TX_DVEND, TX_LEND, TX_PTS };
 enum {

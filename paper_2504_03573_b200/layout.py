@@ -15,6 +15,7 @@ DIM_OF = {SHAPE_QUAD: 2, SHAPE_TRI: 2, SHAPE_HEX: 3}
 CD_WORDS = 64
 CD_SHAPE, CD_N, CD_Q0, CD_Q1, CD_Q2, CD_NC, CD_NPHYS, CD_NFACES = range(8)
 CD_GEOM, CD_COUNT, CD_ELEM_OFF, CD_REC_OFF, CD_EGEO_OFF, CD_EGEO_STRIDE, CD_GLLMASK, CD_KIND = range(8, 16)
+CD_ROLE = 63        # launch role: 0 first, 1 after the halo exchange, 2 ghost (never launched)
 # tensor shapes: per axis a, base CD_TAX + 8 a
 CD_TAX = 16
 TX_V, TX_DV, TX_D, TX_W, TX_VEND, TX_DVEND, TX_LEND, TX_PTS = range(8)

@@ -260,9 +260,13 @@ class PlanBuilder:
 
     def __init__(self, mesh, order_map, *, basis_kind=BasisKind.LAGRANGE, rule_kinds=None,
                  lambda_=1.0, tau_constant=10.0, strategy="p2p", face_absorb="auto",
-                 force_interp=False, p_geom=1, tau_rule="reference", shared_rule="patched"):
+                 force_interp=False, p_geom=1, tau_rule="reference", shared_rule="patched",
+                 element_roles=None):
         self.mesh = mesh
         self.dim = int(mesh.dim)
+        # per-element launch role: 0 = computed first, 1 = computed after the halo
+        # exchange (touches a ghost), 2 = ghost (never computed; neighbour data only)
+        self.roles = None if element_roles is None else np.asarray(element_roles, dtype=np.int64)
         if self.dim not in (2, 3):
             raise ValueError("only 2D and 3D meshes are supported")
         self.kind = as_basis_kind(basis_kind)
@@ -359,9 +363,10 @@ class PlanBuilder:
 
     # ------------------------------------------------------------------
     def _classes(self, nel):
-        """Kernel classes: (expansion, geometry mode), first-appearance order."""
+        """Kernel classes: (expansion, geometry mode, launch role), first-appearance order."""
         geom = np.where(self.regular, L.GEOM_REGULAR, L.GEOM_POINTWISE)
-        key = self.exp_of * 2 + geom
+        role = np.zeros(nel, dtype=np.int64) if self.roles is None else self.roles
+        key = (self.exp_of * 2 + geom) * 3 + role
         _, first = np.unique(key, return_index=True)
         order = key[np.sort(first)]
         self.pool = _Pool()
@@ -372,7 +377,7 @@ class PlanBuilder:
         self.elem_pos = np.zeros(nel, dtype=np.int32)
         self.rec_base = np.zeros(nel, dtype=np.int64)
         for k in order:
-            ei, gm = int(k) // 2, int(k) % 2
+            ei, gm, rl = int(k) // 6, (int(k) // 3) % 2, int(k) % 3
             ids = np.flatnonzero(key == k)
             c, g = self.exp_list[ei], self.geo[ei]
             ci = len(self.class_list)
@@ -388,6 +393,7 @@ class PlanBuilder:
             cd[L.CD_Q0:L.CD_Q0 + d] = c.nq
             cd[L.CD_NC], cd[L.CD_NPHYS], cd[L.CD_NFACES] = c.n_coeffs, c.n_phys, nf
             cd[L.CD_GEOM], cd[L.CD_COUNT] = gm, ids.size
+            cd[L.CD_ROLE] = rl
             cd[L.CD_ELEM_OFF] = sum(x.size for x in elems)
             cd[L.CD_REC_OFF] = rec_off
             rec_off += ids.size * nf

@@ -11,6 +11,9 @@ CUDA tensor).  There is no CPU path.
 Extra keyword arguments (not in the reference):
   tau_rule     "reference": tau = C max(n-1,1)^2 / h (sipg.py:351-360);
                "baseline":  tau = max(n_L, n_R)^2 / h (BASELINE.json "(P+1)^2/h").
+  element_roles  per-element launch role for slab decompositions (0 first,
+               1 after the halo exchange, 2 ghost: never computed); see
+               distributed.py.
   shared_rule  "patched" (default): Gauss-Legendre shared-trace rule on faces
                touching a non-GLL side (the reference produces NaN there,
                SURVEY.md §8c P2); "reference": higher side's kind.
@@ -42,7 +45,8 @@ class HelmholtzOperator:
     def __init__(self, mesh, order_map, *, basis_kind=BasisKind.LAGRANGE, rule_kinds=None,
                  params: HelmholtzParams = HelmholtzParams(), strategy: str = "p2p",
                  batch_width: int = 4, face_absorb: str = "auto", force_interp: bool = False,
-                 p_geom: int = 1, tau_rule: str = "reference", shared_rule: str = "patched"):
+                 p_geom: int = 1, tau_rule: str = "reference", shared_rule: str = "patched",
+                 element_roles=None):
         if strategy not in ("p2p", "p2p_forced", "shared_trace"):
             raise ValueError(f"unknown strategy {strategy!r}")
         if face_absorb not in ("auto", "trace_iproduct"):
@@ -58,7 +62,8 @@ class HelmholtzOperator:
         self.plan = PlanBuilder(mesh, order_map, basis_kind=basis_kind, rule_kinds=rule_kinds,
                                 lambda_=params.lambda_, tau_constant=params.tau_constant,
                                 strategy=strategy, face_absorb=face_absorb, force_interp=force_interp,
-                                p_geom=p_geom, tau_rule=tau_rule, shared_rule=shared_rule).build()
+                                p_geom=p_geom, tau_rule=tau_rule, shared_rule=shared_rule,
+                                element_roles=element_roles).build()
         self.n_dofs = self.plan.n_dofs
         self._dof_off = self.plan.dof_off
         self.certificates = self.plan.certificates
