@@ -269,7 +269,6 @@ def main():
     cls_ms /= reps
 
     # timed region: K full applies, L2 flushed before each, device-timed
-    launches0 = op.native.launches
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -279,6 +278,7 @@ def main():
         for _ in range(n_load):
             apply_once()
         torch.cuda.synchronize()
+        launches0 = op.native.launches
         for s in range(args.steps):
             flush.zero_()
             evs[s][0].record(stream)
