@@ -111,8 +111,13 @@ __device__ __forceinline__ int hex_stride(int axis, int n) { return axis == 0 ? 
 // next element's face records and coefficients stream in (TMA bulk copies on an
 // mbarrier) while the current one computes; the neighbours' coefficients
 // stream in behind BwdTrans / PhysDeriv.
+// 6 resident CTAs per SM for Q <= 8 (caps registers at 168: measured 498 us vs
+// 545 us unconstrained and 525 us with 8 CTAs / 128 registers, cfg3a)
+#ifndef SIPG_HEX_MINB
+#define SIPG_HEX_MINB 6
+#endif
 template <int N, int Q, bool GEN>
-__global__ void __launch_bounds__(Q * Q)
+__global__ void __launch_bounds__(Q * Q, (Q <= 8 ? SIPG_HEX_MINB : 1))
 k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   using H = HexFast<N, Q>;
   constexpr int NT = H::NT, SJ = H::SJ, SI = H::SI, BUF = H::BUF, N3 = H::N3, QQ = Q * Q;
