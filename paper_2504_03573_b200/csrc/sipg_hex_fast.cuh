@@ -127,7 +127,8 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   double* gsm = dsm + H::O_G;
   __shared__ double sW[Q];
   __shared__ int sk[6];               // 1 fast conforming, 2 boundary, 0 generic
-  __shared__ int soff[8];             // block offsets (own coefficients per stage, neighbours)
+  __shared__ int soff[8];
+  __shared__ int fpar[6][4];          // neighbour plane strides (b0, b1, fixed axis), side             // block offsets (own coefficients per stage, neighbours)
   __shared__ __align__(8) uint64_t mbar[3];   // records+own [stage 0, 1], neighbours
   double* B0 = S;
   double* B1 = S + BUF;
@@ -141,7 +142,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   if (t == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
-    mbar_init(&mbar[2], 1);
+    mbar_init(&mbar[2], 6);
     fence_proxy_async();
   }
   if (t < Q) sW[t] = hxW<N, Q>[t];
@@ -175,17 +176,19 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
   }
-  if (t == 32) {                       // neighbour blocks: another warp than the prefetch issuer
-    unsigned total = 0;
-#pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      if (srec[f].type == FT_DIRECT && (srec[f].flags & F_FAST_HEX)) {
-        unsigned nb;
-        soff[2 + f] = bulk_block(NB + f * H::BLK, x + srec[f].nbr_dof, N3, &mbar[2], &nb);
-        total += nb;
-      }
+  if (t >= 32 && t < 38) {              // neighbour blocks: one per thread, another warp than the prefetch issuer
+    const int f = t - 32;
+    unsigned nb = 0;
+    const FaceRec& rf = srec[f];
+    if (rf.type == FT_DIRECT && (rf.flags & F_FAST_HEX)) {
+      soff[2 + f] = bulk_block(NB + f * H::BLK, x + rf.nbr_dof, N3, &mbar[2], &nb);
+      const int ao = rf.nbr_face >> 1;
+      fpar[f][0] = hex_stride(ao == 0 ? 1 : 0, N);
+      fpar[f][1] = hex_stride(ao == 2 ? 1 : 2, N);
+      fpar[f][2] = hex_stride(ao, N);
+      fpar[f][3] = rf.nbr_face & 1;
     }
-    mbar_expect_tx(&mbar[2], total);
+    mbar_expect_tx(&mbar[2], nb);
     cp_async_commit();
   }
 
@@ -266,7 +269,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
-  if (t == 32) cp_async_wait<0>();
+  if (t >= 32 && t < 38) cp_async_wait<0>();
   mbar_wait(&mbar[2], k & 1);
   __syncthreads();
 #pragma unroll
@@ -287,19 +290,13 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
       if (sk[f] != 1) continue;
-      const int fo = srec[f].nbr_face, ao = fo >> 1;
-      const int b0 = ao == 0 ? 1 : 0, b1 = ao == 2 ? 1 : 2;
-      const double* c = NB + f * H::BLK + soff[2 + f] + i0 * hex_stride(b0, N) + i1 * hex_stride(b1, N);
-      const int sa = hex_stride(ao, N);
+      const double* c = NB + f * H::BLK + soff[2 + f] + i0 * fpar[f][0] + i1 * fpar[f][1];
+      const int sa = fpar[f][2], hi = fpar[f][3];
+      const double* dve = &hxDVE<N, Q>[hi * N];
       double pd = 0.0;
-      if (fo & 1) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[N + i], c[i * sa], pd);
-      } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[i], c[i * sa], pd);
-      }
-      NP[(2 * f) * N * N + t] = c[(fo & 1) ? (N - 1) * sa : 0];   // modified-modal boundary mode
+      for (int i = 0; i < N; ++i) pd = fma(dve[i], c[i * sa], pd);
+      NP[(2 * f) * N * N + t] = c[hi ? (N - 1) * sa : 0];   // modified-modal boundary mode
       NP[(2 * f + 1) * N * N + t] = pd;
     }
   }
@@ -429,50 +426,58 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   const double wjk = sW[ta] * sW[tb];
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-#pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      const int a = f >> 1, hi = f & 1;
-      bool own;
-      int p;
-      if (a == 0) {
-        own = i == (hi ? Q - 1 : 0);
-        p = ta * Q + tb;
-      } else if (a == 1) {
-        own = ta == (hi ? Q - 1 : 0);
-        p = i * Q + tb;
-      } else {
-        own = tb == (hi ? Q - 1 : 0);
-        p = i * Q + ta;
-      }
-      if (!own) continue;
-      const int kind = sk[f];
-      if (kind == 0) {
-        if (GEN) {
-          const double* fbf = gfb + f * 4 * QQ;
-          c0 += fbf[p]; c1 += fbf[QQ + p]; c2 += fbf[2 * QQ + p]; c3 += fbf[3 * QQ + p];
-        }
-        continue;
-      }
-      double fv, fd;
-      if (a == 0) {
-        fv = fv01[hi];
-        fd = fd01[hi];
-      } else {
-        fv = FVD[(f - 2) * 2 * QQ + p];
-        fd = FVD[(f - 2) * 2 * QQ + QQ + p];
-      }
-      c0 += fv;
-      c1 = fma(fd, srec[f].gs[0], c1);
-      c2 = fma(fd, srec[f].gs[1], c2);
-      c3 = fma(fd, srec[f].gs[2], c3);
-    }
     const double jw = J * hxW<N, Q>[i] * wjk;
     const double ui = u[i], g0 = d0[i], g1 = d1[i], g2 = d2[i];
-    u[i] = lam * jw * ui + c0;
-    d0[i] = jw * (K0 * g0 + K1 * g1 + K2 * g2) + c1;
-    d1[i] = jw * (K1 * g0 + K3 * g1 + K4 * g2) + c2;
-    d2[i] = jw * (K2 * g0 + K4 * g1 + K5 * g2) + c3;
+    u[i] = lam * jw * ui;
+    d0[i] = jw * (K0 * g0 + K1 * g1 + K2 * g2);
+    d1[i] = jw * (K1 * g0 + K3 * g1 + K4 * g2);
+    d2[i] = jw * (K2 * g0 + K4 * g1 + K5 * g2);
+  }
+  // lift: faces 0/1 at i = 0 / Q-1 of every column (registers), faces 2..5 on the edge columns
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int i = f ? Q - 1 : 0;
+    if (sk[f] == 0) {
+      if (GEN) {
+        const double* fbf = gfb + f * 4 * QQ;
+        const int p = ta * Q + tb;
+        u[i] += fbf[p]; d0[i] += fbf[QQ + p]; d1[i] += fbf[2 * QQ + p]; d2[i] += fbf[3 * QQ + p];
+      }
+      continue;
+    }
+    const double fv = fv01[f], fd = fd01[f];
+    u[i] += fv;
+    d0[i] = fma(fd, srec[f].gs[0], d0[i]);
+    d1[i] = fma(fd, srec[f].gs[1], d1[i]);
+    d2[i] = fma(fd, srec[f].gs[2], d2[i]);
+  }
+#pragma unroll
+  for (int f = 2; f < 6; ++f) {
+    const int a = f >> 1, hi = f & 1;
+    const bool own = a == 1 ? (ta == (hi ? Q - 1 : 0)) : (tb == (hi ? Q - 1 : 0));
+    if (!own) continue;
+    const int q1 = a == 1 ? tb : ta;
+    if (sk[f] == 0) {
+      if (GEN) {
+        const double* fbf = gfb + f * 4 * QQ;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          const int p = i * Q + q1;
+          u[i] += fbf[p]; d0[i] += fbf[QQ + p]; d1[i] += fbf[2 * QQ + p]; d2[i] += fbf[3 * QQ + p];
+        }
+      }
+      continue;
+    }
+    const double gsa = srec[f].gs[0], gsb = srec[f].gs[1], gsc = srec[f].gs[2];
+    const double* fvd = FVD + (f - 2) * 2 * QQ;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const double fv = fvd[i * Q + q1], fd = fvd[QQ + i * Q + q1];
+      u[i] += fv;
+      d0[i] = fma(fd, gsa, d0[i]);
+      d1[i] = fma(fd, gsb, d1[i]);
+      d2[i] = fma(fd, gsc, d2[i]);
+    }
   }
 
   // ---- R = P0 + D0^T P1 (registers) + D1^T P2 + D2^T P3 (shared memory)
