@@ -51,6 +51,9 @@ typedef struct sipg_plan_desc {
   const double* tables;        /* 1-D basis / derivative / transfer tables */
   const double* elem_geom;     /* per-element metric (regular) or per-point (deformed) */
   const double* face_geom;     /* per-face-point swj and G.n where not constant */
+  int64_t n_planes;            /* doubles of published face planes (hex), allocated by the plan */
+  const int64_t* plane_off;    /* n_elements: offset of each element's 6 face-plane pairs (-1: none) */
+  const int64_t* rec_ext;      /* n_records x 2: neighbour face-plane offset | n_o << 48; E tables */
 } sipg_plan_desc;
 
 /* Build the device-resident plan (uploads all tables). */

@@ -33,6 +33,7 @@ class PlanDesc(ctypes.Structure):
         ("elem_class", ctypes.c_void_p), ("elem_pos", ctypes.c_void_p), ("dof_off", ctypes.c_void_p),
         ("face_records", ctypes.c_void_p), ("tables", ctypes.c_void_p),
         ("elem_geom", ctypes.c_void_p), ("face_geom", ctypes.c_void_p),
+        ("n_planes", ctypes.c_int64), ("plane_off", ctypes.c_void_p), ("rec_ext", ctypes.c_void_p),
     ]
 
 
@@ -107,8 +108,10 @@ class NativePlan:
             np.ascontiguousarray(pb.tables, dtype=np.float64),
             np.ascontiguousarray(pb.egeo, dtype=np.float64),
             np.ascontiguousarray(pb.fgeo, dtype=np.float64),
+            np.ascontiguousarray(pb.plane_off, dtype=np.int64),
+            np.ascontiguousarray(pb.rec_ext, dtype=np.int64),
         ]
-        cd, ce, ec, ep, do, rc, tb, eg, fg = self._keep
+        cd, ce, ec, ep, do, rc, tb, eg, fg, po, rx = self._keep
         d = PlanDesc()
         d.abi_version, d.record_bytes = L.ABI_VERSION, L.FACE_REC.itemsize
         d.dim, d.n_classes = pb.dim, cd.shape[0]
@@ -116,8 +119,10 @@ class NativePlan:
         d.n_tables, d.n_elem_geom, d.n_face_geom = tb.size, eg.size, fg.size
         d.lam = pb.lam
         for name, arr in zip(["class_desc", "class_elems", "elem_class", "elem_pos", "dof_off",
-                              "face_records", "tables", "elem_geom", "face_geom"], self._keep):
+                              "face_records", "tables", "elem_geom", "face_geom", "plane_off", "rec_ext"],
+                             self._keep):
             setattr(d, name, arr.ctypes.data)
+        d.n_planes = int(pb.n_planes)
         h = ctypes.c_void_p()
         check(lib.sipg_plan_create(ctypes.byref(d), ctypes.byref(h)), "sipg_plan_create")
         self._lib = lib

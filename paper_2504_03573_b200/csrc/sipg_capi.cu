@@ -38,6 +38,21 @@ const std::vector<KernelEntry>& kernel_table() {
   return t;
 }
 
+const std::vector<PlanesEntry>& planes_table() {
+  static const std::vector<PlanesEntry> t = [] {
+    std::vector<PlanesEntry> v;
+    sipg_register_planes(v);
+    return v;
+  }();
+  return t;
+}
+
+const PlanesEntry* find_planes(int n, int q) {
+  for (const auto& k : planes_table())
+    if (k.n == n && k.q == q) return &k;
+  return nullptr;
+}
+
 const KernelEntry* find_kernel(int shape, int n, int q, int geom, int kind = 0) {
   for (const auto& k : kernel_table())
     if (k.shape == shape && k.n == n && k.q == q && k.geom == geom && k.kind == kind) return &k;
@@ -47,6 +62,23 @@ const KernelEntry* find_kernel(int shape, int n, int q, int geom, int kind = 0) 
 // Does every face of every element of class c take the register-column fast
 // path (boundary or conforming same-class neighbour, identity transfer,
 // constant geometry, no tangential neighbour metric)?  Mirrors k_hex's test.
+int class_face_level(const sipg_plan_desc* d, int c) {
+  const int32_t* cd = d->class_desc + c * CD_WORDS;
+  const FaceRec* recs = (const FaceRec*)d->face_records;
+  int level = 0;
+  for (int64_t r = cd[CD_REC_OFF]; r < cd[CD_REC_OFF] + (int64_t)cd[CD_COUNT] * cd[CD_NFACES]; ++r) {
+    const FaceRec& f = recs[r];
+    if (f.type == FT_BOUNDARY && !(f.flags & F_SELF_PW)) continue;
+    if (f.type == FT_DIRECT && (f.flags & F_FAST_HEX)) continue;
+    if (f.type == FT_SHARED && (f.flags & F_FAST_SHARED) && d->rec_ext && d->rec_ext[2 * r] >= 0) {
+      level = 1;
+      continue;
+    }
+    return 2;
+  }
+  return level;
+}
+
 bool class_all_fast(const sipg_plan_desc* d, int c) {
   const int32_t* cd = d->class_desc + c * CD_WORDS;
   const FaceRec* recs = (const FaceRec*)d->face_records;
@@ -77,7 +109,10 @@ struct sipg_plan {
   std::vector<int32_t> cd_host;
   std::vector<const KernelEntry*> kern;
   std::vector<int> grid;                 // CTAs per class launch (persistent kernels: SMs x occupancy)
-  void* bufs[9];
+  std::vector<const PlanesEntry*> planes_k;   // per class: face-plane publisher (hex) or null
+  bool need_planes = false;
+  double* planes = nullptr;
+  void* bufs[11];
   double* x_stage = nullptr;
   double* y_stage = nullptr;
   int64_t launches = 0;
@@ -127,8 +162,9 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
       // (1 warp-per-element DMMA, 3 CTA-per-element DMMA, 4 DFMA register-column [default, fastest measured])
       const char* ov = getenv("SIPG_HEX_FAST_KERNEL");
       const int fast_kind = ov ? atoi(ov) : 4;
-      k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? fast_kind : 2);
-      if (!k) k = find_kernel(shape, n, q, geom, class_all_fast(d, c) ? 1 : 2);
+      const int level = class_face_level(d, c);
+      k = find_kernel(shape, n, q, geom, level == 0 ? fast_kind : (level == 1 ? 7 : 2));
+      if (!k) k = find_kernel(shape, n, q, geom, level == 0 ? 4 : 2);
       if (k) {
         const int* ax = cd + CD_TAX;
         cudaError_t e = k->upload(d->tables + ax[TX_V], d->tables + ax[TX_D], d->tables + ax[TX_W],
@@ -163,10 +199,40 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     delete p;
     return rc;
   }
-  void* b[9] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d};
+  int64_t *po_d = nullptr, *rx_d = nullptr;
+  if ((d->plane_off && (rc = upload(d->plane_off, d->n_elements, &po_d))) ||
+      (d->rec_ext && (rc = upload(d->rec_ext, 2 * d->n_records, &rx_d)))) {
+    delete p;
+    return rc;
+  }
+  void* b[11] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, po_d, rx_d};
   memcpy(p->bufs, b, sizeof(b));
+  for (const KernelEntry* k : p->kern) p->need_planes = p->need_planes || k->kind == 6 || k->kind == 7;
+  if (p->need_planes && d->n_planes > 0) CK(cudaMalloc((void**)&p->planes, sizeof(double) * d->n_planes));
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD_WORDS;
+    const PlanesEntry* pe = nullptr;
+    if (p->need_planes && cd[CD_SHAPE] == SHAPE_HEX && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7) {
+      pe = find_planes(cd[CD_N], cd[CD_Q0]);
+      const int* ax = cd + CD_TAX;
+      const KernelEntry* kf = find_kernel(SHAPE_HEX, cd[CD_N], cd[CD_Q0], GEOM_REGULAR, 4);
+      if (pe && kf) {   // the publisher reads the (N, Q) constant tables
+        cudaError_t e = kf->upload(d->tables + ax[TX_V], d->tables + ax[TX_D], d->tables + ax[TX_W],
+                                   d->tables + ax[TX_DVEND]);
+        if (e != cudaSuccess) {
+          sipg_plan_destroy(p);
+          return fail(SIPG_ERR_CUDA, std::string("constant table upload: ") + cudaGetErrorString(e));
+        }
+      }
+      if (!pe) {
+        sipg_plan_destroy(p);
+        return fail(SIPG_ERR_UNSUPPORTED, "no face-plane publisher for this hex class");
+      }
+    }
+    p->planes_k.push_back(pe);
+  }
   p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes,
-                  getenv("SIPG_DEBUG") ? atoi(getenv("SIPG_DEBUG")) : 0, 0};
+                  getenv("SIPG_DEBUG") ? atoi(getenv("SIPG_DEBUG")) : 0, 0, p->planes, po_d, rx_d};
   for (const KernelEntry* k : p->kern) {
     if (k->smem == 0) continue;
     cudaError_t e = cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -201,6 +267,20 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
 int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->need_planes) {
+    // publish face planes: role 0 (or all) -> every locally owned element; role 1 -> the
+    // ghost layer (its coefficients have just arrived); role -1 -> everything
+    for (int c = 0; c < p->n_cls; ++c) {
+      const int32_t* cd = p->cd_host.data() + c * CD_WORDS;
+      const int count = cd[CD_COUNT], crole = cd[CD_ROLE];
+      if (!p->planes_k[c] || count == 0) continue;
+      const bool go = role < 0 || (role == 0 && crole != 2) || (role == 1 && crole == 2);
+      if (!go) continue;
+      const int g = count < 148 * 8 ? count : 148 * 8;
+      p->planes_k[c]->fn<<<g, 128, 0, s>>>(p->dp, c, x_dev);
+      ++p->launches;
+    }
+  }
   for (int c = 0; c < p->n_cls; ++c) {
     const int32_t* cd = p->cd_host.data() + c * CD_WORDS;
     const int count = cd[CD_COUNT];
@@ -257,8 +337,10 @@ int64_t sipg_plan_launches(const sipg_plan* p) { return p ? p->launches : -1; }
 int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   if (!p) return -1;
   int k = 0;
-  for (int c = 0; c < p->n_cls; ++c)
+  for (int c = 0; c < p->n_cls; ++c) {
     if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->cd_host[c * CD_WORDS + CD_ROLE] != 2) ++k;
+    if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->planes_k.size() > (size_t)c && p->planes_k[c]) ++k;
+  }
   return k;
 }
 
@@ -266,6 +348,7 @@ int sipg_plan_destroy(sipg_plan* p) {
   if (!p) return 0;
   for (void* b : p->bufs)
     if (b) cudaFree(b);
+  if (p->planes) cudaFree(p->planes);
   if (p->x_stage) cudaFree(p->x_stage);
   if (p->y_stage) cudaFree(p->y_stage);
   delete p;

@@ -3,7 +3,7 @@
 #pragma once
 #include <stdint.h>
 
-#define SIPG_ABI_VERSION 4
+#define SIPG_ABI_VERSION 5
 
 enum { SHAPE_QUAD = 0, SHAPE_TRI = 1, SHAPE_HEX = 2 };
 enum { GEOM_REGULAR = 0, GEOM_POINTWISE = 1 };
@@ -26,7 +26,8 @@ enum { FT_BOUNDARY = 0, FT_DIRECT = 1, FT_SHARED = 2 };
 enum {
   F_SELF_PW = 1, F_OTHER_PW = 2, F_OTHER_ID = 4, F_OTHER_SWAP = 8,
   F_SELF_ID = 16, F_SELF_SWAP = 32, F_SELF_NEG = 64, F_OTHER_NEG = 128,
-  F_FAST_HEX = 256   // conforming same-class hex neighbour, identity grid, constant metric, normal-only
+  F_FAST_HEX = 256,  // conforming same-class hex neighbour, identity grid, constant metric, normal-only
+  F_FAST_SHARED = 512  // hex shared trace, no swap, constant metric, normal-only: planes + 1-D tables
 };
 
 struct FaceRec {            // 128 bytes, numpy dtype layout.FACE_REC
@@ -51,4 +52,8 @@ struct DevPlan {
   int32_t n_cls;
   int32_t debug;               // instrumentation bits (SIPG_DEBUG env): 1 = skip face work (timing only)
   int32_t pad;
+  double* planes;              // published face planes (hex): per element 6 faces x (u-plane, dn-plane)
+  const int64_t* plane_off;    // per element offset into planes (-1: none)
+  const int64_t* rec_ext;      // per face record, 2 words: [0] nbr face planes offset | N_o << 48,
+                               //                           [1] E_o axis-0 table | axis-1 table << 32
 };

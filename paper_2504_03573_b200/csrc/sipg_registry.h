@@ -7,7 +7,8 @@
 using KernelFn = void (*)(const DevPlan, const int, const double*, double*);
 using UploadFn = cudaError_t (*)(const double* V, const double* D, const double* W, const double* dVend);
 
-// kind: 0 = generic smem kernel, one CTA per element (any basis / rule / geometry),
+// kind: 6/7 = planes-consuming hex kernel (k_hexp) without / with fast shared traces,
+//       0 = generic smem kernel, one CTA per element (any basis / rule / geometry),
 //       5 = the same element routine, one warp per element (2-D shapes, persistent),
 //       1 = register-column hex kernel, conforming + boundary faces only,
 //       2 = register-column hex kernel with the generic face path
@@ -18,6 +19,13 @@ struct KernelEntry {
   size_t smem;          // dynamic shared memory bytes
   UploadFn upload;      // constant-table upload (kinds 1, 2)
 };
+
+using PlanesFn = void (*)(const DevPlan, const int, const double*);
+struct PlanesEntry {
+  int n, q;
+  PlanesFn fn;
+};
+void sipg_register_planes(std::vector<PlanesEntry>& v);
 
 void sipg_register_quad(std::vector<KernelEntry>& v);
 void sipg_register_tri(std::vector<KernelEntry>& v);
@@ -40,6 +48,13 @@ KernelEntry sipg_entry();
 #define SIPG_ENTRIES_NQ(S, N)                                                                \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_REGULAR>());                                      \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_POINTWISE>())
+#define SIPG_HEX_PLANES(N)                                                                   \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 6, &sipg::k_hexp<N, N + 1, false>,    \
+                          (N + 1) * (N + 1), sipg::HexPlanes<N, N + 1, false>::smem_bytes(),      \
+                          &sipg::hex_fast_upload<N, N + 1>});                                    \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 7, &sipg::k_hexp<N, N + 1, true>,     \
+                          (N + 1) * (N + 1), sipg::HexPlanes<N, N + 1, true>::smem_bytes(),       \
+                          &sipg::hex_fast_upload<N, N + 1>})
 #define SIPG_HEX_FAST(N)                                                                     \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1, &sipg::k_hex<N, N + 1, false>,  \
                           (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(false),         \

@@ -4,7 +4,7 @@
 """
 import numpy as np
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 SHAPE_QUAD, SHAPE_TRI, SHAPE_HEX = 0, 1, 2
 SHAPE_ID = {"quad": SHAPE_QUAD, "tri": SHAPE_TRI, "hex": SHAPE_HEX}
@@ -38,6 +38,8 @@ F_SELF_NEG = 64     # triangle chain: self face parameter at flux point = -t
 F_OTHER_NEG = 128
 F_FAST_HEX = 256    # conforming same-class hex neighbour, identity grid, constant metric,
                     # normal-only neighbour metric: register-column fast path
+F_FAST_SHARED = 512  # hex shared trace, no axis swap, constant metric, normal-only metrics:
+                     # neighbour planes evaluated at the trace grid with 1-D tables (k_hexp)
 
 FACE_REC = np.dtype([
     ("type", "<i4"), ("flags", "<i4"), ("nbr", "<i4"), ("nbr_face", "<i4"),

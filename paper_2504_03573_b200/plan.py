@@ -18,7 +18,8 @@ import numpy as np
 
 from . import layout as L
 from .mesh import as_shape
-from .polylib import BasisKind, QuadKind, as_basis_kind, as_quad_kind, lagrange_interp_matrix, quad_rule
+from .polylib import (BasisKind, QuadKind, as_basis_kind, as_quad_kind, eval_basis_1d,
+                      lagrange_interp_matrix, quad_rule)
 from .stdregions import DEFAULT_RULES, DIM, FACES, class_tables
 
 REF_VERTS = {
@@ -489,6 +490,14 @@ class PlanBuilder:
                 RE[i], RF[i] = itf.right
             CODE[i] = itf.orientation
         recs = np.zeros(self.n_recs, dtype=L.FACE_REC)
+        self.rec_ext = np.zeros((self.n_recs, 2), dtype=np.int64)
+        self.rec_ext[:, 0] = -1
+        self._rec_face = np.zeros(self.n_recs, dtype=np.int64)
+        for ci, (c, gm, ids) in enumerate(self.class_list):
+            nf = len(c.faces)
+            base = self.rec_base[ids]
+            for f in range(nf):
+                self._rec_face[base + f] = f
         recs["nbr"] = -1
         recs["nbr_face"] = -1
         recs["nbr_rec"] = -1
@@ -607,6 +616,10 @@ class PlanBuilder:
         self._fsize += blk.size
         return off
 
+    def face_ids_of(self, r):
+        """Local face index of (the first of) records r (all share it in a bucket)."""
+        return int(self._rec_face[int(np.atleast_1d(r)[0])])
+
     def _shared_bucket(self, cl, fl, cr, fr, code, le, re_, rl, rr):
         """Shared trace (reference sipg.py:513-554): one grid (max q), one
         metric and one normal (left's; right uses -n)."""
@@ -653,6 +666,29 @@ class PlanBuilder:
             recs["sJ"][r] = swj[:, 0] / wt[0]
             recs["gs"][r, :d] = gxs
             recs["go"][r, :d] = gxo
+            # hex fast shared path: the other side's planes evaluated straight at the trace
+            # points with E_k[t][i] = psi_i(other's parameter of t_k) (no axis swap here)
+            c_o = cr if self_is_left else cl
+            c_s = cl if self_is_left else cr
+            if (d == 3 and not sws and not swo and c_o.kind.value == "modified_modal"
+                    and c_s.kind.value == "modified_modal"
+                    and all(c_.axis[a]["gll"] for c_ in (c_o, c_s) for a in range(3))
+                    and c_o.n <= 9 and rules[0].n <= 11 and rules[1].n <= 11):
+                code_o = code if self_is_left else 0
+                sign = [-1.0 if (code_o >> 1) & 1 else 1.0, -1.0 if code_o & 1 else 1.0]
+                E = [eval_basis_1d(c_o.kind, c_o.n, sign[k] * t_axes[k])[0] for k in range(2)]
+                e0, e1 = self.pool.add(E[0]), self.pool.add(E[1])
+                fs_ = self.face_ids_of(r)
+                ok = regular.copy()
+                a_s = FACES["hex"][fs_].fixed
+                tang_s = [b for b in range(3) if b != a_s]
+                f_o = fr if self_is_left else fl
+                a_o = FACES["hex"][f_o].fixed
+                tang_o = [b for b in range(3) if b != a_o]
+                ok &= (gxs[:, tang_s[0]] == 0.0) & (gxs[:, tang_s[1]] == 0.0)
+                ok &= (gxo[:, tang_o[0]] == 0.0) & (gxo[:, tang_o[1]] == 0.0)
+                recs["flags"][r[ok]] |= L.F_FAST_SHARED
+                self.rec_ext[r[ok], 1] = e0 | (e1 << 32)
             for j in np.flatnonzero(~regular):
                 gn_l = gn_at(cl, fl, invl[j:j + 1], nl[j:j + 1], prm_t)[0]
                 gn_r = gn_at(cr, fr, invr[j:j + 1], -nl[j:j + 1], prm_tr)[0]
@@ -663,5 +699,20 @@ class PlanBuilder:
     def _finish(self):
         nb = self.recs["nbr"]
         self.recs["nbr_dof"] = np.where(nb >= 0, self.dof_off[np.maximum(nb, 0)], -1)
+        # published face planes (hex): per element 6 faces x (boundary-mode plane, normal-
+        # derivative plane), each N^2 doubles padded to even -> 16-byte aligned blocks
+        nel = len(self.ct)
+        nn = np.array([(c.n * c.n + 1) & ~1 if c.shape == "hex" else 0 for c in self.exp_list])[self.exp_of]
+        sizes = 12 * nn
+        self.plane_off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+        self.plane_off[sizes == 0] = -1
+        self.n_planes = int(sizes.sum())
+        has = (nb >= 0)
+        nbr = np.maximum(nb, 0)
+        nfo = self.recs["nbr_face"].astype(np.int64)
+        po = self.plane_off[nbr] + nfo * 2 * nn[nbr]
+        n_o = np.array([c.n for c in self.exp_list])[self.exp_of][nbr].astype(np.int64)
+        ok = has & (self.plane_off[nbr] >= 0)
+        self.rec_ext[ok, 0] = po[ok] | (n_o[ok] << 48)
         self.fgeo = np.concatenate(self._fgeo) if self._fgeo else np.zeros(1)
         self.tables = self.pool.array()
