@@ -176,8 +176,9 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
   }
-  if (t >= 32 && t < 38) {              // neighbour blocks: one per thread, another warp than the prefetch issuer
-    const int f = t - 32;
+  if (t >= NT - 6) {      // neighbour blocks, one per thread: the last 6 threads (NT >= 9),
+                          // never thread 0 (which issues the next-element prefetch)
+    const int f = t - (NT - 6);
     unsigned nb = 0;
     const FaceRec& rf = srec[f];
     if (rf.type == FT_DIRECT && (rf.flags & F_FAST_HEX)) {
@@ -269,7 +270,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       B2[ta * SI + tb * SJ + r] = d2[r];
     }
   }
-  if (t >= 32 && t < 38) cp_async_wait<0>();
+  if (t >= NT - 6) cp_async_wait<0>();
   mbar_wait(&mbar[2], k & 1);
   __syncthreads();
 #pragma unroll

@@ -143,8 +143,9 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
             : (ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2
             : (ty == FT_SHARED && (fl & F_FAST_SHARED)) ? 3 : 0;
     }
-    if (t >= 32 && t < 38) {            // neighbour face planes: one bulk copy per face
-      const int f = t - 32;
+    if (t >= NT - 6) {      // neighbour face planes, one bulk copy per face: the last 6 threads
+                            // (NT >= 9); thread 0 issues the next-element prefetch
+      const int f = t - (NT - 6);
       const int64_t ext = sext[2 * f];
       unsigned nb = 0;
       const int ty = srec[f].type, fl = srec[f].flags;
