@@ -42,14 +42,16 @@ const std::vector<PlanesEntry>& planes_table() {
   static const std::vector<PlanesEntry> t = [] {
     std::vector<PlanesEntry> v;
     sipg_register_planes(v);
+    sipg_register_planes_quad(v);
+    sipg_register_planes_tri(v);
     return v;
   }();
   return t;
 }
 
-const PlanesEntry* find_planes(int n, int q) {
+const PlanesEntry* find_planes(int shape, int n, int q) {
   for (const auto& k : planes_table())
-    if (k.n == n && k.q == q) return &k;
+    if (k.shape == shape && k.n == n && k.q == q) return &k;
   return nullptr;
 }
 
@@ -207,13 +209,24 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   }
   void* b[11] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, po_d, rx_d};
   memcpy(p->bufs, b, sizeof(b));
-  for (const KernelEntry* k : p->kern) p->need_planes = p->need_planes || k->kind == 6 || k->kind == 7;
+  // Published neighbour data: hex planes for the k_hexp classes; 2-D face traces when the mesh has
+  // triangles (a triangle trace costs a collapsed-coordinate chain per face — worth computing once per
+  // face instead of once per reader; quad traces are cheap enough to evaluate in place).
+  for (const KernelEntry* k : p->kern)
+    p->need_planes = p->need_planes || k->kind == 6 || k->kind == 7 || (k->kind == 5 && k->shape == SHAPE_TRI);
+  if (getenv("SIPG_NO_PUBLISH")) p->need_planes = false;   // instrumentation: 2-D kernels evaluate neighbours
   if (p->need_planes && d->n_planes > 0) CK(cudaMalloc((void**)&p->planes, sizeof(double) * d->n_planes));
   for (int c = 0; c < d->n_classes; ++c) {
     const int32_t* cd = d->class_desc + c * CD_WORDS;
     const PlanesEntry* pe = nullptr;
-    if (p->need_planes && cd[CD_SHAPE] == SHAPE_HEX && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7) {
-      pe = find_planes(cd[CD_N], cd[CD_Q0]);
+    if (p->need_planes && cd[CD_SHAPE] != SHAPE_HEX) {
+      pe = find_planes(cd[CD_SHAPE], cd[CD_N], cd[CD_Q0]);
+      if (!pe) {
+        sipg_plan_destroy(p);
+        return fail(SIPG_ERR_UNSUPPORTED, "no face-trace publisher for this 2-D class");
+      }
+    } else if (p->need_planes && cd[CD_SHAPE] == SHAPE_HEX && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7) {
+      pe = find_planes(SHAPE_HEX, cd[CD_N], cd[CD_Q0]);
       const int* ax = cd + CD_TAX;
       const KernelEntry* kf = find_kernel(SHAPE_HEX, cd[CD_N], cd[CD_Q0], GEOM_REGULAR, 4);
       if (pe && kf) {   // the publisher reads the (N, Q) constant tables
@@ -276,8 +289,11 @@ int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_d
       if (!p->planes_k[c] || count == 0) continue;
       const bool go = role < 0 || (role == 0 && crole != 2) || (role == 1 && crole == 2);
       if (!go) continue;
-      const int g = count < 148 * 8 ? count : 148 * 8;
-      p->planes_k[c]->fn<<<g, 128, 0, s>>>(p->dp, c, x_dev);
+      const bool hex = cd[CD_SHAPE] == SHAPE_HEX;
+      const int per = hex ? 1 : 8;
+      int g = (count + per - 1) / per;
+      if (g > 148 * 8) g = 148 * 8;
+      p->planes_k[c]->fn<<<g, hex ? 128 : 256, 0, s>>>(p->dp, c, x_dev);
       ++p->launches;
     }
   }

@@ -34,12 +34,12 @@ void sipg_register_hex(std::vector<KernelEntry>& v) {
 }
 
 void sipg_register_planes(std::vector<PlanesEntry>& v) {
-  v.push_back(PlanesEntry{2, 3, &sipg::k_planes<2, 3>});
-  v.push_back(PlanesEntry{3, 4, &sipg::k_planes<3, 4>});
-  v.push_back(PlanesEntry{4, 5, &sipg::k_planes<4, 5>});
-  v.push_back(PlanesEntry{5, 6, &sipg::k_planes<5, 6>});
-  v.push_back(PlanesEntry{6, 7, &sipg::k_planes<6, 7>});
-  v.push_back(PlanesEntry{7, 8, &sipg::k_planes<7, 8>});
-  v.push_back(PlanesEntry{8, 9, &sipg::k_planes<8, 9>});
-  v.push_back(PlanesEntry{9, 10, &sipg::k_planes<9, 10>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 2, 3, &sipg::k_planes<2, 3>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 3, 4, &sipg::k_planes<3, 4>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 4, 5, &sipg::k_planes<4, 5>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 5, 6, &sipg::k_planes<5, 6>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 6, 7, &sipg::k_planes<6, 7>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 7, 8, &sipg::k_planes<7, 8>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 8, 9, &sipg::k_planes<8, 9>});
+  v.push_back(PlanesEntry{SHAPE_HEX, 9, 10, &sipg::k_planes<9, 10>});
 }

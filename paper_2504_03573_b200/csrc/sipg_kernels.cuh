@@ -553,7 +553,8 @@ template <int SHAPE, int N, int Q, class TM = CtaTeam>
 __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, const int f,
                                           const double* __restrict__ x, double* __restrict__ us,
                                           double* __restrict__ fbf, double* __restrict__ fscr,
-                                          const int tid, const int nt, const double* staged = nullptr) {
+                                          const int tid, const int nt, const double* staged = nullptr,
+                                          const bool staged_traces = false, const int staged_q = 0) {
   using C = Cfg<SHAPE, N, Q>;
   constexpr int D = C::D, NS = C::NS, FP = C::FP;
   const double* T = P.tab;
@@ -568,7 +569,16 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
   int qo0 = 0, qo1 = 1;
   if (r.type != FT_BOUNDARY) {
     TM::sync();
-    no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt, staged);
+    if (staged_traces) {      // published traces of the neighbour face: u, du_0, du_1 on its grid
+      no = staged_q;
+      for (int i = tid; i < 3 * no; i += nt) {
+        const int fl = i / no, pp = i - fl * no;
+        uo[fl * FP + pp] = staged[i];
+      }
+      TM::sync();
+    } else {
+      no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt, staged);
+    }
     const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
     const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
     qo0 = cdo[CD_Q0 + fto.run0];
@@ -777,9 +787,16 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
     TM::sync();
     for (int f = 0; f < C::NF; ++f) {
       if (srec[f].type == FT_BOUNDARY) continue;
-      const int no = P.cd[P.elem_class[srec[f].nbr] * CD_WORDS + CD_NC];
-      const double* src = x + srec[f].nbr_dof;
-      for (int i = tid; i < no; i += nt) cp_async8_(snb + f * C::NBK + i, src + i);
+      const int64_t ext = P.rec_ext ? P.rec_ext[2 * (rbase + f)] : -1;
+      if (ext >= 0 && P.planes) {          // published neighbour traces (3 fields x q_o)
+        const int qo = (int)(ext >> 48);
+        const double* src = P.planes + (ext & ((int64_t(1) << 48) - 1));
+        for (int i = tid; i < 3 * qo; i += nt) cp_async8_(snb + f * C::NBK + i, src + i);
+      } else {
+        const int no = P.cd[P.elem_class[srec[f].nbr] * CD_WORDS + CD_NC];
+        const double* src = x + srec[f].nbr_dof;
+        for (int i = tid; i < no; i += nt) cp_async8_(snb + f * C::NBK + i, src + i);
+      }
     }
     cp_async_commit_();
   }
@@ -832,8 +849,10 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
     const FaceRec r = D == 2 ? srec[f] : P.recs[rbase + f];
     restrict_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, us, tid, nt);
     TM::sync();
+    const int64_t ext = (D == 2 && P.rec_ext && r.type != FT_BOUNDARY) ? P.rec_ext[2 * (rbase + f)] : -1;
+    const bool pub = D == 2 && ext >= 0 && P.planes != nullptr;
     generic_face<SHAPE, N, Q, TM>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt,
-                                  D == 2 ? snb + f * C::NBK : nullptr);
+                                  D == 2 ? snb + f * C::NBK : nullptr, pub, pub ? (int)(ext >> 48) : 0);
     TM::sync();
   }
 
@@ -931,6 +950,36 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
   TM::sync();
   for (int i = tid; i < NC; i += nt) y[dof0 + i] = c[i];
   TM::sync();
+}
+
+// Phase 1 (2-D): every element publishes u, du/deta_0, du/deta_1 on each of its
+// faces' own grids (the reference's trace publish, sipg.py:585-592, with the
+// eta-gradient instead of the normal derivative so a shared trace can apply
+// its own metric).  One warp per element, persistent.
+template <int SHAPE, int N, int Q>
+__global__ void __launch_bounds__(256)
+k_traces2d(const DevPlan P, const int cls, const double* __restrict__ x) {
+  using C = Cfg<SHAPE, N, Q>;
+  constexpr int NF = C::NF, FP = QMAX;
+  __shared__ double sc[8][C::NC + 2];
+  __shared__ double so[8][3 * FP + 2 * (NMAX + 2)];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int* cd = P.cd + cls * CD_WORDS;
+  const int count = cd[CD_COUNT];
+  const int* elist = P.class_elems + cd[CD_ELEM_OFF];
+  for (int iel = blockIdx.x * 8 + warp; iel < count; iel += gridDim.x * 8) {
+    const int e = elist[iel];
+    const double* xe = x + P.dof_off[e];
+    for (int i = lane; i < C::NC; i += 32) sc[warp][i] = __ldg(xe + i);
+    __syncwarp();
+    double* out = P.planes + P.plane_off[e];
+    for (int f = 0; f < NF; ++f) {
+      const int q = eval_face_from_coeffs<WarpTeam>(P, e, f, x, so[warp], FP, so[warp] + 3 * FP, lane, 32,
+                                                    sc[warp]);
+      for (int i = lane; i < 3 * q; i += 32) out[f * 3 * Q + i] = so[warp][(i / q) * FP + (i - (i / q) * q)];
+      __syncwarp();
+    }
+  }
 }
 
 template <int SHAPE, int N, int Q, int GEOM>

@@ -13,3 +13,15 @@ void sipg_register_quad(std::vector<KernelEntry>& v) {
   SIPG_ENTRIES_NQ(SHAPE_QUAD, 9);
   SIPG_ENTRIES_NQ(SHAPE_QUAD, 10);
 }
+
+void sipg_register_planes_quad(std::vector<PlanesEntry>& v) {
+  v.push_back(PlanesEntry{SHAPE_QUAD, 2, 3, &sipg::k_traces2d<SHAPE_QUAD, 2, 3>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 3, 4, &sipg::k_traces2d<SHAPE_QUAD, 3, 4>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 4, 5, &sipg::k_traces2d<SHAPE_QUAD, 4, 5>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 5, 6, &sipg::k_traces2d<SHAPE_QUAD, 5, 6>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 6, 7, &sipg::k_traces2d<SHAPE_QUAD, 6, 7>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 7, 8, &sipg::k_traces2d<SHAPE_QUAD, 7, 8>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 8, 9, &sipg::k_traces2d<SHAPE_QUAD, 8, 9>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 9, 10, &sipg::k_traces2d<SHAPE_QUAD, 9, 10>});
+  v.push_back(PlanesEntry{SHAPE_QUAD, 10, 11, &sipg::k_traces2d<SHAPE_QUAD, 10, 11>});
+}

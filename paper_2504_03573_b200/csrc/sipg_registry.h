@@ -22,10 +22,12 @@ struct KernelEntry {
 
 using PlanesFn = void (*)(const DevPlan, const int, const double*);
 struct PlanesEntry {
-  int n, q;
+  int shape, n, q;
   PlanesFn fn;
 };
 void sipg_register_planes(std::vector<PlanesEntry>& v);
+void sipg_register_planes_quad(std::vector<PlanesEntry>& v);
+void sipg_register_planes_tri(std::vector<PlanesEntry>& v);
 
 void sipg_register_quad(std::vector<KernelEntry>& v);
 void sipg_register_tri(std::vector<KernelEntry>& v);

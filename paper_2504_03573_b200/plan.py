@@ -701,18 +701,28 @@ class PlanBuilder:
         self.recs["nbr_dof"] = np.where(nb >= 0, self.dof_off[np.maximum(nb, 0)], -1)
         # published face planes (hex): per element 6 faces x (boundary-mode plane, normal-
         # derivative plane), each N^2 doubles padded to even -> 16-byte aligned blocks
+        # 2-D: per element, per face, (u, du/deta_0, du/deta_1) on the face's own q points
         nel = len(self.ct)
-        nn = np.array([(c.n * c.n + 1) & ~1 if c.shape == "hex" else 0 for c in self.exp_list])[self.exp_of]
-        sizes = 12 * nn
+        is2d = self.dim == 2
+        if is2d:
+            qe = np.array([c.nq[0] for c in self.exp_list])[self.exp_of]
+            nfe = np.array([len(c.faces) for c in self.exp_list])[self.exp_of]
+            per_face = 3 * qe
+            sizes = nfe * per_face
+            sizes = (sizes + 1) & ~1
+        else:
+            nn = np.array([(c.n * c.n + 1) & ~1 if c.shape == "hex" else 0 for c in self.exp_list])[self.exp_of]
+            per_face = 2 * nn
+            sizes = 12 * nn
         self.plane_off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
         self.plane_off[sizes == 0] = -1
         self.n_planes = int(sizes.sum())
         has = (nb >= 0)
         nbr = np.maximum(nb, 0)
         nfo = self.recs["nbr_face"].astype(np.int64)
-        po = self.plane_off[nbr] + nfo * 2 * nn[nbr]
-        n_o = np.array([c.n for c in self.exp_list])[self.exp_of][nbr].astype(np.int64)
+        po = self.plane_off[nbr] + nfo * per_face[nbr]
+        size_o = (qe if is2d else np.array([c.n for c in self.exp_list])[self.exp_of])[nbr].astype(np.int64)
         ok = has & (self.plane_off[nbr] >= 0)
-        self.rec_ext[ok, 0] = po[ok] | (n_o[ok] << 48)
+        self.rec_ext[ok, 0] = po[ok] | (size_o[ok] << 48)
         self.fgeo = np.concatenate(self._fgeo) if self._fgeo else np.zeros(1)
         self.tables = self.pool.array()
