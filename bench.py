@@ -34,6 +34,15 @@ HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.js
 OP_KW = dict(basis_kind="modified_modal", tau_rule="baseline", shared_rule="patched")
 
 
+KERNEL_NAMES = {0: "k_apply", 1: "k_hexw", 2: "k_hex_mma", 3: "k_hex_mma", 4: "k_hex", 5: "k_apply_w",
+                6: "k_hexp", 7: "k_hexp"}
+
+
+def kernel_label(info, rd):
+    name = KERNEL_NAMES.get(info["kernel"], f"kind{info['kernel']}")
+    return f"{name}<{rd['shape']},n={rd['n']},q={rd['q']},geom={rd['geom']}>"
+
+
 def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -333,6 +342,30 @@ def main():
         e2e = float(t.item())
     check = float(np.abs(yp.numpy()[own] - y.cpu().numpy()[own]).max())
 
+    # copy floor of the e2e step: the same bytes H2D alone, D2H alone, and both at once
+    def copy_ms(h2d, d2h):
+        s2 = torch.cuda.Stream()
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            s2.wait_stream(stream)
+            if h2d:
+                x[own].copy_(xp[own], non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    yp[own].copy_(y[own], non_blocking=True)
+            stream.wait_stream(s2)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(min(ts))
+    copy_floor = {"h2d_ms": copy_ms(True, False), "d2h_ms": copy_ms(False, True),
+                  "both_concurrent_ms": copy_ms(True, True)}
+    if dop is None:
+        copy_floor["stream_chunks"] = op.native.stream_chunks()
+
     if rank == 0:
         rows = roofline.per_class(op.plan)
         b_alg = sum(r["bytes"] for r in rows)
@@ -364,7 +397,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": ach_gbs, "peak": peak, "unit": "GB/s",
                          "frac": ach_gbs / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "kernel": f"k_apply<{rd['shape']},n={rd['n']},q={rd['q']},geom={rd['geom']}>",
+                         "kernel": kernel_label(op.native.class_info(dom), rd),
                          "kernel_ms": float(cls_ms[dom]), "kernel_share": float(cls_ms[dom] / cls_ms.sum()),
                          "algorithmic_bytes_per_launch": rd["bytes"]},
             "roofline_fp64": {"achieved": ach_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -376,7 +409,9 @@ def main():
                              "fp64_frac": f_alg / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
             "e2e": {"value": n_total / (e2e * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": e2e,
                     "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * n_owned,
-                    "path": "sipg_apply_host (pinned host x -> H2D -> apply -> D2H -> host y)",
+                    "path": ("sipg_apply_host: pinned host x -> H2D by DoF chunk, overlapped with the "
+                             "per-stage apply and the D2H of finished y chunks -> host y"),
+                    "copy_floor": copy_floor,
                     "max_abs_diff_vs_device_y": check},
             "gpu_launches": int(launches),
             "clocks": clocks,

@@ -83,6 +83,11 @@ const char* sipg_last_error(void);
 /* Introspection: kernel launches issued so far / per apply; layout constants. */
 int64_t sipg_plan_launches(const sipg_plan* plan);
 int sipg_plan_kernels_per_apply(const sipg_plan* plan);
+/* Number of DoF chunks sipg_apply_host pipelines (H2D chunk k || compute stage k-1 || D2H), 0 when
+ * the host apply runs copy -> apply -> copy (mesh order not chunkable, or a distributed local plan). */
+int sipg_plan_stream_chunks(const sipg_plan* plan);
+/* Kernel launches one sipg_apply_host issues (publishers + compute, by stage when streamed). */
+int sipg_plan_host_launches_per_apply(const sipg_plan* plan);
 int sipg_abi_layout(int32_t* out, int32_t n);
 int sipg_supported(int32_t shape, int32_t n_modes, int32_t n_quad);
 

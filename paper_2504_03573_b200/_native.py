@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsipg.so"
 
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
+           "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
            "sipg_apply_role"]
 
@@ -63,6 +64,9 @@ def load() -> ctypes.CDLL:
     lib.sipg_plan_launches.restype = i64
     lib.sipg_plan_kernels_per_apply.argtypes = [vp]
     lib.sipg_plan_kernels_per_apply.restype = ctypes.c_int
+    for nm in ("sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply"):
+        getattr(lib, nm).argtypes = [vp]
+        getattr(lib, nm).restype = ctypes.c_int
     lib.sipg_abi_layout.argtypes = [ctypes.POINTER(i32), i32]
     lib.sipg_abi_layout.restype = ctypes.c_int
     lib.sipg_supported.argtypes = [i32, i32, i32]
@@ -163,6 +167,13 @@ class NativePlan:
     @property
     def kernels_per_apply(self) -> int:
         return int(self._lib.sipg_plan_kernels_per_apply(self.handle))
+
+    def stream_chunks(self) -> int:
+        """DoF chunks the host apply pipelines (0: not streamed)."""
+        return int(self._lib.sipg_plan_stream_chunks(self.handle))
+
+    def host_launches_per_apply(self) -> int:
+        return int(self._lib.sipg_plan_host_launches_per_apply(self.handle))
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:

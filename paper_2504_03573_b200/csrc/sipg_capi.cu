@@ -118,7 +118,131 @@ struct sipg_plan {
   double* x_stage = nullptr;
   double* y_stage = nullptr;
   int64_t launches = 0;
+  std::vector<int> per_sm;               // resident CTAs per SM of each class's kernel
+  int sms = 148;
+  // Streamed host apply (sipg_apply_host): x is copied H2D in K DoF chunks; chunk k's elements
+  // publish their planes/traces as soon as it lands, and the elements whose neighbourhood lies in
+  // chunks <= k ("stage k") compute right after; y chunks go back D2H as soon as their last stage
+  // is done.  The rows are sub-ranges of the class lists (classes are in ascending element order),
+  // so the kernels run unchanged on a second descriptor array.
+  struct Launch { int row, grid; const KernelEntry* k; const PlanesEntry* pe; };
+  bool streamed = false;
+  int n_chunks = 0;
+  std::vector<int64_t> chunk_dof;        // K + 1 dof boundaries
+  std::vector<std::vector<Launch>> pub, comp;
+  std::vector<int> d2h_stage;            // per chunk: the stage after which its y is complete
+  DevPlan dps{};
+  int32_t* cds_d = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_comp;
+  cudaEvent_t ev_start = nullptr;
 };
+
+namespace {
+
+int launch_grid(const KernelEntry* k, int count, int per_sm, int sms) {
+  if (k->kind == 0) return count;   // CTA per element
+  const int epc = (k->kind == 1 || k->kind == 5) ? k->threads / 32 : 1;   // warp-per-element kernels
+  const int g = (count + epc - 1) / epc;
+  return g < per_sm * sms ? g : per_sm * sms;
+}
+
+int publish_grid(const int32_t* cd, int count) {
+  const int per = cd[CD_SHAPE] == SHAPE_HEX ? 1 : 8;
+  const int g = (count + per - 1) / per;
+  return g < 148 * 8 ? g : 148 * 8;
+}
+
+// Build the streamed-apply schedule (see sipg_plan).  Returns false when the mesh ordering does not
+// allow it (a class whose element list is not monotone in stage) — the host apply then runs
+// copy -> apply -> copy.
+bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
+  const int64_t nel = d->n_elements, ndof = d->n_dofs;
+  const int64_t bytes = ndof * 8;
+  // chunks of >= 6 MB (~0.1 ms of PCIe each); SIPG_STREAM_CHUNK_BYTES overrides (tests use small meshes)
+  const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
+  const int64_t chunk_bytes = cb ? atoll(cb) : (6ll << 20);
+  int K = (int)(bytes / (chunk_bytes > 0 ? chunk_bytes : 1));
+  if (K > 64) K = 64;
+  if (K < 2) return false;
+  for (int c = 0; c < d->n_classes; ++c)
+    if (d->class_desc[c * CD_WORDS + CD_ROLE] != 0) return false;   // distributed local plans: no
+  std::vector<int32_t> chunk(nel), stage(nel);
+  p->chunk_dof.assign(K + 1, 0);
+  int64_t e = 0;
+  for (int k = 0; k < K; ++k) {
+    const int64_t target = ndof * (k + 1) / K;
+    const int64_t e0 = e;
+    while (e < nel && (d->dof_off[e + 1] <= target || k == K - 1)) chunk[e++] = k;
+    if (e == e0) return false;
+    p->chunk_dof[k + 1] = d->dof_off[e];
+  }
+  const FaceRec* recs = (const FaceRec*)d->face_records;
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD_WORDS;
+    const int nf = cd[CD_NFACES];
+    for (int i = 0; i < cd[CD_COUNT]; ++i) {
+      const int el = d->class_elems[cd[CD_ELEM_OFF] + i];
+      int st = chunk[el];
+      for (int f = 0; f < nf; ++f) {
+        const int nb = recs[(int64_t)cd[CD_REC_OFF] + (int64_t)i * nf + f].nbr;
+        if (nb >= 0 && chunk[nb] > st) st = chunk[nb];
+      }
+      // an element may run later than its neighbourhood allows: keep stages monotone along the
+      // class list so each stage is one contiguous sub-range of it
+      if (i > 0 && stage[d->class_elems[cd[CD_ELEM_OFF] + i - 1]] > st) st = stage[d->class_elems[cd[CD_ELEM_OFF] + i - 1]];
+      stage[el] = st;
+    }
+  }
+  // rows are appended after the original classes: kernels look neighbours' classes up by
+  // elem_class in the same descriptor array
+  std::vector<int32_t> rows(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD_WORDS);
+  p->pub.assign(K, {});
+  p->comp.assign(K, {});
+  p->d2h_stage.assign(K, 0);
+  for (int64_t el = 0; el < nel; ++el)
+    if (stage[el] > p->d2h_stage[chunk[el]]) p->d2h_stage[chunk[el]] = stage[el];
+  auto add_row = [&](const int32_t* cd, int i0, int i1) {
+    const int r = (int)(rows.size() / CD_WORDS);
+    rows.insert(rows.end(), cd, cd + CD_WORDS);
+    int32_t* w = rows.data() + (int64_t)r * CD_WORDS;
+    w[CD_COUNT] = i1 - i0;
+    w[CD_ELEM_OFF] += i0;
+    w[CD_REC_OFF] += i0 * cd[CD_NFACES];
+    w[CD_EGEO_OFF] += i0 * cd[CD_EGEO_STRIDE];
+    return r;
+  };
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD_WORDS;
+    const int n = cd[CD_COUNT];
+    const int32_t* el = d->class_elems + cd[CD_ELEM_OFF];
+    for (int pass = 0; pass < 2; ++pass) {   // 0: publisher rows by chunk, 1: compute rows by stage
+      if (pass == 0 && !p->planes_k[c]) continue;
+      const std::vector<int32_t>& key = pass == 0 ? chunk : stage;
+      int i0 = 0;
+      while (i0 < n) {
+        const int k = key[el[i0]];
+        int i1 = i0;
+        while (i1 < n && key[el[i1]] == k) ++i1;
+        for (int j = i1; j < n; ++j)
+          if (key[el[j]] <= k) return false;   // not monotone: no streaming
+        const int r = add_row(cd, i0, i1);
+        if (pass == 0)
+          p->pub[k].push_back({r, publish_grid(cd, i1 - i0), nullptr, p->planes_k[c]});
+        else
+          p->comp[k].push_back({r, launch_grid(p->kern[c], i1 - i0, p->per_sm[c], p->sms), p->kern[c], nullptr});
+        i0 = i1;
+      }
+    }
+  }
+  if (upload(rows.data(), (int64_t)rows.size(), &p->cds_d)) return false;
+  p->dps = p->dp;
+  p->dps.cd = p->cds_d;
+  p->n_chunks = K;
+  return true;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -261,18 +385,19 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   for (int c = 0; c < p->n_cls; ++c) {
     const KernelEntry* k = p->kern[c];
     const int count = p->cd_host[c * CD_WORDS + CD_COUNT];
-    int g = count;
+    int per_sm = 1;
     if (k->kind != 0) {
-      int per_sm = 0;
       cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k->fn, k->threads, k->smem);
       if (e != cudaSuccess || per_sm <= 0) {
         sipg_plan_destroy(p);
         return fail(SIPG_ERR_CUDA, "occupancy query failed for a persistent kernel");
       }
-      g = count < per_sm * sms ? count : per_sm * sms;
     }
-    p->grid.push_back(g);
+    p->per_sm.push_back(per_sm);
+    p->grid.push_back(launch_grid(k, count, p->per_sm.back(), sms));
   }
+  p->sms = sms;
+  p->streamed = !getenv("SIPG_NO_STREAM") && build_stream_schedule(p, d);
   *out = p;
   return 0;
 }
@@ -289,11 +414,7 @@ int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_d
       if (!p->planes_k[c] || count == 0) continue;
       const bool go = role < 0 || (role == 0 && crole != 2) || (role == 1 && crole == 2);
       if (!go) continue;
-      const bool hex = cd[CD_SHAPE] == SHAPE_HEX;
-      const int per = hex ? 1 : 8;
-      int g = (count + per - 1) / per;
-      if (g > 148 * 8) g = 148 * 8;
-      p->planes_k[c]->fn<<<g, hex ? 128 : 256, 0, s>>>(p->dp, c, x_dev);
+      p->planes_k[c]->fn<<<publish_grid(cd, count), cd[CD_SHAPE] == SHAPE_HEX ? 128 : 256, 0, s>>>(p->dp, c, x_dev);
       ++p->launches;
     }
   }
@@ -340,10 +461,55 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
     CK(cudaMalloc((void**)&p->x_stage, bytes));
     CK(cudaMalloc((void**)&p->y_stage, bytes));
   }
-  CK(cudaMemcpyAsync(p->x_stage, x_host, bytes, cudaMemcpyHostToDevice, s));
-  int rc = sipg_apply(p, p->x_stage, p->y_stage, stream);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(y_host, p->y_stage, bytes, cudaMemcpyDeviceToHost, s));
+  if (!p->streamed) {
+    CK(cudaMemcpyAsync(p->x_stage, x_host, bytes, cudaMemcpyHostToDevice, s));
+    int rc = sipg_apply(p, p->x_stage, p->y_stage, stream);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(y_host, p->y_stage, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+  }
+  const int K = p->n_chunks;
+  if (!p->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+    p->ev_h2d.resize(K);
+    p->ev_comp.resize(K);
+    for (int k = 0; k < K; ++k) {
+      CK(cudaEventCreateWithFlags(&p->ev_h2d[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&p->ev_comp[k], cudaEventDisableTiming));
+    }
+  }
+  // order after whatever the caller queued on `s` (and the previous apply's readers of the stage buffers)
+  CK(cudaEventRecord(p->ev_start, s));
+  CK(cudaStreamWaitEvent(p->s_h2d, p->ev_start, 0));
+  CK(cudaStreamWaitEvent(p->s_d2h, p->ev_start, 0));
+  for (int k = 0; k < K; ++k) {
+    const int64_t a = p->chunk_dof[k], b = p->chunk_dof[k + 1];
+    CK(cudaMemcpyAsync(p->x_stage + a, x_host + a, sizeof(double) * (b - a), cudaMemcpyHostToDevice, p->s_h2d));
+    CK(cudaEventRecord(p->ev_h2d[k], p->s_h2d));
+  }
+  for (int k = 0; k < K; ++k) {
+    CK(cudaStreamWaitEvent(s, p->ev_h2d[k], 0));
+    for (const auto& L : p->pub[k]) {
+      L.pe->fn<<<L.grid, p->dps.dim == 3 ? 128 : 256, 0, s>>>(p->dps, L.row, p->x_stage);
+      ++p->launches;
+    }
+    for (const auto& L : p->comp[k]) {
+      L.k->fn<<<L.grid, L.k->threads, L.k->smem, s>>>(p->dps, L.row, p->x_stage, p->y_stage);
+      ++p->launches;
+    }
+    CK(cudaEventRecord(p->ev_comp[k], s));
+    for (int j = 0; j < K; ++j) {
+      if (p->d2h_stage[j] != k) continue;
+      const int64_t a = p->chunk_dof[j], b = p->chunk_dof[j + 1];
+      CK(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[k], 0));
+      CK(cudaMemcpyAsync(y_host + a, p->y_stage + a, sizeof(double) * (b - a), cudaMemcpyDeviceToHost, p->s_d2h));
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(p->s_d2h));
   CK(cudaStreamSynchronize(s));
   return 0;
 }
@@ -360,12 +526,28 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   return k;
 }
 
+int sipg_plan_stream_chunks(const sipg_plan* p) { return p && p->streamed ? p->n_chunks : 0; }
+
+int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
+  if (!p) return -1;
+  if (!p->streamed) return sipg_plan_kernels_per_apply(p);
+  int k = 0;
+  for (int i = 0; i < p->n_chunks; ++i) k += (int)(p->pub[i].size() + p->comp[i].size());
+  return k;
+}
+
 int sipg_plan_destroy(sipg_plan* p) {
   if (!p) return 0;
   for (void* b : p->bufs)
     if (b) cudaFree(b);
   if (p->planes) cudaFree(p->planes);
   if (p->x_stage) cudaFree(p->x_stage);
+  if (p->cds_d) cudaFree(p->cds_d);
+  if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+  for (cudaEvent_t e : p->ev_h2d) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_comp) cudaEventDestroy(e);
+  if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->y_stage) cudaFree(p->y_stage);
   delete p;
   return 0;
