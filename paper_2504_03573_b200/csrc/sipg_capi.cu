@@ -140,6 +140,12 @@ struct sipg_plan {
 
 namespace {
 
+__global__ void k_stamp(unsigned long long* buf, int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  buf[i] = t;
+}
+
 int launch_grid(const KernelEntry* k, int count, int per_sm, int sms) {
   if (k->kind == 0) return count;   // CTA per element
   const int epc = (k->kind == 1 || k->kind == 5) ? k->threads / 32 : 1;   // warp-per-element kernels
@@ -159,23 +165,35 @@ int publish_grid(const int32_t* cd, int count) {
 bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
   const int64_t nel = d->n_elements, ndof = d->n_dofs;
   const int64_t bytes = ndof * 8;
-  // chunks of >= 6 MB (~0.1 ms of PCIe each); SIPG_STREAM_CHUNK_BYTES overrides (tests use small meshes)
+  // chunk size: >= 8 MB (~0.16 ms of PCIe), and >= 1.5 MB per launch a stage issues (per-class
+  // stage launches get short and tail-bound on multi-class meshes; measured on cfg3a / cfg3b);
+  // SIPG_STREAM_CHUNK_BYTES overrides (tests use small meshes)
+  int launches_per_stage = 0;
+  for (int c = 0; c < d->n_classes; ++c)
+    if (d->class_desc[c * CD_WORDS + CD_COUNT] > 0) launches_per_stage += p->planes_k[c] ? 2 : 1;
+  int64_t chunk_bytes = (int64_t)launches_per_stage * (3ll << 19);
+  if (chunk_bytes < (8ll << 20)) chunk_bytes = 8ll << 20;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
-  const int64_t chunk_bytes = cb ? atoll(cb) : (6ll << 20);
+  if (cb) chunk_bytes = atoll(cb);
   int K = (int)(bytes / (chunk_bytes > 0 ? chunk_bytes : 1));
   if (K > 64) K = 64;
   if (K < 2) return false;
   for (int c = 0; c < d->n_classes; ++c)
     if (d->class_desc[c * CD_WORDS + CD_ROLE] != 0) return false;   // distributed local plans: no
   std::vector<int32_t> chunk(nel), stage(nel);
+  // copy chunks: 4 KB-aligned DoF ranges (DMA runs markedly slower on unaligned host ranges when
+  // both directions are busy); an element belongs to the chunk in which its last DoF arrives
   p->chunk_dof.assign(K + 1, 0);
-  int64_t e = 0;
-  for (int k = 0; k < K; ++k) {
-    const int64_t target = ndof * (k + 1) / K;
-    const int64_t e0 = e;
-    while (e < nel && (d->dof_off[e + 1] <= target || k == K - 1)) chunk[e++] = k;
-    if (e == e0) return false;
-    p->chunk_dof[k + 1] = d->dof_off[e];
+  for (int k = 1; k < K; ++k) p->chunk_dof[k] = (ndof * k / K) & ~(int64_t)511;
+  p->chunk_dof[K] = ndof;
+  for (int k = 0; k < K; ++k)
+    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return false;
+  {
+    int k = 0;
+    for (int64_t e = 0; e < nel; ++e) {
+      while (d->dof_off[e + 1] > p->chunk_dof[k + 1]) ++k;
+      chunk[e] = k;
+    }
   }
   const FaceRec* recs = (const FaceRec*)d->face_records;
   for (int c = 0; c < d->n_classes; ++c) {
@@ -200,8 +218,14 @@ bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
   p->pub.assign(K, {});
   p->comp.assign(K, {});
   p->d2h_stage.assign(K, 0);
-  for (int64_t el = 0; el < nel; ++el)
-    if (stage[el] > p->d2h_stage[chunk[el]]) p->d2h_stage[chunk[el]] = stage[el];
+  {   // y range j is complete once every element overlapping it has run
+    int j = 0;
+    for (int64_t el = 0; el < nel; ++el) {
+      while (d->dof_off[el] >= p->chunk_dof[j + 1]) ++j;
+      for (int jj = j; jj < K && p->chunk_dof[jj] < d->dof_off[el + 1]; ++jj)
+        if (stage[el] > p->d2h_stage[jj]) p->d2h_stage[jj] = stage[el];
+    }
+  }
   auto add_row = [&](const int32_t* cd, int i0, int i1) {
     const int r = (int)(rows.size() / CD_WORDS);
     rows.insert(rows.end(), cd, cd + CD_WORDS);
@@ -481,7 +505,18 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
       CK(cudaEventCreateWithFlags(&p->ev_comp[k], cudaEventDisableTiming));
     }
   }
+  // SIPG_STREAM_TRACE (instrumentation): timestamps of every chunk copy / stage, printed to stderr
+  const bool trace = getenv("SIPG_STREAM_TRACE") != nullptr;
+  static unsigned long long* tbuf = nullptr;
+  if (trace && !tbuf) cudaMalloc((void**)&tbuf, sizeof(unsigned long long) * 1024);
+  int nmark = 0;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace || nmark >= 1024) return;
+    k_stamp<<<1, 1, 0, st>>>(tbuf, nmark++);
+  };
+  std::vector<char> tkind;
   // order after whatever the caller queued on `s` (and the previous apply's readers of the stage buffers)
+  mark(s); tkind.push_back('S');
   CK(cudaEventRecord(p->ev_start, s));
   CK(cudaStreamWaitEvent(p->s_h2d, p->ev_start, 0));
   CK(cudaStreamWaitEvent(p->s_d2h, p->ev_start, 0));
@@ -489,28 +524,42 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
     const int64_t a = p->chunk_dof[k], b = p->chunk_dof[k + 1];
     CK(cudaMemcpyAsync(p->x_stage + a, x_host + a, sizeof(double) * (b - a), cudaMemcpyHostToDevice, p->s_h2d));
     CK(cudaEventRecord(p->ev_h2d[k], p->s_h2d));
+    mark(p->s_h2d); tkind.push_back('H');
   }
   for (int k = 0; k < K; ++k) {
     CK(cudaStreamWaitEvent(s, p->ev_h2d[k], 0));
+    const bool skip = getenv("SIPG_STREAM_NOCOMPUTE") != nullptr;   // instrumentation: copies only
     for (const auto& L : p->pub[k]) {
+      if (skip) break;
       L.pe->fn<<<L.grid, p->dps.dim == 3 ? 128 : 256, 0, s>>>(p->dps, L.row, p->x_stage);
       ++p->launches;
     }
     for (const auto& L : p->comp[k]) {
+      if (skip) break;
       L.k->fn<<<L.grid, L.k->threads, L.k->smem, s>>>(p->dps, L.row, p->x_stage, p->y_stage);
       ++p->launches;
     }
     CK(cudaEventRecord(p->ev_comp[k], s));
+    mark(s); tkind.push_back('C');
     for (int j = 0; j < K; ++j) {
       if (p->d2h_stage[j] != k) continue;
       const int64_t a = p->chunk_dof[j], b = p->chunk_dof[j + 1];
-      CK(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[k], 0));
+      // SIPG_STREAM_DIAG=1 (instrumentation, wrong results): D2H gated on the copies only
+      static const bool diag = getenv("SIPG_STREAM_DIAG") != nullptr;
+      CK(cudaStreamWaitEvent(p->s_d2h, diag ? p->ev_h2d[k] : p->ev_comp[k], 0));
       CK(cudaMemcpyAsync(y_host + a, p->y_stage + a, sizeof(double) * (b - a), cudaMemcpyDeviceToHost, p->s_d2h));
+      mark(p->s_d2h); tkind.push_back('D');
     }
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(p->s_d2h));
   CK(cudaStreamSynchronize(s));
+  if (trace) {
+    std::vector<unsigned long long> t(nmark);
+    cudaMemcpy(t.data(), tbuf, sizeof(unsigned long long) * nmark, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < nmark; ++i) fprintf(stderr, "%c%.3f ", tkind[i], (double)(t[i] - t[0]) * 1e-6);
+    fprintf(stderr, "\n");
+  }
   return 0;
 }
 

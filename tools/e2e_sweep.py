@@ -18,7 +18,7 @@ n = pb.n_dofs
 xp = torch.from_numpy(case.draw_x(n)).pin_memory()
 yp = torch.empty(n, dtype=torch.float64).pin_memory()
 s = torch.cuda.current_stream()
-for cb in ["none", str(2 << 20), str(4 << 20), str(6 << 20), str(12 << 20), str(24 << 20)]:
+for cb in ["none", str(2 << 20), str(3 << 20), str(4 << 20), str(6 << 20), str(8 << 20), str(12 << 20)]:
     if cb == "none":
         os.environ["SIPG_NO_STREAM"] = "1"
     else:
