@@ -14,7 +14,8 @@ import numpy as np
 
 from . import layout as L
 
-LIB_PATH = Path(__file__).resolve().parent / "libsipg.so"
+LIB_PATH = Path(os.environ.get("SIPG_LIB_PATH", "")) if os.environ.get("SIPG_LIB_PATH") else \
+    Path(__file__).resolve().parent / "libsipg.so"   # SIPG_LIB_PATH: instrumentation builds
 
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",

@@ -29,14 +29,16 @@ def _stale(obj: Path, deps) -> bool:
     return not obj.exists() or any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 
-def build_native(force: bool = False, verbose: bool = True, extra_flags=()) -> Path:
+def build_native(force: bool = False, verbose: bool = True, extra_flags=(), out: Path = OUT,
+                 build_dir: Path = BUILD) -> Path:
     nv = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    OUT_, BUILD_ = Path(out), Path(build_dir)
+    BUILD_.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "sipg.h"]
     objs, jobs = [], []
     for src in SOURCES:
         s = CSRC / src
-        o = BUILD / (Path(src).stem + ".o")
+        o = BUILD_ / (Path(src).stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             jobs.append([nv, *ARCH, *FLAGS, *extra_flags, "-c", str(s), "-o", str(o)])
@@ -47,15 +49,20 @@ def build_native(force: bool = False, verbose: bool = True, extra_flags=()) -> P
                     raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
                 if verbose:
                     print("built", cmd[-1])
-    if force or jobs or _stale(OUT, objs):
-        cmd = [nv, *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-lcudart"]
+    if force or jobs or _stale(OUT_, objs):
+        cmd = [nv, *ARCH, "-shared", "-o", str(OUT_), *map(str, objs), "-lcudart"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {res.stdout}\n{res.stderr}")
         if verbose:
-            print("linked", OUT)
-    return OUT
+            print("linked", OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":
-    build_native()
+    import sys
+    if len(sys.argv) > 2:   # instrumentation variant: build.py OUT.so -DFLAG ...
+        o = Path(sys.argv[1])
+        build_native(extra_flags=sys.argv[2:], out=o, build_dir=o.parent / (o.stem + "_build"))
+    else:
+        build_native()

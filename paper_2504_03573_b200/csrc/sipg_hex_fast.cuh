@@ -26,6 +26,141 @@ template <int N, int Q> __constant__ double hxD[Q * Q];     // collocation deriv
 template <int N, int Q> __constant__ double hxW[Q];         // GLL weights
 template <int N, int Q> __constant__ double hxDVE[2 * N];   // psi_i'(-1), psi_i'(+1)
 
+// Even-odd (parity) factorisation of the 1-D operators.  On symmetric GLL points
+// x_{Q-1-p} = -x_p the modified-modal modes satisfy psi_0(-x) = psi_{N-1}(x) and
+// psi_c(-x) = (-1)^(c-1) psi_c(x) (bubbles), and the collocation derivative
+// D[Q-1-p][Q-1-m] = -D[p][m]; every contraction splits into an even and an odd
+// half of about a quarter of the size each (half the FMAs).  Tables (built and
+// checked on the host by hex_fast_upload):
+//   VE[p][a], p < H:  a = 0: (psi_0 + psi_{N-1})/2 (= 1/2), a >= 1: psi_{2a-1}
+//   VO[p][b], p < QH: b = 0: (psi_0 - psi_{N-1})/2,        b >= 1: psi_{2b}
+//   DP[p][m] = (D[p][m] + D[p][Q-1-m]) / 2, p < QH, m < H
+//   DM[p][m] = (D[p][m] - D[p][Q-1-m]) / 2, p < H,  m < QH
+template <int N, int Q> struct EO {
+  static constexpr int H = (Q + 1) / 2, QH = Q / 2, NE = 1 + (N - 1) / 2, NO = 1 + (N - 2) / 2;
+};
+template <int N, int Q> __constant__ double eoVE[EO<N, Q>::H * EO<N, Q>::NE];
+template <int N, int Q> __constant__ double eoVO[EO<N, Q>::QH * EO<N, Q>::NO];
+template <int N, int Q> __constant__ double eoDP[EO<N, Q>::QH * EO<N, Q>::H];
+template <int N, int Q> __constant__ double eoDM[EO<N, Q>::H * EO<N, Q>::QH];
+
+// u[p] = sum_c V[p][c] v[c]
+template <int N, int Q>
+__device__ __forceinline__ void eo_fwdV(const double (&v)[N], double (&u)[Q]) {
+  using E = EO<N, Q>;
+  double ve[E::NE], vo[E::NO];
+  ve[0] = v[0] + v[N - 1];
+  vo[0] = v[0] - v[N - 1];
+#pragma unroll
+  for (int a = 1; a < E::NE; ++a) ve[a] = v[2 * a - 1];
+#pragma unroll
+  for (int b = 1; b < E::NO; ++b) vo[b] = v[2 * b];
+#pragma unroll
+  for (int p = 0; p < E::H; ++p) {
+    double e = 0.0, o = 0.0;
+#pragma unroll
+    for (int a = 0; a < E::NE; ++a) e = fma(eoVE<N, Q>[p * E::NE + a], ve[a], e);
+    if (p < E::QH) {
+#pragma unroll
+      for (int b = 0; b < E::NO; ++b) o = fma(eoVO<N, Q>[p * E::NO + b], vo[b], o);
+      u[p] = e + o;
+      u[Q - 1 - p] = e - o;
+    } else {
+      u[p] = e;   // middle point (odd Q)
+    }
+  }
+}
+
+// o[c] = sum_p V[p][c] u[p]
+template <int N, int Q>
+__device__ __forceinline__ void eo_bwdV(const double (&u)[Q], double (&o)[N]) {
+  using E = EO<N, Q>;
+  double sp[E::H], sm[E::QH];
+#pragma unroll
+  for (int p = 0; p < E::QH; ++p) {
+    sp[p] = u[p] + u[Q - 1 - p];
+    sm[p] = u[p] - u[Q - 1 - p];
+  }
+  if (Q & 1) sp[E::H - 1] = u[E::QH];
+  double oe[E::NE], oo[E::NO];
+#pragma unroll
+  for (int a = 0; a < E::NE; ++a) {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p < E::H; ++p) acc = fma(eoVE<N, Q>[p * E::NE + a], sp[p], acc);
+    oe[a] = acc;
+  }
+#pragma unroll
+  for (int b = 0; b < E::NO; ++b) {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p < E::QH; ++p) acc = fma(eoVO<N, Q>[p * E::NO + b], sm[p], acc);
+    oo[b] = acc;
+  }
+  o[0] = oe[0] + oo[0];
+  o[N - 1] = oe[0] - oo[0];
+#pragma unroll
+  for (int a = 1; a < E::NE; ++a) o[2 * a - 1] = oe[a];
+#pragma unroll
+  for (int b = 1; b < E::NO; ++b) o[2 * b] = oo[b];
+}
+
+// d[p] = sum_m D[p][m] u[m]
+template <int N, int Q>
+__device__ __forceinline__ void eo_fwdD(const double (&u)[Q], double (&d)[Q]) {
+  using E = EO<N, Q>;
+  double sp[E::H], sm[E::QH];
+#pragma unroll
+  for (int m = 0; m < E::QH; ++m) {
+    sp[m] = u[m] + u[Q - 1 - m];
+    sm[m] = u[m] - u[Q - 1 - m];
+  }
+  if (Q & 1) sp[E::H - 1] = u[E::QH];
+#pragma unroll
+  for (int p = 0; p < E::H; ++p) {
+    double o = 0.0;
+#pragma unroll
+    for (int m = 0; m < E::QH; ++m) o = fma(eoDM<N, Q>[p * E::QH + m], sm[m], o);
+    if (p < E::QH) {
+      double e = 0.0;
+#pragma unroll
+      for (int m = 0; m < E::H; ++m) e = fma(eoDP<N, Q>[p * E::H + m], sp[m], e);
+      d[p] = e + o;
+      d[Q - 1 - p] = o - e;
+    } else {
+      d[p] = o;
+    }
+  }
+}
+
+// r[m] = sum_p D[p][m] g[p]
+template <int N, int Q>
+__device__ __forceinline__ void eo_trD(const double (&g)[Q], double (&r)[Q]) {
+  using E = EO<N, Q>;
+  double gp[E::H], gm[E::QH];
+#pragma unroll
+  for (int p = 0; p < E::QH; ++p) {
+    gp[p] = g[p] + g[Q - 1 - p];
+    gm[p] = g[p] - g[Q - 1 - p];
+  }
+  if (Q & 1) gp[E::H - 1] = g[E::QH];
+#pragma unroll
+  for (int m = 0; m < E::H; ++m) {
+    double yv = 0.0;
+#pragma unroll
+    for (int p = 0; p < E::QH; ++p) yv = fma(eoDP<N, Q>[p * E::H + m], gm[p], yv);
+    if (m < E::QH) {
+      double xv = 0.0;
+#pragma unroll
+      for (int p = 0; p < E::H; ++p) xv = fma(eoDM<N, Q>[p * E::QH + m], gp[p], xv);
+      r[m] = xv + yv;
+      r[Q - 1 - m] = yv - xv;
+    } else {
+      r[m] = yv;
+    }
+  }
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -175,6 +310,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   if (t < 6) {
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
+    if (!GEN && (P.debug & 2)) sk[t] = 0;   // instrumentation (SIPG_DEBUG=2): no face work, wrong result
   }
   if (t >= NT - 6) {      // neighbour blocks, one per thread: the last 6 threads (NT >= 9),
                           // never thread 0 (which issues the next-element prefetch)
@@ -198,12 +334,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[N], o[Q];
 #pragma unroll
     for (int c = 0; c < N; ++c) v[c] = C[(ta * N + tb) * N + c];
-#pragma unroll
-    for (int k = 0; k < Q; ++k) o[k] = 0.0;
-#pragma unroll
-    for (int c = 0; c < N; ++c)
-#pragma unroll
-      for (int k = 0; k < Q; ++k) o[k] = fma(hxV<N, Q>[k * N + c], v[c], o[k]);
+    eo_fwdV<N, Q>(v, o);
 #pragma unroll
     for (int k = 0; k < Q; ++k) B1[ta * SI + tb * SJ + k] = o[k];
   }
@@ -212,12 +343,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[N], o[Q];
 #pragma unroll
     for (int b = 0; b < N; ++b) v[b] = B1[ta * SI + b * SJ + tb];
-#pragma unroll
-    for (int j = 0; j < Q; ++j) o[j] = 0.0;
-#pragma unroll
-    for (int b = 0; b < N; ++b)
-#pragma unroll
-      for (int j = 0; j < Q; ++j) o[j] = fma(hxV<N, Q>[j * N + b], v[b], o[j]);
+    eo_fwdV<N, Q>(v, o);
 #pragma unroll
     for (int j = 0; j < Q; ++j) B2[ta * SI + j * SJ + tb] = o[j];
   }
@@ -227,23 +353,12 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) v[a] = B2[a * SI + ta * SJ + tb];
-#pragma unroll
-    for (int i = 0; i < Q; ++i) u[i] = 0.0;
-#pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-      for (int i = 0; i < Q; ++i) u[i] = fma(hxV<N, Q>[i * N + a], v[a], u[i]);
+    eo_fwdV<N, Q>(v, u);
   }
   // ---- PhysDeriv: axis 0 in registers; axes 1, 2 through shared memory
 #pragma unroll
-  for (int i = 0; i < Q; ++i) {
-    d0[i] = 0.0;
-    B0[i * SI + ta * SJ + tb] = u[i];
-  }
-#pragma unroll
-  for (int m = 0; m < Q; ++m)
-#pragma unroll
-    for (int i = 0; i < Q; ++i) d0[i] = fma(hxD<N, Q>[i * Q + m], u[m], d0[i]);
+  for (int i = 0; i < Q; ++i) B0[i * SI + ta * SJ + tb] = u[i];
+  eo_fwdD<N, Q>(u, d0);
   __syncthreads();
   {
     double v[Q], w[Q];
@@ -252,18 +367,8 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       v[m] = B0[ta * SI + m * SJ + tb];     // line along axis 1: thread (i=ta, k=tb)
       w[m] = B0[ta * SI + tb * SJ + m];     // line along axis 2: thread (i=ta, j=tb)
     }
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-      d1[r] = 0.0;
-      d2[r] = 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < Q; ++m)
-#pragma unroll
-      for (int r = 0; r < Q; ++r) {
-        d1[r] = fma(hxD<N, Q>[r * Q + m], v[m], d1[r]);
-        d2[r] = fma(hxD<N, Q>[r * Q + m], w[m], d2[r]);
-      }
+    eo_fwdD<N, Q>(v, d1);
+    eo_fwdD<N, Q>(w, d2);
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
       B1[ta * SI + r * SJ + tb] = d1[r];
@@ -308,12 +413,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[N], o[Q];
 #pragma unroll
     for (int i0 = 0; i0 < N; ++i0) v[i0] = NP[fp * N * N + i0 * N + i1];
-#pragma unroll
-    for (int p0 = 0; p0 < Q; ++p0) o[p0] = 0.0;
-#pragma unroll
-    for (int i0 = 0; i0 < N; ++i0)
-#pragma unroll
-      for (int p0 = 0; p0 < Q; ++p0) o[p0] = fma(hxV<N, Q>[p0 * N + i0], v[i0], o[p0]);
+    eo_fwdV<N, Q>(v, o);
 #pragma unroll
     for (int p0 = 0; p0 < Q; ++p0) T1[fp * Q * N + p0 * N + i1] = o[p0];
   }
@@ -324,12 +424,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[N], o[Q];
 #pragma unroll
     for (int i1 = 0; i1 < N; ++i1) v[i1] = T1[fp * Q * N + p0 * N + i1];
-#pragma unroll
-    for (int p1 = 0; p1 < Q; ++p1) o[p1] = 0.0;
-#pragma unroll
-    for (int i1 = 0; i1 < N; ++i1)
-#pragma unroll
-      for (int p1 = 0; p1 < Q; ++p1) o[p1] = fma(hxV<N, Q>[p1 * N + i1], v[i1], o[p1]);
+    eo_fwdV<N, Q>(v, o);
 #pragma unroll
     for (int p1 = 0; p1 < Q; ++p1) U2[fp * QQ + p0 * Q + p1] = o[p1];
   }
@@ -487,10 +582,12 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     B1[i * SI + ta * SJ + tb] = d1[i];
     B2[i * SI + ta * SJ + tb] = d2[i];
   }
+  {
+    double r[Q];
+    eo_trD<N, Q>(d0, r);
 #pragma unroll
-  for (int m = 0; m < Q; ++m)
-#pragma unroll
-    for (int i = 0; i < Q; ++i) u[i] = fma(hxD<N, Q>[m * Q + i], d0[m], u[i]);
+    for (int i = 0; i < Q; ++i) u[i] += r[i];
+  }
   __syncthreads();
   {
     double v[Q], w[Q];
@@ -499,18 +596,8 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       v[m] = B1[ta * SI + m * SJ + tb];   // (i=ta, ., k=tb)
       w[m] = B2[ta * SI + tb * SJ + m];   // (i=ta, j=tb, .)
     }
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-      d1[r] = 0.0;
-      d2[r] = 0.0;
-    }
-#pragma unroll
-    for (int m = 0; m < Q; ++m)
-#pragma unroll
-      for (int r = 0; r < Q; ++r) {
-        d1[r] = fma(hxD<N, Q>[m * Q + r], v[m], d1[r]);
-        d2[r] = fma(hxD<N, Q>[m * Q + r], w[m], d2[r]);
-      }
+    eo_trD<N, Q>(v, d1);
+    eo_trD<N, Q>(w, d2);
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
       B1[ta * SI + r * SJ + tb] = d1[r];
@@ -523,12 +610,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   for (int i = 0; i < Q; ++i) u[i] += B1[i * SI + ta * SJ + tb] + B2[i * SI + ta * SJ + tb];
   {
     double o[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) o[a] = 0.0;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-#pragma unroll
-      for (int a = 0; a < N; ++a) o[a] = fma(hxV<N, Q>[i * N + a], u[i], o[a]);
+    eo_bwdV<N, Q>(u, o);
 #pragma unroll
     for (int a = 0; a < N; ++a) B0[a * SI + ta * SJ + tb] = o[a];
   }
@@ -537,12 +619,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[Q], o[N];
 #pragma unroll
     for (int j = 0; j < Q; ++j) v[j] = B0[ta * SI + j * SJ + tb];
-#pragma unroll
-    for (int b = 0; b < N; ++b) o[b] = 0.0;
-#pragma unroll
-    for (int j = 0; j < Q; ++j)
-#pragma unroll
-      for (int b = 0; b < N; ++b) o[b] = fma(hxV<N, Q>[j * N + b], v[j], o[b]);
+    eo_bwdV<N, Q>(v, o);
 #pragma unroll
     for (int b = 0; b < N; ++b) B1[ta * SI + b * SJ + tb] = o[b];
   }
@@ -551,12 +628,7 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[Q], o[N];
 #pragma unroll
     for (int k = 0; k < Q; ++k) v[k] = B1[ta * SI + tb * SJ + k];
-#pragma unroll
-    for (int c = 0; c < N; ++c) o[c] = 0.0;
-#pragma unroll
-    for (int k = 0; k < Q; ++k)
-#pragma unroll
-      for (int c = 0; c < N; ++c) o[c] = fma(hxV<N, Q>[k * N + c], v[k], o[c]);
+    eo_bwdV<N, Q>(v, o);
     double* ye = y + dof0 + (ta * N + tb) * N;
 #pragma unroll
     for (int c = 0; c < N; ++c) ye[c] = o[c];
@@ -567,9 +639,83 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 }
 
 // Upload the constant tables of one (N, Q) instantiation (from the plan's pool).
+// The even-odd tables are derived here and checked by reassembling V and D from
+// them (the parity symmetry holds for modified-modal modes on GLL points).
 template <int N, int Q>
 cudaError_t hex_fast_upload(const double* V, const double* D, const double* W, const double* dVend) {
+  using E = EO<N, Q>;
+  double ve[E::H * E::NE], vo[E::QH * E::NO], dp[E::QH * E::H], dm[E::H * E::QH];
+  for (int p = 0; p < E::H; ++p) {
+    ve[p * E::NE] = 0.5 * (V[p * N] + V[p * N + N - 1]);
+    for (int a = 1; a < E::NE; ++a) ve[p * E::NE + a] = V[p * N + 2 * a - 1];
+  }
+  for (int p = 0; p < E::QH; ++p) {
+    vo[p * E::NO] = 0.5 * (V[p * N] - V[p * N + N - 1]);
+    for (int b = 1; b < E::NO; ++b) vo[p * E::NO + b] = V[p * N + 2 * b];
+  }
+  for (int p = 0; p < E::QH; ++p)
+    for (int m = 0; m < E::H; ++m) dp[p * E::H + m] = 0.5 * (D[p * Q + m] + D[p * Q + Q - 1 - m]);
+  for (int p = 0; p < E::H; ++p)
+    for (int m = 0; m < E::QH; ++m) dm[p * E::QH + m] = 0.5 * (D[p * Q + m] - D[p * Q + Q - 1 - m]);
+  // check: apply the even-odd forms (same formulas as eo_fwdV / eo_fwdD / eo_bwdV / eo_trD)
+  // to unit vectors and compare with V, D, V^T, D^T
+  double vmax = 0.0, dmax = 0.0, verr = 0.0, derr = 0.0;
+  for (int c = 0; c < N; ++c) {             // column c of V; row c of V^T
+    double v[N] = {}, u[Q];
+    v[c] = 1.0;
+    double vev[E::NE], vov[E::NO];
+    vev[0] = v[0] + v[N - 1];
+    vov[0] = v[0] - v[N - 1];
+    for (int a = 1; a < E::NE; ++a) vev[a] = v[2 * a - 1];
+    for (int b = 1; b < E::NO; ++b) vov[b] = v[2 * b];
+    for (int p = 0; p < E::H; ++p) {
+      double ev = 0.0, ov = 0.0;
+      for (int a = 0; a < E::NE; ++a) ev += ve[p * E::NE + a] * vev[a];
+      if (p < E::QH) {
+        for (int b = 0; b < E::NO; ++b) ov += vo[p * E::NO + b] * vov[b];
+        u[p] = ev + ov;
+        u[Q - 1 - p] = ev - ov;
+      } else {
+        u[p] = ev;
+      }
+    }
+    for (int p = 0; p < Q; ++p) {
+      vmax = fmax(vmax, fabs(V[p * N + c]));
+      verr = fmax(verr, fabs(u[p] - V[p * N + c]));
+    }
+  }
+  for (int m = 0; m < Q; ++m) {             // column m of D
+    double u[Q] = {}, d[Q], sp[E::H], sm[E::QH > 0 ? E::QH : 1];
+    u[m] = 1.0;
+    for (int k = 0; k < E::QH; ++k) {
+      sp[k] = u[k] + u[Q - 1 - k];
+      sm[k] = u[k] - u[Q - 1 - k];
+    }
+    if (Q & 1) sp[E::H - 1] = u[E::QH];
+    for (int p = 0; p < E::H; ++p) {
+      double ov = 0.0;
+      for (int k = 0; k < E::QH; ++k) ov += dm[p * E::QH + k] * sm[k];
+      if (p < E::QH) {
+        double ev = 0.0;
+        for (int k = 0; k < E::H; ++k) ev += dp[p * E::H + k] * sp[k];
+        d[p] = ev + ov;
+        d[Q - 1 - p] = ov - ev;
+      } else {
+        d[p] = ov;
+      }
+    }
+    for (int p = 0; p < Q; ++p) {
+      dmax = fmax(dmax, fabs(D[p * Q + m]));
+      derr = fmax(derr, fabs(d[p] - D[p * Q + m]));
+    }
+  }
+  if (verr > 1e-13 * (vmax > 1.0 ? vmax : 1.0) || derr > 1e-12 * (dmax > 1.0 ? dmax : 1.0))
+    return cudaErrorInvalidValue;   // tables lack the parity symmetry: not a GLL / modified-modal class
   cudaError_t e;
+  if ((e = cudaMemcpyToSymbol(eoVE<N, Q>, ve, sizeof(ve))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(eoVO<N, Q>, vo, sizeof(vo))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(eoDP<N, Q>, dp, sizeof(dp))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(eoDM<N, Q>, dm, sizeof(dm))) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(hxV<N, Q>, V, sizeof(double) * Q * N)) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(hxD<N, Q>, D, sizeof(double) * Q * Q)) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(hxW<N, Q>, W, sizeof(double) * Q)) != cudaSuccess) return e;
