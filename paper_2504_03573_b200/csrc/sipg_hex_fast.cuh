@@ -223,18 +223,21 @@ struct HexFast {
   static constexpr int BLK = (N3 + 2 + 1) & ~1;    // one coefficient block (+ alignment slack), even
   // neighbour region: 6 coefficient blocks; later stage-1 output + face flux buffers
   static constexpr int NBR = 6 * BLK > 12 * Q * N + 16 * Q * Q ? 6 * BLK : 12 * Q * N + 16 * Q * Q;
-  // scratch: 3 padded Q^3 buffers; later planes (12 N^2) + stage-2 output (12 Q^2)
-  static constexpr int SCR0 = 3 * BUF > 12 * N * N + 12 * Q * Q ? 3 * BUF : 12 * N * N + 12 * Q * Q;
+  // scratch: 2 padded Q^3 buffers; later the neighbour planes (12 N^2), then (overlaid) the
+  // stage-2 traces (12 Q^2).  Kept small so that 7 CTAs fit per SM (Q = 8: 30 KB per CTA).
+  static constexpr int SF = 12 * N * N > 12 * Q * Q ? 12 * N * N : 12 * Q * Q;
+  static constexpr int SCR0 = 2 * BUF > SF ? 2 * BUF : SF;
   static constexpr int SCR = (SCR0 + 1) & ~1;
   // generic-face scratch (dynamic smem): us (4 FP), fscr, fb (6*4*Q*Q)
   static constexpr int FP = QMAX * QMAX;
   static constexpr int GFB = 4 * FP + 16 * FP + 4 * QMAX * QMAX + 2 * NMAX * NMAX + 3 * QMAX * NMAX;
   static constexpr int GSZ = GFB + 6 * 4 * Q * Q;
   // dynamic shared memory (doubles, 16-byte aligned regions):
-  //   REC[2] (6 records = 96 doubles each) | CO[2] own coefficients | NB | S | generic scratch
+  //   REC[2] (6 records = 96 doubles each) | CO own coefficients | NB | S | generic scratch
+  // (the next element's coefficients land in CO as soon as BwdTrans has consumed the current ones)
   static constexpr int O_REC = 0;
   static constexpr int O_CO = 2 * 96;
-  static constexpr int O_NB = O_CO + 2 * BLK;
+  static constexpr int O_NB = O_CO + BLK;
   static constexpr int O_S = O_NB + NBR;
   static constexpr int O_G = O_S + SCR;
   static size_t smem_bytes(bool gen) { return sizeof(double) * (size_t)(O_G + (gen ? GSZ : 0)); }
@@ -249,7 +252,7 @@ __device__ __forceinline__ int hex_stride(int axis, int n) { return axis == 0 ? 
 // 6 resident CTAs per SM for Q <= 8 (caps registers at 168: measured 498 us vs
 // 545 us unconstrained and 525 us with 8 CTAs / 128 registers, cfg3a)
 #ifndef SIPG_HEX_MINB
-#define SIPG_HEX_MINB 6
+#define SIPG_HEX_MINB 7
 #endif
 template <int N, int Q, bool GEN>
 __global__ void __launch_bounds__(Q * Q, (Q <= 8 ? SIPG_HEX_MINB : 1))
@@ -263,11 +266,11 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   __shared__ double sW[Q];
   __shared__ int sk[6];               // 1 fast conforming, 2 boundary, 0 generic
   __shared__ int soff[8];
+  __shared__ int64_t sdof[2];
   __shared__ int fpar[6][4];          // neighbour plane strides (b0, b1, fixed axis), side             // block offsets (own coefficients per stage, neighbours)
   __shared__ __align__(8) uint64_t mbar[3];   // records+own [stage 0, 1], neighbours
   double* B0 = S;
   double* B1 = S + BUF;
-  double* B2 = S + 2 * BUF;
   const int t = threadIdx.x;
   const int ta = t / Q, tb = t - (t / Q) * Q;
   const int* cd = P.cd + cls * CD_WORDS;
@@ -283,30 +286,33 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   if (t < Q) sW[t] = hxW<N, Q>[t];
   __syncthreads();
   // issue records + own coefficients of element `iel` into stage `st`
-  auto issue_own = [&](int iel, int st) {
+  // (thread 0) dof offsets are loaded one issue ahead so the TMA issue never waits on the
+  // elist -> dof_off load chain
+  auto issue_own = [&](int iel, int st, int64_t dof) {
     const FaceRec* rsrc = P.recs + cd[CD_REC_OFF] + (int64_t)iel * 6;
     bulk_g2s(dsm + H::O_REC + st * 96, rsrc, 6 * sizeof(FaceRec), &mbar[st]);
     unsigned nb;
-    soff[st] = bulk_block(dsm + H::O_CO + st * H::BLK, x + P.dof_off[elist[iel]], N3, &mbar[st], &nb);
+    sdof[st] = dof;
+    soff[st] = bulk_block(dsm + H::O_CO, x + dof, N3, &mbar[st], &nb);
     mbar_expect_tx(&mbar[st], 6 * sizeof(FaceRec) + nb);
     cp_async_commit();
   };
-  if (t == 0 && blockIdx.x < count) issue_own(blockIdx.x, 0);
+  int64_t dnext = 0;
+  if (t == 0 && blockIdx.x < count) {
+    issue_own(blockIdx.x, 0, P.dof_off[elist[blockIdx.x]]);
+    if (blockIdx.x + gridDim.x < count) dnext = P.dof_off[elist[blockIdx.x + gridDim.x]];
+  }
 
   int k = 0;
   for (int iel = blockIdx.x; iel < count; iel += gridDim.x, ++k) {
   const int st = k & 1;
   const bool more = iel + (int)gridDim.x < count;
-  if (t == 0 && more) issue_own(iel + gridDim.x, st ^ 1);
-  if (t == 0) {
-    if (more) cp_async_wait<1>(); else cp_async_wait<0>();
-  }
+  if (t == 0) cp_async_wait<0>();
   mbar_wait(&mbar[st], (k >> 1) & 1);
   __syncthreads();
   const FaceRec* srec = reinterpret_cast<const FaceRec*>(dsm + H::O_REC + st * 96);
-  const double* C = dsm + H::O_CO + st * H::BLK + soff[st];
-  const int e = elist[iel];
-  const int64_t dof0 = P.dof_off[e];
+  const double* C = dsm + H::O_CO + soff[st];
+  const int64_t dof0 = sdof[st];
   if (t < 6) {
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
@@ -338,21 +344,26 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 #pragma unroll
     for (int k = 0; k < Q; ++k) B1[ta * SI + tb * SJ + k] = o[k];
   }
+  fence_proxy_async();   // the reads of CO above before the next element's TMA writes into it
   __syncthreads();
+  if (t == 0 && more) {
+    issue_own(iel + gridDim.x, st ^ 1, dnext);
+    if (iel + 2 * (int)gridDim.x < count) dnext = P.dof_off[elist[iel + 2 * gridDim.x]];
+  }
   if (ta < N) {
     double v[N], o[Q];
 #pragma unroll
     for (int b = 0; b < N; ++b) v[b] = B1[ta * SI + b * SJ + tb];
     eo_fwdV<N, Q>(v, o);
 #pragma unroll
-    for (int j = 0; j < Q; ++j) B2[ta * SI + j * SJ + tb] = o[j];
+    for (int j = 0; j < Q; ++j) B0[ta * SI + j * SJ + tb] = o[j];
   }
   __syncthreads();
   double u[Q], d0[Q], d1[Q], d2[Q];
   {
     double v[N];
 #pragma unroll
-    for (int a = 0; a < N; ++a) v[a] = B2[a * SI + ta * SJ + tb];
+    for (int a = 0; a < N; ++a) v[a] = B0[a * SI + ta * SJ + tb];
     eo_fwdV<N, Q>(v, u);
   }
   // ---- PhysDeriv: axis 0 in registers; axes 1, 2 through shared memory
@@ -370,10 +381,10 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     eo_fwdD<N, Q>(v, d1);
     eo_fwdD<N, Q>(w, d2);
 #pragma unroll
-    for (int r = 0; r < Q; ++r) {
-      B1[ta * SI + r * SJ + tb] = d1[r];
-      B2[ta * SI + tb * SJ + r] = d2[r];
-    }
+    for (int r = 0; r < Q; ++r) B1[ta * SI + r * SJ + tb] = d1[r];
+    __syncthreads();   // every line of B0 read
+#pragma unroll
+    for (int r = 0; r < Q; ++r) B0[ta * SI + tb * SJ + r] = d2[r];
   }
   if (t >= NT - 6) cp_async_wait<0>();
   mbar_wait(&mbar[2], k & 1);
@@ -381,13 +392,13 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
     d1[i] = B1[i * SI + ta * SJ + tb];
-    d2[i] = B2[i * SI + ta * SJ + tb];
+    d2[i] = B0[i * SI + ta * SJ + tb];
   }
   __syncthreads();   // S reused from here on
 
   // ---- fast faces: neighbour (u, du_normal) on the face grid from its coefficients
   double* NP = S;                      // [f][pl][i0][i1], 12 N^2
-  double* U2 = S + 12 * N * N;         // [f][pl][p0][p1], 12 Q^2
+  double* U2 = S;                      // [f][pl][p0][p1], 12 Q^2 (overlays NP once stage 1 is done)
   double* T1 = NB;                     // [f][pl][p0][i1], 12 Q N (neighbour blocks dead by then)
   double* OWN = NB + 12 * Q * N;       // faces 2..5: own (u, g_s) [f-2][2][QQ]
   double* FVD = OWN + 8 * QQ;          // faces 2..5: (fv, fd) [f-2][2][QQ]
@@ -398,10 +409,14 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
       if (sk[f] != 1) continue;
       const double* c = NB + f * H::BLK + soff[2 + f] + i0 * fpar[f][0] + i1 * fpar[f][1];
       const int sa = fpar[f][2], hi = fpar[f][3];
-      const double* dve = &hxDVE<N, Q>[hi * N];
       double pd = 0.0;
+      if (hi) {   // face-uniform branch: both endpoint rows stay compile-time constant operands
 #pragma unroll
-      for (int i = 0; i < N; ++i) pd = fma(dve[i], c[i * sa], pd);
+        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[N + i], c[i * sa], pd);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) pd = fma(hxDVE<N, Q>[i], c[i * sa], pd);
+      }
       NP[(2 * f) * N * N + t] = c[hi ? (N - 1) * sa : 0];   // modified-modal boundary mode
       NP[(2 * f + 1) * N * N + t] = pd;
     }
@@ -579,8 +594,8 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   // ---- R = P0 + D0^T P1 (registers) + D1^T P2 + D2^T P3 (shared memory)
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    B1[i * SI + ta * SJ + tb] = d1[i];
-    B2[i * SI + ta * SJ + tb] = d2[i];
+    B0[i * SI + ta * SJ + tb] = d1[i];
+    B1[i * SI + ta * SJ + tb] = d2[i];
   }
   {
     double r[Q];
@@ -593,21 +608,21 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
     double v[Q], w[Q];
 #pragma unroll
     for (int m = 0; m < Q; ++m) {
-      v[m] = B1[ta * SI + m * SJ + tb];   // (i=ta, ., k=tb)
-      w[m] = B2[ta * SI + tb * SJ + m];   // (i=ta, j=tb, .)
+      v[m] = B0[ta * SI + m * SJ + tb];   // (i=ta, ., k=tb)
+      w[m] = B1[ta * SI + tb * SJ + m];   // (i=ta, j=tb, .)
     }
     eo_trD<N, Q>(v, d1);
     eo_trD<N, Q>(w, d2);
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
-      B1[ta * SI + r * SJ + tb] = d1[r];
-      B2[ta * SI + tb * SJ + r] = d2[r];
+      B0[ta * SI + r * SJ + tb] = d1[r];
+      B1[ta * SI + tb * SJ + r] = d2[r];
     }
   }
   __syncthreads();
   // ---- IProduct: axis 0 in registers (thread (j,k)), then axes 1 and 2
 #pragma unroll
-  for (int i = 0; i < Q; ++i) u[i] += B1[i * SI + ta * SJ + tb] + B2[i * SI + ta * SJ + tb];
+  for (int i = 0; i < Q; ++i) u[i] += B0[i * SI + ta * SJ + tb] + B1[i * SI + ta * SJ + tb];
   {
     double o[N];
     eo_bwdV<N, Q>(u, o);
