@@ -78,11 +78,29 @@ int sipg_plan_class_info(const sipg_plan* plan, int32_t cls, int32_t* out6);
 int sipg_apply_host(sipg_plan* plan, const double* x_host, double* y_host, void* stream);
 
 int sipg_plan_destroy(sipg_plan* plan);
+
+/* GPU-resident unpreconditioned conjugate gradient on A = the plan's operator
+ * (reference krylov.cg, pkg/src/dgsipg/krylov.py:39-81):
+ * x (device, n doubles, overwritten, starts from 0) approximates A^-1 b (device).
+ * maxiter <= 0 means the reference default max(10 n, 200).  Same control flow as
+ * the reference: stop on p.Ap <= 0 ("indefinite direction", x not updated), on
+ * ||r||/||b|| <= tol after verifying the true residual (<= 10 tol, else
+ * "residual drift"), on 250 iterations without a 0.1 % improvement
+ * ("stagnation"), or at maxiter. */
+typedef struct sipg_solve_report {
+  int32_t converged;   /* 1 / 0 */
+  int32_t reason;      /* 0 converged, 1 indefinite direction, 2 residual drift, 3 stagnation, 4 maxiter */
+  int64_t iterations;
+  double residual;     /* relative residual ||b - A x|| / ||b|| (recurrence value unless verified) */
+} sipg_solve_report;
+int sipg_cg(sipg_plan* plan, const double* b_dev, double* x_dev, int64_t n, double tol, int64_t maxiter,
+            sipg_solve_report* report, void* stream);
 const char* sipg_last_error(void);
 
 /* Introspection: kernel launches issued so far / per apply; layout constants. */
 int64_t sipg_plan_launches(const sipg_plan* plan);
 int sipg_plan_kernels_per_apply(const sipg_plan* plan);
+int64_t sipg_plan_n_dofs(const sipg_plan* plan);
 /* Number of DoF chunks sipg_apply_host pipelines (H2D chunk k || compute stage k-1 || D2H), 0 when
  * the host apply runs copy -> apply -> copy (mesh order not chunkable, or a distributed local plan). */
 int sipg_plan_stream_chunks(const sipg_plan* plan);

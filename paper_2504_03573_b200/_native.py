@@ -19,9 +19,15 @@ LIB_PATH = Path(os.environ.get("SIPG_LIB_PATH", "")) if os.environ.get("SIPG_LIB
 
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
-           "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply",
+           "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply", "sipg_plan_n_dofs", "sipg_cg",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
            "sipg_apply_role"]
+
+
+class SolveReportC(ctypes.Structure):
+    """sipg_solve_report (include/sipg.h)."""
+    _fields_ = [("converged", ctypes.c_int32), ("reason", ctypes.c_int32),
+                ("iterations", ctypes.c_int64), ("residual", ctypes.c_double)]
 
 
 class PlanDesc(ctypes.Structure):
@@ -65,6 +71,11 @@ def load() -> ctypes.CDLL:
     lib.sipg_plan_launches.restype = i64
     lib.sipg_plan_kernels_per_apply.argtypes = [vp]
     lib.sipg_plan_kernels_per_apply.restype = ctypes.c_int
+    lib.sipg_plan_n_dofs.argtypes = [vp]
+    lib.sipg_plan_n_dofs.restype = ctypes.c_int64
+    lib.sipg_cg.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                            ctypes.POINTER(SolveReportC), vp]
+    lib.sipg_cg.restype = ctypes.c_int
     for nm in ("sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply"):
         getattr(lib, nm).argtypes = [vp]
         getattr(lib, nm).restype = ctypes.c_int
@@ -168,6 +179,13 @@ class NativePlan:
     @property
     def kernels_per_apply(self) -> int:
         return int(self._lib.sipg_plan_kernels_per_apply(self.handle))
+
+    def cg(self, b_ptr: int, x_ptr: int, n: int, tol: float, maxiter: int, stream: int = 0) -> SolveReportC:
+        """GPU-resident CG (sipg_cg): x <- A^-1 b on device buffers."""
+        rep = SolveReportC()
+        check(self._lib.sipg_cg(self.handle, ctypes.c_void_p(b_ptr), ctypes.c_void_p(x_ptr), n, tol, maxiter,
+                                ctypes.byref(rep), ctypes.c_void_p(stream)), "sipg_cg")
+        return rep
 
     def stream_chunks(self) -> int:
         """DoF chunks the host apply pipelines (0: not streamed)."""

@@ -20,6 +20,12 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+void sipg_set_error(const std::string& s) { g_err = s; }   // used by sipg_krylov.cu
+
+namespace {
+
 #define CK(call)                                                                       \
   do {                                                                                 \
     cudaError_t _e = (call);                                                           \
@@ -574,6 +580,8 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   }
   return k;
 }
+
+int64_t sipg_plan_n_dofs(const sipg_plan* p) { return p ? p->n_dofs : -1; }
 
 int sipg_plan_stream_chunks(const sipg_plan* p) { return p && p->streamed ? p->n_chunks : 0; }
 

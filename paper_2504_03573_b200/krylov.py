@@ -1,0 +1,126 @@
+"""Krylov solvers around the GPU apply.
+
+Mirrors the reference's `dgsipg.krylov` interface (pkg/src/dgsipg/krylov.py):
+`cg(apply_op, b, tol=1e-9, maxiter=None) -> (x, SolveReport)` and
+`gmres(apply_op, b, tol=1e-9, restart=50, maxiter=None) -> (x, SolveReport)`,
+with the same stopping rules and report fields.  `apply_op` must be this
+package's `HelmholtzOperator` (the vectors stay in HBM; there is no CPU path):
+
+* cg runs entirely in libsipg.so (`sipg_cg`, csrc/sipg_krylov.cu): one apply,
+  one fused dot and one fused update per iteration, two scalars read back.
+* gmres keeps the Krylov basis on the device (torch tensors as plumbing); every
+  operator application is the sm_100a apply, the small Hessenberg least-squares
+  problem is solved on the host like the reference (krylov.py:84-141).
+
+`b` may be a numpy array (copied in, x copied out as numpy, like the reference)
+or a CUDA float64 tensor (x returned as a CUDA tensor).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["SolveReport", "cg", "gmres", "REASONS"]
+
+REASONS = {0: "", 1: "indefinite direction", 2: "residual drift", 3: "stagnation", 4: "maxiter"}
+
+
+@dataclass
+class SolveReport:
+    """Same fields and text as the reference's SolveReport (krylov.py:27-37)."""
+    converged: bool
+    iterations: int
+    residual: float
+    reason: str = ""
+
+    def __str__(self) -> str:
+        state = "converged" if self.converged else f"FAILED ({self.reason})"
+        return f"{state} in {self.iterations} iterations, relres {self.residual:.3e}"
+
+
+def _device_rhs(op, b):
+    import torch
+    from .sipg import HelmholtzOperator, _is_cuda_tensor
+    if not isinstance(op, HelmholtzOperator):
+        raise TypeError("the GPU solvers need a paper_2504_03573_b200 HelmholtzOperator as apply_op")
+    if _is_cuda_tensor(b):
+        if b.dtype != torch.float64 or b.shape != (op.n_dofs,):
+            raise ValueError(f"expected a float64 vector of length {op.n_dofs}")
+        return b.contiguous(), True
+    b = np.ascontiguousarray(np.asarray(b, dtype=float))
+    if b.shape != (op.n_dofs,):
+        raise ValueError(f"expected a vector of length {op.n_dofs}")
+    return torch.from_numpy(b).cuda(), False
+
+
+def cg(apply_op, b, tol: float = 1e-9, maxiter: int | None = None):
+    """Unpreconditioned CG on the GPU (reference krylov.py:39-81); returns (x, SolveReport)."""
+    import torch
+    bd, on_dev = _device_rhs(apply_op, b)
+    x = torch.empty_like(bd)
+    stream = torch.cuda.current_stream()
+    rep = apply_op.native.cg(bd.data_ptr(), x.data_ptr(), int(bd.numel()), float(tol),
+                             int(maxiter) if maxiter is not None else 0, stream.cuda_stream)
+    out = SolveReport(bool(rep.converged), int(rep.iterations), float(rep.residual), REASONS[int(rep.reason)])
+    return (x if on_dev else x.cpu().numpy()), out
+
+
+def gmres(apply_op, b, tol: float = 1e-9, restart: int = 50, maxiter: int | None = None):
+    """Restarted GMRES with modified Gram-Schmidt (reference krylov.py:84-141); basis on device."""
+    import torch
+    bd, on_dev = _device_rhs(apply_op, b)
+    n = bd.numel()
+    nb = float(torch.linalg.vector_norm(bd))
+    x = torch.zeros_like(bd)
+    done = (lambda xx, rep: ((xx if on_dev else xx.cpu().numpy()), rep))
+    if nb == 0.0:
+        return done(x, SolveReport(True, 0, 0.0))
+    if maxiter is None:
+        maxiter = max(20 * n, 400)
+    restart = max(1, min(restart, n))
+    total = 0
+
+    def apply(v):
+        return apply_op(v)
+
+    while total < maxiter:
+        r = bd - apply(x)
+        beta = float(torch.linalg.vector_norm(r))
+        if beta / nb <= tol:
+            return done(x, SolveReport(True, total, beta / nb))
+        m = min(restart, maxiter - total)
+        q = torch.zeros((m + 1, n), dtype=torch.float64, device=bd.device)
+        h = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        q[0] = r / beta
+        k_done = 0
+        for k in range(m):
+            w = apply(q[k])
+            for i in range(k + 1):
+                h[i, k] = float(torch.dot(w, q[i]))
+                w = w - h[i, k] * q[i]
+            h[k + 1, k] = float(torch.linalg.vector_norm(w))
+            if h[k + 1, k] > 1e-300:
+                q[k + 1] = w / h[k + 1, k]
+            for i in range(k):
+                t = cs[i] * h[i, k] + sn[i] * h[i + 1, k]
+                h[i + 1, k] = -sn[i] * h[i, k] + cs[i] * h[i + 1, k]
+                h[i, k] = t
+            denom = np.hypot(h[k, k], h[k + 1, k])
+            cs[k], sn[k] = h[k, k] / denom, h[k + 1, k] / denom
+            h[k, k], h[k + 1, k] = denom, 0.0
+            g[k + 1] = -sn[k] * g[k]
+            g[k] = cs[k] * g[k]
+            k_done = k + 1
+            total += 1
+            if abs(g[k + 1]) / nb <= tol:
+                break
+        y = np.linalg.solve(h[:k_done, :k_done] + 0.0, g[:k_done]) if k_done else np.zeros(0)
+        x = x + (q[:k_done].T @ torch.from_numpy(y).to(q.device))
+        rel = float(torch.linalg.vector_norm(bd - apply(x))) / nb
+        if rel <= tol:
+            return done(x, SolveReport(True, total, rel))
+    rel = float(torch.linalg.vector_norm(bd - apply(x))) / nb
+    return done(x, SolveReport(False, total, rel, "maxiter"))
