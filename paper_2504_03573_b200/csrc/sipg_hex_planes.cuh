@@ -52,6 +52,145 @@ k_planes(const DevPlan P, const int cls, const double* __restrict__ x) {
   }
 }
 
+// Shared-trace scratch layout (doubles, from SHX): tables E0, E1 (QT x NMAX), I0, I1 (QT x QMAX),
+// weights (2 QT), T (2 QT NMAX), UO (2 QT^2), SI (2 QT QMAX), SS (2 QT^2), FL (2 QT^2), G (2 QMAX QT)
+struct ShScr {
+  double* base;
+  __device__ double* tE0() const { return base; }
+  __device__ double* tE1() const { return base + QMAX * NMAX; }
+  __device__ double* tI0() const { return base + 2 * QMAX * NMAX; }
+  __device__ double* tI1() const { return base + 2 * QMAX * NMAX + QMAX * QMAX; }
+  __device__ double* tw0() const { return base + 2 * QMAX * NMAX + 2 * QMAX * QMAX; }
+  __device__ double* tw1() const { return tw0() + 2 * QMAX; }
+  __device__ double* sT() const { return tw1() + 2 * QMAX; }
+  __device__ double* sUO() const { return sT() + 2 * QMAX * NMAX; }
+  __device__ double* sSI() const { return sUO() + 2 * QMAX * QMAX; }
+  __device__ double* sSS() const { return sSI() + 2 * QMAX * QMAX; }
+  __device__ double* sFL() const { return sSS() + 2 * QMAX * QMAX; }
+  __device__ double* sG() const { return sFL() + 2 * QMAX * QMAX; }
+};
+
+// One fast shared-trace face (F_FAST_SHARED): the neighbour's published planes evaluated at the
+// trace points with its 1-D tables, the own trace interpolated there, the SIP flux on the trace
+// grid (self normal n, other -n, one metric: reference sipg.py:640-650) and the transposed
+// interpolation back to the own face grid.  NO / QT > 0: compile-time neighbour order and trace
+// size (the common cases, fully unrolled); 0: runtime sizes.  Called by every thread of the CTA.
+template <int N, int Q, int NO, int QT>
+__device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const int t, const int f,
+                                         const FaceRec& r, const int64_t e01, const double* pl,
+                                         const double* __restrict__ T, const double* OWN, double* FVD,
+                                         const ShScr sc) {
+  constexpr int NT = Q * Q, QQ = Q * Q;
+  const int no = NO ? NO : no_rt, qt = QT ? QT : qt_rt;
+  double *tE0 = sc.tE0(), *tE1 = sc.tE1(), *tI0 = sc.tI0(), *tI1 = sc.tI1(), *tw0 = sc.tw0(), *tw1 = sc.tw1();
+  double *sT = sc.sT(), *sUO = sc.sUO(), *sSI = sc.sSI(), *sSS = sc.sSS(), *sFL = sc.sFL(), *sG = sc.sG();
+  const double* gE0 = T + (int)(e01 & 0xffffffff);
+  const double* gE1 = T + (int)(e01 >> 32);
+  const bool sid = (r.flags & F_SELF_ID) != 0;
+  for (int i = t; i < qt * no; i += NT) { tE0[i] = __ldg(gE0 + i); tE1[i] = __ldg(gE1 + i); }
+  if (!sid)
+    for (int i = t; i < qt * Q; i += NT) { tI0[i] = __ldg(T + r.ts0 + i); tI1[i] = __ldg(T + r.ts1 + i); }
+  for (int i = t; i < qt; i += NT) { tw0[i] = __ldg(T + r.wt0 + i); tw1[i] = __ldg(T + r.wt1 + i); }
+  __syncthreads();
+  const int nno = (no * no + 1) & ~1;
+  // other: planes -> trace points, axis 0
+#pragma unroll 2
+  for (int it = t; it < 2 * qt * no; it += NT) {
+    const int plx = it / (qt * no), r0 = it - plx * qt * no, p0 = r0 / no, i1 = r0 - p0 * no;
+    double s = 0.0;
+#pragma unroll
+    for (int i0 = 0; i0 < (NO ? NO : NMAX); ++i0)
+      if (NO || i0 < no) s = fma(tE0[p0 * no + i0], pl[plx * nno + i0 * no + i1], s);
+    sT[it] = s;
+  }
+  // own: face grid -> trace points, axis 0
+  if (!sid)
+#pragma unroll 2
+    for (int it = t; it < 2 * qt * Q; it += NT) {
+      const int plx = it / (qt * Q), r0 = it - plx * qt * Q, p0 = r0 / Q, q1 = r0 - p0 * Q;
+      const double* o = OWN + f * 2 * QQ + plx * QQ;
+      double s = 0.0;
+#pragma unroll
+      for (int q0 = 0; q0 < Q; ++q0) s = fma(tI0[p0 * Q + q0], o[q0 * Q + q1], s);
+      sSI[it] = s;
+    }
+  __syncthreads();
+  // axis 1 for both
+#pragma unroll 2
+  for (int it = t; it < 2 * qt * qt; it += NT) {
+    const int plx = it / (qt * qt), r0 = it - plx * qt * qt, p0 = r0 / qt, p1 = r0 - p0 * qt;
+    double s = 0.0;
+#pragma unroll
+    for (int i1 = 0; i1 < (NO ? NO : NMAX); ++i1)
+      if (NO || i1 < no) s = fma(tE1[p1 * no + i1], sT[plx * qt * no + p0 * no + i1], s);
+    sUO[it] = s;
+    if (!sid) {
+      double w = 0.0;
+#pragma unroll
+      for (int q1 = 0; q1 < Q; ++q1) w = fma(tI1[p1 * Q + q1], sSI[plx * qt * Q + p0 * Q + q1], w);
+      sSS[it] = w;
+    }
+  }
+  __syncthreads();
+  const int ao = r.nbr_face >> 1;
+  const double goa = r.go[ao], sJ = r.sJ, tau = r.tau;
+  for (int p = t; p < qt * qt; p += NT) {
+    const int p0 = p / qt, p1 = p - p0 * qt;
+    const double us = sid ? OWN[f * 2 * QQ + p] : sSS[p];
+    const double gs = sid ? OWN[f * 2 * QQ + QQ + p] : sSS[qt * qt + p];
+    const double jump = us - sUO[p];
+    const double avg = 0.5 * (gs - goa * sUO[qt * qt + p]);
+    const double swj = sJ * tw0[p0] * tw1[p1];
+    const double fv = (tau * jump - avg) * swj, fd = -0.5 * jump * swj;
+    if (sid) {
+      FVD[f * 2 * QQ + p] = fv;
+      FVD[f * 2 * QQ + QQ + p] = fd;
+    } else {
+      sFL[p] = fv;
+      sFL[qt * qt + p] = fd;
+    }
+  }
+  if (!sid) {
+    __syncthreads();
+    // back to the own face grid: transposed interpolation along both axes
+#pragma unroll 2
+    for (int it = t; it < 2 * Q * qt; it += NT) {
+      const int plx = it / (Q * qt), r0 = it - plx * Q * qt, q0 = r0 / qt, p1 = r0 - q0 * qt;
+      double s = 0.0;
+#pragma unroll
+      for (int p0 = 0; p0 < (QT ? QT : QMAX); ++p0)
+        if (QT || p0 < qt) s = fma(tI0[p0 * Q + q0], sFL[plx * qt * qt + p0 * qt + p1], s);
+      sG[it] = s;
+    }
+    __syncthreads();
+    for (int it = t; it < 2 * QQ; it += NT) {
+      const int plx = it / QQ, r0 = it - plx * QQ, q0 = r0 / Q, q1 = r0 - q0 * Q;
+      double s = 0.0;
+#pragma unroll
+      for (int p1 = 0; p1 < (QT ? QT : QMAX); ++p1)
+        if (QT || p1 < qt) s = fma(tI1[p1 * Q + q1], sG[plx * Q * qt + q0 * qt + p1], s);
+      FVD[f * 2 * QQ + it] = s;
+    }
+  }
+}
+
+// compile-time dispatch over the neighbour order NO in [LO, HI] (trace size max(Q, NO + 1),
+// the GLL / GLL case F_FAST_SHARED covers); anything else takes the runtime-size variant
+template <int N, int Q, int LO, int HI>
+__device__ __forceinline__ void sf_dispatch(const int no, const int qt, const int t, const int f, const FaceRec& r,
+                                            const int64_t e01, const double* pl, const double* T,
+                                            const double* OWN, double* FVD, const ShScr sc) {
+  if constexpr (LO > HI) {
+    shared_face<N, Q, 0, 0>(no, qt, t, f, r, e01, pl, T, OWN, FVD, sc);
+  } else {
+    constexpr int QTV = Q > LO + 1 ? Q : LO + 1;
+    if (LO != N && no == LO && qt == QTV)
+      shared_face<N, Q, LO, QTV>(no, qt, t, f, r, e01, pl, T, OWN, FVD, sc);
+    else
+      sf_dispatch<N, Q, LO + 1, HI>(no, qt, t, f, r, e01, pl, T, OWN, FVD, sc);
+  }
+}
+
 template <int N, int Q, bool SH>
 struct HexPlanes {
   static constexpr int NT = Q * Q;
@@ -67,8 +206,8 @@ struct HexPlanes {
   static constexpr int FACE = 36 * QQ + 12 * Q * N;
   // shared-trace scratch (SH): tables, T, UO, SI, SS, FL, G
   static constexpr int QT = QMAX;
-  static constexpr int SHS = SH ? (4 * QT * NMAX + 4 * QT + 2 * QT * NMAX + 2 * QT * QT + 2 * QT * QMAX +
-                                   2 * QT * QT + 2 * QT * QT + 2 * QMAX * QT + 16) : 0;
+  static constexpr int SHS = SH ? (2 * QT * NMAX + 2 * QT * QMAX + 4 * QT + 2 * QT * NMAX + 8 * QT * QT +
+                                   2 * QMAX * QT + 16) : 0;   // ShScr
   static constexpr int S0 = 3 * BUF > FACE + SHS ? 3 * BUF : FACE + SHS;
   static constexpr int SCR = (S0 + 1) & ~1;
   // dynamic shared memory (doubles): REC[2] | CO[2] | NBP[6] | S
@@ -166,12 +305,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[N], o[Q];
 #pragma unroll
       for (int c = 0; c < N; ++c) v[c] = C[(ta * N + tb) * N + c];
-#pragma unroll
-      for (int k = 0; k < Q; ++k) o[k] = 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c)
-#pragma unroll
-        for (int k = 0; k < Q; ++k) o[k] = fma(hxV<N, Q>[k * N + c], v[c], o[k]);
+      eo_fwdV<N, Q>(v, o);
 #pragma unroll
       for (int k = 0; k < Q; ++k) B1[ta * SI + tb * SJ + k] = o[k];
     }
@@ -180,12 +314,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[N], o[Q];
 #pragma unroll
       for (int b = 0; b < N; ++b) v[b] = B1[ta * SI + b * SJ + tb];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) o[j] = 0.0;
-#pragma unroll
-      for (int b = 0; b < N; ++b)
-#pragma unroll
-        for (int j = 0; j < Q; ++j) o[j] = fma(hxV<N, Q>[j * N + b], v[b], o[j]);
+      eo_fwdV<N, Q>(v, o);
 #pragma unroll
       for (int j = 0; j < Q; ++j) B2[ta * SI + j * SJ + tb] = o[j];
     }
@@ -195,22 +324,11 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[N];
 #pragma unroll
       for (int a = 0; a < N; ++a) v[a] = B2[a * SI + ta * SJ + tb];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) u[i] = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a)
-#pragma unroll
-        for (int i = 0; i < Q; ++i) u[i] = fma(hxV<N, Q>[i * N + a], v[a], u[i]);
+      eo_fwdV<N, Q>(v, u);
     }
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-      d0[i] = 0.0;
-      B0[i * SI + ta * SJ + tb] = u[i];
-    }
-#pragma unroll
-    for (int m = 0; m < Q; ++m)
-#pragma unroll
-      for (int i = 0; i < Q; ++i) d0[i] = fma(hxD<N, Q>[i * Q + m], u[m], d0[i]);
+    for (int i = 0; i < Q; ++i) B0[i * SI + ta * SJ + tb] = u[i];
+    eo_fwdD<N, Q>(u, d0);
     __syncthreads();
     {
       double v[Q], w[Q];
@@ -219,18 +337,8 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
         v[m] = B0[ta * SI + m * SJ + tb];
         w[m] = B0[ta * SI + tb * SJ + m];
       }
-#pragma unroll
-      for (int r = 0; r < Q; ++r) {
-        d1[r] = 0.0;
-        d2[r] = 0.0;
-      }
-#pragma unroll
-      for (int m = 0; m < Q; ++m)
-#pragma unroll
-        for (int r = 0; r < Q; ++r) {
-          d1[r] = fma(hxD<N, Q>[r * Q + m], v[m], d1[r]);
-          d2[r] = fma(hxD<N, Q>[r * Q + m], w[m], d2[r]);
-        }
+      eo_fwdD<N, Q>(v, d1);
+      eo_fwdD<N, Q>(w, d2);
 #pragma unroll
       for (int r = 0; r < Q; ++r) {
         B1[ta * SI + r * SJ + tb] = d1[r];
@@ -259,12 +367,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[N], o[Q];
 #pragma unroll
       for (int i0 = 0; i0 < N; ++i0) v[i0] = pl[i0 * N + i1];
-#pragma unroll
-      for (int p0 = 0; p0 < Q; ++p0) o[p0] = 0.0;
-#pragma unroll
-      for (int i0 = 0; i0 < N; ++i0)
-#pragma unroll
-        for (int p0 = 0; p0 < Q; ++p0) o[p0] = fma(hxV<N, Q>[p0 * N + i0], v[i0], o[p0]);
+      eo_fwdV<N, Q>(v, o);
 #pragma unroll
       for (int p0 = 0; p0 < Q; ++p0) T1[fp * Q * N + p0 * N + i1] = o[p0];
     }
@@ -295,110 +398,19 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[N], o[Q];
 #pragma unroll
       for (int i1 = 0; i1 < N; ++i1) v[i1] = T1[fp * Q * N + p0 * N + i1];
-#pragma unroll
-      for (int p1 = 0; p1 < Q; ++p1) o[p1] = 0.0;
-#pragma unroll
-      for (int i1 = 0; i1 < N; ++i1)
-#pragma unroll
-        for (int p1 = 0; p1 < Q; ++p1) o[p1] = fma(hxV<N, Q>[p1 * N + i1], v[i1], o[p1]);
+      eo_fwdV<N, Q>(v, o);
 #pragma unroll
       for (int p1 = 0; p1 < Q; ++p1) U2[fp * QQ + p0 * Q + p1] = o[p1];
     }
     // ---- fast shared traces, one face at a time (runtime trace / neighbour sizes)
     if (SH) {
-      double* tE0 = SHX;                       // E_o axis 0 (qt x no)
-      double* tE1 = tE0 + H::QT * NMAX;        // E_o axis 1
-      double* tI0 = tE1 + H::QT * NMAX;        // own -> trace, axis 0 (qt x Q)
-      double* tI1 = tI0 + H::QT * NMAX;        // own -> trace, axis 1
-      double* tw0 = tI1 + H::QT * NMAX;        // trace weights
-      double* tw1 = tw0 + 2 * H::QT;
-      double* sT = tw1 + 2 * H::QT;            // [pl][p0][i1]   2 qt no
-      double* sUO = sT + 2 * H::QT * NMAX;     // [pl][p0][p1]   2 qt qt  other at trace
-      double* sSI = sUO + 2 * H::QT * H::QT;   // [pl][p0][q1]   2 qt Q   own stage 1
-      double* sSS = sSI + 2 * H::QT * QMAX;    // [pl][p0][p1]   2 qt qt  own at trace
-      double* sFL = sSS + 2 * H::QT * H::QT;   // [pl][p0][p1]   2 qt qt  flux at trace
-      double* sG = sFL + 2 * H::QT * H::QT;    // [pl][q0][p1]   2 Q qt   back, stage 1
       for (int f = 0; f < 6; ++f) {
         if (sk[f] != 3) continue;
         __syncthreads();
         const FaceRec& r = srec[f];
-        const int no = sno[f], qt = r.nt0;
-        const int64_t e01 = sext[2 * f + 1];
-        const double* gE0 = T + (int)(e01 & 0xffffffff);
-        const double* gE1 = T + (int)(e01 >> 32);
-        const bool sid = (r.flags & F_SELF_ID) != 0;
-        for (int i = t; i < qt * no; i += NT) { tE0[i] = __ldg(gE0 + i); tE1[i] = __ldg(gE1 + i); }
-        if (!sid)
-          for (int i = t; i < qt * Q; i += NT) { tI0[i] = __ldg(T + r.ts0 + i); tI1[i] = __ldg(T + r.ts1 + i); }
-        for (int i = t; i < qt; i += NT) { tw0[i] = __ldg(T + r.wt0 + i); tw1[i] = __ldg(T + r.wt1 + i); }
-        __syncthreads();
-        const int nno = (no * no + 1) & ~1;
-        const double* pl = NBP + f * 2 * NNX;
-        // other: planes -> trace points
-        for (int it = t; it < 2 * qt * no; it += NT) {
-          const int plx = it / (qt * no), r0 = it - plx * qt * no, p0 = r0 / no, i1 = r0 - p0 * no;
-          double s = 0.0;
-          for (int i0 = 0; i0 < no; ++i0) s = fma(tE0[p0 * no + i0], pl[plx * nno + i0 * no + i1], s);
-          sT[it] = s;
-        }
-        // own: face grid -> trace points (stage 1)
-        if (!sid)
-          for (int it = t; it < 2 * qt * Q; it += NT) {
-            const int plx = it / (qt * Q), r0 = it - plx * qt * Q, p0 = r0 / Q, q1 = r0 - p0 * Q;
-            const double* o = OWN + f * 2 * QQ + plx * QQ;
-            double s = 0.0;
-            for (int q0 = 0; q0 < Q; ++q0) s = fma(tI0[p0 * Q + q0], o[q0 * Q + q1], s);
-            sSI[it] = s;
-          }
-        __syncthreads();
-        for (int it = t; it < 2 * qt * qt; it += NT) {
-          const int plx = it / (qt * qt), r0 = it - plx * qt * qt, p0 = r0 / qt, p1 = r0 - p0 * qt;
-          double s = 0.0;
-          for (int i1 = 0; i1 < no; ++i1) s = fma(tE1[p1 * no + i1], sT[plx * qt * no + p0 * no + i1], s);
-          sUO[it] = s;
-          if (!sid) {
-            double w = 0.0;
-            for (int q1 = 0; q1 < Q; ++q1) w = fma(tI1[p1 * Q + q1], sSI[plx * qt * Q + p0 * Q + q1], w);
-            sSS[it] = w;
-          }
-        }
-        __syncthreads();
-        // SIP flux on the trace grid (self normal n, other -n; one metric: reference sipg.py:640-650)
-        const int ao = r.nbr_face >> 1;
-        const double goa = r.go[ao];
-        for (int p = t; p < qt * qt; p += NT) {
-          const int p0 = p / qt, p1 = p - p0 * qt;
-          const double us = sid ? OWN[f * 2 * QQ + p] : sSS[p];
-          const double gs = sid ? OWN[f * 2 * QQ + QQ + p] : sSS[qt * qt + p];
-          const double jump = us - sUO[p];
-          const double avg = 0.5 * (gs - goa * sUO[qt * qt + p]);
-          const double swj = r.sJ * tw0[p0] * tw1[p1];
-          const double fv = (r.tau * jump - avg) * swj, fd = -0.5 * jump * swj;
-          if (sid) {
-            FVD[f * 2 * QQ + p] = fv;
-            FVD[f * 2 * QQ + QQ + p] = fd;
-          } else {
-            sFL[p] = fv;
-            sFL[qt * qt + p] = fd;
-          }
-        }
-        if (!sid) {
-          __syncthreads();
-          // back to the own face grid: transposed interpolation along both axes
-          for (int it = t; it < 2 * Q * qt; it += NT) {
-            const int plx = it / (Q * qt), r0 = it - plx * Q * qt, q0 = r0 / qt, p1 = r0 - q0 * qt;
-            double s = 0.0;
-            for (int p0 = 0; p0 < qt; ++p0) s = fma(tI0[p0 * Q + q0], sFL[plx * qt * qt + p0 * qt + p1], s);
-            sG[it] = s;
-          }
-          __syncthreads();
-          for (int it = t; it < 2 * QQ; it += NT) {
-            const int plx = it / QQ, r0 = it - plx * QQ, q0 = r0 / Q, q1 = r0 - q0 * Q;
-            double s = 0.0;
-            for (int p1 = 0; p1 < qt; ++p1) s = fma(tI1[p1 * Q + q1], sG[plx * Q * qt + q0 * qt + p1], s);
-            FVD[f * 2 * QQ + it] = s;
-          }
-        }
+        ShScr sc{SHX};
+        sf_dispatch<N, Q, (N - 3 > 2 ? N - 3 : 2), (N + 3 < NMAX ? N + 3 : NMAX)>(
+            sno[f], r.nt0, t, f, r, sext[2 * f + 1], NBP + f * 2 * NNX, T, OWN, FVD, sc);
       }
     }
     __syncthreads();
@@ -474,10 +486,12 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       B1[i * SI + ta * SJ + tb] = d1[i];
       B2[i * SI + ta * SJ + tb] = d2[i];
     }
+    {
+      double rr[Q];
+      eo_trD<N, Q>(d0, rr);
 #pragma unroll
-    for (int m = 0; m < Q; ++m)
-#pragma unroll
-      for (int i = 0; i < Q; ++i) u[i] = fma(hxD<N, Q>[m * Q + i], d0[m], u[i]);
+      for (int i = 0; i < Q; ++i) u[i] += rr[i];
+    }
     __syncthreads();
     {
       double v[Q], w[Q];
@@ -486,18 +500,8 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
         v[m] = B1[ta * SI + m * SJ + tb];
         w[m] = B2[ta * SI + tb * SJ + m];
       }
-#pragma unroll
-      for (int r = 0; r < Q; ++r) {
-        d1[r] = 0.0;
-        d2[r] = 0.0;
-      }
-#pragma unroll
-      for (int m = 0; m < Q; ++m)
-#pragma unroll
-        for (int r = 0; r < Q; ++r) {
-          d1[r] = fma(hxD<N, Q>[m * Q + r], v[m], d1[r]);
-          d2[r] = fma(hxD<N, Q>[m * Q + r], w[m], d2[r]);
-        }
+      eo_trD<N, Q>(v, d1);
+      eo_trD<N, Q>(w, d2);
 #pragma unroll
       for (int r = 0; r < Q; ++r) {
         B1[ta * SI + r * SJ + tb] = d1[r];
@@ -509,12 +513,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
     for (int i = 0; i < Q; ++i) u[i] += B1[i * SI + ta * SJ + tb] + B2[i * SI + ta * SJ + tb];
     {
       double o[N];
-#pragma unroll
-      for (int a = 0; a < N; ++a) o[a] = 0.0;
-#pragma unroll
-      for (int i = 0; i < Q; ++i)
-#pragma unroll
-        for (int a = 0; a < N; ++a) o[a] = fma(hxV<N, Q>[i * N + a], u[i], o[a]);
+      eo_bwdV<N, Q>(u, o);
 #pragma unroll
       for (int a = 0; a < N; ++a) B0[a * SI + ta * SJ + tb] = o[a];
     }
@@ -523,12 +522,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[Q], o[N];
 #pragma unroll
       for (int j = 0; j < Q; ++j) v[j] = B0[ta * SI + j * SJ + tb];
-#pragma unroll
-      for (int b = 0; b < N; ++b) o[b] = 0.0;
-#pragma unroll
-      for (int j = 0; j < Q; ++j)
-#pragma unroll
-        for (int b = 0; b < N; ++b) o[b] = fma(hxV<N, Q>[j * N + b], v[j], o[b]);
+      eo_bwdV<N, Q>(v, o);
 #pragma unroll
       for (int b = 0; b < N; ++b) B1[ta * SI + b * SJ + tb] = o[b];
     }
@@ -537,12 +531,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
       double v[Q], o[N];
 #pragma unroll
       for (int k = 0; k < Q; ++k) v[k] = B1[ta * SI + tb * SJ + k];
-#pragma unroll
-      for (int c = 0; c < N; ++c) o[c] = 0.0;
-#pragma unroll
-      for (int k = 0; k < Q; ++k)
-#pragma unroll
-        for (int c = 0; c < N; ++c) o[c] = fma(hxV<N, Q>[k * N + c], v[k], o[c]);
+      eo_bwdV<N, Q>(v, o);
       double* ye = y + dof0 + (ta * N + tb) * N;
 #pragma unroll
       for (int c = 0; c < N; ++c) ye[c] = o[c];
