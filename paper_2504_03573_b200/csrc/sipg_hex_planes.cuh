@@ -174,6 +174,10 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
   }
 }
 
+// compiled neighbour-order variants: |NO - N| <= SIPG_SF_RANGE (code size vs instruction cache)
+#ifndef SIPG_SF_RANGE
+#define SIPG_SF_RANGE 3
+#endif
 // compile-time dispatch over the neighbour order NO in [LO, HI] (trace size max(Q, NO + 1),
 // the GLL / GLL case F_FAST_SHARED covers); anything else takes the runtime-size variant
 template <int N, int Q, int LO, int HI>
@@ -409,7 +413,8 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
         __syncthreads();
         const FaceRec& r = srec[f];
         ShScr sc{SHX};
-        sf_dispatch<N, Q, (N - 3 > 2 ? N - 3 : 2), (N + 3 < NMAX ? N + 3 : NMAX)>(
+        sf_dispatch<N, Q, (N - SIPG_SF_RANGE > 2 ? N - SIPG_SF_RANGE : 2),
+                    (N + SIPG_SF_RANGE < NMAX ? N + SIPG_SF_RANGE : NMAX)>(
             sno[f], r.nt0, t, f, r, sext[2 * f + 1], NBP + f * 2 * NNX, T, OWN, FVD, sc);
       }
     }
