@@ -171,14 +171,16 @@ int publish_grid(const int32_t* cd, int count) {
 bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
   const int64_t nel = d->n_elements, ndof = d->n_dofs;
   const int64_t bytes = ndof * 8;
-  // chunk size: >= 8 MB (~0.16 ms of PCIe), and >= 1.5 MB per launch a stage issues (per-class
-  // stage launches get short and tail-bound on multi-class meshes; measured on cfg3a / cfg3b);
+  // chunk size: >= 12 MB (~0.22 ms of PCIe), and >= 1.5 MB per launch a stage issues (per-class
+  // stage launches get short and tail-bound on multi-class meshes; measured on cfg3a / cfg3b).
+  // Measured and rejected: kernels storing y straight into page-locked host memory (no D2H
+  // copies) — equal on cfg3a, 13 % slower on cfg3b, even with whole-warp y stores.
   // SIPG_STREAM_CHUNK_BYTES overrides (tests use small meshes)
   int launches_per_stage = 0;
   for (int c = 0; c < d->n_classes; ++c)
     if (d->class_desc[c * CD_WORDS + CD_COUNT] > 0) launches_per_stage += p->planes_k[c] ? 2 : 1;
   int64_t chunk_bytes = (int64_t)launches_per_stage * (3ll << 19);
-  if (chunk_bytes < (8ll << 20)) chunk_bytes = 8ll << 20;
+  if (chunk_bytes < (12ll << 20)) chunk_bytes = 12ll << 20;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
   if (cb) chunk_bytes = atoll(cb);
   int K = (int)(bytes / (chunk_bytes > 0 ? chunk_bytes : 1));

@@ -18,7 +18,8 @@ n = pb.n_dofs
 xp = torch.from_numpy(case.draw_x(n)).pin_memory()
 yp = torch.empty(n, dtype=torch.float64).pin_memory()
 s = torch.cuda.current_stream()
-for cb in ["none", str(2 << 20), str(3 << 20), str(4 << 20), str(6 << 20), str(8 << 20), str(12 << 20)]:
+CHUNKS = os.environ.get("SWEEP_CHUNKS", "none,2,4,8,12").split(",")
+for cb in [c if c == "none" else str(int(float(c) * (1 << 20))) for c in CHUNKS]:
     if cb == "none":
         os.environ["SIPG_NO_STREAM"] = "1"
     else:
