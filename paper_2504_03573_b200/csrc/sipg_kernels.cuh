@@ -474,7 +474,11 @@ struct Cfg {
   static constexpr int NBK = NMAX * NMAX + 2;                 // staged neighbour block (2-D)
   static constexpr int e_rec = (e_fs + FSZ + 1) & ~1;          // NF face records (16 doubles each)
   static constexpr int e_nb = e_rec + NF * 16;
-  static constexpr int ESZ = e_nb + (D == 2 ? NF * NBK : 0);
+  // 2-D warp kernel: next element's coefficients and records, double-buffered (prefetched)
+  static constexpr int NCP = (NC + 1) & ~1;
+  static constexpr int e_pre = e_nb + (D == 2 ? NF * NBK : 0);
+  static constexpr int RPW = NF * 16 + 2 * NF;    // prefetched records + their rec_ext words
+  static constexpr int ESZ = e_pre + (D == 2 ? 2 * (NCP + RPW) : 0);
   static constexpr int TOTAL = TABP + ESZ;
 };
 
@@ -579,10 +583,15 @@ __device__ __noinline__ void generic_face(const DevPlan& P, const FaceRec& r, co
     } else {
       no = eval_face_from_coeffs<TM>(P, r.nbr, r.nbr_face, x, uo, FP, nscr, tid, nt, staged);
     }
-    const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
-    const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
-    qo0 = cdo[CD_Q0 + fto.run0];
-    qo1 = fto.run1 >= 0 ? cdo[CD_Q0 + fto.run1] : 1;
+    if (staged_traces && D == 2) {
+      qo0 = staged_q;
+      qo1 = 1;
+    } else {
+      const int* cdo = P.cd + P.elem_class[r.nbr] * CD_WORDS;
+      const FaceTopo fto = face_topo(cdo[CD_SHAPE], r.nbr_face);
+      qo0 = cdo[CD_Q0 + fto.run0];
+      qo1 = fto.run1 >= 0 ? cdo[CD_Q0 + fto.run1] : 1;
+    }
   }
   TM::sync();
   const double tau = r.tau;
@@ -733,16 +742,18 @@ __device__ __forceinline__ void stage_tables(const DevPlan& P, const int* cd, do
 // One element: volume terms, faces, lift, transposed pass; written to y once.
 // `es` is the element's scratch (Cfg layout without the table region), `tb`
 // the staged tables; the team (CTA or warp) is tid / nt with TM::sync().
-template <int SHAPE, int N, int Q, int GEOM, class TM>
+// PREF (2-D warp kernel): the element's coefficients (cpre) and face records (rpre) were
+// prefetched by the caller during the previous element, and dof_pre is its DoF offset.
+template <int SHAPE, int N, int Q, int GEOM, class TM, bool PREF = false>
 __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, const int i_el,
                                            const double* __restrict__ x, double* __restrict__ y,
-                                           double* es, const double* tb, const int tid, const int nt) {
+                                           double* es, const double* tb, const int tid, const int nt,
+                                           double* cpre = nullptr, FaceRec* rpre = nullptr, int64_t dof_pre = 0) {
   using C = Cfg<SHAPE, N, Q>;
   constexpr int D = C::D, NP = C::NP, NS = C::NS, FP = C::FP, NC = C::NC;
-  const int e = P.class_elems[cd[CD_ELEM_OFF] + i_el];
-  const int64_t dof0 = P.dof_off[e];
+  const int64_t dof0 = PREF ? dof_pre : P.dof_off[P.class_elems[cd[CD_ELEM_OFF] + i_el]];
   const int gllmask = cd[CD_GLLMASK];
-  double* c = es + C::e_c;
+  double* c = PREF ? cpre : es + C::e_c;
   double* u = es + C::e_u;
   double* du = es + C::e_du;
   double* t1 = es + C::e_t1;
@@ -773,21 +784,23 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
     gmo = gst + NG + 1;
   }
   // 2-D: records and neighbour coefficient blocks fetched asynchronously up front
-  FaceRec* srec = reinterpret_cast<FaceRec*>(es + C::e_rec);
+  FaceRec* srec = PREF ? rpre : reinterpret_cast<FaceRec*>(es + C::e_rec);
   double* snb = es + C::e_nb;
   const int rbase = cd[CD_REC_OFF] + i_el * C::NF;
-  if (D == 2) {
+  if (D == 2 && !PREF) {
     for (int i = tid; i < C::NF * 16; i += nt)
       cp_async8_(reinterpret_cast<double*>(srec) + i, reinterpret_cast<const double*>(P.recs + rbase) + i);
     cp_async_commit_();
   }
-  for (int i = tid; i < NC; i += nt) c[i] = ldg(x + dof0 + i);
+  if (!PREF)
+    for (int i = tid; i < NC; i += nt) c[i] = ldg(x + dof0 + i);
   if (D == 2) {
-    cp_async_wait_all_();
+    if (!PREF) cp_async_wait_all_();
     TM::sync();
     for (int f = 0; f < C::NF; ++f) {
       if (srec[f].type == FT_BOUNDARY) continue;
-      const int64_t ext = P.rec_ext ? P.rec_ext[2 * (rbase + f)] : -1;
+      const int64_t ext = PREF ? reinterpret_cast<const int64_t*>(srec + C::NF)[2 * f]
+                               : (P.rec_ext ? P.rec_ext[2 * (rbase + f)] : -1);
       if (ext >= 0 && P.planes) {          // published neighbour traces (3 fields x q_o)
         const int qo = (int)(ext >> 48);
         const double* src = P.planes + (ext & ((int64_t(1) << 48) - 1));
@@ -849,7 +862,9 @@ __device__ __forceinline__ void apply_elem(const DevPlan& P, const int* cd, cons
     const FaceRec r = D == 2 ? srec[f] : P.recs[rbase + f];
     restrict_face<SHAPE, N, Q>(u, du, Lt, gllmask, f, us, tid, nt);
     TM::sync();
-    const int64_t ext = (D == 2 && P.rec_ext && r.type != FT_BOUNDARY) ? P.rec_ext[2 * (rbase + f)] : -1;
+    const int64_t ext = (D == 2 && P.rec_ext && r.type != FT_BOUNDARY)
+                            ? (PREF ? reinterpret_cast<const int64_t*>(srec + C::NF)[2 * f] : P.rec_ext[2 * (rbase + f)])
+                            : -1;
     const bool pub = D == 2 && ext >= 0 && P.planes != nullptr;
     generic_face<SHAPE, N, Q, TM>(P, r, f, x, us, fb + f * (1 + D) * NS, fs + 4 * FP, tid, nt,
                                   D == 2 ? snb + f * C::NBK : nullptr, pub, pub ? (int)(ext >> 48) : 0);
@@ -1005,8 +1020,44 @@ k_apply_w(const DevPlan P, const int cls, const double* __restrict__ x, double* 
   __syncthreads();
   double* es = sm + C::TABP + warp * C::ESZ;
   const int count = cd[CD_COUNT];
-  for (int i_el = blockIdx.x * WPC + warp; i_el < count; i_el += gridDim.x * WPC)
-    apply_elem<SHAPE, N, Q, GEOM, WarpTeam>(P, cd, i_el, x, y, es, sm, lane, 32);
+  const int* elist = P.class_elems + cd[CD_ELEM_OFF];
+  const int stride = gridDim.x * WPC;
+  // software pipeline across the warp's elements: element k+1's records and coefficients are
+  // copied (cp.async) while element k computes; DoF offsets are loaded one more element ahead
+  double* cb = es + C::e_pre;
+  double* rbd = es + C::e_pre + 2 * C::NCP;     // [2][NF records | 2 NF rec_ext words]
+  auto issue = [&](int iel, int b, int64_t dof) {
+    const int64_t r0 = cd[CD_REC_OFF] + (int64_t)iel * C::NF;
+    const double* rs = reinterpret_cast<const double*>(P.recs + r0);
+    double* rd = rbd + b * C::RPW;
+    for (int i = lane; i < C::NF * 16; i += 32) cp_async8_(rd + i, rs + i);
+    if (P.rec_ext)
+      for (int i = lane; i < 2 * C::NF; i += 32)
+        cp_async8_(rd + C::NF * 16 + i, reinterpret_cast<const double*>(P.rec_ext + 2 * r0) + i);
+      else if (lane < 2 * C::NF) rd[C::NF * 16 + lane] = __longlong_as_double(-1ll);
+    for (int i = lane; i < C::NC; i += 32) cp_async8_(cb + b * C::NCP + i, x + dof + i);
+    cp_async_commit_();
+  };
+  int i_el = blockIdx.x * WPC + warp;
+  int64_t dcur = 0, dnext = 0;
+  if (i_el < count) {
+    dcur = P.dof_off[elist[i_el]];
+    issue(i_el, 0, dcur);
+    if (i_el + stride < count) dnext = P.dof_off[elist[i_el + stride]];
+  }
+  for (int k = 0; i_el < count; i_el += stride, ++k) {
+    const int b = k & 1;
+    cp_async_wait_all_();   // this element's prefetch (and the previous element's groups)
+    __syncwarp();
+    const int64_t dthis = dcur;
+    if (i_el + stride < count) {
+      issue(i_el + stride, b ^ 1, dnext);
+      dcur = dnext;
+      if (i_el + 2 * stride < count) dnext = P.dof_off[elist[i_el + 2 * stride]];
+    }
+    apply_elem<SHAPE, N, Q, GEOM, WarpTeam, true>(P, cd, i_el, x, y, es, sm, lane, 32, cb + b * C::NCP,
+                                                  reinterpret_cast<FaceRec*>(rbd + b * C::RPW), dthis);
+  }
 }
 
 }  // namespace sipg
