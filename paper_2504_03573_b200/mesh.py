@@ -24,10 +24,12 @@ class Shape(enum.Enum):
     QUAD = "quad"
     TRI = "tri"
     HEX = "hex"
+    PRISM = "prism"   # config 4 only (mesh3d.py): not in the reference
+    TET = "tet"
 
     @property
     def dim(self) -> int:
-        return {"seg": 1, "quad": 2, "tri": 2, "hex": 3}[self.value]
+        return {"seg": 1, "quad": 2, "tri": 2, "hex": 3, "prism": 3, "tet": 3}[self.value]
 
 
 def as_shape(s) -> Shape:
