@@ -56,6 +56,29 @@ typedef struct sipg_plan_desc {
   const int64_t* rec_ext;      /* n_records x 2: neighbour face-plane offset | n_o << 48; E tables */
 } sipg_plan_desc;
 
+/* Config 4 (3-D hybrid hex / prism / tet; not in the reference): the plan of
+ * paper_2504_03573_b200/plan3d.py — element classes (shape, n_modes) with their basis tables,
+ * affine element geometry, one 96-byte slot per (element, coupling) (face, trace map, tau,
+ * surface Jacobian, metric-normal vector, published-trace offsets).  The same reference
+ * interfaces are replaced (HelmholtzOperator.__init__ / lhs_eval, sipg.py:234-281, 558-602);
+ * sipg_apply / sipg_apply_host / sipg_cg / sipg_plan_destroy accept the resulting plan. */
+typedef struct sipg_h3_desc {
+  int32_t abi_version;      /* SIPG_H3_ABI_VERSION of the library (1) */
+  int32_t slot_bytes;       /* 96 */
+  int32_t n_classes;
+  int32_t class_words;      /* 16 int32 per class */
+  int64_t n_elements, n_dofs, n_slots, n_tables, n_pub;
+  double lambda;
+  const int32_t* class_desc;   /* n_classes x 16 */
+  const int32_t* class_elems;  /* n_elements: element ids grouped by class */
+  const int64_t* dof_off;      /* n_elements + 1 */
+  const double* elem_geom;     /* n_elements x 8: |det J|, S = (dxi/dx)(dxi/dx)^T (6), pad */
+  const int64_t* slot_off;     /* n_elements + 1: slots of element e are [slot_off[e], slot_off[e+1]) */
+  const void* slots;           /* n_slots x 96 bytes */
+  const double* tables;        /* basis tables, trace weights, trace maps */
+} sipg_h3_desc;
+int sipg_h3_plan_create(const sipg_h3_desc* desc, sipg_plan** plan);
+
 /* Build the device-resident plan (uploads all tables). */
 int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);
 

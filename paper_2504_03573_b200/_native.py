@@ -21,7 +21,7 @@ EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destr
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
            "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply", "sipg_plan_n_dofs", "sipg_cg",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
-           "sipg_apply_role"]
+           "sipg_apply_role", "sipg_h3_plan_create"]
 
 
 class SolveReportC(ctypes.Structure):
@@ -45,6 +45,19 @@ class PlanDesc(ctypes.Structure):
     ]
 
 
+class H3Desc(ctypes.Structure):
+    """sipg_h3_desc (include/sipg.h): config-4 hybrid hex / prism / tet plans."""
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("slot_bytes", ctypes.c_int32),
+        ("n_classes", ctypes.c_int32), ("class_words", ctypes.c_int32),
+        ("n_elements", ctypes.c_int64), ("n_dofs", ctypes.c_int64), ("n_slots", ctypes.c_int64),
+        ("n_tables", ctypes.c_int64), ("n_pub", ctypes.c_int64), ("lam", ctypes.c_double),
+        ("class_desc", ctypes.c_void_p), ("class_elems", ctypes.c_void_p), ("dof_off", ctypes.c_void_p),
+        ("elem_geom", ctypes.c_void_p), ("slot_off", ctypes.c_void_p), ("slots", ctypes.c_void_p),
+        ("tables", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -58,6 +71,7 @@ def load() -> ctypes.CDLL:
     lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.sipg_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)]
+    lib.sipg_h3_plan_create.argtypes = [ctypes.POINTER(H3Desc), ctypes.POINTER(vp)]
     lib.sipg_plan_create.restype = ctypes.c_int
     lib.sipg_apply.argtypes = [vp, vp, vp, vp]
     lib.sipg_apply.restype = ctypes.c_int
@@ -114,6 +128,9 @@ class NativePlan:
 
     def __init__(self, pb):
         lib = load()
+        if getattr(pb, "is_h3", False):
+            self._init_h3(lib, pb)
+            return
         self._keep = [
             np.ascontiguousarray(pb.class_desc, dtype=np.int32),
             np.ascontiguousarray(pb.class_elems, dtype=np.int32),
@@ -146,6 +163,31 @@ class NativePlan:
         self.n_dofs = pb.n_dofs
         self.n_classes = int(cd.shape[0])
         self._keep = None          # tables now live on the device
+
+    def _init_h3(self, lib, pb):
+        from .plan3d import CD3_WORDS, H3_ABI_VERSION, SLOT
+        keep = [np.ascontiguousarray(pb.class_desc, dtype=np.int32),
+                np.ascontiguousarray(pb.class_elems, dtype=np.int32),
+                np.ascontiguousarray(pb.dof_off, dtype=np.int64),
+                np.ascontiguousarray(pb.egeo, dtype=np.float64),
+                np.ascontiguousarray(pb.slot_off, dtype=np.int64),
+                np.ascontiguousarray(pb.slots),
+                np.ascontiguousarray(pb.tables, dtype=np.float64)]
+        d = H3Desc()
+        d.abi_version, d.slot_bytes = H3_ABI_VERSION, SLOT.itemsize
+        d.n_classes, d.class_words = keep[0].shape[0], CD3_WORDS
+        d.n_elements, d.n_dofs, d.n_slots = keep[1].size, pb.n_dofs, keep[5].size
+        d.n_tables, d.n_pub, d.lam = keep[6].size, pb.n_pub, pb.lam
+        for name, arr in zip(["class_desc", "class_elems", "dof_off", "elem_geom", "slot_off", "slots", "tables"],
+                             keep):
+            setattr(d, name, arr.ctypes.data)
+        h = ctypes.c_void_p()
+        check(lib.sipg_h3_plan_create(ctypes.byref(d), ctypes.byref(h)), "sipg_h3_plan_create")
+        self._lib = lib
+        self.handle = h
+        self.n_dofs = pb.n_dofs
+        self.n_classes = int(keep[0].shape[0])
+        self._keep = None
 
     def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
         check(self._lib.sipg_apply(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),

@@ -15,7 +15,7 @@ BUILD = PKG / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(PKG.parent / "include")]
-SOURCES = ["sipg_capi.cu", "sipg_quad.cu", "sipg_tri.cu", "sipg_hex.cu", "sipg_krylov.cu"]
+SOURCES = ["sipg_capi.cu", "sipg_quad.cu", "sipg_tri.cu", "sipg_hex.cu", "sipg_krylov.cu", "sipg_h3.cu"]
 
 
 def _nvcc():

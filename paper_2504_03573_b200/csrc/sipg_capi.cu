@@ -10,6 +10,7 @@
 #include "sipg_plan.h"
 #include "../../include/sipg.h"
 #include "sipg_registry.h"
+#include "sipg_h3_registry.h"
 
 namespace {
 
@@ -110,7 +111,17 @@ int upload(const T* host, int64_t count, T** dev) {
 
 }  // namespace
 
+// config-4 hybrid hex / prism / tet plan (sipg_h3.cuh)
+struct H3State {
+  H3Plan hp{};
+  std::vector<int32_t> cd;
+  std::vector<const H3Entry*> kern;
+  void* bufs[7] = {};
+  double* pub = nullptr;
+};
+
 struct sipg_plan {
+  H3State* h3 = nullptr;
   DevPlan dp;
   int n_cls;
   int64_t n_dofs;
@@ -434,9 +445,101 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   return 0;
 }
 
+int h3_apply(sipg_plan* p, const double* x_dev, double* y_dev, cudaStream_t s) {
+  H3State* h = p->h3;
+  for (int pass = 0; pass < 2; ++pass) {   // publish every class's traces, then apply
+    for (int c = 0; c < p->n_cls; ++c) {
+      const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+      if (count == 0) continue;
+      const H3Entry* k = h->kern[c];
+      if (pass == 0)
+        k->pub<<<count, k->threads, k->smem_pub, s>>>(h->hp, c, x_dev, y_dev);
+      else
+        k->apply<<<count, k->threads, k->smem_apply, s>>>(h->hp, c, x_dev, y_dev);
+      ++p->launches;
+    }
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
+  if (!d || !out) return fail(SIPG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (d->abi_version != SIPG_H3_ABI_VERSION) return fail(SIPG_ERR_ARG, "hybrid plan ABI version mismatch");
+  if (d->slot_bytes != (int32_t)sizeof(H3Slot) || d->class_words != CD3_WORDS)
+    return fail(SIPG_ERR_ARG, "hybrid plan layout mismatch");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SIPG_ERR_NO_DEVICE, "no CUDA device available (the SIP apply has no CPU fallback)");
+  static const std::vector<H3Entry> table = [] {
+    std::vector<H3Entry> v;
+    sipg_register_h3(v);
+    return v;
+  }();
+  sipg_plan* p = new sipg_plan();
+  memset(p->bufs, 0, sizeof(p->bufs));
+  p->h3 = new H3State();
+  H3State* h = p->h3;
+  p->n_cls = d->n_classes;
+  p->n_dofs = d->n_dofs;
+  h->cd.assign(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD3_WORDS);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    const H3Entry* k = nullptr;
+    for (const auto& e : table)
+      if (e.shape == cd[CD3_SHAPE] && e.n == cd[CD3_N] && cd[CD3_Q] == e.n + 1) k = &e;
+    if (!k) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a hybrid kernel for shape=" + std::to_string(cd[CD3_SHAPE]) +
+                                            " n_modes=" + std::to_string(cd[CD3_N]));
+    }
+    h->kern.push_back(k);
+  }
+  int rc = 0;
+  int32_t *cd_d, *ce_d;
+  int64_t *dof_d, *so_d;
+  double *eg_d, *tab_d;
+  H3Slot* sl_d;
+  if ((rc = upload(d->class_desc, (int64_t)d->n_classes * CD3_WORDS, &cd_d)) ||
+      (rc = upload(d->class_elems, d->n_elements, &ce_d)) || (rc = upload(d->dof_off, d->n_elements + 1, &dof_d)) ||
+      (rc = upload(d->elem_geom, d->n_elements * H3_EGEO, &eg_d)) ||
+      (rc = upload(d->slot_off, d->n_elements + 1, &so_d)) ||
+      (rc = upload((const H3Slot*)d->slots, d->n_slots, &sl_d)) || (rc = upload(d->tables, d->n_tables, &tab_d))) {
+    sipg_plan_destroy(p);
+    return rc;
+  }
+  void* b[7] = {cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d};
+  memcpy(h->bufs, b, sizeof(b));
+  if (d->n_pub > 0) {
+    cudaError_t e = cudaMalloc((void**)&h->pub, sizeof(double) * d->n_pub);
+    if (e != cudaSuccess) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, std::string("published-trace buffer: ") + cudaGetErrorString(e));
+    }
+  }
+  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda};
+  for (const H3Entry* k : h->kern) {
+    cudaError_t e1 = cudaFuncSetAttribute((const void*)k->pub, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)k->smem_pub);
+    cudaError_t e2 = cudaFuncSetAttribute((const void*)k->apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)k->smem_apply);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, "cudaFuncSetAttribute (hybrid kernels)");
+    }
+  }
+  *out = p;
+  return 0;
+}
+
 int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->h3) {
+    if (role > 0) return 0;   // single-GPU hybrid plans have no halo role
+    return h3_apply(p, x_dev, y_dev, s);
+  }
   if (p->need_planes) {
     // publish face planes: role 0 (or all) -> every locally owned element; role 1 -> the
     // ghost layer (its coefficients have just arrived); role -1 -> everything
@@ -468,6 +571,7 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
 
 int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev || cls < 0 || cls >= p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) return fail(SIPG_ERR_UNSUPPORTED, "per-class apply is not available on hybrid 3-D plans");
   const int count = p->cd_host[cls * CD_WORDS + CD_COUNT];
   if (count == 0) return 0;
   const KernelEntry* k = p->kern[cls];
@@ -479,6 +583,12 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
 
 int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
   if (!p || cls < 0 || cls >= p->n_cls || !out6) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) {   // shape codes 3/4/5 = hex/prism/tet of a hybrid plan; kernel kind 8
+    const int32_t* cd = p->h3->cd.data() + cls * CD3_WORDS;
+    out6[0] = 3 + cd[CD3_SHAPE]; out6[1] = cd[CD3_N]; out6[2] = cd[CD3_Q]; out6[3] = 0;
+    out6[4] = cd[CD3_COUNT]; out6[5] = 8;
+    return 0;
+  }
   const int32_t* cd = p->cd_host.data() + cls * CD_WORDS;
   out6[0] = cd[CD_SHAPE]; out6[1] = cd[CD_N]; out6[2] = cd[CD_Q0]; out6[3] = cd[CD_GEOM]; out6[4] = cd[CD_COUNT];
   out6[5] = p->kern[cls]->kind;
@@ -576,6 +686,10 @@ int64_t sipg_plan_launches(const sipg_plan* p) { return p ? p->launches : -1; }
 int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   if (!p) return -1;
   int k = 0;
+  if (p->h3) {
+    for (int c = 0; c < p->n_cls; ++c) k += p->h3->cd[c * CD3_WORDS + CD3_COUNT] > 0 ? 2 : 0;
+    return k;
+  }
   for (int c = 0; c < p->n_cls; ++c) {
     if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->cd_host[c * CD_WORDS + CD_ROLE] != 2) ++k;
     if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->planes_k.size() > (size_t)c && p->planes_k[c]) ++k;
@@ -597,6 +711,13 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
 
 int sipg_plan_destroy(sipg_plan* p) {
   if (!p) return 0;
+  if (p->h3) {
+    for (void* b : p->h3->bufs)
+      if (b) cudaFree(b);
+    if (p->h3->pub) cudaFree(p->h3->pub);
+    delete p->h3;
+    p->h3 = nullptr;
+  }
   for (void* b : p->bufs)
     if (b) cudaFree(b);
   if (p->planes) cudaFree(p->planes);

@@ -51,6 +51,7 @@ class HybridMesh3D:
     elements: list
     interfaces: list
     dim: int = 3
+    is_hybrid3d = True
 
     @property
     def n_elements(self) -> int:

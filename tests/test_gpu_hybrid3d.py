@@ -1,0 +1,77 @@
+"""Config 4 on the GPU (through the C-ABI): the hybrid hex / prism / tet apply against the CPU
+oracle (oracle/hybrid3d.py; parity unpinned by the reference, which has no prism / tet —
+SURVEY.md a18), bar: relative max-norm <= 1e-12 (BASELINE north_star)."""
+import numpy as np
+import pytest
+
+from conftest import rel_maxnorm
+from oracle import hybrid3d as h
+from paper_2504_03573_b200 import configs
+from paper_2504_03573_b200.mesh import OrderMap
+from paper_2504_03573_b200.mesh3d import generate_hybrid3d
+from paper_2504_03573_b200.sipg import HelmholtzOperator, HelmholtzParams
+
+pytestmark = pytest.mark.gpu
+KW = dict(basis_kind="modified_modal", tau_rule="baseline")
+
+
+def _oracle(mesh, om, lam=1.0):
+    return h.HybridOracle3D(mesh.shapes, [el.verts for el in mesh.elements], mesh.vertices,
+                            om.n_modes, om.n_quad, lambda_=lam)
+
+
+@pytest.mark.parametrize("nx,seed", [(2, 0), (3, 1), (4, 2), (5, 3)])
+def test_cfg4_matches_oracle(nx, seed):
+    case = configs.build_case("cfg4", nx, seed=seed)
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    x = case.draw_x(op.n_dofs)
+    ref = _oracle(case.mesh, case.order_map)
+    assert np.array_equal(op._dof_off, ref.dof_off)
+    assert rel_maxnorm(op(x), ref(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("p_hex,p_prism,P", [(0.0, 0.0, 2), (0.0, 1.0, 3), (1.0, 1.0, 4), (0.0, 0.0, 6),
+                                             (0.0, 1.0, 6), (0.5, 0.5, 1)])
+def test_single_shape_and_order_meshes(p_hex, p_prism, P):
+    m = generate_hybrid3d(3, np.random.default_rng(7), p_hex=p_hex, p_prism=p_prism)
+    om = OrderMap(np.full(m.n_elements, P + 1), np.full(m.n_elements, P + 2))
+    op = HelmholtzOperator(m, om, **KW)
+    x = np.random.default_rng(8).uniform(-1, 1, op.n_dofs)
+    assert rel_maxnorm(op(x), _oracle(m, om)(x)) <= 1e-12
+
+
+def test_linearity_zero_and_determinism():
+    case = configs.build_case("cfg4", 6, seed=4)
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    rng = np.random.default_rng(1)
+    a, b = rng.uniform(-1, 1, op.n_dofs), rng.uniform(-1, 1, op.n_dofs)
+    ya, yb, yab = op(a), op(b), op(2.0 * a - 3.0 * b)
+    assert rel_maxnorm(yab, 2.0 * ya - 3.0 * yb) <= 1e-13
+    assert not np.any(op(np.zeros(op.n_dofs)))
+    assert np.array_equal(op(a), ya)
+
+
+def _global_poly_coeffs(op_ref, fun):
+    c = np.zeros(op_ref.n_dofs)
+    for e, ex in enumerate(op_ref.exps):
+        x = op_ref.x0[e] + (ex.xi + 1.0) @ op_ref.F[e].T
+        c[op_ref.dof_off[e]:op_ref.dof_off[e + 1]] = np.linalg.lstsq(ex.Phi, fun(x), rcond=None)[0]
+    return c
+
+
+def test_consistency_on_global_quadratic_lambda0():
+    """Size-independent property: with lambda = 0 and u a global quadratic, every element without a
+    boundary face sees exactly -lap(u) * int(phi_i) (Galerkin consistency of SIP)."""
+    case = configs.build_case("cfg4", 8, seed=9)
+    op = HelmholtzOperator(case.mesh, case.order_map, params=HelmholtzParams(lambda_=0.0), **KW)
+    ref = _oracle(case.mesh, case.order_map, lam=0.0)
+    c = _global_poly_coeffs(ref, lambda x: x[:, 0] ** 2 + 2 * x[:, 1] ** 2 - x[:, 2] * x[:, 0] + x[:, 1])
+    y = op(c)
+    bnd = {l[0] for l, r, _ in ref.couplings if r is None}
+    worst = 0.0
+    for e, ex in enumerate(ref.exps):
+        if e in bnd:
+            continue
+        ip = ex.Phi.T @ (ex.ref_w * ref.detJ[e])
+        worst = max(worst, np.abs(y[ref.dof_off[e]:ref.dof_off[e + 1]] + 6.0 * ip).max())
+    assert worst < 1e-10
