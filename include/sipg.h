@@ -92,7 +92,9 @@ int sipg_apply(sipg_plan* plan, const double* x_dev, double* y_dev, void* stream
 int sipg_apply_role(sipg_plan* plan, int32_t role, const double* x_dev, double* y_dev, void* stream);
 
 /* One element class only (instrumentation: per-kernel timing).  Classes are
- * independent, so applying every class once equals sipg_apply. */
+ * independent, so applying every class once equals sipg_apply.  Hybrid 3-D plans
+ * (sipg_h3_plan_create) have 2 n_classes launch units: the publish kernels
+ * (0..n-1) must run before the apply kernels (n..2n-1). */
 int sipg_apply_class(sipg_plan* plan, int32_t cls, const double* x_dev, double* y_dev, void* stream);
 /* (shape, n_modes, n_quad, geometry mode, element count, kernel kind) of a class. */
 int sipg_plan_class_info(const sipg_plan* plan, int32_t cls, int32_t* out6);

@@ -186,7 +186,7 @@ class NativePlan:
         self._lib = lib
         self.handle = h
         self.n_dofs = pb.n_dofs
-        self.n_classes = int(keep[0].shape[0])
+        self.n_classes = 2 * int(keep[0].shape[0])   # launch units: publish kernels, then apply kernels
         self._keep = None
 
     def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:

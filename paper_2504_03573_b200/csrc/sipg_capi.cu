@@ -570,8 +570,22 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
 }
 
 int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
-  if (!p || !x_dev || !y_dev || cls < 0 || cls >= p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
-  if (p->h3) return fail(SIPG_ERR_UNSUPPORTED, "per-class apply is not available on hybrid 3-D plans");
+  if (!p || !x_dev || !y_dev || cls < 0 || (cls >= p->n_cls && !p->h3)) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) {   // hybrid plans: launch units 0..n-1 = publish kernels, n..2n-1 = apply kernels
+    if (cls >= 2 * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+    H3State* h = p->h3;
+    const int c = cls % p->n_cls;
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    if (count == 0) return 0;
+    const H3Entry* k = h->kern[c];
+    if (cls < p->n_cls)
+      k->pub<<<count, k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+    else
+      k->apply<<<count, k->threads, k->smem_apply, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+    ++p->launches;
+    CK(cudaGetLastError());
+    return 0;
+  }
   const int count = p->cd_host[cls * CD_WORDS + CD_COUNT];
   if (count == 0) return 0;
   const KernelEntry* k = p->kern[cls];
@@ -582,11 +596,11 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
 }
 
 int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
-  if (!p || cls < 0 || cls >= p->n_cls || !out6) return fail(SIPG_ERR_ARG, "bad argument");
-  if (p->h3) {   // shape codes 3/4/5 = hex/prism/tet of a hybrid plan; kernel kind 8
-    const int32_t* cd = p->h3->cd.data() + cls * CD3_WORDS;
+  if (!p || cls < 0 || !out6 || cls >= (p->h3 ? 2 : 1) * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) {   // shape codes 3/4/5 = hex/prism/tet of a hybrid plan; kernel kind 8 publish, 9 apply
+    const int32_t* cd = p->h3->cd.data() + (cls % p->n_cls) * CD3_WORDS;
     out6[0] = 3 + cd[CD3_SHAPE]; out6[1] = cd[CD3_N]; out6[2] = cd[CD3_Q]; out6[3] = 0;
-    out6[4] = cd[CD3_COUNT]; out6[5] = 8;
+    out6[4] = cd[CD3_COUNT]; out6[5] = cls < p->n_cls ? 8 : 9;
     return 0;
   }
   const int32_t* cd = p->cd_host.data() + cls * CD_WORDS;

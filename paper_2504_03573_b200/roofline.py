@@ -15,7 +15,39 @@ import numpy as np
 from . import layout as L
 
 
+def _per_class_h3(pb):
+    """Hybrid 3-D plans (plan3d.py): one row per launch unit — the publish kernels (recomputed
+    BwdTrans / PhysDeriv / traces: not part of the algorithmic count, 0 bytes / flops) followed by
+    the apply kernels, which carry the element's whole algorithmic count.  BwdTrans of the
+    collapsed shapes, stage by stage: prism n_tri n q + n_tri q^2 + (n+1) q^3, tet
+    n_c q + (n_tri+1) q^2 + (n+1) q^3."""
+    from .plan3d import CD3_COUNT, CD3_N, CD3_NC, CD3_Q, CD3_SHAPE
+    names = {0: "hex", 1: "prism", 2: "tet"}
+    nfaces = {0: 6, 1: 5, 2: 4}
+    rows = []
+    for unit in ("pub", "apply"):
+        for ci, cd in enumerate(pb.class_desc):
+            s, n, q, nc, cnt = int(cd[CD3_SHAPE]), int(cd[CD3_N]), int(cd[CD3_Q]), int(cd[CD3_NC]), int(cd[CD3_COUNT])
+            ntri = n * (n + 1) // 2
+            if s == 0:
+                bt = q * n ** 3 + q * q * n * n + q ** 3 * n
+            elif s == 1:
+                bt = ntri * n * q + ntri * q * q + (n + 1) * q ** 3
+            else:
+                bt = nc * q + (ntri + 1) * q * q + (n + 1) * q ** 3
+            d = 3
+            fl = 2 * (2 * bt + 2 * d * q ** (d + 1) + (2 * d * d + 1) * q ** d)
+            gb = 8 * (d * d + 1) + nfaces[s] * 8 * (d + 2)
+            a = unit == "apply"
+            rows.append({"cls": ci, "shape": names[s], "n": n, "q": q, "geom": 0, "count": cnt,
+                         "unit": unit, "dofs": cnt * nc if a else 0,
+                         "bytes": cnt * (16 * nc + gb) if a else 0, "flops": cnt * fl if a else 0})
+    return rows
+
+
 def per_class(pb):
+    if getattr(pb, "is_h3", False):
+        return _per_class_h3(pb)
     rows = []
     for ci, (c, geom, ids) in enumerate(pb.class_list):
         d, n, q = c.dim, c.n, c.nq[0]
