@@ -116,6 +116,7 @@ struct H3State {
   H3Plan hp{};
   std::vector<int32_t> cd;
   std::vector<const H3Entry*> kern;
+  std::vector<int> grid_pub, grid_apply;   // persistent grids: min(count, SMs x resident CTAs)
   void* bufs[7] = {};
   double* pub = nullptr;
 };
@@ -453,9 +454,9 @@ int h3_apply(sipg_plan* p, const double* x_dev, double* y_dev, cudaStream_t s) {
       if (count == 0) continue;
       const H3Entry* k = h->kern[c];
       if (pass == 0)
-        k->pub<<<count, k->threads, k->smem_pub, s>>>(h->hp, c, x_dev, y_dev);
+        k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, s>>>(h->hp, c, x_dev, y_dev);
       else
-        k->apply<<<count, k->threads, k->smem_apply, s>>>(h->hp, c, x_dev, y_dev);
+        k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, s>>>(h->hp, c, x_dev, y_dev);
       ++p->launches;
     }
   }
@@ -529,6 +530,24 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       return fail(SIPG_ERR_CUDA, "cudaFuncSetAttribute (hybrid kernels)");
     }
   }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int c = 0; c < p->n_cls; ++c) {
+    const H3Entry* k = h->kern[c];
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    int occ_p = 1, occ_a = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, (const void*)k->pub, k->threads, k->smem_pub) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)k->apply, k->threads, k->smem_apply) !=
+            cudaSuccess ||
+        occ_p <= 0 || occ_a <= 0) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, "occupancy query failed for a hybrid kernel");
+    }
+    h->grid_pub.push_back(count < occ_p * sms ? count : occ_p * sms);
+    h->grid_apply.push_back(count < occ_a * sms ? count : occ_a * sms);
+  }
   *out = p;
   return 0;
 }
@@ -579,9 +598,9 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
     if (count == 0) return 0;
     const H3Entry* k = h->kern[c];
     if (cls < p->n_cls)
-      k->pub<<<count, k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+      k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
     else
-      k->apply<<<count, k->threads, k->smem_apply, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+      k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
     ++p->launches;
     CK(cudaGetLastError());
     return 0;

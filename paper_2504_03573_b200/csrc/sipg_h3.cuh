@@ -6,14 +6,16 @@
 // stdregions.py:266-383; restated and property-tested in oracle/hybrid3d.py).  Plan layout:
 // paper_2504_03573_b200/plan3d.py.
 //
-// Two kernels per element class (shape, n), one CTA per element:
-//   k_h3<S, N, true>  (publish): BwdTrans -> PhysDeriv -> per interior coupling, u and n.grad u on
-//                     the element's own face grid (endpoint rows along the fixed axis), mapped to
-//                     the coupling's trace points (identity or a dense nt x q^2 map) -> published.
-//   k_h3<S, N, false> (apply):   the same own traces, the partner's published traces, the SIP flux
-//                     (jump, average, penalty), lifted by the transposed map and the transposed
-//                     endpoint rows into the volume-point accumulators, plus the volume terms
-//                     lambda jw u and jw G G^T grad u; then one transposed pass
+// Two kernels per element class (shape, n), persistent CTAs, one element at a time per CTA:
+//   k_h3<S, N, true>  (publish): BwdTrans -> per interior coupling, u and n.grad u on the element's
+//                     own face grid (endpoint rows E and E D along the fixed axis, collocation along
+//                     the face for the tangential derivatives), mapped to the coupling's trace
+//                     points (identity, tensor X (x) Y, or dense for subface quads) -> published.
+//   k_h3<S, N, false> (apply):   BwdTrans, PhysDeriv, own traces of every coupling at once, the
+//                     volume terms lambda jw u and jw G G^T grad u in place, then per batch of
+//                     couplings the partner's published traces, the SIP flux (jump, average,
+//                     penalty), the transposed maps and the transposed endpoint rows into the
+//                     volume-point accumulators; one transposed pass
 //                     y = Phi^T (W0 + sum_k D_k^T W_k)   (IProduct + IProductDeriv, sipg.py:575-582).
 // Every element's y is written by exactly one CTA (no atomics, deterministic).
 #pragma once
@@ -26,14 +28,15 @@ enum { H3_HEX = 0, H3_PRISM = 1, H3_TET = 2 };
 #define CD3_WORDS 16
 enum {
   CD3_SHAPE = 0, CD3_N, CD3_Q, CD3_NC, CD3_COUNT, CD3_ELEM_OFF, CD3_T_PTS, CD3_T_D, CD3_T_W, CD3_T_E,
-  CD3_T_A, CD3_T_B, CD3_T_C, CD3_ROLE
+  CD3_T_A, CD3_T_B, CD3_T_C, CD3_ROLE, CD3_T_R, CD3_T_ED
 };
+enum { MAP_ID = 0, MAP_TENSOR = 1, MAP_DENSE = 2, MAP_ROW = 3 };
 #define H3_EGEO 8
 
 struct H3Slot {   // numpy dtype plan3d.SLOT
-  int32_t face, kind, nt, mkind, moff, wtoff, elem, partner;
+  int32_t face, kind, nt, mkind, moff, moff2, nab, wtoff, elem, partner;
   int64_t pub_self, pub_other;
-  double tau, sJ, v[3], pad;
+  double tau, sJ, v[3];
 };
 static_assert(sizeof(H3Slot) == 96, "H3Slot layout");
 
@@ -64,11 +67,14 @@ struct Cfg {
   static constexpr int S1 = S == H3_HEX ? N * N * Q : NPM * Q;
   static constexpr int S2 = S == H3_HEX ? N * Q2 : NG * Q2;
   static constexpr int NCP = (NC + 1) & ~1;
-  static constexpr int NI = 4 * NPM + 4 + NC;                        // int tables
-  static constexpr int doubles(bool pub) {
-    return NCP + 4 * Q3 + (pub ? 0 : 4 * Q3) + S1 + S2 + 5 * Q2 + 4 * TMAX;
+  static constexpr int NI = 4 * NPM + 4 + NC + 16;                   // int tables + batch offsets
+  static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);   // slots per element
+  static constexpr int SB = 4;                                       // slots per map batch
+  static constexpr int SLOTD = 12;                                   // doubles per slot header
+  static constexpr int doubles() {
+    return NCP + 4 * Q3 + S1 + S2 + NSMAX * (2 * Q2 + SLOTD) + SB * 4 * TMAX;
   }
-  static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
+  static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
 };
 
 // (fixed axis, side, run axis 0, run axis 1) per shape and local face (plan3d.FACES)
@@ -78,25 +84,41 @@ __constant__ int8_t c_faces[3][6][4] = {
     {{2, -1, 0, 1}, {1, -1, 0, 2}, {0, 1, 1, 2}, {0, -1, 1, 2}, {0, 0, 0, 0}, {0, 0, 0, 0}},
 };
 
-// collapse chain d eta_k / d xi_j (upper triangular, c22 = 1, c10 = c20 = c21 = 0)
+// collapse chain d eta_k / d xi_j (upper triangular, c22 = 1, c10 = c20 = c21 = 0) from
+// p0 = 1 + eta0, p1 = 1 + eta1, r1 = 1 / (1 - eta1), r2 = 1 / (1 - eta2)
 struct Chain {
   double c00, c01, c02, c11, c12;
 };
 template <int S>
-__device__ __forceinline__ Chain chain(double e0, double e1, double e2) {
+__device__ __forceinline__ Chain chain_t(double p0, double p1, double r1, double r2) {
   Chain c{1.0, 0.0, 0.0, 1.0, 0.0};
   if (S == H3_PRISM) {
-    const double r = 1.0 / (1.0 - e2);
-    c.c00 = 2.0 * r;
-    c.c02 = (1.0 + e0) * r;
+    c.c00 = 2.0 * r2;
+    c.c02 = p0 * r2;
   } else if (S == H3_TET) {
-    const double r2 = 1.0 / (1.0 - e2), r12 = r2 / (1.0 - e1);
+    const double r12 = r1 * r2;
     c.c00 = 4.0 * r12;
-    c.c01 = c.c02 = 2.0 * (1.0 + e0) * r12;
+    c.c01 = c.c02 = 2.0 * p0 * r12;
     c.c11 = 2.0 * r2;
-    c.c12 = (1.0 + e1) * r2;
+    c.c12 = p1 * r2;
   }
   return c;
+}
+
+// chain at own-face-grid point (ia, ib) of a face (fixed axis fx at side sd, run axes ra, rb)
+template <int S>
+__device__ __forceinline__ Chain face_chain(const double* __restrict__ pts, const double* __restrict__ R, int Q,
+                                            int fx, int sd, int ra, int rb, int ia, int ib) {
+  if (S == H3_HEX) return Chain{1.0, 0.0, 0.0, 1.0, 0.0};
+  // eta = +1 occurs only on axis 0 (tet / prism slanted face), where r is unused
+  const double ea = __ldg(pts + ra * Q + ia), eb = __ldg(pts + rb * Q + ib);
+  const double rra = __ldg(R + ra * Q + ia), rrb = __ldg(R + rb * Q + ib);
+  const double es = (double)sd, rs = sd < 0 ? 0.5 : 0.0;
+  const double e0 = fx == 0 ? es : (ra == 0 ? ea : eb);
+  const double e1 = fx == 1 ? es : (ra == 1 ? ea : eb);
+  const double r1 = fx == 1 ? rs : (ra == 1 ? rra : rrb);
+  const double r2 = fx == 2 ? rs : (ra == 2 ? rra : rrb);
+  return chain_t<S>(1.0 + e0, 1.0 + e1, r1, r2);
 }
 
 // group of triangle pseudo-mode (i, j) (plan tri_tables gid): row 0 -> 0 except (0,1) -> 1,
@@ -277,183 +299,401 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// per-element shared-memory layout
+template <int S, int N>
+struct Lay {
+  using C = Cfg<S, N>;
+  double *c, *u, *du, *s1, *s2, *F, *hdr, *tb;
+  int *gstart, *gmem, *gof, *coff, *mofr;
+  __device__ Lay(double* sm) {
+    c = sm;
+    u = c + C::NCP;
+    du = u + C::Q3;
+    s1 = du + 3 * C::Q3;
+    s2 = s1 + C::S1;
+    F = s2 + C::S2;                      // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    hdr = F + C::NSMAX * 2 * C::Q2;      // [NSMAX][12]: slot headers
+    tb = hdr + C::NSMAX * C::SLOTD;      // [SB][4][TMAX]: trace values / flux / map temporaries
+    gstart = (int*)(tb + C::SB * 4 * TMAX);
+    gmem = gstart + C::NPM + 2;
+    gof = gmem + C::NPM;
+    coff = gof + C::NPM;
+    mofr = coff + C::NPM + 2;
+  }
+};
+
+__device__ __forceinline__ const H3Slot& slot_hdr(const double* hdr, int s) {
+  return *reinterpret_cast<const H3Slot*>(hdr + 12 * s);
+}
+
+// which slot of a batch [b0, b0 + nb) an item belongs to, given per-slot item counts
+template <typename CountFn>
+__device__ __forceinline__ int item_slot(int b0, int nb, int& it, CountFn cnt) {
+  for (int s = b0; s < b0 + nb; ++s) {
+    const int n = cnt(s);
+    if (it < n) return s;
+    it -= n;
+  }
+  return -1;
+}
+
+template <typename CountFn>
+__device__ __forceinline__ int batch_items(int b0, int nb, CountFn cnt) {
+  int n = 0;
+  for (int s = b0; s < b0 + nb; ++s) n += cnt(s);
+  return n;
+}
+
+__device__ __forceinline__ void unpack_nab(int nab, int& n1, int& n2, int& swap) {
+  n1 = nab & 255;
+  n2 = (nab >> 8) & 255;
+  swap = (nab >> 16) & 1;
+}
+
+// own-face-grid arrays (F[s][0], F[s][1]) -> trace arrays (tb[j][0], tb[j][1]) for the slots of a
+// batch; with `pub`, the trace values go straight to the published buffer instead
+template <int Q>
+__device__ void map_forward(const double* hdr, const double* F, double* tb, int b0, int nb, const double* tab,
+                            double* pub, bool only_interior) {
+  constexpr int Q2 = Q * Q;
+  const int t = threadIdx.x;
+  auto active = [&](int s) { return !only_interior || slot_hdr(hdr, s).kind == 1; };
+  // stage 1: tensor X contraction over own axis 0; dense and identity complete here
+  auto c1 = [&](int s) -> int {
+    if (!active(s)) return 0;
+    const H3Slot& h = slot_hdr(hdr, s);
+    if (h.mkind == MAP_TENSOR) return (h.nab & 255) * Q;
+    if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
+    return h.mkind == MAP_DENSE ? h.nt : Q2;
+  };
+  const int n1tot = batch_items(b0, nb, c1);
+  for (int it0 = t; it0 < n1tot; it0 += NT) {
+    int it = it0;
+    const int s = item_slot(b0, nb, it, c1);
+    const H3Slot& h = slot_hdr(hdr, s);
+    const double* fu = F + s * 2 * Q2;
+    const double* fg = fu + Q2;
+    double* tu = tb + (s - b0) * 4 * TMAX;
+    double* tg = tu + TMAX;
+    if (h.mkind == MAP_ROW) {
+      // subface quad side: tmp[pb][i_par] = sum_i_perp Y[pb][i_perp] f(i_par, i_perp)
+      const int pb = it / Q, ipar = it % Q, perp = (h.nab >> 16) & 1;
+      const double* Yr = tab + h.moff2 + pb * Q;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int ip = 0; ip < Q; ++ip) {
+        const double m = __ldg(Yr + ip);
+        const int o = perp ? ipar * Q + ip : ip * Q + ipar;
+        a0 = fma(m, fu[o], a0);
+        a1 = fma(m, fg[o], a1);
+      }
+      tu[2 * TMAX + it] = a0;
+      tu[3 * TMAX + it] = a1;
+    } else if (h.mkind == MAP_TENSOR) {
+      const int r1 = it / Q, ib = it % Q;
+      const double* X = tab + h.moff + r1 * Q;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int ia = 0; ia < Q; ++ia) {
+        const double m = __ldg(X + ia);
+        a0 = fma(m, fu[ia * Q + ib], a0);
+        a1 = fma(m, fg[ia * Q + ib], a1);
+      }
+      tu[2 * TMAX + it] = a0;
+      tu[3 * TMAX + it] = a1;
+    } else {
+      double a0, a1;
+      if (h.mkind == MAP_DENSE) {
+        const double* M = tab + h.moff + (int64_t)it * Q2;
+        a0 = 0.0;
+        a1 = 0.0;
+        for (int a = 0; a < Q2; ++a) {
+          const double m = __ldg(M + a);
+          a0 = fma(m, fu[a], a0);
+          a1 = fma(m, fg[a], a1);
+        }
+      } else {
+        a0 = fu[it];
+        a1 = fg[it];
+      }
+      if (pub) {
+        double* dst = pub + h.pub_self;
+        dst[2 * it] = a0;
+        dst[2 * it + 1] = a1;
+      } else {
+        tu[it] = a0;
+        tg[it] = a1;
+      }
+    }
+  }
+  __syncthreads();
+  // stage 2: tensor Y contraction over own axis 1
+  auto c2 = [&](int s) -> int {
+    if (!active(s)) return 0;
+    const H3Slot& h = slot_hdr(hdr, s);
+    return (h.mkind == MAP_TENSOR || h.mkind == MAP_ROW) ? h.nt : 0;
+  };
+  const int n2tot = batch_items(b0, nb, c2);
+  if (n2tot == 0) return;
+  for (int it0 = t; it0 < n2tot; it0 += NT) {
+    int it = it0;
+    const int s = item_slot(b0, nb, it, c2);
+    const H3Slot& h = slot_hdr(hdr, s);
+    int n1, n2, sw;
+    unpack_nab(h.nab, n1, n2, sw);
+    double* tu = tb + (s - b0) * 4 * TMAX;
+    int p;
+    const double *Y, *m0, *m1;
+    if (h.mkind == MAP_ROW) {   // t[pa, pb] = sum_i_par X[pb][pa][i_par] tmp[pb][i_par]
+      const int pa = it / n2, pb = it % n2;
+      p = it;
+      Y = tab + h.moff + (pb * n1 + pa) * Q;
+      m0 = tu + 2 * TMAX + pb * Q;
+      m1 = tu + 3 * TMAX + pb * Q;
+    } else {
+      const int r1 = it / n2, r2 = it % n2;
+      p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
+      Y = tab + h.moff2 + r2 * Q;
+      m0 = tu + 2 * TMAX + r1 * Q;
+      m1 = tu + 3 * TMAX + r1 * Q;
+    }
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int ib = 0; ib < Q; ++ib) {
+      const double m = __ldg(Y + ib);
+      a0 = fma(m, m0[ib], a0);
+      a1 = fma(m, m1[ib], a1);
+    }
+    if (pub) {
+      double* dst = pub + h.pub_self;
+      dst[2 * p] = a0;
+      dst[2 * p + 1] = a1;
+    } else {
+      tu[p] = a0;
+      tu[TMAX + p] = a1;
+    }
+  }
+  __syncthreads();
+}
+
+// trace arrays (tb[j][0], tb[j][1]) -> own-face-grid arrays F[s][0], F[s][1] (transposed maps)
+template <int Q>
+__device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, int nb, const double* tab) {
+  constexpr int Q2 = Q * Q;
+  const int t = threadIdx.x;
+  auto c1 = [&](int s) -> int {
+    const H3Slot& h = slot_hdr(hdr, s);
+    if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
+    return h.mkind == MAP_TENSOR ? (h.nab & 255) * Q : 0;
+  };
+  const int n1tot = batch_items(b0, nb, c1);
+  if (n1tot > 0) {
+    for (int it0 = t; it0 < n1tot; it0 += NT) {
+      int it = it0;
+      const int s = item_slot(b0, nb, it, c1);
+      const H3Slot& h = slot_hdr(hdr, s);
+      int n1, n2, sw;
+      unpack_nab(h.nab, n1, n2, sw);
+      const int r1 = it / Q, ib = it % Q;
+      double* tv = tb + (s - b0) * 4 * TMAX;
+      double a0 = 0.0, a1 = 0.0;
+      if (h.mkind == MAP_ROW) {   // tmp[pb][i_par] = sum_pa X[pb][pa][i_par] g[pa, pb]
+        for (int pa = 0; pa < n1; ++pa) {
+          const double m = __ldg(tab + h.moff + (r1 * n1 + pa) * Q + ib);
+          a0 = fma(m, tv[pa * n2 + r1], a0);
+          a1 = fma(m, tv[TMAX + pa * n2 + r1], a1);
+        }
+        tv[2 * TMAX + it] = a0;
+        tv[3 * TMAX + it] = a1;
+        continue;
+      }
+      for (int r2 = 0; r2 < n2; ++r2) {
+        const double m = __ldg(tab + h.moff2 + r2 * Q + ib);
+        const int p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
+        a0 = fma(m, tv[p], a0);
+        a1 = fma(m, tv[TMAX + p], a1);
+      }
+      tv[2 * TMAX + it] = a0;
+      tv[3 * TMAX + it] = a1;
+    }
+    __syncthreads();
+  }
+  const int n2tot = nb * Q2;
+  for (int it0 = t; it0 < n2tot; it0 += NT) {
+    const int s = b0 + it0 / Q2, a = it0 % Q2;
+    const H3Slot& h = slot_hdr(hdr, s);
+    double* tv = tb + (s - b0) * 4 * TMAX;
+    double a0, a1;
+    if (h.mkind == MAP_ROW) {   // F(i_par, i_perp) = sum_pb Y[pb][i_perp] tmp[pb][i_par]
+      const int n2 = (h.nab >> 8) & 255, perp = (h.nab >> 16) & 1;
+      const int ipar = perp ? a / Q : a % Q, iperp = perp ? a % Q : a / Q;
+      a0 = 0.0;
+      a1 = 0.0;
+      for (int pb = 0; pb < n2; ++pb) {
+        const double m = __ldg(tab + h.moff2 + pb * Q + iperp);
+        a0 = fma(m, tv[2 * TMAX + pb * Q + ipar], a0);
+        a1 = fma(m, tv[3 * TMAX + pb * Q + ipar], a1);
+      }
+    } else if (h.mkind == MAP_TENSOR) {
+      const int n1 = h.nab & 255, ia = a / Q, ib = a % Q;
+      a0 = 0.0;
+      a1 = 0.0;
+      for (int r1 = 0; r1 < n1; ++r1) {
+        const double m = __ldg(tab + h.moff + r1 * Q + ia);
+        a0 = fma(m, tv[2 * TMAX + r1 * Q + ib], a0);
+        a1 = fma(m, tv[3 * TMAX + r1 * Q + ib], a1);
+      }
+    } else if (h.mkind == MAP_DENSE) {
+      a0 = 0.0;
+      a1 = 0.0;
+      for (int p = 0; p < h.nt; ++p) {
+        const double m = __ldg(tab + h.moff + (int64_t)p * Q2 + a);
+        a0 = fma(m, tv[p], a0);
+        a1 = fma(m, tv[TMAX + p], a1);
+      }
+    } else {
+      a0 = tv[a];
+      a1 = tv[TMAX + a];
+    }
+    F[s * 2 * Q2 + a] = a0;
+    F[s * 2 * Q2 + Q2 + a] = a1;
+  }
+  __syncthreads();
+}
+
 template <int S, int N, bool PUB>
 __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                            double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3;
   extern __shared__ double sm[];
-  double* c = sm;
-  double* u = c + C::NCP;
-  double* du = u + Q3;
-  double* W = du + 3 * Q3;
-  double* s1 = W + (PUB ? 0 : 4 * Q3);
-  double* s2 = s1 + C::S1;
-  double* gnc = s2 + C::S2;      // 3 Q2: G.n per own-face-grid point
-  double* fa = gnc + 3 * Q2;     // own-grid u, then lifted fv
-  double* fb = fa + Q2;          // own-grid n.grad u, then lifted fd
-  double* tr = fb + Q2;          // 4 TMAX: trace u, g, fv, fd
-  int* gstart = (int*)(tr + 4 * TMAX);
-  int* gmem = gstart + C::NPM + 2;
-  int* gof = gmem + C::NPM;
-  int* coff = gof + C::NPM;
-  int* mofr = coff + C::NPM + 2;
+  Lay<S, N> L(sm);
   const int t = threadIdx.x;
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
   const double* pts = P.tab + cd[CD3_T_PTS];
+  const double* Rt = P.tab + cd[CD3_T_R];
   const double* Dt = P.tab + cd[CD3_T_D];
   const double* Wr = P.tab + cd[CD3_T_W];
   const double* Et = P.tab + cd[CD3_T_E];
+  const double* EDt = P.tab + cd[CD3_T_ED];
   const double* At = P.tab + cd[CD3_T_A];
   const double* Bt = S == H3_HEX ? At : P.tab + cd[CD3_T_B];
   const double* Ct = S == H3_HEX ? At : P.tab + cd[CD3_T_C];
-  if (S != H3_HEX) build_int_tables<S, N>(gstart, gmem, gof, coff, mofr);
+  if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
   __syncthreads();
   for (int i = blockIdx.x; i < count; i += gridDim.x) {
     const int e = P.class_elems[cd[CD3_ELEM_OFF] + i];
     const int64_t dof = P.dof_off[e];
-    for (int r = t; r < C::NC; r += NT) c[r] = __ldg(x + dof + r);
+    const int64_t sb = P.slot_off[e];
+    const int ns = (int)(P.slot_off[e + 1] - sb);
+    for (int r = t; r < C::NC; r += NT) L.c[r] = __ldg(x + dof + r);
+    {
+      const double* src = reinterpret_cast<const double*>(P.slots + sb);
+      for (int r = t; r < ns * C::SLOTD; r += NT) L.hdr[r] = __ldg(src + r);
+    }
     __syncthreads();
-    bwd<S, N>(c, u, s1, s2, At, Bt, Ct, gstart, gmem, coff);
+    bwd<S, N>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
+    if (PUB) {
+      // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
+      // d/d eta_fixed (E D), collocation on the face grid for the two tangential derivatives
+      for (int it = t; it < ns * Q2; it += NT) {
+        const int s = it / Q2, a = it % Q2;
+        const H3Slot& h = slot_hdr(L.hdr, s);
+        if (h.kind != 1) continue;
+        const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
+        const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
+        const int st_f = fx == 0 ? Q2 : (fx == 1 ? Q : 1);
+        const int st_a = ra == 0 ? Q2 : (ra == 1 ? Q : 1);
+        const int st_b = rb == 0 ? Q2 : (rb == 1 ? Q : 1);
+        const double* E = Et + (fx * 2 + (sd > 0)) * Q;
+        const double* ED = EDt + (fx * 2 + (sd > 0)) * Q;
+        const int base = (a / Q) * st_a + (a % Q) * st_b;
+        double uf = 0.0, un = 0.0;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const double uv = L.u[base + k * st_f];
+          uf = fma(__ldg(E + k), uv, uf);
+          un = fma(__ldg(ED + k), uv, un);
+        }
+        L.F[s * 2 * Q2 + a] = uf;
+        L.F[s * 2 * Q2 + Q2 + a] = un;
+      }
+      __syncthreads();
+      for (int it = t; it < ns * Q2; it += NT) {
+        const int s = it / Q2, a = it % Q2;
+        const H3Slot& h = slot_hdr(L.hdr, s);
+        if (h.kind != 1) continue;
+        const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
+        const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
+        const int ia = a / Q, ib = a % Q;
+        const double* fu = L.F + s * 2 * Q2;
+        double da = 0.0, db = 0.0;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          da = fma(__ldg(Dt + ra * Q2 + ia * Q + j), fu[j * Q + ib], da);
+          db = fma(__ldg(Dt + rb * Q2 + ib * Q + j), fu[ia * Q + j], db);
+        }
+        const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
+        const double g0 = ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2];
+        const double g1 = ch.c11 * h.v[1] + ch.c12 * h.v[2];
+        const double g2 = h.v[2];
+        const double gf = fx == 0 ? g0 : (fx == 1 ? g1 : g2);
+        const double ga = ra == 0 ? g0 : (ra == 1 ? g1 : g2);
+        const double gb = rb == 0 ? g0 : (rb == 1 ? g1 : g2);
+        L.F[s * 2 * Q2 + Q2 + a] = gf * fu[Q2 + a] + ga * da + gb * db;
+      }
+      __syncthreads();
+      for (int b0 = 0; b0 < ns; b0 += C::SB)
+        map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, true);
+      continue;
+    }
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
     for (int o = t; o < Q3; o += NT) {
       const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        a0 = fma(__ldg(Dt + k0 * Q + j), u[j * Q2 + k1 * Q + k2], a0);
-        a1 = fma(__ldg(Dt + Q2 + k1 * Q + j), u[k0 * Q2 + j * Q + k2], a1);
-        a2 = fma(__ldg(Dt + 2 * Q2 + k2 * Q + j), u[k0 * Q2 + k1 * Q + j], a2);
+        a0 = fma(__ldg(Dt + k0 * Q + j), L.u[j * Q2 + k1 * Q + k2], a0);
+        a1 = fma(__ldg(Dt + Q2 + k1 * Q + j), L.u[k0 * Q2 + j * Q + k2], a1);
+        a2 = fma(__ldg(Dt + 2 * Q2 + k2 * Q + j), L.u[k0 * Q2 + k1 * Q + j], a2);
       }
-      du[o] = a0;
-      du[Q3 + o] = a1;
-      du[2 * Q3 + o] = a2;
-      if (!PUB) W[o] = W[Q3 + o] = W[2 * Q3 + o] = W[3 * Q3 + o] = 0.0;
+      L.du[o] = a0;
+      L.du[Q3 + o] = a1;
+      L.du[2 * Q3 + o] = a2;
     }
     __syncthreads();
-    const int64_t sb = P.slot_off[e], se = P.slot_off[e + 1];
-    for (int64_t si = sb; si < se; ++si) {
-      const H3Slot* sl = P.slots + si;
-      const int kind = sl->kind;
-      if (PUB && kind == 0) continue;
-      const int face = sl->face, nt = sl->nt, mk = sl->mkind;
-      const int fx = c_faces[S][face][0], sd = c_faces[S][face][1], ra = c_faces[S][face][2],
-                rb = c_faces[S][face][3];
+    // own-face-grid u and n.grad u of every slot (face_values_from_phys, endpoint rows)
+    for (int it = t; it < ns * Q2; it += NT) {
+      const int s = it / Q2, a = it % Q2;
+      const H3Slot& h = slot_hdr(L.hdr, s);
+      const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
+      const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
       const int st_f = fx == 0 ? Q2 : (fx == 1 ? Q : 1);
       const int st_a = ra == 0 ? Q2 : (ra == 1 ? Q : 1);
       const int st_b = rb == 0 ? Q2 : (rb == 1 ? Q : 1);
       const double* E = Et + (fx * 2 + (sd > 0)) * Q;
-      const double v0 = sl->v[0], v1 = sl->v[1], v2 = sl->v[2];
-      // 1. own face grid: u and n.grad u through the endpoint rows of the fixed axis (face_values_from_phys)
-      for (int a = t; a < Q2; a += NT) {
-        const int ia = a / Q, ib = a % Q;
-        const int base = ia * st_a + ib * st_b;
-        double uf = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+      const int ia = a / Q, ib = a % Q;
+      const int base = ia * st_a + ib * st_b;
+      double uf = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          const double ek = __ldg(E + k);
-          const int vi = base + k * st_f;
-          uf = fma(ek, u[vi], uf);
-          d0 = fma(ek, du[vi], d0);
-          d1 = fma(ek, du[Q3 + vi], d1);
-          d2 = fma(ek, du[2 * Q3 + vi], d2);
-        }
-        double eta[3];
-        eta[fx] = (double)sd;
-        eta[ra] = __ldg(pts + ra * Q + ia);
-        eta[rb] = __ldg(pts + rb * Q + ib);
-        const Chain ch = chain<S>(eta[0], eta[1], eta[2]);
-        const double g0 = ch.c00 * v0 + ch.c01 * v1 + ch.c02 * v2;
-        const double g1 = ch.c11 * v1 + ch.c12 * v2;
-        const double g2 = v2;
-        gnc[a] = g0;
-        gnc[Q2 + a] = g1;
-        gnc[2 * Q2 + a] = g2;
-        fa[a] = uf;
-        fb[a] = g0 * d0 + g1 * d1 + g2 * d2;
-      }
-      __syncthreads();
-      // 2. to the trace points
-      const double* M = mk ? P.tab + sl->moff : nullptr;
-      double* ut = tr;
-      double* gt = tr + TMAX;
-      if (mk) {
-        for (int p = t; p < nt; p += NT) {
-          double a0 = 0.0, a1 = 0.0;
-          const double* row = M + (int64_t)p * Q2;
-          for (int a = 0; a < Q2; ++a) {
-            const double m = __ldg(row + a);
-            a0 = fma(m, fa[a], a0);
-            a1 = fma(m, fb[a], a1);
-          }
-          ut[p] = a0;
-          gt[p] = a1;
-        }
-      } else {
-        ut = fa;
-        gt = fb;
-      }
-      __syncthreads();
-      if (PUB) {
-        double* dst = P.pub + sl->pub_self;
-        for (int p = t; p < nt; p += NT) {
-          dst[2 * p] = ut[p];
-          dst[2 * p + 1] = gt[p];
-        }
-        __syncthreads();
-        continue;
-      }
-      // 3. SIP flux at the trace points (sipg.py:622-650, 663-677): boundary jump 2u, average g
-      double* fv = tr + 2 * TMAX;
-      double* fd = tr + 3 * TMAX;
-      {
-        const double tau = sl->tau, sJ = sl->sJ;
-        const double* wt = P.tab + sl->wtoff;
-        const double* nb = kind ? P.pub + sl->pub_other : nullptr;
-        for (int p = t; p < nt; p += NT) {
-          const double un = kind ? nb[2 * p] : -ut[p];
-          const double gn = kind ? nb[2 * p + 1] : -gt[p];
-          const double j = ut[p] - un, cc = 0.5 * (gt[p] - gn);
-          const double w = sJ * __ldg(wt + p);
-          fv[p] = (tau * j - cc) * w;
-          fd[p] = -0.5 * j * w;
-        }
-      }
-      __syncthreads();
-      // 4. back to the own face grid (transposed map)
-      const double* fvA = fv;
-      const double* fdA = fd;
-      if (mk) {
-        for (int a = t; a < Q2; a += NT) {
-          double a0 = 0.0, a1 = 0.0;
-          for (int p = 0; p < nt; ++p) {
-            const double m = __ldg(M + (int64_t)p * Q2 + a);
-            a0 = fma(m, fv[p], a0);
-            a1 = fma(m, fd[p], a1);
-          }
-          fa[a] = a0;
-          fb[a] = a1;
-        }
-        fvA = fa;
-        fdA = fb;
-        __syncthreads();
-      }
-      // 5. transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep)
-      for (int o = t; o < Q * Q2; o += NT) {
-        const int k = o / Q2, a = o % Q2;
-        const int vi = (a / Q) * st_a + (a % Q) * st_b + k * st_f;
+      for (int k = 0; k < Q; ++k) {
         const double ek = __ldg(E + k);
-        const double fvk = ek * fvA[a], fdk = ek * fdA[a];
-        W[vi] += fvk;
-        W[Q3 + vi] = fma(gnc[a], fdk, W[Q3 + vi]);
-        W[2 * Q3 + vi] = fma(gnc[Q2 + a], fdk, W[2 * Q3 + vi]);
-        W[3 * Q3 + vi] = fma(gnc[2 * Q2 + a], fdk, W[3 * Q3 + vi]);
+        const int vi = base + k * st_f;
+        uf = fma(ek, L.u[vi], uf);
+        d0 = fma(ek, L.du[vi], d0);
+        d1 = fma(ek, L.du[Q3 + vi], d1);
+        d2 = fma(ek, L.du[2 * Q3 + vi], d2);
       }
-      __syncthreads();
+      const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
+      const double g0 = ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2];
+      const double g1 = ch.c11 * h.v[1] + ch.c12 * h.v[2];
+      L.F[s * 2 * Q2 + a] = uf;
+      L.F[s * 2 * Q2 + Q2 + a] = g0 * d0 + g1 * d1 + h.v[2] * d2;
     }
-    if (PUB) continue;
-    // volume terms (sipg.py:575-582): lambda jw u, jw G G^T grad u with G = chain * dxi/dx
+    __syncthreads();
+    // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du)
     {
       const double* eg = P.egeo + (int64_t)e * H3_EGEO;
       const double dJ = __ldg(eg), S00 = __ldg(eg + 1), S01 = __ldg(eg + 2), S02 = __ldg(eg + 3),
@@ -461,34 +701,93 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
       const double lam = P.lam;
       for (int o = t; o < Q3; o += NT) {
         const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-        const Chain ch = chain<S>(__ldg(pts + k0), __ldg(pts + Q + k1), __ldg(pts + 2 * Q + k2));
+        const Chain ch = chain_t<S>(1.0 + __ldg(pts + k0), 1.0 + __ldg(pts + Q + k1), __ldg(Rt + Q + k1),
+                                    __ldg(Rt + 2 * Q + k2));
         const double jw = dJ * __ldg(Wr + o);
-        const double d0 = du[o], d1 = du[Q3 + o], d2 = du[2 * Q3 + o];
+        const double d0 = L.du[o], d1 = L.du[Q3 + o], d2 = L.du[2 * Q3 + o];
         const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
         const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
         const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
-        W[o] = fma(lam * jw, u[o], W[o]);
-        W[Q3 + o] += jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
-        W[2 * Q3 + o] += jw * (ch.c11 * f1 + ch.c12 * f2);
-        W[3 * Q3 + o] += jw * f2;
+        L.u[o] *= lam * jw;
+        L.du[o] = jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
+        L.du[Q3 + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
+        L.du[2 * Q3 + o] = jw * f2;
       }
     }
     __syncthreads();
-    // T = W0 + sum_k D_k^T W_k  (into u)
+    for (int b0 = 0; b0 < ns; b0 += C::SB) {
+      const int nb = min(C::SB, ns - b0);
+      map_forward<Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, nullptr, false);
+      // SIP flux at the trace points (sipg.py:622-650, 663-677); boundary: jump 2u, average g
+      {
+        auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
+        const int tot = batch_items(b0, nb, cnt);
+        for (int it0 = t; it0 < tot; it0 += NT) {
+          int p = it0;
+          const int s = item_slot(b0, nb, p, cnt);
+          const H3Slot& h = slot_hdr(L.hdr, s);
+          double* tv = L.tb + (s - b0) * 4 * TMAX;
+          const double ut = tv[p], gt = tv[TMAX + p];
+          double un, gn;
+          if (h.kind) {
+            const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+            un = nbv.x;
+            gn = nbv.y;
+          } else {
+            un = -ut;
+            gn = -gt;
+          }
+          const double j = ut - un, cc = 0.5 * (gt - gn);
+          const double w = h.sJ * __ldg(P.tab + h.wtoff + p);
+          tv[p] = (h.tau * j - cc) * w;
+          tv[TMAX + p] = -0.5 * j * w;
+        }
+      }
+      __syncthreads();
+      map_transpose<Q>(L.hdr, L.F, L.tb, b0, nb, P.tab);
+      // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep)
+      for (int o = t; o < Q3; o += NT) {
+        const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+        for (int s = b0; s < b0 + nb; ++s) {
+          const H3Slot& h = slot_hdr(L.hdr, s);
+          const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
+          const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
+          const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
+          const double ek = __ldg(Et + (fx * 2 + (sd > 0)) * Q + kf);
+          if (ek == 0.0) continue;
+          const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
+          const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
+          const int a = ia * Q + ib;
+          const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
+          const double fv = ek * L.F[s * 2 * Q2 + a], fd = ek * L.F[s * 2 * Q2 + Q2 + a];
+          w0 += fv;
+          w1 = fma(ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2], fd, w1);
+          w2 = fma(ch.c11 * h.v[1] + ch.c12 * h.v[2], fd, w2);
+          w3 = fma(h.v[2], fd, w3);
+        }
+        L.u[o] += w0;
+        L.du[o] += w1;
+        L.du[Q3 + o] += w2;
+        L.du[2 * Q3 + o] += w3;
+      }
+      __syncthreads();
+    }
+    // T = W0 + sum_k D_k^T W_k  (in place)
     for (int o = t; o < Q3; o += NT) {
       const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-      double a = W[o];
+      double a = L.u[o];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        a = fma(__ldg(Dt + j * Q + k0), W[Q3 + j * Q2 + k1 * Q + k2], a);
-        a = fma(__ldg(Dt + Q2 + j * Q + k1), W[2 * Q3 + k0 * Q2 + j * Q + k2], a);
-        a = fma(__ldg(Dt + 2 * Q2 + j * Q + k2), W[3 * Q3 + k0 * Q2 + k1 * Q + j], a);
+        a = fma(__ldg(Dt + j * Q + k0), L.du[j * Q2 + k1 * Q + k2], a);
+        a = fma(__ldg(Dt + Q2 + j * Q + k1), L.du[Q3 + k0 * Q2 + j * Q + k2], a);
+        a = fma(__ldg(Dt + 2 * Q2 + j * Q + k2), L.du[2 * Q3 + k0 * Q2 + k1 * Q + j], a);
       }
-      u[o] = a;
+      L.u[o] = a;
     }
     __syncthreads();
-    bwd_t<S, N>(u, y + dof, s1, s2, At, Bt, Ct, gof, mofr);
+    bwd_t<S, N>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
     __syncthreads();
   }
 }

@@ -40,15 +40,24 @@ H3_ABI_VERSION = 1
 # class descriptor words (int32[CD3_WORDS]) — csrc/sipg_h3.cuh
 CD3_WORDS = 16
 (CD3_SHAPE, CD3_N, CD3_Q, CD3_NC, CD3_COUNT, CD3_ELEM_OFF, CD3_T_PTS, CD3_T_D, CD3_T_W, CD3_T_E,
- CD3_T_A, CD3_T_B, CD3_T_C, CD3_ROLE) = range(14)
+ CD3_T_A, CD3_T_B, CD3_T_C, CD3_ROLE, CD3_T_R, CD3_T_ED) = range(16)
+NSMAX = {"hex": 12, "prism": 8, "tet": 4}     # slots per element (subface quads carry two)
 
 SLOT = np.dtype([
     ("face", "<i4"), ("kind", "<i4"), ("nt", "<i4"), ("mkind", "<i4"),
-    ("moff", "<i4"), ("wtoff", "<i4"), ("elem", "<i4"), ("partner", "<i4"),
+    ("moff", "<i4"), ("moff2", "<i4"), ("nab", "<i4"), ("wtoff", "<i4"),
+    ("elem", "<i4"), ("partner", "<i4"),
     ("pub_self", "<i8"), ("pub_other", "<i8"),
-    ("tau", "<f8"), ("sJ", "<f8"), ("v", "<f8", (3,)), ("pad", "<f8"),
+    ("tau", "<f8"), ("sJ", "<f8"), ("v", "<f8", (3,)),
 ])
 assert SLOT.itemsize == 96
+# trace maps (own face grid q x q -> trace points): 0 identity, 1 tensor X (n1 x q) then Y (n2 x q)
+# with trace index r1 * n2 + r2 (or r2 * n1 + r1 when swapped; nab = n1 | n2 << 8 | swap << 16),
+# 2 dense (nt x q^2, subface quad sides)
+# 3 row (subface quad side): the trace's second axis (collapsed b) fixes the own axis `perp`
+# (Y[pb] over it), the own axis `par` varies along each trace row (X[pb][pa] over it);
+# nab = nta | ntb << 8 | perp << 16
+MAP_ID, MAP_TENSOR, MAP_DENSE, MAP_ROW = 0, 1, 2, 3
 EGEO_STRIDE = 8
 
 # faces: (fixed eta axis, side, run axes, triangular, outward normal in xi) — oracle FACES3 order
@@ -139,6 +148,7 @@ class ClassTables3:
     def __init__(self, shape, n, q):
         self.shape, self.n, self.q = shape, n, q
         kinds = AXIS_KINDS[shape]
+        self.kinds = kinds
         self.rules = [quad_rule(k, q) for k in kinds]
         self.pts = [r.points for r in self.rules]
         self.wts = [r.weights for r in self.rules]
@@ -151,7 +161,13 @@ class ClassTables3:
             w = w * 0.5 * (1.0 - eta[:, 1]) * (0.5 * (1.0 - eta[:, 2])) ** 2
         self.wref = w
         self.nc = n_coeffs(shape, n)
+        E = [lagrange_interp_matrix(p, [sd])[0] for p in self.pts for sd in (-1.0, 1.0)]
+        Dm = [diff_matrix(p) for p in self.pts]
         parts = {"pts": np.concatenate(self.pts),
+                 # 1 / (1 - eta) for the collapse chain (used on the GL collapsed axes only)
+                 "R": np.concatenate([np.where(p < 1.0, 1.0 / np.maximum(1.0 - p, 1e-300), 0.0) for p in self.pts]),
+                 "ED": np.concatenate([E[2 * a + sd] @ Dm[a] for a in range(3) for sd in (0, 1)]),
+                 "WA": np.concatenate(self.wts),
                  "D": np.concatenate([diff_matrix(p).reshape(-1) for p in self.pts]),
                  "W": w,
                  "E": np.concatenate([lagrange_interp_matrix(p, [s])[0] for p in self.pts for s in (-1.0, 1.0)])}
@@ -281,7 +297,7 @@ class Plan3DBuilder:
             self.ct.append(ct)
             cd[c, [CD3_SHAPE, CD3_N, CD3_Q, CD3_NC, CD3_COUNT, CD3_ELEM_OFF]] = [s, n, n + 1, ct.nc, ids.size, off]
             for w, name in ((CD3_T_PTS, "pts"), (CD3_T_D, "D"), (CD3_T_W, "W"), (CD3_T_E, "E"),
-                            (CD3_T_A, "A"), (CD3_T_B, "B"), (CD3_T_C, "C")):
+                            (CD3_T_A, "A"), (CD3_T_B, "B"), (CD3_T_C, "C"), (CD3_T_R, "R"), (CD3_T_ED, "ED")):
                 cd[c, w] = self.pool.add(ct.parts[name]) if name in ct.parts else -1
             elems.append(ids)
             off += ids.size
@@ -355,68 +371,102 @@ class Plan3DBuilder:
         S["partner"][sr] = ri
         right_slot = np.full(nI, -1, dtype=np.int64)
         right_slot[ri] = sr
-        # trace rules and maps, per bucket (kind, left class, left face, right class, right face)
+        # trace grids: the own face grid of the side with the larger q (ties and subfaces: the left /
+        # triangle side), its weights and surface Jacobian; that side maps by the identity, the other
+        # through the geometry (exact: every rule here integrates the face terms exactly, so the
+        # choice only moves rounding, cf. sipg.py:513-554).  A lower-q triangle side of a subface
+        # interpolates to the GL(q_quad) collapsed rule on its own triangle.
         clsL = self.class_of[le]
         clsR = np.where(inter, self.class_of[np.maximum(re_, 0)], -1)
-        bkey = np.stack([kind, clsL, lf, clsR, rf], axis=1)
+        qL = self.nq[le]
+        qR = np.where(inter, self.nq[np.maximum(re_, 0)], 0)
+        owner_right = inter & (kind == 0) & (qR > qL)
+        bkey = np.stack([kind, clsL, lf, clsR, rf, owner_right.astype(np.int64)], axis=1)
         ub, binv = np.unique(bkey, axis=0, return_inverse=True)
         binv = binv.reshape(-1)
-        for b, (kd, cl, fl, cr, fr) in enumerate(ub):
+        for b, (kd, cl, fl, cr, fr, orr) in enumerate(ub):
             sel = np.flatnonzero(binv == b)
-            ctl = self.ct[cl]
-            fixed, side, run, tri, _ = FACES[ctl.shape][fl]
             if kd == 2:
-                taxes = [ctl.pts[run[0]], ctl.pts[run[1]]]
-                wt = ctl.face_wt[fl]
+                ct = self.ct[cl]
+                S["nt"][sel] = ct.q * ct.q
+                S["wtoff"][sel] = self.pool.add(ct.face_wt[fl])
+                S["mkind"][sel], S["moff"][sel], S["moff2"][sel] = MAP_ID, -1, -1
+                continue
+            # H: trace-grid owner, O: the other side
+            if orr:
+                eH, fH, cH, eO, fO, cO, sH, sO = re_[sel], fr, cr, le[sel], fl, cl, right_slot[sel], sel
             else:
-                ctr = self.ct[cr]
-                qt = max(ctl.q, ctr.q)
-                both_gll = ctl.shape == HEX and ctr.shape == HEX
-                kk = GLL if (both_gll and not tri) else GL
-                r = quad_rule(kk, qt)
+                eH, fH, cH, eO, fO, cO, sH, sO = le[sel], fl, cl, re_[sel], fr, cr, sel, right_slot[sel]
+            ctH, ctO = self.ct[cH], self.ct[cO]
+            hfix, hside, hrun, htri, _ = FACES[ctH.shape][fH]
+            if kd == 1 and ctO.q > ctH.q:      # subface, the quad side has the larger q
+                r = quad_rule(GL, ctO.q)
                 taxes = [r.points, r.points]
-                wt = np.multiply.outer(r.weights, r.weights)
-                if tri:
-                    wt = wt * 0.5 * (1.0 - r.points)[None, :]
-                wt = wt.reshape(-1)
+                wt = np.multiply.outer(r.weights, r.weights) * 0.5 * (1.0 - r.points)[None, :]
+                self._set_tensor(S, sH, lagrange_interp_matrix(ctH.pts[hrun[0]], taxes[0]),
+                                 lagrange_interp_matrix(ctH.pts[hrun[1]], taxes[1]), False, ctH.q)
+            else:
+                taxes = [ctH.pts[hrun[0]], ctH.pts[hrun[1]]]
+                wt = ctH.face_wt[fH]
+                S["mkind"][sH], S["moff"][sH], S["moff2"][sH] = MAP_ID, -1, -1
+            wt = np.asarray(wt).reshape(-1)
             nt = wt.size
             wtoff = self.pool.add(wt)
-            S["nt"][sel] = nt
-            S["wtoff"][sel] = wtoff
-            if kd != 2:
-                S["nt"][right_slot[sel]] = nt
-                S["wtoff"][right_slot[sel]] = wtoff
-            # left map: own grid -> trace grid (tensor)
-            La = lagrange_interp_matrix(ctl.pts[run[0]], taxes[0])
-            Lb = lagrange_interp_matrix(ctl.pts[run[1]], taxes[1])
-            self._set_map(S, sel, np.kron(La, Lb), ctl.q)
-            if kd == 2:
-                continue
-            # right map: trace points through the geometry into the right face parameters
-            ctr = self.ct[cr]
-            rfix, rside, rrun, _, _ = FACES[ctr.shape][fr]
+            for idx in (sH, sO):
+                S["nt"][idx] = nt
+                S["wtoff"][idx] = wtoff
+            # the owner's surface Jacobian (its face parameters carry the weights)
+            _, sJH = self._face_frame(eH, int(fH))
+            S["sJ"][sH] = S["sJ"][sO] = sJH
+            # the other side's parameters of the trace points, through the geometry
+            ofix, oside, orun, _, _ = FACES[ctO.shape][fO]
             g = np.meshgrid(*taxes, indexing="ij")
-            eta_l = np.zeros((nt, 3))
-            eta_l[:, fixed] = side
-            eta_l[:, run[0]] = g[0].reshape(-1)
-            eta_l[:, run[1]] = g[1].reshape(-1)
-            xi_l = xi_of_eta(ctl.shape, eta_l)
-            eL, eR = le[sel], re_[sel]
-            x = self.x0[eL][:, None, :] + np.einsum("wij,pj->wpi", self.F[eL], xi_l + 1.0)
-            xi_r = np.einsum("wjm,wpm->wpj", self.dxidx[eR], x - self.x0[eR][:, None, :]) - 1.0
-            eta_r = eta_of_xi(ctr.shape, xi_r)
-            if np.abs(eta_r[..., rfix] - rside).max() > 1e-9:
+            eta_h = np.zeros((nt, 3))
+            eta_h[:, hfix] = hside
+            eta_h[:, hrun[0]] = g[0].reshape(-1)
+            eta_h[:, hrun[1]] = g[1].reshape(-1)
+            xi_h = xi_of_eta(ctH.shape, eta_h)
+            x = self.x0[eH][:, None, :] + np.einsum("wij,pj->wpi", self.F[eH], xi_h + 1.0)
+            xi_o = np.einsum("wjm,wpm->wpj", self.dxidx[eO], x - self.x0[eO][:, None, :]) - 1.0
+            with np.errstate(divide="ignore", invalid="ignore"):
+                eta_o = eta_of_xi(ctO.shape, xi_o)
+            # the fixed coordinate is undefined on a collapsed edge that the face contains
+            fx_ok = np.where(np.isfinite(eta_o[..., ofix]), eta_o[..., ofix], oside)
+            if np.abs(fx_ok - oside).max() > 1e-9 or not np.all(np.isfinite(eta_o[..., list(orun)])):
                 raise ValueError("trace points do not lie on the neighbour's face")
-            prm = np.stack([eta_r[..., rrun[0]], eta_r[..., rrun[1]]], axis=-1)        # (W, nt, 2)
+            prm = np.stack([eta_o[..., orun[0]], eta_o[..., orun[1]]], axis=-1)        # (W, nt, 2)
             keyr = np.round(prm.reshape(len(sel), -1), 11)
-            uv, first, vinv = np.unique(keyr, axis=0, return_index=True, return_inverse=True)
+            _, first, vinv = np.unique(keyr, axis=0, return_index=True, return_inverse=True)
             vinv = vinv.reshape(-1)
+            na, nb = taxes[0].size, taxes[1].size
             for v, i0 in enumerate(first):
-                p = prm[i0]
-                Ma = lagrange_interp_matrix(ctr.pts[rrun[0]], p[:, 0])
-                Mb = lagrange_interp_matrix(ctr.pts[rrun[1]], p[:, 1])
-                M = np.einsum("pa,pb->pab", Ma, Mb).reshape(nt, -1)
-                self._set_map(S, right_slot[sel[vinv == v]], M, ctr.q)
+                idx = sO[vinv == v]
+                p = prm[i0].reshape(na, nb, 2)
+                pa, pb = p[..., 0], p[..., 1]
+                tol = 1e-12
+                if np.ptp(pa, axis=1).max() < tol and np.ptp(pb, axis=0).max() < tol:
+                    self._set_tensor(S, idx, lagrange_interp_matrix(ctO.pts[orun[0]], pa[:, 0]),
+                                     lagrange_interp_matrix(ctO.pts[orun[1]], pb[0, :]), False, ctO.q)
+                elif np.ptp(pa, axis=0).max() < tol and np.ptp(pb, axis=1).max() < tol:
+                    # own axis 0 follows the trace's second index: r1 runs over trace axis b
+                    self._set_tensor(S, idx, lagrange_interp_matrix(ctO.pts[orun[0]], pa[0, :]),
+                                     lagrange_interp_matrix(ctO.pts[orun[1]], pb[:, 0]), True, ctO.q)
+                elif np.ptp(pa, axis=0).max() < tol or np.ptp(pb, axis=0).max() < tol:
+                    perp = 0 if np.ptp(pa, axis=0).max() < tol else 1
+                    par = 1 - perp
+                    pp = p[..., par]                                              # (na, nb)
+                    X = np.stack([lagrange_interp_matrix(ctO.pts[orun[par]], pp[:, j]) for j in range(nb)])
+                    Y = lagrange_interp_matrix(ctO.pts[orun[perp]], p[0, :, perp])
+                    S["mkind"][idx] = MAP_ROW
+                    S["moff"][idx] = self.pool.add(X)                              # (nb, na, q)
+                    S["moff2"][idx] = self.pool.add(Y)                             # (nb, q)
+                    S["nab"][idx] = na | (nb << 8) | (perp << 16)
+                else:
+                    Ma = lagrange_interp_matrix(ctO.pts[orun[0]], pa.reshape(-1))
+                    Mb = lagrange_interp_matrix(ctO.pts[orun[1]], pb.reshape(-1))
+                    S["mkind"][idx] = MAP_DENSE
+                    S["moff"][idx] = self.pool.add(np.einsum("pa,pb->pab", Ma, Mb).reshape(nt, -1))
+                    S["moff2"][idx] = -1
         # order by (element, face, coupling) and publish offsets
         order = np.lexsort((np.arange(ns), S["face"], S["elem"]))
         newpos = np.empty(ns, dtype=np.int64)
@@ -430,13 +480,21 @@ class Plan3DBuilder:
         self.n_pub = int(pub.sum())
         self.slots = S
         counts = np.bincount(S["elem"], minlength=len(self.shapes))
+        lim = np.array([NSMAX[s] for s in self.shapes])
+        if np.any(counts > lim):
+            raise ValueError("an element couples to more faces than its kernel holds")
         self.slot_off = np.zeros(len(self.shapes) + 1, dtype=np.int64)
         self.slot_off[1:] = np.cumsum(counts)
 
-    def _set_map(self, S, idx, M, q):
-        if M.shape == (q * q, q * q) and np.abs(M - np.eye(q * q)).max() < 1e-12:
-            S["mkind"][idx] = 0
-            S["moff"][idx] = -1
+    def _set_tensor(self, S, idx, X, Y, swap, q):
+        """Trace map M[p(r1, r2), (ia, ib)] = X[r1, ia] Y[r2, ib]; p = r1 n2 + r2, or r2 n1 + r1 when
+        swapped (the trace's first axis follows own axis 1)."""
+        n1, n2 = X.shape[0], Y.shape[0]
+        if not swap and n1 == q and n2 == q and np.abs(X - np.eye(q)).max() < 1e-12 and \
+                np.abs(Y - np.eye(q)).max() < 1e-12:
+            S["mkind"][idx], S["moff"][idx], S["moff2"][idx] = MAP_ID, -1, -1
             return
-        S["mkind"][idx] = 1
-        S["moff"][idx] = self.pool.add(M)
+        S["mkind"][idx] = MAP_TENSOR
+        S["moff"][idx] = self.pool.add(X)
+        S["moff2"][idx] = self.pool.add(Y)
+        S["nab"][idx] = n1 | (n2 << 8) | (int(swap) << 16)

@@ -44,6 +44,30 @@ def tri_groups(N, tet):
     return np.array(gof), coff, np.array(mofr)
 
 
+def slot_map(T, sl, Q):
+    """Dense nt x q^2 matrix of a slot's trace map (None: identity)."""
+    mk, nt = int(sl["mkind"]), int(sl["nt"])
+    if mk == 0:
+        return None
+    if mk == 2:
+        return T[sl["moff"]:sl["moff"] + nt * Q * Q].reshape(nt, Q * Q)
+    nab = int(sl["nab"])
+    n1, n2, swap = nab & 255, (nab >> 8) & 255, (nab >> 16) & 1
+    if mk == 3:       # row map: M[(pa, pb), own(i_par, i_perp)] = X[pb, pa, i_par] Y[pb, i_perp]
+        X = T[sl["moff"]:sl["moff"] + n2 * n1 * Q].reshape(n2, n1, Q)
+        Y = T[sl["moff2"]:sl["moff2"] + n2 * Q].reshape(n2, Q)
+        M4 = np.einsum("bai,bj->abij", X, Y)            # (pa, pb, i_par, i_perp)
+        if swap == 0:                                    # perp = own axis 0
+            M4 = M4.transpose(0, 1, 3, 2)
+        return M4.reshape(nt, Q * Q)
+    X = T[sl["moff"]:sl["moff"] + n1 * Q].reshape(n1, Q)
+    Y = T[sl["moff2"]:sl["moff2"] + n2 * Q].reshape(n2, Q)
+    M4 = np.einsum("ra,sb->rsab", X, Y)                  # (r1, r2, ia, ib)
+    if swap:
+        M4 = M4.transpose(1, 0, 2, 3)                    # p = r2 n1 + r1
+    return M4.reshape(nt, Q * Q)
+
+
 def phi_matrix(pb, c):
     """Dense Phi (Q^3 x NC) of class c from the staged tables (applying bwd to unit vectors)."""
     cd = pb.class_desc[c]
@@ -110,8 +134,8 @@ def emulate(pb, x, skip_faces=False, skip_volume=False):
                 gn[2, ia, ib] = v[2]
         gf = sum(gn[k] * dfs[k] for k in range(3))
         uf, gf = uf.reshape(-1), gf.reshape(-1)
-        if sl["mkind"]:
-            M = T[sl["moff"]:sl["moff"] + sl["nt"] * Q * Q].reshape(sl["nt"], Q * Q)
+        M = slot_map(T, sl, Q)
+        if M is not None:
             return M @ uf, M @ gf, M, gn.reshape(3, -1), (fx, sd, ra, rb, Ek)
         return uf, gf, None, gn.reshape(3, -1), (fx, sd, ra, rb, Ek)
 
