@@ -7,7 +7,7 @@ namespace {
 template <int S, int N>
 H3Entry entry() {
   using C = h3::Cfg<S, N>;
-  return H3Entry{S, N, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::NT, C::smem_bytes(),
+  return H3Entry{S, N, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(),
                  C::smem_bytes()};
 }
 template <int S>

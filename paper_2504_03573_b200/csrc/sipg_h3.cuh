@@ -54,7 +54,9 @@ struct H3Plan {
 
 namespace h3 {
 
-constexpr int NT = 128;
+// threads per CTA: 256 for q >= 8 (512 volume points), else 128
+template <int Q>
+constexpr int nthreads() { return Q >= 8 ? 256 : 128; }
 constexpr int TMAX = 64;   // trace points per coupling: q_t = max(q_L, q_R) <= 8
 
 template <int S, int N>
@@ -71,8 +73,13 @@ struct Cfg {
   static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);   // slots per element
   static constexpr int SB = 4;                                       // slots per map batch
   static constexpr int SLOTD = 12;                                   // doubles per slot header
+  // class tables staged in shared memory once per CTA (persistent kernels)
+  static constexpr int TA = S == H3_HEX ? Q * N : Q * NG;
+  static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
+  static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
+  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TA + TB + TC;
   static constexpr int doubles() {
-    return NCP + 4 * Q3 + S1 + S2 + NSMAX * (2 * Q2 + SLOTD) + SB * 4 * TMAX;
+    return TABD + NCP + 4 * Q3 + S1 + S2 + NSMAX * (2 * Q2 + SLOTD) + SB * 4 * TMAX;
   }
   static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
 };
@@ -111,8 +118,8 @@ __device__ __forceinline__ Chain face_chain(const double* __restrict__ pts, cons
                                             int fx, int sd, int ra, int rb, int ia, int ib) {
   if (S == H3_HEX) return Chain{1.0, 0.0, 0.0, 1.0, 0.0};
   // eta = +1 occurs only on axis 0 (tet / prism slanted face), where r is unused
-  const double ea = __ldg(pts + ra * Q + ia), eb = __ldg(pts + rb * Q + ib);
-  const double rra = __ldg(R + ra * Q + ia), rrb = __ldg(R + rb * Q + ib);
+  const double ea = *(pts + ra * Q + ia), eb = *(pts + rb * Q + ib);
+  const double rra = *(R + ra * Q + ia), rrb = *(R + rb * Q + ib);
   const double es = (double)sd, rs = sd < 0 ? 0.5 : 0.0;
   const double e0 = fx == 0 ? es : (ra == 0 ? ea : eb);
   const double e1 = fx == 1 ? es : (ra == 1 ? ea : eb);
@@ -165,14 +172,14 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
                     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                     const int* gstart, const int* gmem, const int* coff) {
   using C = Cfg<S, N>;
-  constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NG = C::NG;
+  constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NG = C::NG, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
     for (int o = t; o < N * N * Q; o += NT) {
       const int k2 = o % Q, i01 = o / Q;
       double a = 0.0;
 #pragma unroll
-      for (int i2 = 0; i2 < N; ++i2) a = fma(__ldg(A + k2 * N + i2), c[i01 * N + i2], a);
+      for (int i2 = 0; i2 < N; ++i2) a = fma(*(A + k2 * N + i2), c[i01 * N + i2], a);
       s1[o] = a;
     }
     __syncthreads();
@@ -180,7 +187,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       const int k2 = o % Q, k1 = (o / Q) % Q, i0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int i1 = 0; i1 < N; ++i1) a = fma(__ldg(A + k1 * N + i1), s1[(i0 * N + i1) * Q + k2], a);
+      for (int i1 = 0; i1 < N; ++i1) a = fma(*(A + k1 * N + i1), s1[(i0 * N + i1) * Q + k2], a);
       s2[o] = a;
     }
     __syncthreads();
@@ -188,7 +195,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       const int k12 = o % Q2, k0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int i0 = 0; i0 < N; ++i0) a = fma(__ldg(A + k0 * N + i0), s2[i0 * Q2 + k12], a);
+      for (int i0 = 0; i0 < N; ++i0) a = fma(*(A + k0 * N + i0), s2[i0 * Q2 + k12], a);
       u[o] = a;
     }
     __syncthreads();
@@ -200,9 +207,9 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     double a = 0.0;
     if (S == H3_PRISM) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) a = fma(__ldg(Ct + k * N + l), c[m * N + l], a);
+      for (int l = 0; l < N; ++l) a = fma(*(Ct + k * N + l), c[m * N + l], a);
     } else {
-      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(__ldg(Ct + r * Q + k), c[r], a);
+      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(*(Ct + r * Q + k), c[r], a);
     }
     s1[o] = a;
   }
@@ -214,7 +221,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     double a = 0.0;
     for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
       const int m = gmem[q];
-      a = fma(__ldg(B + m * Q + kb), s1[m * Q + ko], a);
+      a = fma(*(B + m * Q + kb), s1[m * Q + ko], a);
     }
     s2[o] = a;
   }
@@ -223,7 +230,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     const int k12 = o % Q2, k0 = o / Q2;
     double a = 0.0;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) a = fma(__ldg(A + k0 * NG + g), s2[g * Q2 + k12], a);
+    for (int g = 0; g < NG; ++g) a = fma(*(A + k0 * NG + g), s2[g * Q2 + k12], a);
     u[o] = a;
   }
   __syncthreads();
@@ -235,14 +242,14 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
                       const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                       const int* gof, const int* mofr) {
   using C = Cfg<S, N>;
-  constexpr int Q = C::Q, Q2 = C::Q2, NG = C::NG;
+  constexpr int Q = C::Q, Q2 = C::Q2, NG = C::NG, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
     for (int o = t; o < N * Q2; o += NT) {
       const int k12 = o % Q2, i0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * N + i0), T[k0 * Q2 + k12], a);
+      for (int k0 = 0; k0 < Q; ++k0) a = fma(*(A + k0 * N + i0), T[k0 * Q2 + k12], a);
       s2[o] = a;
     }
     __syncthreads();
@@ -250,7 +257,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int k2 = o % Q, i1 = (o / Q) % N, i0 = o / (N * Q);
       double a = 0.0;
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(A + k1 * N + i1), s2[(i0 * Q + k1) * Q + k2], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(A + k1 * N + i1), s2[(i0 * Q + k1) * Q + k2], a);
       s1[o] = a;
     }
     __syncthreads();
@@ -258,7 +265,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int i2 = o % N, i01 = o / N;
       double a = 0.0;
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(A + k2 * N + i2), s1[i01 * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(A + k2 * N + i2), s1[i01 * Q + k2], a);
       y[o] = a;
     }
     return;
@@ -267,7 +274,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     const int k12 = o % Q2, g = o / Q2;
     double a = 0.0;
 #pragma unroll
-    for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * NG + g), T[k0 * Q2 + k12], a);
+    for (int k0 = 0; k0 < Q; ++k0) a = fma(*(A + k0 * NG + g), T[k0 * Q2 + k12], a);
     s2[o] = a;
   }
   __syncthreads();
@@ -276,10 +283,10 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     double a = 0.0;
     if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(B + m * Q + k2), s2[(g * Q + k) * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(B + m * Q + k2), s2[(g * Q + k) * Q + k2], a);
     } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(B + m * Q + k1), s2[(g * Q + k1) * Q + k], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(B + m * Q + k1), s2[(g * Q + k1) * Q + k], a);
     }
     s1[o] = a;
   }
@@ -289,11 +296,11 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     if (S == H3_PRISM) {
       const int m = r / N, l = r % N;
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(Ct + k1 * N + l), s1[m * Q + k1], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(Ct + k1 * N + l), s1[m * Q + k1], a);
     } else {
       const int m = mofr[r];
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(Ct + r * Q + k2), s1[m * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(Ct + r * Q + k2), s1[m * Q + k2], a);
     }
     y[r] = a;
   }
@@ -305,9 +312,20 @@ template <int S, int N>
 struct Lay {
   using C = Cfg<S, N>;
   double *c, *u, *du, *s1, *s2, *F, *hdr, *tb;
+  double *pts, *R, *D, *W, *E, *ED, *A, *B, *Ct;
   int *gstart, *gmem, *gof, *coff, *mofr;
   __device__ Lay(double* sm) {
-    c = sm;
+    constexpr int Q = C::Q, Q2 = C::Q2;
+    pts = sm;
+    R = pts + 3 * Q;
+    D = R + 3 * Q;
+    W = D + 3 * Q2;          // w0 (Q) then w1 w2 Duffy (Q2)
+    E = W + Q + Q2;
+    ED = E + 6 * Q;
+    A = ED + 6 * Q;
+    B = A + C::TA;
+    Ct = B + C::TB;
+    c = sm + C::TABD;
     u = c + C::NCP;
     du = u + C::Q3;
     s1 = du + 3 * C::Q3;
@@ -356,7 +374,7 @@ __device__ __forceinline__ void unpack_nab(int nab, int& n1, int& n2, int& swap)
 template <int Q>
 __device__ void map_forward(const double* hdr, const double* F, double* tb, int b0, int nb, const double* tab,
                             double* pub, bool only_interior) {
-  constexpr int Q2 = Q * Q;
+  constexpr int Q2 = Q * Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
   auto active = [&](int s) { return !only_interior || slot_hdr(hdr, s).kind == 1; };
   // stage 1: tensor X contraction over own axis 0; dense and identity complete here
@@ -480,7 +498,7 @@ __device__ void map_forward(const double* hdr, const double* F, double* tb, int 
 // trace arrays (tb[j][0], tb[j][1]) -> own-face-grid arrays F[s][0], F[s][1] (transposed maps)
 template <int Q>
 __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, int nb, const double* tab) {
-  constexpr int Q2 = Q * Q;
+  constexpr int Q2 = Q * Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
   auto c1 = [&](int s) -> int {
     const H3Slot& h = slot_hdr(hdr, s);
@@ -563,24 +581,41 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
 }
 
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
-                                           double* __restrict__ y) {
+__global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+                                                          double* __restrict__ y) {
   using C = Cfg<S, N>;
-  constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3;
+  constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
   extern __shared__ double sm[];
   Lay<S, N> L(sm);
   const int t = threadIdx.x;
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
-  const double* pts = P.tab + cd[CD3_T_PTS];
-  const double* Rt = P.tab + cd[CD3_T_R];
-  const double* Dt = P.tab + cd[CD3_T_D];
-  const double* Wr = P.tab + cd[CD3_T_W];
-  const double* Et = P.tab + cd[CD3_T_E];
-  const double* EDt = P.tab + cd[CD3_T_ED];
-  const double* At = P.tab + cd[CD3_T_A];
-  const double* Bt = S == H3_HEX ? At : P.tab + cd[CD3_T_B];
-  const double* Ct = S == H3_HEX ? At : P.tab + cd[CD3_T_C];
+  {   // stage the class tables (a few KB) in shared memory
+    auto cp = [&](double* dst, int word, int n) {
+      const double* src = P.tab + cd[word];
+      for (int r = t; r < n; r += NT) dst[r] = __ldg(src + r);
+    };
+    cp(L.pts, CD3_T_PTS, 3 * Q);
+    cp(L.R, CD3_T_R, 3 * Q);
+    cp(L.D, CD3_T_D, 3 * Q2);
+    cp(L.W, CD3_T_W, Q + Q2);
+    cp(L.E, CD3_T_E, 6 * Q);
+    cp(L.ED, CD3_T_ED, 6 * Q);
+    cp(L.A, CD3_T_A, C::TA);
+    if (S != H3_HEX) {
+      cp(L.B, CD3_T_B, C::TB);
+      cp(L.Ct, CD3_T_C, C::TC);
+    }
+  }
+  const double* pts = L.pts;
+  const double* Rt = L.R;
+  const double* Dt = L.D;
+  const double* Wr = L.W;
+  const double* Et = L.E;
+  const double* EDt = L.ED;
+  const double* At = L.A;
+  const double* Bt = S == H3_HEX ? L.A : L.B;
+  const double* Ct = S == H3_HEX ? L.A : L.Ct;
   if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
   __syncthreads();
   for (int i = blockIdx.x; i < count; i += gridDim.x) {
@@ -614,8 +649,8 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
           const double uv = L.u[base + k * st_f];
-          uf = fma(__ldg(E + k), uv, uf);
-          un = fma(__ldg(ED + k), uv, un);
+          uf = fma(*(E + k), uv, uf);
+          un = fma(*(ED + k), uv, un);
         }
         L.F[s * 2 * Q2 + a] = uf;
         L.F[s * 2 * Q2 + Q2 + a] = un;
@@ -632,8 +667,8 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
         double da = 0.0, db = 0.0;
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
-          da = fma(__ldg(Dt + ra * Q2 + ia * Q + j), fu[j * Q + ib], da);
-          db = fma(__ldg(Dt + rb * Q2 + ib * Q + j), fu[ia * Q + j], db);
+          da = fma(*(Dt + ra * Q2 + ia * Q + j), fu[j * Q + ib], da);
+          db = fma(*(Dt + rb * Q2 + ib * Q + j), fu[ia * Q + j], db);
         }
         const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
         const double g0 = ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2];
@@ -655,9 +690,9 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        a0 = fma(__ldg(Dt + k0 * Q + j), L.u[j * Q2 + k1 * Q + k2], a0);
-        a1 = fma(__ldg(Dt + Q2 + k1 * Q + j), L.u[k0 * Q2 + j * Q + k2], a1);
-        a2 = fma(__ldg(Dt + 2 * Q2 + k2 * Q + j), L.u[k0 * Q2 + k1 * Q + j], a2);
+        a0 = fma(*(Dt + k0 * Q + j), L.u[j * Q2 + k1 * Q + k2], a0);
+        a1 = fma(*(Dt + Q2 + k1 * Q + j), L.u[k0 * Q2 + j * Q + k2], a1);
+        a2 = fma(*(Dt + 2 * Q2 + k2 * Q + j), L.u[k0 * Q2 + k1 * Q + j], a2);
       }
       L.du[o] = a0;
       L.du[Q3 + o] = a1;
@@ -679,7 +714,7 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
       double uf = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
-        const double ek = __ldg(E + k);
+        const double ek = *(E + k);
         const int vi = base + k * st_f;
         uf = fma(ek, L.u[vi], uf);
         d0 = fma(ek, L.du[vi], d0);
@@ -701,9 +736,9 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
       const double lam = P.lam;
       for (int o = t; o < Q3; o += NT) {
         const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-        const Chain ch = chain_t<S>(1.0 + __ldg(pts + k0), 1.0 + __ldg(pts + Q + k1), __ldg(Rt + Q + k1),
-                                    __ldg(Rt + 2 * Q + k2));
-        const double jw = dJ * __ldg(Wr + o);
+        const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
+                                    *(Rt + 2 * Q + k2));
+        const double jw = dJ * Wr[k0] * Wr[Q + k1 * Q + k2];
         const double d0 = L.du[o], d1 = L.du[Q3 + o], d2 = L.du[2 * Q3 + o];
         const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
@@ -755,7 +790,7 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
           const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
           const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
           const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
-          const double ek = __ldg(Et + (fx * 2 + (sd > 0)) * Q + kf);
+          const double ek = *(Et + (fx * 2 + (sd > 0)) * Q + kf);
           if (ek == 0.0) continue;
           const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
           const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
@@ -780,9 +815,9 @@ __global__ void __launch_bounds__(NT) k_h3(const H3Plan P, const int cls, const 
       double a = L.u[o];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        a = fma(__ldg(Dt + j * Q + k0), L.du[j * Q2 + k1 * Q + k2], a);
-        a = fma(__ldg(Dt + Q2 + j * Q + k1), L.du[Q3 + k0 * Q2 + j * Q + k2], a);
-        a = fma(__ldg(Dt + 2 * Q2 + j * Q + k2), L.du[2 * Q3 + k0 * Q2 + k1 * Q + j], a);
+        a = fma(*(Dt + j * Q + k0), L.du[j * Q2 + k1 * Q + k2], a);
+        a = fma(*(Dt + Q2 + j * Q + k1), L.du[Q3 + k0 * Q2 + j * Q + k2], a);
+        a = fma(*(Dt + 2 * Q2 + j * Q + k2), L.du[2 * Q3 + k0 * Q2 + k1 * Q + j], a);
       }
       L.u[o] = a;
     }

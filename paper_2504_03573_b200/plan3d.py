@@ -169,7 +169,8 @@ class ClassTables3:
                  "ED": np.concatenate([E[2 * a + sd] @ Dm[a] for a in range(3) for sd in (0, 1)]),
                  "WA": np.concatenate(self.wts),
                  "D": np.concatenate([diff_matrix(p).reshape(-1) for p in self.pts]),
-                 "W": w,
+                 # volume weights w0[k0] * (w1 w2 Duffy)[k1, k2] (the Duffy factor depends on eta1, eta2)
+                 "W": np.concatenate([self.wts[0], (w.reshape(q, q, q)[0] / self.wts[0][0]).reshape(-1)]),
                  "E": np.concatenate([lagrange_interp_matrix(p, [s])[0] for p in self.pts for s in (-1.0, 1.0)])}
         mm = BasisKind.MODIFIED_MODAL
         if shape == HEX:

@@ -75,3 +75,33 @@ def test_consistency_on_global_quadratic_lambda0():
         ip = ex.Phi.T @ (ex.ref_w * ref.detJ[e])
         worst = max(worst, np.abs(y[ref.dof_off[e]:ref.dof_off[e + 1]] + 6.0 * ip).max())
     assert worst < 1e-10
+
+
+_FIXDIR = __import__("pathlib").Path(__file__).resolve().parent / "golden" / "oracle_cfg4"
+
+
+@pytest.mark.parametrize("path", sorted(_FIXDIR.glob("cfg4_n*.npz")), ids=lambda p: p.stem)
+def test_gpu_matches_frozen_oracle_fixtures(path):
+    g = np.load(path)
+    case = configs.build_case("cfg4", int(g["nx"]), int(g["seed"]))
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    assert rel_maxnorm(op(g["x"]), g["y"]) <= 1e-12
+
+
+@pytest.mark.parametrize("path", sorted(_FIXDIR.glob("cfg4_full.npz")), ids=lambda p: p.stem)
+def test_gpu_full_size_cfg4_digests(path):
+    """BASELINE size (48^3 cubes, 25.2 M DoFs): sampled entries, seeded projections and norms of the
+    oracle's y (make_cfg4.py full), bar 1e-12."""
+    g = np.load(path)
+    case = configs.build_case("cfg4", int(g["nx"]), int(g["seed"]))
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    assert np.array_equal(op._dof_off, g["dof_off"])
+    y = op(case.draw_x(op.n_dofs))
+    ymax = float(g["ymax"])
+    err = float(np.abs(y[g["sample_idx"]] - g["sample_y"]).max()) / ymax
+    print(f"cfg4 full: sampled rel error {err:.3e}")
+    assert err <= 1e-12
+    assert abs(np.abs(y).max() - ymax) <= 1e-12 * ymax
+    R = np.random.default_rng(1234).uniform(-1.0, 1.0, (4, op.n_dofs))
+    proj = R @ y
+    assert np.all(np.abs(proj - g["proj"]) <= 1e-12 * np.abs(R).sum(axis=1) * ymax)

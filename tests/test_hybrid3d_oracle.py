@@ -133,3 +133,18 @@ def test_cfg4_recipe_counts():
     assert n_hex + n_pri // 2 + n_tet // 6 == cubes
     assert 0.25 < n_hex / cubes < 0.55 and 0.15 < n_tet / 6 / cubes < 0.45
     assert set(np.unique(case.order_map.n_modes)) == {4, 5, 6, 7}
+
+
+FIX = sorted((__import__("pathlib").Path(__file__).resolve().parent / "golden" / "oracle_cfg4").glob("cfg4_n*.npz"))
+
+
+@pytest.mark.parametrize("path", FIX, ids=[p.stem for p in FIX])
+def test_oracle_matches_frozen_cfg4_fixtures(path):
+    """tests/golden/oracle_cfg4 freezes the property-tested oracle (make_cfg4.py)."""
+    g = np.load(path)
+    case = configs.build_case("cfg4", int(g["nx"]), int(g["seed"]))
+    op = _oracle(case)
+    assert np.array_equal(op.dof_off, g["dof_off"])
+    x = case.draw_x(op.n_dofs)
+    assert np.array_equal(x, g["x"])
+    assert rel_maxnorm(op(x), g["y"]) <= 1e-14

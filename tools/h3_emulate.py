@@ -107,7 +107,8 @@ def emulate(pb, x, skip_faces=False, skip_volume=False):
         Phi = phi_matrix(pb, c)
         pts = T[cd[CD3_T_PTS]:cd[CD3_T_PTS] + 3 * Q].reshape(3, Q)
         D = T[cd[CD3_T_D]:cd[CD3_T_D] + 3 * Q * Q].reshape(3, Q, Q)
-        Wr = T[cd[CD3_T_W]:cd[CD3_T_W] + Q ** 3]
+        Wt = T[cd[CD3_T_W]:cd[CD3_T_W] + Q + Q * Q]
+        Wr = np.multiply.outer(Wt[:Q], Wt[Q:]).reshape(-1)
         E = T[cd[CD3_T_E]:cd[CD3_T_E] + 6 * Q].reshape(3, 2, Q)
         ctx[c] = (S, N, Q, Phi, pts, D, Wr, E)
 
