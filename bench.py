@@ -235,17 +235,23 @@ def main():
         n_owned = n
     else:
         # weak scaling: `world` copies of the config box stacked in x, one slab per rank
-        from paper_2504_03573_b200.distributed import DistributedHelmholtz
         from paper_2504_03573_b200.partition import stack_box_config
         m, om, rng = stack_box_config(args.config, world, nx=args.nx, seed=args.seed)
         t0 = time.perf_counter()
-        dop = DistributedHelmholtz(m, om, rank, world, dist, **OP_KW)
+        if getattr(m, "is_hybrid3d", False):       # config 4: hex / prism / tet slabs (distributed3d.py)
+            from paper_2504_03573_b200.distributed3d import DistributedHelmholtz3D, dof_offsets3d
+            dop = DistributedHelmholtz3D(m, om, rank, world, dist, **OP_KW)
+            n_glob = int(dof_offsets3d(m, om)[-1])
+        else:
+            from paper_2504_03573_b200.distributed import DistributedHelmholtz
+            from paper_2504_03573_b200.partition import _dof_offsets
+            dop = DistributedHelmholtz(m, om, rank, world, dist, **OP_KW)
+            n_glob = int(_dof_offsets(om, m)[-1])
         setup_s = time.perf_counter() - t0
         op = dop.op
         n = op.n_dofs
         n_elements = int(dop.lp.owned_mask.sum())
-        from paper_2504_03573_b200.partition import _dof_offsets
-        x_glob = rng.uniform(-1.0, 1.0, int(_dof_offsets(om, m)[-1]))
+        x_glob = rng.uniform(-1.0, 1.0, n_glob)
         x_host = np.zeros(n)
         x_host[dop.owned] = x_glob[dop.lp.dof_lo:dop.lp.dof_hi]
         n_owned = dop.lp.dof_hi - dop.lp.dof_lo

@@ -446,12 +446,18 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   return 0;
 }
 
-int h3_apply(sipg_plan* p, const double* x_dev, double* y_dev, cudaStream_t s) {
+// role -1: publish every class, apply roles 0 and 1; role 0: publish the owned classes (roles 0, 1),
+// apply role 0; role 1 (after the halo exchange): publish the ghost classes (role 2), apply role 1
+int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
-  for (int pass = 0; pass < 2; ++pass) {   // publish every class's traces, then apply
+  for (int pass = 0; pass < 2; ++pass) {   // publish traces, then apply
     for (int c = 0; c < p->n_cls; ++c) {
       const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+      const int crole = h->cd[c * CD3_WORDS + CD3_ROLE];
       if (count == 0) continue;
+      if (pass == 0 && role == 0 && crole == 2) continue;
+      if (pass == 0 && role == 1 && crole != 2) continue;
+      if (pass == 1 && (crole == 2 || (role >= 0 && crole != role))) continue;
       const H3Entry* k = h->kern[c];
       if (pass == 0)
         k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, s>>>(h->hp, c, x_dev, y_dev);
@@ -555,10 +561,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
 int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->h3) {
-    if (role > 0) return 0;   // single-GPU hybrid plans have no halo role
-    return h3_apply(p, x_dev, y_dev, s);
-  }
+  if (p->h3) return h3_apply(p, role, x_dev, y_dev, s);
   if (p->need_planes) {
     // publish face planes: role 0 (or all) -> every locally owned element; role 1 -> the
     // ghost layer (its coefficients have just arrived); role -1 -> everything
@@ -720,7 +723,10 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
   if (!p) return -1;
   int k = 0;
   if (p->h3) {
-    for (int c = 0; c < p->n_cls; ++c) k += p->h3->cd[c * CD3_WORDS + CD3_COUNT] > 0 ? 2 : 0;
+    for (int c = 0; c < p->n_cls; ++c) {
+      const int32_t* cd = p->h3->cd.data() + c * CD3_WORDS;
+      if (cd[CD3_COUNT] > 0) k += cd[CD3_ROLE] == 2 ? 1 : 2;
+    }
     return k;
   }
   for (int c = 0; c < p->n_cls; ++c) {

@@ -72,23 +72,26 @@ class HybridMesh3D:
         return [(f.left, f.right, "boundary" if f.right is None else f.tag) for f in self.interfaces]
 
 
-def generate_hybrid3d(nx: int, rng: np.random.Generator, extent=(0.0, 1.0),
+def generate_hybrid3d(nx, rng: np.random.Generator, extent=(0.0, 1.0),
                       p_hex: float = P_HEX, p_prism: float = P_PRISM) -> HybridMesh3D:
-    lo, hi = extent
-    ax = np.linspace(lo, hi, nx + 1)
-    g = np.meshgrid(ax, ax, ax, indexing="ij")
+    """`nx`: cubes per axis (int) or (nx, ny, nz); `extent`: (lo, hi) for every axis or one pair
+    per axis (weak-scaling boxes are stacked along x, partition.stack_box_config)."""
+    nxs = (int(nx),) * 3 if np.ndim(nx) == 0 else tuple(int(v) for v in nx)
+    ext = (tuple(extent),) * 3 if np.ndim(extent) == 1 else tuple(tuple(e) for e in extent)
+    axes = [np.linspace(lo, hi, n + 1) for (lo, hi), n in zip(ext, nxs)]
+    g = np.meshgrid(*axes, indexing="ij")
     verts = np.stack([a.reshape(-1) for a in g], axis=-1)
-    m = nx + 1
+    my, mz = nxs[1] + 1, nxs[2] + 1
 
     def vid(i, j, k):
-        return (i * m + j) * m + k
-    u = np.empty(nx ** 3)
+        return (i * my + j) * mz + k
+    u = np.empty(int(np.prod(nxs)))
     els = []
     perms = list(itertools.permutations(range(3)))
     t = 0
-    for i in range(nx):
-        for j in range(nx):
-            for k in range(nx):
+    for i in range(nxs[0]):
+        for j in range(nxs[1]):
+            for k in range(nxs[2]):
                 r = rng.uniform()
                 u[t] = r
                 t += 1

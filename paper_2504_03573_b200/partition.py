@@ -157,6 +157,10 @@ def stack_box_config(name: str, world: int, nx=None, seed: int = 0):
             raise ValueError("cfg2 weak scaling: use the square config per rank")
         m = generate_hybrid(nx, rng)
         P = rng.integers(2, 9, m.n_elements)
+    elif name == "cfg4":
+        from .mesh3d import generate_hybrid3d
+        m = generate_hybrid3d((nx * world, nx, nx), rng, ((0.0, float(world)), (0.0, 1.0), (0.0, 1.0)))
+        P = rng.integers(3, 7, m.n_elements)
     else:
         raise KeyError(name)
     om = OrderMap(np.asarray(P + 1, dtype=np.int64), np.asarray(P + 2, dtype=np.int64))

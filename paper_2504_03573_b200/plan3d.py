@@ -201,6 +201,15 @@ class ClassTables3:
             self.face_cross.append(_face_cross_xi(shape, fixed, side, run))
 
 
+_CT_CACHE = {}
+
+
+def _class_tables(shape, n):
+    if (shape, n) not in _CT_CACHE:
+        _CT_CACHE[(shape, n)] = ClassTables3(shape, n, n + 1)
+    return _CT_CACHE[(shape, n)]
+
+
 class Pool:
     """Deduplicating double pool."""
 
@@ -285,18 +294,20 @@ class Plan3DBuilder:
 
     # -- classes / tables -------------------------------------------------------------------------
     def _classes(self):
-        keys = sorted(set(zip(self.sid.tolist(), self.nm.tolist())))
+        roles = np.zeros(len(self.shapes), dtype=np.int64) if self.roles is None else self.roles
+        keys = sorted(set(zip(self.sid.tolist(), self.nm.tolist(), roles.tolist())))
         self.class_of = np.zeros(len(self.shapes), dtype=np.int64)
         cd = np.zeros((len(keys), CD3_WORDS), dtype=np.int32)
         elems, self.ct = [], []
         off = 0
         names = {v: k for k, v in SHAPE_ID.items()}
-        for c, (s, n) in enumerate(keys):
-            ids = np.flatnonzero((self.sid == s) & (self.nm == n))
+        for c, (s, n, role) in enumerate(keys):
+            ids = np.flatnonzero((self.sid == s) & (self.nm == n) & (roles == role))
             self.class_of[ids] = c
-            ct = ClassTables3(names[s], n, n + 1)
+            ct = _class_tables(names[s], n)
             self.ct.append(ct)
-            cd[c, [CD3_SHAPE, CD3_N, CD3_Q, CD3_NC, CD3_COUNT, CD3_ELEM_OFF]] = [s, n, n + 1, ct.nc, ids.size, off]
+            cd[c, [CD3_SHAPE, CD3_N, CD3_Q, CD3_NC, CD3_COUNT, CD3_ELEM_OFF, CD3_ROLE]] = \
+                [s, n, n + 1, ct.nc, ids.size, off, role]
             for w, name in ((CD3_T_PTS, "pts"), (CD3_T_D, "D"), (CD3_T_W, "W"), (CD3_T_E, "E"),
                             (CD3_T_A, "A"), (CD3_T_B, "B"), (CD3_T_C, "C"), (CD3_T_R, "R"), (CD3_T_ED, "ED")):
                 cd[c, w] = self.pool.add(ct.parts[name]) if name in ct.parts else -1

@@ -60,7 +60,7 @@ class HelmholtzOperator:
         self.timers = {"setup": 0.0, "total": 0.0, "applies": 0}
         t0 = time.perf_counter()
         if getattr(mesh, "is_hybrid3d", False):
-            self._init_hybrid3d(mesh, order_map, basis_kind, params, tau_rule, t0)
+            self._init_hybrid3d(mesh, order_map, basis_kind, params, tau_rule, t0, element_roles)
             return
         self.plan = PlanBuilder(mesh, order_map, basis_kind=basis_kind, rule_kinds=rule_kinds,
                                 lambda_=params.lambda_, tau_constant=params.tau_constant,
@@ -73,7 +73,7 @@ class HelmholtzOperator:
         self.native = _native.NativePlan(self.plan)
         self.timers["setup"] = time.perf_counter() - t0
 
-    def _init_hybrid3d(self, mesh, order_map, basis_kind, params, tau_rule, t0):
+    def _init_hybrid3d(self, mesh, order_map, basis_kind, params, tau_rule, t0, element_roles=None):
         """Config 4 (hex / prism / tet, mesh3d.HybridMesh3D): every coupling on the shared-trace route
         with the BASELINE penalty (plan3d.py; the reference has no prism / tet)."""
         from .plan3d import Plan3DBuilder
@@ -81,7 +81,7 @@ class HelmholtzOperator:
             raise ValueError("hybrid 3-D meshes use the modified modal basis")
         if tau_rule != "baseline":
             raise ValueError("hybrid 3-D meshes use tau_rule='baseline' (max(n_L, n_R)^2 / h)")
-        self.plan = Plan3DBuilder(mesh, order_map, lambda_=params.lambda_).build()
+        self.plan = Plan3DBuilder(mesh, order_map, lambda_=params.lambda_, element_roles=element_roles).build()
         self.n_dofs = self.plan.n_dofs
         self._dof_off = self.plan.dof_off
         self.certificates = []
