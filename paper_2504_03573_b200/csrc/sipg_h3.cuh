@@ -56,7 +56,7 @@ namespace h3 {
 
 // threads per CTA: 256 for q >= 8 (512 volume points), else 128
 template <int Q>
-constexpr int nthreads() { return Q >= 8 ? 256 : 128; }
+constexpr int nthreads() { return 128; }
 constexpr int TMAX = 64;   // trace points per coupling: q_t = max(q_L, q_R) <= 8
 
 template <int S, int N>
@@ -77,10 +77,9 @@ struct Cfg {
   static constexpr int TA = S == H3_HEX ? Q * N : Q * NG;
   static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
   static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
-  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TA + TB + TC;
-  static constexpr int doubles() {
-    return TABD + NCP + 4 * Q3 + S1 + S2 + NSMAX * (2 * Q2 + SLOTD) + SB * 4 * TMAX;
-  }
+  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q;   // A / B / C stay in global (L1)
+  static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
+  static constexpr int doubles() { return TABD + NCP + 4 * Q3 + NSMAX * (2 * Q2 + SLOTD) + SCR; }
   static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
 };
 
@@ -179,7 +178,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       const int k2 = o % Q, i01 = o / Q;
       double a = 0.0;
 #pragma unroll
-      for (int i2 = 0; i2 < N; ++i2) a = fma(*(A + k2 * N + i2), c[i01 * N + i2], a);
+      for (int i2 = 0; i2 < N; ++i2) a = fma(__ldg(A + k2 * N + i2), c[i01 * N + i2], a);
       s1[o] = a;
     }
     __syncthreads();
@@ -187,7 +186,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       const int k2 = o % Q, k1 = (o / Q) % Q, i0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int i1 = 0; i1 < N; ++i1) a = fma(*(A + k1 * N + i1), s1[(i0 * N + i1) * Q + k2], a);
+      for (int i1 = 0; i1 < N; ++i1) a = fma(__ldg(A + k1 * N + i1), s1[(i0 * N + i1) * Q + k2], a);
       s2[o] = a;
     }
     __syncthreads();
@@ -195,7 +194,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       const int k12 = o % Q2, k0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int i0 = 0; i0 < N; ++i0) a = fma(*(A + k0 * N + i0), s2[i0 * Q2 + k12], a);
+      for (int i0 = 0; i0 < N; ++i0) a = fma(__ldg(A + k0 * N + i0), s2[i0 * Q2 + k12], a);
       u[o] = a;
     }
     __syncthreads();
@@ -207,9 +206,9 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     double a = 0.0;
     if (S == H3_PRISM) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) a = fma(*(Ct + k * N + l), c[m * N + l], a);
+      for (int l = 0; l < N; ++l) a = fma(__ldg(Ct + k * N + l), c[m * N + l], a);
     } else {
-      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(*(Ct + r * Q + k), c[r], a);
+      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(__ldg(Ct + r * Q + k), c[r], a);
     }
     s1[o] = a;
   }
@@ -221,7 +220,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     double a = 0.0;
     for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
       const int m = gmem[q];
-      a = fma(*(B + m * Q + kb), s1[m * Q + ko], a);
+      a = fma(__ldg(B + m * Q + kb), s1[m * Q + ko], a);
     }
     s2[o] = a;
   }
@@ -230,7 +229,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     const int k12 = o % Q2, k0 = o / Q2;
     double a = 0.0;
 #pragma unroll
-    for (int g = 0; g < NG; ++g) a = fma(*(A + k0 * NG + g), s2[g * Q2 + k12], a);
+    for (int g = 0; g < NG; ++g) a = fma(__ldg(A + k0 * NG + g), s2[g * Q2 + k12], a);
     u[o] = a;
   }
   __syncthreads();
@@ -249,7 +248,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int k12 = o % Q2, i0 = o / Q2;
       double a = 0.0;
 #pragma unroll
-      for (int k0 = 0; k0 < Q; ++k0) a = fma(*(A + k0 * N + i0), T[k0 * Q2 + k12], a);
+      for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * N + i0), T[k0 * Q2 + k12], a);
       s2[o] = a;
     }
     __syncthreads();
@@ -257,7 +256,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int k2 = o % Q, i1 = (o / Q) % N, i0 = o / (N * Q);
       double a = 0.0;
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(A + k1 * N + i1), s2[(i0 * Q + k1) * Q + k2], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(A + k1 * N + i1), s2[(i0 * Q + k1) * Q + k2], a);
       s1[o] = a;
     }
     __syncthreads();
@@ -265,7 +264,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int i2 = o % N, i01 = o / N;
       double a = 0.0;
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(A + k2 * N + i2), s1[i01 * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(A + k2 * N + i2), s1[i01 * Q + k2], a);
       y[o] = a;
     }
     return;
@@ -274,7 +273,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     const int k12 = o % Q2, g = o / Q2;
     double a = 0.0;
 #pragma unroll
-    for (int k0 = 0; k0 < Q; ++k0) a = fma(*(A + k0 * NG + g), T[k0 * Q2 + k12], a);
+    for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * NG + g), T[k0 * Q2 + k12], a);
     s2[o] = a;
   }
   __syncthreads();
@@ -283,10 +282,10 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     double a = 0.0;
     if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(B + m * Q + k2), s2[(g * Q + k) * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(B + m * Q + k2), s2[(g * Q + k) * Q + k2], a);
     } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(B + m * Q + k1), s2[(g * Q + k1) * Q + k], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(B + m * Q + k1), s2[(g * Q + k1) * Q + k], a);
     }
     s1[o] = a;
   }
@@ -296,11 +295,11 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     if (S == H3_PRISM) {
       const int m = r / N, l = r % N;
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(*(Ct + k1 * N + l), s1[m * Q + k1], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(Ct + k1 * N + l), s1[m * Q + k1], a);
     } else {
       const int m = mofr[r];
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(*(Ct + r * Q + k2), s1[m * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(Ct + r * Q + k2), s1[m * Q + k2], a);
     }
     y[r] = a;
   }
@@ -312,7 +311,7 @@ template <int S, int N>
 struct Lay {
   using C = Cfg<S, N>;
   double *c, *u, *du, *s1, *s2, *F, *hdr, *tb;
-  double *pts, *R, *D, *W, *E, *ED, *A, *B, *Ct;
+  double *pts, *R, *D, *W, *E, *ED;
   int *gstart, *gmem, *gof, *coff, *mofr;
   __device__ Lay(double* sm) {
     constexpr int Q = C::Q, Q2 = C::Q2;
@@ -322,18 +321,15 @@ struct Lay {
     W = D + 3 * Q2;          // w0 (Q) then w1 w2 Duffy (Q2)
     E = W + Q + Q2;
     ED = E + 6 * Q;
-    A = ED + 6 * Q;
-    B = A + C::TA;
-    Ct = B + C::TB;
     c = sm + C::TABD;
     u = c + C::NCP;
     du = u + C::Q3;
-    s1 = du + 3 * C::Q3;
-    s2 = s1 + C::S1;
-    F = s2 + C::S2;                      // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    F = du + 3 * C::Q3;                  // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hdr = F + C::NSMAX * 2 * C::Q2;      // [NSMAX][12]: slot headers
-    tb = hdr + C::NSMAX * C::SLOTD;      // [SB][4][TMAX]: trace values / flux / map temporaries
-    gstart = (int*)(tb + C::SB * 4 * TMAX);
+    tb = hdr + C::NSMAX * C::SLOTD;      // [SB][4][TMAX]: trace values / flux / map temporaries,
+    s1 = tb;                             // shared with the BwdTrans stages (never live together)
+    s2 = s1 + C::S1;
+    gstart = (int*)(tb + C::SCR);
     gmem = gstart + C::NPM + 2;
     gof = gmem + C::NPM;
     coff = gof + C::NPM;
@@ -345,23 +341,28 @@ __device__ __forceinline__ const H3Slot& slot_hdr(const double* hdr, int s) {
   return *reinterpret_cast<const H3Slot*>(hdr + 12 * s);
 }
 
-// which slot of a batch [b0, b0 + nb) an item belongs to, given per-slot item counts
-template <typename CountFn>
-__device__ __forceinline__ int item_slot(int b0, int nb, int& it, CountFn cnt) {
-  for (int s = b0; s < b0 + nb; ++s) {
-    const int n = cnt(s);
-    if (it < n) return s;
-    it -= n;
+// items of a batch of <= 4 slots [b0, b0 + nb): prefix offsets computed once per phase, the slot of
+// an item found with three compares (no loops over slot headers per item)
+struct Batch {
+  int b0, o1, o2, o3, tot;
+  template <typename CountFn>
+  __device__ __forceinline__ Batch(int b0_, int nb, CountFn cnt) : b0(b0_) {
+    const int c0 = cnt(b0);
+    const int c1 = nb > 1 ? cnt(b0 + 1) : 0;
+    const int c2 = nb > 2 ? cnt(b0 + 2) : 0;
+    const int c3 = nb > 3 ? cnt(b0 + 3) : 0;
+    o1 = c0;
+    o2 = o1 + c1;
+    o3 = o2 + c2;
+    tot = o3 + c3;
   }
-  return -1;
-}
-
-template <typename CountFn>
-__device__ __forceinline__ int batch_items(int b0, int nb, CountFn cnt) {
-  int n = 0;
-  for (int s = b0; s < b0 + nb; ++s) n += cnt(s);
-  return n;
-}
+  // global item -> slot; `it` becomes the index within the slot
+  __device__ __forceinline__ int slot(int& it) const {
+    const int j = (it >= o1) + (it >= o2) + (it >= o3);
+    it -= j == 0 ? 0 : (j == 1 ? o1 : (j == 2 ? o2 : o3));
+    return b0 + j;
+  }
+};
 
 __device__ __forceinline__ void unpack_nab(int nab, int& n1, int& n2, int& swap) {
   n1 = nab & 255;
@@ -385,10 +386,10 @@ __device__ void map_forward(const double* hdr, const double* F, double* tb, int 
     if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
     return h.mkind == MAP_DENSE ? h.nt : Q2;
   };
-  const int n1tot = batch_items(b0, nb, c1);
-  for (int it0 = t; it0 < n1tot; it0 += NT) {
+  const Batch B1(b0, nb, c1);
+  for (int it0 = t; it0 < B1.tot; it0 += NT) {
     int it = it0;
-    const int s = item_slot(b0, nb, it, c1);
+    const int s = B1.slot(it);
     const H3Slot& h = slot_hdr(hdr, s);
     const double* fu = F + s * 2 * Q2;
     const double* fg = fu + Q2;
@@ -452,11 +453,11 @@ __device__ void map_forward(const double* hdr, const double* F, double* tb, int 
     const H3Slot& h = slot_hdr(hdr, s);
     return (h.mkind == MAP_TENSOR || h.mkind == MAP_ROW) ? h.nt : 0;
   };
-  const int n2tot = batch_items(b0, nb, c2);
-  if (n2tot == 0) return;
-  for (int it0 = t; it0 < n2tot; it0 += NT) {
+  const Batch B2(b0, nb, c2);
+  if (B2.tot == 0) return;
+  for (int it0 = t; it0 < B2.tot; it0 += NT) {
     int it = it0;
-    const int s = item_slot(b0, nb, it, c2);
+    const int s = B2.slot(it);
     const H3Slot& h = slot_hdr(hdr, s);
     int n1, n2, sw;
     unpack_nab(h.nab, n1, n2, sw);
@@ -505,11 +506,11 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
     if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
     return h.mkind == MAP_TENSOR ? (h.nab & 255) * Q : 0;
   };
-  const int n1tot = batch_items(b0, nb, c1);
-  if (n1tot > 0) {
-    for (int it0 = t; it0 < n1tot; it0 += NT) {
+  const Batch B1(b0, nb, c1);
+  if (B1.tot > 0) {
+    for (int it0 = t; it0 < B1.tot; it0 += NT) {
       int it = it0;
-      const int s = item_slot(b0, nb, it, c1);
+      const int s = B1.slot(it);
       const H3Slot& h = slot_hdr(hdr, s);
       int n1, n2, sw;
       unpack_nab(h.nab, n1, n2, sw);
@@ -581,7 +582,7 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
 }
 
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
@@ -601,11 +602,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const 
     cp(L.W, CD3_T_W, Q + Q2);
     cp(L.E, CD3_T_E, 6 * Q);
     cp(L.ED, CD3_T_ED, 6 * Q);
-    cp(L.A, CD3_T_A, C::TA);
-    if (S != H3_HEX) {
-      cp(L.B, CD3_T_B, C::TB);
-      cp(L.Ct, CD3_T_C, C::TC);
-    }
   }
   const double* pts = L.pts;
   const double* Rt = L.R;
@@ -613,9 +609,9 @@ __global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const 
   const double* Wr = L.W;
   const double* Et = L.E;
   const double* EDt = L.ED;
-  const double* At = L.A;
-  const double* Bt = S == H3_HEX ? L.A : L.B;
-  const double* Ct = S == H3_HEX ? L.A : L.Ct;
+  const double* At = P.tab + cd[CD3_T_A];
+  const double* Bt = S == H3_HEX ? At : P.tab + cd[CD3_T_B];
+  const double* Ct = S == H3_HEX ? At : P.tab + cd[CD3_T_C];
   if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
   __syncthreads();
   for (int i = blockIdx.x; i < count; i += gridDim.x) {
@@ -757,10 +753,10 @@ __global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const 
       // SIP flux at the trace points (sipg.py:622-650, 663-677); boundary: jump 2u, average g
       {
         auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
-        const int tot = batch_items(b0, nb, cnt);
-        for (int it0 = t; it0 < tot; it0 += NT) {
+        const Batch BF(b0, nb, cnt);
+        for (int it0 = t; it0 < BF.tot; it0 += NT) {
           int p = it0;
-          const int s = item_slot(b0, nb, p, cnt);
+          const int s = BF.slot(p);
           const H3Slot& h = slot_hdr(L.hdr, s);
           double* tv = L.tb + (s - b0) * 4 * TMAX;
           const double ut = tv[p], gt = tv[TMAX + p];
@@ -781,31 +777,48 @@ __global__ void __launch_bounds__(nthreads<N + 1>()) k_h3(const H3Plan P, const 
       }
       __syncthreads();
       map_transpose<Q>(L.hdr, L.F, L.tb, b0, nb, P.tab);
-      // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep)
-      for (int o = t; o < Q3; o += NT) {
-        const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+      // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep):
+      // each thread owns PT volume points; slots outer (decoded once), points inner
+      {
+        constexpr int PT = (Q3 + NT - 1) / NT;
+        double w[PT][4];
+#pragma unroll
+        for (int j = 0; j < PT; ++j) w[j][0] = w[j][1] = w[j][2] = w[j][3] = 0.0;
         for (int s = b0; s < b0 + nb; ++s) {
           const H3Slot& h = slot_hdr(L.hdr, s);
           const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
           const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
-          const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
-          const double ek = *(Et + (fx * 2 + (sd > 0)) * Q + kf);
-          if (ek == 0.0) continue;
-          const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
-          const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
-          const int a = ia * Q + ib;
-          const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
-          const double fv = ek * L.F[s * 2 * Q2 + a], fd = ek * L.F[s * 2 * Q2 + Q2 + a];
-          w0 += fv;
-          w1 = fma(ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2], fd, w1);
-          w2 = fma(ch.c11 * h.v[1] + ch.c12 * h.v[2], fd, w2);
-          w3 = fma(h.v[2], fd, w3);
+          const double* E = Et + (fx * 2 + (sd > 0)) * Q;
+          const double v0 = h.v[0], v1 = h.v[1], v2 = h.v[2];
+          const double* Fv = L.F + s * 2 * Q2;
+#pragma unroll
+          for (int j = 0; j < PT; ++j) {
+            const int o = t + j * NT;
+            if (PT * NT > Q3 && o >= Q3) break;
+            const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+            const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
+            const double ek = E[kf];
+            if (ek == 0.0) continue;
+            const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
+            const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
+            const int a = ia * Q + ib;
+            const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
+            const double fv = ek * Fv[a], fd = ek * Fv[Q2 + a];
+            w[j][0] += fv;
+            w[j][1] = fma(ch.c00 * v0 + ch.c01 * v1 + ch.c02 * v2, fd, w[j][1]);
+            w[j][2] = fma(ch.c11 * v1 + ch.c12 * v2, fd, w[j][2]);
+            w[j][3] = fma(v2, fd, w[j][3]);
+          }
         }
-        L.u[o] += w0;
-        L.du[o] += w1;
-        L.du[Q3 + o] += w2;
-        L.du[2 * Q3 + o] += w3;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+          const int o = t + j * NT;
+          if (PT * NT > Q3 && o >= Q3) break;
+          L.u[o] += w[j][0];
+          L.du[o] += w[j][1];
+          L.du[Q3 + o] += w[j][2];
+          L.du[2 * Q3 + o] += w[j][3];
+        }
       }
       __syncthreads();
     }
