@@ -502,6 +502,13 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
                                             " n_modes=" + std::to_string(cd[CD3_N]));
     }
     h->kern.push_back(k);
+    // __constant__ 1-D tables (one (shape, n) class per instantiation; role-split classes share them)
+    const double* tab = d->tables;
+    cudaError_t e = k->upload(tab + cd[CD3_T_D], tab + cd[CD3_T_A], cd[CD3_SHAPE] == 1 ? tab + cd[CD3_T_C] : nullptr);
+    if (e != cudaSuccess) {
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, std::string("hybrid constant tables: ") + cudaGetErrorString(e));
+    }
   }
   int rc = 0;
   int32_t *cd_d, *ce_d;

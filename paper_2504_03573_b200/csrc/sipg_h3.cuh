@@ -77,7 +77,9 @@ struct Cfg {
   static constexpr int TA = S == H3_HEX ? Q * N : Q * NG;
   static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
   static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
-  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q;   // A / B / C stay in global (L1)
+  // small 1-D tables + the ragged triangle-group rows B (and the tet C rows) in shared memory;
+  // A / D / prism psi are __constant__ (register pencils)
+  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB + (S == H3_TET ? TC : 0);
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
   static constexpr int doubles() { return TABD + NCP + 4 * Q3 + NSMAX * (2 * Q2 + SLOTD) + SCR; }
   static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
@@ -165,6 +167,116 @@ __device__ void build_int_tables(int* gstart, int* gmem, int* gof, int* coff, in
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Register pencils with __constant__ 1-D tables (the k_hex recipe): a thread loads one line of
+// values along an axis into registers and produces the whole output line; with the loops fully
+// unrolled every table entry is a compile-time constant-bank operand of its DFMA (uniform
+// across the warp), so a contraction costs one shared-memory load per input value.
+template <int S, int N> __constant__ double c3D[3 * (N + 1) * (N + 1)];                 // D_a[k][j]
+template <int S, int N> __constant__ double c3A[(N + 1) * (S == H3_HEX ? N : N + 1)];   // A[k][g] / V[k][i]
+template <int S, int N> __constant__ double c3P[(N + 1) * N];                           // prism psi[k][l]
+
+template <int S, int N>
+cudaError_t h3_upload(const double* D, const double* A, const double* psi) {
+  constexpr int Q = N + 1, NA = S == H3_HEX ? N : N + 1;
+  cudaError_t e = cudaMemcpyToSymbol(c3D<S, N>, D, sizeof(double) * 3 * Q * Q);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c3A<S, N>, A, sizeof(double) * Q * NA);
+  if (e == cudaSuccess && S == H3_PRISM) e = cudaMemcpyToSymbol(c3P<S, N>, psi, sizeof(double) * Q * N);
+  return e;
+}
+
+// out[k] = sum_j M[k][j] in[j]  (M row-major K x J in constant memory at compile-time offset)
+template <int K, int J, typename Tab>
+__device__ __forceinline__ void cmat(const Tab& M, int off, const double (&in)[J], double (&out)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) a = fma(M[off + k * J + j], in[j], a);
+    out[k] = a;
+  }
+}
+// out[j] = sum_k M[k][j] in[k]  (transposed)
+template <int K, int J, typename Tab>
+__device__ __forceinline__ void cmatT(const Tab& M, int off, const double (&in)[K], double (&out)[J]) {
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) a = fma(M[off + k * J + j], in[k], a);
+    out[j] = a;
+  }
+}
+
+// du_a = D_a u along each eta axis: 3 Q^2 pencils
+template <int S, int N>
+__device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ du) {
+  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>();
+  for (int it = threadIdx.x; it < 3 * Q2; it += NT) {
+    const int a = it / Q2, r = it % Q2;
+    const int base = a == 0 ? r : (a == 1 ? (r / Q) * Q2 + r % Q : r * Q);
+    const int st = a == 0 ? Q2 : (a == 1 ? Q : 1);
+    double col[Q], out[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) col[j] = u[base + j * st];
+    if (a == 0) cmat<Q, Q>(c3D<S, N>, 0, col, out);
+    else if (a == 1) cmat<Q, Q>(c3D<S, N>, Q2, col, out);
+    else cmat<Q, Q>(c3D<S, N>, 2 * Q2, col, out);
+    double* d = du + a * Q3;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) d[base + k * st] = out[k];
+  }
+}
+
+// T = W0 + sum_a D_a^T W_a, in place into W0 (three passes, one per axis)
+template <int S, int N>
+__device__ void pencil_dt(double* __restrict__ W0, const double* __restrict__ W) {
+  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>();
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int r = threadIdx.x; r < Q2; r += NT) {
+      const int base = a == 0 ? r : (a == 1 ? (r / Q) * Q2 + r % Q : r * Q);
+      const int st = a == 0 ? Q2 : (a == 1 ? Q : 1);
+      double col[Q], out[Q];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) col[j] = W[a * Q3 + base + j * st];
+      cmatT<Q, Q>(c3D<S, N>, a * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) W0[base + k * st] += out[k];
+    }
+    __syncthreads();
+  }
+}
+
+// u[k0][k12] = sum_g A[k0][g] s2[g][k12]   (outermost BwdTrans stage, all shapes)
+template <int S, int N>
+__device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict__ u) {
+  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>();
+  for (int r = threadIdx.x; r < Q2; r += NT) {
+    double col[NA], out[Q];
+#pragma unroll
+    for (int g = 0; g < NA; ++g) col[g] = s2[g * Q2 + r];
+    cmat<Q, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+    for (int k = 0; k < Q; ++k) u[k * Q2 + r] = out[k];
+  }
+}
+
+// s2[g][k12] = sum_k0 A[k0][g] T[k0][k12]   (its transpose)
+template <int S, int N>
+__device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restrict__ s2) {
+  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>();
+  for (int r = threadIdx.x; r < Q2; r += NT) {
+    double col[Q], out[NA];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) col[k] = T[k * Q2 + r];
+    cmatT<Q, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+    for (int g = 0; g < NA; ++g) s2[g * Q2 + r] = out[g];
+  }
+}
+
 // u = Phi c on the q^3 grid (generalised tensor product; stages as plan3d.ClassTables3 tables)
 template <int S, int N>
 __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double* s1, double* s2,
@@ -174,64 +286,70 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NG = C::NG, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
-    for (int o = t; o < N * N * Q; o += NT) {
-      const int k2 = o % Q, i01 = o / Q;
-      double a = 0.0;
+    for (int r = t; r < N * N; r += NT) {        // (i0, i1) pencils: i2 -> k2
+      double col[N], out[Q];
 #pragma unroll
-      for (int i2 = 0; i2 < N; ++i2) a = fma(__ldg(A + k2 * N + i2), c[i01 * N + i2], a);
-      s1[o] = a;
+      for (int i = 0; i < N; ++i) col[i] = c[r * N + i];
+      cmat<Q, N>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) s1[r * Q + k] = out[k];
     }
     __syncthreads();
-    for (int o = t; o < N * Q2; o += NT) {
-      const int k2 = o % Q, k1 = (o / Q) % Q, i0 = o / Q2;
-      double a = 0.0;
+    for (int r = t; r < N * Q; r += NT) {        // (i0, k2) pencils: i1 -> k1
+      const int i0 = r / Q, k2 = r % Q;
+      double col[N], out[Q];
 #pragma unroll
-      for (int i1 = 0; i1 < N; ++i1) a = fma(__ldg(A + k1 * N + i1), s1[(i0 * N + i1) * Q + k2], a);
-      s2[o] = a;
+      for (int i = 0; i < N; ++i) col[i] = s1[(i0 * N + i) * Q + k2];
+      cmat<Q, N>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) s2[(i0 * Q + k) * Q + k2] = out[k];
     }
     __syncthreads();
-    for (int o = t; o < Q3; o += NT) {
-      const int k12 = o % Q2, k0 = o / Q2;
-      double a = 0.0;
-#pragma unroll
-      for (int i0 = 0; i0 < N; ++i0) a = fma(__ldg(A + k0 * N + i0), s2[i0 * Q2 + k12], a);
-      u[o] = a;
-    }
+    pencil_stage_a<S, N>(s2, u);
     __syncthreads();
     return;
   }
   // stage 1: the innermost family (prism: psi on eta1 per triangle mode; tet: C rows on eta2)
-  for (int o = t; o < C::NPM * Q; o += NT) {
-    const int k = o % Q, m = o / Q;
-    double a = 0.0;
-    if (S == H3_PRISM) {
+  if (S == H3_PRISM) {
+    for (int m = t; m < C::NPM; m += NT) {     // triangle-mode pencils: l -> k1
+      double col[N], out[Q];
 #pragma unroll
-      for (int l = 0; l < N; ++l) a = fma(__ldg(Ct + k * N + l), c[m * N + l], a);
-    } else {
-      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(__ldg(Ct + r * Q + k), c[r], a);
+      for (int l = 0; l < N; ++l) col[l] = c[m * N + l];
+      cmat<Q, N>(c3P<S, N>, 0, col, out);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) s1[m * Q + k] = out[k];
     }
-    s1[o] = a;
+  } else {
+    for (int o = t; o < C::NPM * Q; o += NT) {
+      const int k = o % Q, m = o / Q;
+      double a = 0.0;
+      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(Ct[r * Q + k], c[r], a);
+      s1[o] = a;
+    }
   }
   __syncthreads();
   // stage 2: group sums with the B rows (prism: B on eta2, s1 over eta1; tet: B on eta1, s1 over eta2)
-  for (int o = t; o < NG * Q2; o += NT) {
-    const int k2 = o % Q, k1 = (o / Q) % Q, g = o / Q2;
-    const int kb = S == H3_PRISM ? k2 : k1, ko = S == H3_PRISM ? k1 : k2;
-    double a = 0.0;
+  // (g, ko) pencils over kb: prism kb = k2, ko = k1; tet kb = k1, ko = k2
+  for (int it = t; it < NG * Q; it += NT) {
+    const int g = it / Q, ko = it % Q;
+    double out[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) out[k] = 0.0;
     for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
       const int m = gmem[q];
-      a = fma(__ldg(B + m * Q + kb), s1[m * Q + ko], a);
+      const double sv = s1[m * Q + ko];
+      const double* Br = B + m * Q;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) out[k] = fma(Br[k], sv, out[k]);
     }
-    s2[o] = a;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      if (S == H3_PRISM) s2[(g * Q + ko) * Q + k] = out[k];
+      else s2[(g * Q + k) * Q + ko] = out[k];
+    }
   }
   __syncthreads();
-  for (int o = t; o < Q3; o += NT) {
-    const int k12 = o % Q2, k0 = o / Q2;
-    double a = 0.0;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) a = fma(__ldg(A + k0 * NG + g), s2[g * Q2 + k12], a);
-    u[o] = a;
-  }
+  pencil_stage_a<S, N>(s2, u);
   __syncthreads();
 }
 
@@ -244,62 +362,60 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
   constexpr int Q = C::Q, Q2 = C::Q2, NG = C::NG, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
-    for (int o = t; o < N * Q2; o += NT) {
-      const int k12 = o % Q2, i0 = o / Q2;
-      double a = 0.0;
+    pencil_stage_a_t<S, N>(T, s2);             // k0 -> i0
+    __syncthreads();
+    for (int r = t; r < N * Q; r += NT) {        // (i0, k2) pencils: k1 -> i1
+      const int i0 = r / Q, k2 = r % Q;
+      double col[Q], out[N];
 #pragma unroll
-      for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * N + i0), T[k0 * Q2 + k12], a);
-      s2[o] = a;
+      for (int k = 0; k < Q; ++k) col[k] = s2[(i0 * Q + k) * Q + k2];
+      cmatT<Q, N>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int i = 0; i < N; ++i) s1[(i0 * N + i) * Q + k2] = out[i];
     }
     __syncthreads();
-    for (int o = t; o < N * N * Q; o += NT) {
-      const int k2 = o % Q, i1 = (o / Q) % N, i0 = o / (N * Q);
-      double a = 0.0;
+    for (int r = t; r < N * N; r += NT) {        // (i0, i1) pencils: k2 -> i2
+      double col[Q], out[N];
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(A + k1 * N + i1), s2[(i0 * Q + k1) * Q + k2], a);
-      s1[o] = a;
-    }
-    __syncthreads();
-    for (int o = t; o < N * N * N; o += NT) {
-      const int i2 = o % N, i01 = o / N;
-      double a = 0.0;
+      for (int k = 0; k < Q; ++k) col[k] = s1[r * Q + k];
+      cmatT<Q, N>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(A + k2 * N + i2), s1[i01 * Q + k2], a);
-      y[o] = a;
+      for (int i = 0; i < N; ++i) y[r * N + i] = out[i];
     }
     return;
   }
-  for (int o = t; o < NG * Q2; o += NT) {
-    const int k12 = o % Q2, g = o / Q2;
-    double a = 0.0;
-#pragma unroll
-    for (int k0 = 0; k0 < Q; ++k0) a = fma(__ldg(A + k0 * NG + g), T[k0 * Q2 + k12], a);
-    s2[o] = a;
-  }
+  pencil_stage_a_t<S, N>(T, s2);
   __syncthreads();
   for (int o = t; o < C::NPM * Q; o += NT) {
     const int k = o % Q, m = o / Q, g = gof[m];
     double a = 0.0;
     if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(B + m * Q + k2), s2[(g * Q + k) * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(B[m * Q + k2], s2[(g * Q + k) * Q + k2], a);
     } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(B + m * Q + k1), s2[(g * Q + k1) * Q + k], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(B[m * Q + k1], s2[(g * Q + k1) * Q + k], a);
     }
     s1[o] = a;
   }
   __syncthreads();
+  if (S == H3_PRISM) {
+    for (int m = t; m < C::NPM; m += NT) {     // triangle-mode pencils: k1 -> l
+      double col[Q], out[N];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) col[k] = s1[m * Q + k];
+      cmatT<Q, N>(c3P<S, N>, 0, col, out);
+#pragma unroll
+      for (int l = 0; l < N; ++l) y[m * N + l] = out[l];
+    }
+    return;
+  }
   for (int r = t; r < C::NC; r += NT) {
     double a = 0.0;
-    if (S == H3_PRISM) {
-      const int m = r / N, l = r % N;
-#pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(__ldg(Ct + k1 * N + l), s1[m * Q + k1], a);
-    } else {
+    {
       const int m = mofr[r];
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(__ldg(Ct + r * Q + k2), s1[m * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(Ct[r * Q + k2], s1[m * Q + k2], a);
     }
     y[r] = a;
   }
@@ -311,7 +427,7 @@ template <int S, int N>
 struct Lay {
   using C = Cfg<S, N>;
   double *c, *u, *du, *s1, *s2, *F, *hdr, *tb;
-  double *pts, *R, *D, *W, *E, *ED;
+  double *pts, *R, *D, *W, *E, *ED, *B, *Ct;
   int *gstart, *gmem, *gof, *coff, *mofr;
   __device__ Lay(double* sm) {
     constexpr int Q = C::Q, Q2 = C::Q2;
@@ -321,6 +437,8 @@ struct Lay {
     W = D + 3 * Q2;          // w0 (Q) then w1 w2 Duffy (Q2)
     E = W + Q + Q2;
     ED = E + 6 * Q;
+    B = ED + 6 * Q;
+    Ct = B + C::TB;
     c = sm + C::TABD;
     u = c + C::NCP;
     du = u + C::Q3;
@@ -497,8 +615,9 @@ __device__ void map_forward(const double* hdr, const double* F, double* tb, int 
 }
 
 // trace arrays (tb[j][0], tb[j][1]) -> own-face-grid arrays F[s][0], F[s][1] (transposed maps)
-template <int Q>
-__device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, int nb, const double* tab) {
+template <int S, int Q>
+__device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, int nb, const double* tab,
+                              const double* pts, const double* R) {
   constexpr int Q2 = Q * Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
   auto c1 = [&](int s) -> int {
@@ -579,10 +698,25 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
     F[s * 2 * Q2 + Q2 + a] = a1;
   }
   __syncthreads();
+  // (G n)_k fd on the own face grid for the scatter (the chain evaluated once per face point), into
+  // the now consumed trace buffers
+  for (int it0 = t; it0 < n2tot; it0 += NT) {
+    const int s = b0 + it0 / Q2, a = it0 % Q2;
+    const H3Slot& h = slot_hdr(hdr, s);
+    const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
+    const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
+    const Chain ch = face_chain<S>(pts, R, Q, fx, sd, ra, rb, a / Q, a % Q);
+    const double fd = F[s * 2 * Q2 + Q2 + a];
+    double* gd = tb + (s - b0) * 4 * TMAX;
+    gd[a] = (ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2]) * fd;
+    gd[Q2 + a] = (ch.c11 * h.v[1] + ch.c12 * h.v[2]) * fd;
+    gd[2 * Q2 + a] = h.v[2] * fd;
+  }
+  __syncthreads();
 }
 
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
@@ -602,6 +736,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
     cp(L.W, CD3_T_W, Q + Q2);
     cp(L.E, CD3_T_E, 6 * Q);
     cp(L.ED, CD3_T_ED, 6 * Q);
+    if (S != H3_HEX) cp(L.B, CD3_T_B, C::TB);
+    if (S == H3_TET) cp(L.Ct, CD3_T_C, C::TC);
   }
   const double* pts = L.pts;
   const double* Rt = L.R;
@@ -610,8 +746,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
   const double* Et = L.E;
   const double* EDt = L.ED;
   const double* At = P.tab + cd[CD3_T_A];
-  const double* Bt = S == H3_HEX ? At : P.tab + cd[CD3_T_B];
-  const double* Ct = S == H3_HEX ? At : P.tab + cd[CD3_T_C];
+  const double* Bt = S == H3_HEX ? At : L.B;
+  const double* Ct = S == H3_TET ? L.Ct : At;
   if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
   __syncthreads();
   for (int i = blockIdx.x; i < count; i += gridDim.x) {
@@ -681,19 +817,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
       continue;
     }
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
-    for (int o = t; o < Q3; o += NT) {
-      const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        a0 = fma(*(Dt + k0 * Q + j), L.u[j * Q2 + k1 * Q + k2], a0);
-        a1 = fma(*(Dt + Q2 + k1 * Q + j), L.u[k0 * Q2 + j * Q + k2], a1);
-        a2 = fma(*(Dt + 2 * Q2 + k2 * Q + j), L.u[k0 * Q2 + k1 * Q + j], a2);
-      }
-      L.du[o] = a0;
-      L.du[Q3 + o] = a1;
-      L.du[2 * Q3 + o] = a2;
-    }
+    pencil_deriv<S, N>(L.u, L.du);
     __syncthreads();
     // own-face-grid u and n.grad u of every slot (face_values_from_phys, endpoint rows)
     for (int it = t; it < ns * Q2; it += NT) {
@@ -776,7 +900,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
         }
       }
       __syncthreads();
-      map_transpose<Q>(L.hdr, L.F, L.tb, b0, nb, P.tab);
+      map_transpose<S, Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, pts, Rt);
       // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep):
       // each thread owns PT volume points; slots outer (decoded once), points inner
       {
@@ -789,8 +913,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
           const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
           const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
           const double* E = Et + (fx * 2 + (sd > 0)) * Q;
-          const double v0 = h.v[0], v1 = h.v[1], v2 = h.v[2];
           const double* Fv = L.F + s * 2 * Q2;
+          const double* gd = L.tb + (s - b0) * 4 * TMAX;
 #pragma unroll
           for (int j = 0; j < PT; ++j) {
             const int o = t + j * NT;
@@ -802,12 +926,10 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
             const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
             const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
             const int a = ia * Q + ib;
-            const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
-            const double fv = ek * Fv[a], fd = ek * Fv[Q2 + a];
-            w[j][0] += fv;
-            w[j][1] = fma(ch.c00 * v0 + ch.c01 * v1 + ch.c02 * v2, fd, w[j][1]);
-            w[j][2] = fma(ch.c11 * v1 + ch.c12 * v2, fd, w[j][2]);
-            w[j][3] = fma(v2, fd, w[j][3]);
+            w[j][0] = fma(ek, Fv[a], w[j][0]);
+            w[j][1] = fma(ek, gd[a], w[j][1]);
+            w[j][2] = fma(ek, gd[Q2 + a], w[j][2]);
+            w[j][3] = fma(ek, gd[2 * Q2 + a], w[j][3]);
           }
         }
 #pragma unroll
@@ -823,18 +945,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 8 ? 5 : 6) k_h3(
       __syncthreads();
     }
     // T = W0 + sum_k D_k^T W_k  (in place)
-    for (int o = t; o < Q3; o += NT) {
-      const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-      double a = L.u[o];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        a = fma(*(Dt + j * Q + k0), L.du[j * Q2 + k1 * Q + k2], a);
-        a = fma(*(Dt + Q2 + j * Q + k1), L.du[Q3 + k0 * Q2 + j * Q + k2], a);
-        a = fma(*(Dt + 2 * Q2 + j * Q + k2), L.du[2 * Q3 + k0 * Q2 + k1 * Q + j], a);
-      }
-      L.u[o] = a;
-    }
-    __syncthreads();
+    pencil_dt<S, N>(L.u, L.du);
     bwd_t<S, N>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
     __syncthreads();
   }
