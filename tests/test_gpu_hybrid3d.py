@@ -105,3 +105,27 @@ def test_gpu_full_size_cfg4_digests(path):
     R = np.random.default_rng(1234).uniform(-1.0, 1.0, (4, op.n_dofs))
     proj = R @ y
     assert np.all(np.abs(proj - g["proj"]) <= 1e-12 * np.abs(R).sum(axis=1) * ymax)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 3])
+def test_single_cube_all_boundary(seed):
+    """nx = 1: one cube (a hex, 2 prisms or 6 tets), every outer face on the boundary."""
+    case = configs.build_case("cfg4", 1, seed=seed)
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    x = case.draw_x(op.n_dofs)
+    assert rel_maxnorm(op(x), _oracle(case.mesh, case.order_map)(x)) <= 1e-12
+
+
+def test_torch_zero_copy_and_cg():
+    """CUDA tensors in / out (no host copies), and the GPU-resident CG on the hybrid operator."""
+    import torch
+    from paper_2504_03573_b200.krylov import cg
+    case = configs.build_case("cfg4", 3, seed=2)
+    op = HelmholtzOperator(case.mesh, case.order_map, **KW)
+    x = case.draw_x(op.n_dofs)
+    y_dev = op(torch.from_numpy(x).cuda())
+    assert y_dev.is_cuda and np.array_equal(y_dev.cpu().numpy(), op(x))
+    b = op(x)
+    sol, rep = cg(op, b, tol=1e-8, maxiter=4000)
+    res = np.linalg.norm(b - op(np.asarray(sol))) / np.linalg.norm(b)
+    assert rep.iterations > 0 and res <= 1e-4, (rep, res)
