@@ -19,6 +19,7 @@
 //                     y = Phi^T (W0 + sum_k D_k^T W_k)   (IProduct + IProductDeriv, sipg.py:575-582).
 // Every element's y is written by exactly one CTA (no atomics, deterministic).
 #pragma once
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -81,7 +82,9 @@ struct Cfg {
   // A / D / prism psi are __constant__ (register pencils)
   static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB + (S == H3_TET ? TC : 0);
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
-  static constexpr int doubles() { return TABD + NCP + 4 * Q3 + NSMAX * (2 * Q2 + SLOTD) + SCR; }
+  // coefficients and slot headers are double-buffered: the next element's arrive (cp.async) while
+  // the current one computes
+  static constexpr int doubles() { return TABD + 2 * NCP + 4 * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + SCR; }
   static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
 };
 
@@ -426,7 +429,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
 template <int S, int N>
 struct Lay {
   using C = Cfg<S, N>;
-  double *c, *u, *du, *s1, *s2, *F, *hdr, *tb;
+  double *c, *u, *du, *s1, *s2, *F, *hdr, *tb, *cbuf, *hbuf;
   double *pts, *R, *D, *W, *E, *ED, *B, *Ct;
   int *gstart, *gmem, *gof, *coff, *mofr;
   __device__ Lay(double* sm) {
@@ -439,12 +442,14 @@ struct Lay {
     ED = E + 6 * Q;
     B = ED + 6 * Q;
     Ct = B + C::TB;
-    c = sm + C::TABD;
-    u = c + C::NCP;
+    cbuf = sm + C::TABD;                 // [2][NCP]
+    c = cbuf;
+    u = cbuf + 2 * C::NCP;
     du = u + C::Q3;
     F = du + 3 * C::Q3;                  // [NSMAX][2][Q2]: own-face-grid arrays per slot
-    hdr = F + C::NSMAX * 2 * C::Q2;      // [NSMAX][12]: slot headers
-    tb = hdr + C::NSMAX * C::SLOTD;      // [SB][4][TMAX]: trace values / flux / map temporaries,
+    hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
+    hdr = hbuf;
+    tb = hbuf + 2 * C::NSMAX * C::SLOTD; // [SB][4][TMAX]: trace values / flux / map temporaries,
     s1 = tb;                             // shared with the BwdTrans stages (never live together)
     s2 = s1 + C::S1;
     gstart = (int*)(tb + C::SCR);
@@ -749,18 +754,50 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
   const double* Bt = S == H3_HEX ? At : L.B;
   const double* Ct = S == H3_TET ? L.Ct : At;
   if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
-  __syncthreads();
-  for (int i = blockIdx.x; i < count; i += gridDim.x) {
-    const int e = P.class_elems[cd[CD3_ELEM_OFF] + i];
-    const int64_t dof = P.dof_off[e];
-    const int64_t sb = P.slot_off[e];
-    const int ns = (int)(P.slot_off[e + 1] - sb);
-    for (int r = t; r < C::NC; r += NT) L.c[r] = __ldg(x + dof + r);
-    {
-      const double* src = reinterpret_cast<const double*>(P.slots + sb);
-      for (int r = t; r < ns * C::SLOTD; r += NT) L.hdr[r] = __ldg(src + r);
+  // element pipeline: scalars (element id, DoF and slot offsets) two elements ahead in registers,
+  // coefficients + slot headers one element ahead by cp.async into the other buffer
+  const int G = gridDim.x;
+  const int32_t* ce = P.class_elems + cd[CD3_ELEM_OFF];
+  auto scalars = [&](int i, int64_t& dof, int64_t& sb, int& ns) {
+    if (i < count) {
+      const int e = __ldg(ce + i);
+      dof = __ldg(P.dof_off + e);
+      sb = __ldg(P.slot_off + e);
+      ns = (int)(__ldg(P.slot_off + e + 1) - sb);
     }
+  };
+  auto issue = [&](int buf, int64_t dof, int64_t sb, int ns) {
+    double* cd_ = L.cbuf + buf * C::NCP;
+    double* hd_ = L.hbuf + buf * C::NSMAX * C::SLOTD;
+    for (int r = t; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
+    const double* src = reinterpret_cast<const double*>(P.slots + sb);
+    for (int r = t; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
+    __pipeline_commit();
+  };
+  int64_t dof = 0, sb = 0, dof1 = 0, sb1 = 0;
+  int ns = 0, ns1 = 0;
+  scalars(blockIdx.x, dof, sb, ns);
+  if ((int)blockIdx.x < count) issue(0, dof, sb, ns);
+  scalars(blockIdx.x + G, dof1, sb1, ns1);
+  int it_el = 0;
+  for (int i = blockIdx.x; i < count; i += G, ++it_el) {
+    const int bsel = it_el & 1;
+    __pipeline_wait_prior(0);
     __syncthreads();
+    L.c = L.cbuf + bsel * C::NCP;
+    L.hdr = L.hbuf + bsel * C::NSMAX * C::SLOTD;
+    if (i + G < count) issue(bsel ^ 1, dof1, sb1, ns1);
+    const int64_t cur_dof = dof;
+    dof = dof1;
+    sb = sb1;
+    const int cur_ns = ns;
+    ns = ns1;
+    scalars(i + 2 * G, dof1, sb1, ns1);
+    const int e = __ldg(ce + i);
+    (void)sb;
+    {
+      const int64_t dof = cur_dof;
+      const int ns = cur_ns;
     bwd<S, N>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
     if (PUB) {
       // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
@@ -948,6 +985,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
     pencil_dt<S, N>(L.u, L.du);
     bwd_t<S, N>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
     __syncthreads();
+    }
   }
 }
 

@@ -11,7 +11,9 @@ for a in sys.argv[3:]:
     n, r = a.split(":")
     lo, hi = map(int, r.split("-"))
     ranges.append((n, lo, hi))
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+import os
+kf = os.environ.get("NCU_KERNEL")
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + (["--kernel-name-base", "demangled", "-k", kf] if kf else []),
                      capture_output=True, text=True).stdout.splitlines()
 fname, line = "?", None
 samp, inst = defaultdict(int), defaultdict(int)
