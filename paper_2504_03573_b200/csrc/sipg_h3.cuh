@@ -212,24 +212,27 @@ __device__ __forceinline__ void cmatT(const Tab& M, int off, const double (&in)[
   }
 }
 
-// du_a = D_a u along each eta axis: 3 Q^2 pencils
-template <int S, int N>
-__device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ du) {
+// du_a = D_a u along each eta axis: Q^2 pencils per axis (one compile-time axis per loop: a runtime
+// axis switch over three unrolled constant-operand contractions makes ptxas spill)
+template <int S, int N, int A>
+__device__ __forceinline__ void pencil_deriv_axis(const double* __restrict__ u, double* __restrict__ du) {
   constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>();
-  for (int it = threadIdx.x; it < 3 * Q2; it += NT) {
-    const int a = it / Q2, r = it % Q2;
-    const int base = a == 0 ? r : (a == 1 ? (r / Q) * Q2 + r % Q : r * Q);
-    const int st = a == 0 ? Q2 : (a == 1 ? Q : 1);
+  constexpr int st = A == 0 ? Q2 : (A == 1 ? Q : 1);
+  for (int r = threadIdx.x; r < Q2; r += NT) {
+    const int base = A == 0 ? r : (A == 1 ? (r / Q) * Q2 + r % Q : r * Q);
     double col[Q], out[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) col[j] = u[base + j * st];
-    if (a == 0) cmat<Q, Q>(c3D<S, N>, 0, col, out);
-    else if (a == 1) cmat<Q, Q>(c3D<S, N>, Q2, col, out);
-    else cmat<Q, Q>(c3D<S, N>, 2 * Q2, col, out);
-    double* d = du + a * Q3;
+    cmat<Q, Q>(c3D<S, N>, A * Q2, col, out);
 #pragma unroll
-    for (int k = 0; k < Q; ++k) d[base + k * st] = out[k];
+    for (int k = 0; k < Q; ++k) du[A * Q3 + base + k * st] = out[k];
   }
+}
+template <int S, int N>
+__device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ du) {
+  pencil_deriv_axis<S, N, 0>(u, du);
+  pencil_deriv_axis<S, N, 1>(u, du);
+  pencil_deriv_axis<S, N, 2>(u, du);
 }
 
 // T = W0 + sum_a D_a^T W_a, in place into W0 (three passes, one per axis)
@@ -939,45 +942,30 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       __syncthreads();
       map_transpose<S, Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, pts, Rt);
       // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep):
-      // each thread owns PT volume points; slots outer (decoded once), points inner
-      {
-        constexpr int PT = (Q3 + NT - 1) / NT;
-        double w[PT][4];
-#pragma unroll
-        for (int j = 0; j < PT; ++j) w[j][0] = w[j][1] = w[j][2] = w[j][3] = 0.0;
+      // per owned volume point, the contributions of the batch's faces (fv and the precomputed
+      // (G n)_k fd on the face grid) through their endpoint rows
+      for (int o = t; o < Q3; o += NT) {
+        const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+        const int a0 = k1 * Q + k2, a1 = k0 * Q + k2, a2 = k0 * Q + k1;   // face point for fixed axis 0/1/2
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
         for (int s = b0; s < b0 + nb; ++s) {
-          const H3Slot& h = slot_hdr(L.hdr, s);
-          const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
-          const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
-          const double* E = Et + (fx * 2 + (sd > 0)) * Q;
+          const int face = slot_hdr(L.hdr, s).face;
+          const int fx = c_faces[S][face][0], sd = c_faces[S][face][1];
+          const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
+          const int a = fx == 0 ? a0 : (fx == 1 ? a1 : a2);
+          const double ek = Et[(fx * 2 + (sd > 0)) * Q + kf];
+          if (ek == 0.0) continue;
           const double* Fv = L.F + s * 2 * Q2;
           const double* gd = L.tb + (s - b0) * 4 * TMAX;
-#pragma unroll
-          for (int j = 0; j < PT; ++j) {
-            const int o = t + j * NT;
-            if (PT * NT > Q3 && o >= Q3) break;
-            const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-            const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
-            const double ek = E[kf];
-            if (ek == 0.0) continue;
-            const int ia = ra == 0 ? k0 : (ra == 1 ? k1 : k2);
-            const int ib = rb == 0 ? k0 : (rb == 1 ? k1 : k2);
-            const int a = ia * Q + ib;
-            w[j][0] = fma(ek, Fv[a], w[j][0]);
-            w[j][1] = fma(ek, gd[a], w[j][1]);
-            w[j][2] = fma(ek, gd[Q2 + a], w[j][2]);
-            w[j][3] = fma(ek, gd[2 * Q2 + a], w[j][3]);
-          }
+          w0 = fma(ek, Fv[a], w0);
+          w1 = fma(ek, gd[a], w1);
+          w2 = fma(ek, gd[Q2 + a], w2);
+          w3 = fma(ek, gd[2 * Q2 + a], w3);
         }
-#pragma unroll
-        for (int j = 0; j < PT; ++j) {
-          const int o = t + j * NT;
-          if (PT * NT > Q3 && o >= Q3) break;
-          L.u[o] += w[j][0];
-          L.du[o] += w[j][1];
-          L.du[Q3 + o] += w[j][2];
-          L.du[2 * Q3 + o] += w[j][3];
-        }
+        L.u[o] += w0;
+        L.du[o] += w1;
+        L.du[Q3 + o] += w2;
+        L.du[2 * Q3 + o] += w3;
       }
       __syncthreads();
     }
