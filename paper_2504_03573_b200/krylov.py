@@ -8,6 +8,10 @@ package's `HelmholtzOperator` (the vectors stay in HBM; there is no CPU path):
 
 * cg runs entirely in libsipg.so (`sipg_cg`, csrc/sipg_krylov.cu): one apply,
   one fused dot and one fused update per iteration, two scalars read back.
+* probe_dense / asymmetry_norm / block_sparsity (reference krylov.py:144-183,
+  the paper's symmetry study): the columns are sm_100a applies of device-resident unit vectors
+  written straight into a device matrix; the two diagnostics are host post-processing of that
+  matrix, as in the reference.
 * gmres keeps the Krylov basis on the device (torch tensors as plumbing); every
   operator application is the sm_100a apply, the small Hessenberg least-squares
   problem is solved on the host like the reference (krylov.py:84-141).
@@ -21,7 +25,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["SolveReport", "cg", "gmres", "REASONS"]
+__all__ = ["SolveReport", "cg", "gmres", "REASONS", "probe_dense", "asymmetry_norm", "block_sparsity",
+           "DEFAULT_PROBE_LIMIT"]
+
+DEFAULT_PROBE_LIMIT = 20000     # reference krylov.py:24
 
 REASONS = {0: "", 1: "indefinite direction", 2: "residual drift", 3: "stagnation", 4: "maxiter"}
 
@@ -124,3 +131,42 @@ def gmres(apply_op, b, tol: float = 1e-9, restart: int = 50, maxiter: int | None
             return done(x, SolveReport(True, total, rel))
     rel = float(torch.linalg.vector_norm(bd - apply(x))) / nb
     return done(x, SolveReport(False, total, rel, "maxiter"))
+
+
+def probe_dense(apply_op, n: int, limit: int = DEFAULT_PROBE_LIMIT) -> np.ndarray:
+    """Assemble the operator column by column from unit-vector applications (reference
+    krylov.py:144-156): every column is one device apply of e_j; returns a numpy (n, n) matrix."""
+    import torch
+    if n > limit:
+        raise ValueError(f"probe size {n} exceeds the limit {limit}; use a smaller mesh")
+    _device_rhs(apply_op, np.zeros(n))          # type / length checks of the reference call
+    e = torch.zeros(n, dtype=torch.float64, device="cuda")
+    at = torch.empty((n, n), dtype=torch.float64, device="cuda")   # row j = column j of A
+    stream = torch.cuda.current_stream().cuda_stream
+    for j in range(n):
+        e[j] = 1.0
+        apply_op.apply_into(e.data_ptr(), at[j].data_ptr(), stream)
+        e[j] = 0.0
+    return np.ascontiguousarray(at.cpu().numpy().T)
+
+
+def asymmetry_norm(m) -> float:
+    """||M - M^T||_1 / ||M||_1 with the max-absolute-column-sum norm (reference krylov.py:159-164)."""
+    m = np.asarray(m)
+    num = np.abs(m - m.T).sum(axis=0).max()
+    den = np.abs(m).sum(axis=0).max()
+    return float(num / den) if den else 0.0
+
+
+def block_sparsity(m, offsets, tol: float = 1e-12) -> np.ndarray:
+    """Element-block nonzero pattern of a probed matrix (reference krylov.py:167-183):
+    (n_elem, n_elem) booleans, blocks with an entry above tol x the largest entry."""
+    m = np.asarray(m)
+    off = np.asarray(offsets)
+    ne = len(off) - 1
+    scale = np.abs(m).max()
+    a = np.abs(m)
+    # block maxima: reduce rows within element i, then columns within element j
+    rows = np.maximum.reduceat(a, off[:-1], axis=0) if ne else np.zeros((0, a.shape[1]))
+    blk = np.maximum.reduceat(rows, off[:-1], axis=1) if ne else np.zeros((0, 0))
+    return blk > tol * scale

@@ -109,3 +109,42 @@ def test_gpu_gmres_matches_cg_solution():
     xg, rg = gmres(op, b, tol=1e-11, restart=op.n_dofs)   # full GMRES (the restarted one crawls here)
     assert rc.converged and rg.converged
     assert rel_maxnorm(xg, xc) <= 1e-7
+
+
+def test_block_sparsity_and_asymmetry_match_reference_semantics():
+    """reference krylov.py:159-183 restated as loops."""
+    from paper_2504_03573_b200.krylov import asymmetry_norm, block_sparsity
+    rng = np.random.default_rng(0)
+    m = rng.standard_normal((12, 12))
+    m[0:3, 5:8] = 0.0
+    off = np.array([0, 3, 5, 8, 12])
+    ref = np.zeros((4, 4), dtype=bool)
+    for i in range(4):
+        for j in range(4):
+            ref[i, j] = np.abs(m[off[i]:off[i + 1], off[j]:off[j + 1]]).max() > 1e-12 * np.abs(m).max()
+    assert np.array_equal(block_sparsity(m, off), ref)
+    num = np.abs(m - m.T).sum(axis=0).max()
+    assert asymmetry_norm(m) == float(num / np.abs(m).sum(axis=0).max())
+    assert asymmetry_norm(np.zeros((3, 3))) == 0.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nx", [("cfg1", 2), ("cfg4", 1)])
+def test_gpu_probe_dense_symmetric(name, nx):
+    """Table-2 style symmetry probe (PAPER Table 2, reference krylov.py:144-164) on the GPU apply."""
+    from paper_2504_03573_b200 import configs
+    from paper_2504_03573_b200.krylov import asymmetry_norm, block_sparsity, probe_dense
+    from paper_2504_03573_b200.sipg import HelmholtzOperator
+    case = configs.build_case(name, nx, seed=3)
+    kw = dict(basis_kind="modified_modal", tau_rule="baseline")
+    if name != "cfg4":
+        kw["shared_rule"] = "patched"
+    op = HelmholtzOperator(case.mesh, case.order_map, **kw)
+    A = probe_dense(op, op.n_dofs)
+    x = case.draw_x(op.n_dofs)
+    assert np.abs(A @ x - op(x)).max() <= 1e-12 * np.abs(A).sum(axis=1).max()
+    assert asymmetry_norm(A) < 1e-12
+    pat = block_sparsity(A, op._dof_off)
+    assert np.all(np.diag(pat))
+    with pytest.raises(ValueError):
+        probe_dense(op, op.n_dofs, limit=op.n_dofs - 1)
