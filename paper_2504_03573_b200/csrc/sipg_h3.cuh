@@ -808,7 +808,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       for (int it = t; it < ns * Q2; it += NT) {
         const int s = it / Q2, a = it % Q2;
         const H3Slot& h = slot_hdr(L.hdr, s);
-        if (h.kind != 1) continue;
         const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
         const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
         const int st_f = fx == 0 ? Q2 : (fx == 1 ? Q : 1);
@@ -831,7 +830,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       for (int it = t; it < ns * Q2; it += NT) {
         const int s = it / Q2, a = it % Q2;
         const H3Slot& h = slot_hdr(L.hdr, s);
-        if (h.kind != 1) continue;
         const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
         const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
         const int ia = a / Q, ib = a % Q;
@@ -853,40 +851,11 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       }
       __syncthreads();
       for (int b0 = 0; b0 < ns; b0 += C::SB)
-        map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, true);
+        map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, false);
       continue;
     }
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
     pencil_deriv<S, N>(L.u, L.du);
-    __syncthreads();
-    // own-face-grid u and n.grad u of every slot (face_values_from_phys, endpoint rows)
-    for (int it = t; it < ns * Q2; it += NT) {
-      const int s = it / Q2, a = it % Q2;
-      const H3Slot& h = slot_hdr(L.hdr, s);
-      const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
-      const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
-      const int st_f = fx == 0 ? Q2 : (fx == 1 ? Q : 1);
-      const int st_a = ra == 0 ? Q2 : (ra == 1 ? Q : 1);
-      const int st_b = rb == 0 ? Q2 : (rb == 1 ? Q : 1);
-      const double* E = Et + (fx * 2 + (sd > 0)) * Q;
-      const int ia = a / Q, ib = a % Q;
-      const int base = ia * st_a + ib * st_b;
-      double uf = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        const double ek = *(E + k);
-        const int vi = base + k * st_f;
-        uf = fma(ek, L.u[vi], uf);
-        d0 = fma(ek, L.du[vi], d0);
-        d1 = fma(ek, L.du[Q3 + vi], d1);
-        d2 = fma(ek, L.du[2 * Q3 + vi], d2);
-      }
-      const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, ia, ib);
-      const double g0 = ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2];
-      const double g1 = ch.c11 * h.v[1] + ch.c12 * h.v[2];
-      L.F[s * 2 * Q2 + a] = uf;
-      L.F[s * 2 * Q2 + Q2 + a] = g0 * d0 + g1 * d1 + h.v[2] * d2;
-    }
     __syncthreads();
     // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du)
     {
@@ -913,8 +882,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
     __syncthreads();
     for (int b0 = 0; b0 < ns; b0 += C::SB) {
       const int nb = min(C::SB, ns - b0);
-      map_forward<Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, nullptr, false);
-      // SIP flux at the trace points (sipg.py:622-650, 663-677); boundary: jump 2u, average g
+      // SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and partner
+      // traces (the publish kernel evaluated both); boundary: jump 2u, average g
       {
         auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
         const Batch BF(b0, nb, cnt);
@@ -923,7 +892,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
           const int s = BF.slot(p);
           const H3Slot& h = slot_hdr(L.hdr, s);
           double* tv = L.tb + (s - b0) * 4 * TMAX;
-          const double ut = tv[p], gt = tv[TMAX + p];
+          const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+          const double ut = own.x, gt = own.y;
           double un, gn;
           if (h.kind) {
             const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);

@@ -18,8 +18,8 @@ Layout (all element-major, element ids = mesh order = DoF order):
   Duffy factor), v = (dxi/dx) n (n = the left side's outward unit normal, -n on
   the right side, sipg.py:545), and the published-trace offsets of this slot and
   of its partner.
-* published traces: per interior slot, (u, n.grad u) interleaved at the trace
-  points (phase 1 writes them, phase 2 reads the partner's).
+* published traces: per slot, (u, n.grad u) interleaved at the trace points (phase 1 writes them,
+  phase 2 reads its own and its partner's).
 """
 from __future__ import annotations
 
@@ -485,9 +485,10 @@ class Plan3DBuilder:
         newpos[order] = np.arange(ns)
         S = S[order]
         S["partner"] = np.where(S["partner"] >= 0, newpos[np.maximum(S["partner"], 0)], -1)
-        pub = np.where(S["kind"] == 1, 2 * S["nt"].astype(np.int64), 0)
+        # every slot publishes its own trace (the apply kernel reads its own and its partner's)
+        pub = 2 * S["nt"].astype(np.int64)
         off = np.concatenate([[0], np.cumsum(pub)[:-1]])
-        S["pub_self"] = np.where(S["kind"] == 1, off, -1)
+        S["pub_self"] = off
         S["pub_other"] = np.where(S["partner"] >= 0, S["pub_self"][np.maximum(S["partner"], 0)], -1)
         self.n_pub = int(pub.sum())
         self.slots = S

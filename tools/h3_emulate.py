@@ -157,7 +157,7 @@ def emulate(pb, x, skip_faces=False, skip_volume=False):
                 for si in range(pb.slot_off[e], pb.slot_off[e + 1]):
                     sl = S_[si]
                     if phase == 0:
-                        if sl["kind"] == 1:
+                        if True:        # every slot publishes its own trace
                             ut, gt, *_ = own_trace(c, e, u, du, sl)
                             nt = sl["nt"]
                             pub[sl["pub_self"]:sl["pub_self"] + 2 * nt:2] = ut
@@ -165,8 +165,10 @@ def emulate(pb, x, skip_faces=False, skip_volume=False):
                         continue
                     if skip_faces:
                         continue
-                    ut, gt, M, gn, (fx, sd, ra, rb, Ek) = own_trace(c, e, u, du, sl)
+                    _, _, M, gn, (fx, sd, ra, rb, Ek) = own_trace(c, e, u, du, sl)
                     nt = sl["nt"]
+                    ut = pub[sl["pub_self"]:sl["pub_self"] + 2 * nt:2]
+                    gt = pub[sl["pub_self"] + 1:sl["pub_self"] + 2 * nt:2]
                     if sl["kind"]:
                         un = pub[sl["pub_other"]:sl["pub_other"] + 2 * nt:2]
                         gnb = pub[sl["pub_other"] + 1:sl["pub_other"] + 2 * nt:2]
