@@ -913,29 +913,44 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       map_transpose<S, Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, pts, Rt);
       // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep):
       // per owned volume point, the contributions of the batch's faces (fv and the precomputed
-      // (G n)_k fd on the face grid) through their endpoint rows
-      for (int o = t; o < Q3; o += NT) {
-        const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-        const int a0 = k1 * Q + k2, a1 = k0 * Q + k2, a2 = k0 * Q + k1;   // face point for fixed axis 0/1/2
-        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-        for (int s = b0; s < b0 + nb; ++s) {
-          const int face = slot_hdr(L.hdr, s).face;
-          const int fx = c_faces[S][face][0], sd = c_faces[S][face][1];
-          const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
-          const int a = fx == 0 ? a0 : (fx == 1 ? a1 : a2);
-          const double ek = Et[(fx * 2 + (sd > 0)) * Q + kf];
-          if (ek == 0.0) continue;
-          const double* Fv = L.F + s * 2 * Q2;
-          const double* gd = L.tb + (s - b0) * 4 * TMAX;
-          w0 = fma(ek, Fv[a], w0);
-          w1 = fma(ek, gd[a], w1);
-          w2 = fma(ek, gd[Q2 + a], w2);
-          w3 = fma(ek, gd[2 * Q2 + a], w3);
+      // (G n)_k fd on the face grid) through their endpoint rows; the slot decode is hoisted into
+      // registers (the batch has at most SB = 4 slots)
+      {
+        int fxs[C::SB];
+        const double* Es[C::SB];
+        const double* Fs[C::SB];
+        const double* Gs[C::SB];
+#pragma unroll
+        for (int j = 0; j < C::SB; ++j) {
+          const int sj = j < nb ? b0 + j : b0;
+          const int face = slot_hdr(L.hdr, sj).face;
+          fxs[j] = c_faces[S][face][0];
+          Es[j] = Et + (fxs[j] * 2 + (c_faces[S][face][1] > 0)) * Q;
+          Fs[j] = L.F + sj * 2 * Q2;
+          Gs[j] = L.tb + j * 4 * TMAX;
         }
-        L.u[o] += w0;
-        L.du[o] += w1;
-        L.du[Q3 + o] += w2;
-        L.du[2 * Q3 + o] += w3;
+        for (int o = t; o < Q3; o += NT) {
+          const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+          const int a0 = k1 * Q + k2, a1 = k0 * Q + k2, a2 = k0 * Q + k1;   // face point, fixed axis 0/1/2
+          double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < C::SB; ++j) {
+            if (j >= nb) break;
+            const int fx = fxs[j];
+            const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
+            const int a = fx == 0 ? a0 : (fx == 1 ? a1 : a2);
+            const double ek = Es[j][kf];
+            if (ek == 0.0) continue;
+            w0 = fma(ek, Fs[j][a], w0);
+            w1 = fma(ek, Gs[j][a], w1);
+            w2 = fma(ek, Gs[j][Q2 + a], w2);
+            w3 = fma(ek, Gs[j][2 * Q2 + a], w3);
+          }
+          L.u[o] += w0;
+          L.du[o] += w1;
+          L.du[Q3 + o] += w2;
+          L.du[2 * Q3 + o] += w3;
+        }
       }
       __syncthreads();
     }
