@@ -118,6 +118,11 @@ struct H3State {
   std::vector<const H3Entry*> kern;
   std::vector<int> grid_pub, grid_apply;   // persistent grids: min(count, SMs x resident CTAs)
   std::vector<int> cap_pub, cap_apply;     // SMs x resident CTAs
+  // streamed host apply (see build_stream_schedule_h3): per stage, publish rows and apply rows
+  struct Launch { int row, grid; const H3Entry* k; };
+  std::vector<std::vector<Launch>> st_pub, st_comp;
+  int32_t* rows_d = nullptr;
+  H3Plan hps{};
   void* bufs[7] = {};
   double* pub = nullptr;
 };
@@ -554,6 +559,101 @@ int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStr
   return 0;
 }
 
+// Streamed host apply for hybrid plans: x arrives in 4 KB-aligned DoF chunks; as chunk k lands, its
+// elements publish their traces, and the elements whose partners all lie in chunks <= k ("stage k")
+// apply; y chunks go back as soon as their last stage is done (same pipeline as the standard plans,
+// build_stream_schedule).  Rows are sub-ranges of the class lists appended after the classes.
+bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
+  H3State* h = p->h3;
+  const int64_t nel = d->n_elements, ndof = d->n_dofs;
+  int launches_per_stage = 0;
+  for (int c = 0; c < d->n_classes; ++c) {
+    if (d->class_desc[c * CD3_WORDS + CD3_ROLE] != 0) return false;    // distributed local plans: no
+    if (d->class_desc[c * CD3_WORDS + CD3_COUNT] > 0) launches_per_stage += 2;
+  }
+  // 24 MB chunks (the stage rows run side by side, so short launches cost little; measured on cfg4:
+  // 36 MB 10.7 ms, 24 MB 10.1 ms, 12 MB 10.2 ms per host apply)
+  (void)launches_per_stage;
+  int64_t chunk_bytes = 24ll << 20;
+  const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
+  if (cb) chunk_bytes = atoll(cb);
+  int K = (int)(ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1));
+  if (K > 64) K = 64;
+  if (K < 2) return false;
+  p->chunk_dof.assign(K + 1, 0);
+  for (int k = 1; k < K; ++k) p->chunk_dof[k] = (ndof * k / K) & ~(int64_t)511;
+  p->chunk_dof[K] = ndof;
+  for (int k = 0; k < K; ++k)
+    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return false;
+  std::vector<int32_t> chunk(nel), stage(nel);
+  {
+    int k = 0;
+    for (int64_t e = 0; e < nel; ++e) {
+      while (d->dof_off[e + 1] > p->chunk_dof[k + 1]) ++k;
+      chunk[e] = k;
+    }
+  }
+  const H3Slot* sl = (const H3Slot*)d->slots;
+  for (int64_t e = 0; e < nel; ++e) {
+    int st = chunk[e];
+    for (int64_t q = d->slot_off[e]; q < d->slot_off[e + 1]; ++q)
+      if (sl[q].kind == 1 && sl[q].partner >= 0) {
+        const int nb = sl[sl[q].partner].elem;
+        if (chunk[nb] > st) st = chunk[nb];
+      }
+    stage[e] = st;
+  }
+  std::vector<int32_t> rows(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD3_WORDS);
+  h->st_pub.assign(K, {});
+  h->st_comp.assign(K, {});
+  p->pub.assign(K, {});      // the standard plans' stage lists stay empty
+  p->comp.assign(K, {});
+  for (int c = 0; c < d->n_classes; ++c) {   // stages monotone along each class list
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    const int32_t* el = d->class_elems + cd[CD3_ELEM_OFF];
+    for (int i = 1; i < cd[CD3_COUNT]; ++i)
+      if (stage[el[i]] < stage[el[i - 1]]) stage[el[i]] = stage[el[i - 1]];
+  }
+  p->d2h_stage.assign(K, 0);
+  {
+    int j = 0;
+    for (int64_t e = 0; e < nel; ++e) {
+      while (d->dof_off[e] >= p->chunk_dof[j + 1]) ++j;
+      for (int jj = j; jj < K && p->chunk_dof[jj] < d->dof_off[e + 1]; ++jj)
+        if (stage[e] > p->d2h_stage[jj]) p->d2h_stage[jj] = stage[e];
+    }
+  }
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    const int n = cd[CD3_COUNT];
+    const int32_t* el = d->class_elems + cd[CD3_ELEM_OFF];
+    for (int pass = 0; pass < 2; ++pass) {
+      const std::vector<int32_t>& key = pass == 0 ? chunk : stage;
+      int i0 = 0;
+      while (i0 < n) {
+        const int k = key[el[i0]];
+        int i1 = i0;
+        while (i1 < n && key[el[i1]] == k) ++i1;
+        for (int j = i1; j < n; ++j)
+          if (key[el[j]] <= k) return false;
+        const int r = (int)(rows.size() / CD3_WORDS);
+        rows.insert(rows.end(), cd, cd + CD3_WORDS);
+        rows[(int64_t)r * CD3_WORDS + CD3_COUNT] = i1 - i0;
+        rows[(int64_t)r * CD3_WORDS + CD3_ELEM_OFF] += i0;
+        const int cap = pass == 0 ? h->cap_pub[c] : h->cap_apply[c];
+        const int g = (i1 - i0) < cap ? (i1 - i0) : cap;
+        (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c]});
+        i0 = i1;
+      }
+    }
+  }
+  if (upload(rows.data(), (int64_t)rows.size(), &h->rows_d)) return false;
+  h->hps = h->hp;
+  h->hps.cd = h->rows_d;
+  p->n_chunks = K;
+  return true;
+}
+
 int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   if (!d || !out) return fail(SIPG_ERR_ARG, "null argument");
   *out = nullptr;
@@ -647,6 +747,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     h->cap_pub.push_back(occ_p * sms);
     h->cap_apply.push_back(occ_a * sms);
   }
+  p->streamed = !getenv("SIPG_NO_STREAM") && build_stream_schedule_h3(p, d);
   *out = p;
   return 0;
 }
@@ -799,6 +900,23 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
   for (int k = 0; k < K; ++k) {
     CK(cudaStreamWaitEvent(s, p->ev_h2d[k], 0));
     const bool skip = getenv("SIPG_STREAM_NOCOMPUTE") != nullptr;   // instrumentation: copies only
+    if (p->h3 && !skip) {   // each stage's rows are small: run them side by side (fork / join)
+      H3State* h = p->h3;
+      int rc = group_begin(p, s, (int)h->st_pub[k].size(), (int)h->st_pub[k].size());
+      if (rc) return rc;
+      for (const auto& L : h->st_pub[k]) {
+        L.k->pub<<<L.grid, L.k->threads, L.k->smem_pub, group_stream(p)>>>(h->hps, L.row, p->x_stage, p->y_stage);
+        ++p->launches;
+      }
+      if ((rc = group_end(p))) return rc;
+      if ((rc = group_begin(p, s, (int)h->st_comp[k].size(), (int)h->st_comp[k].size()))) return rc;
+      for (const auto& L : h->st_comp[k]) {
+        L.k->apply<<<L.grid, L.k->threads, L.k->smem_apply, group_stream(p)>>>(h->hps, L.row, p->x_stage,
+                                                                                 p->y_stage);
+        ++p->launches;
+      }
+      if ((rc = group_end(p))) return rc;
+    }
     for (const auto& L : p->pub[k]) {
       if (skip) break;
       L.pe->fn<<<L.grid, p->dps.dim == 3 ? 128 : 256, 0, s>>>(p->dps, L.row, p->x_stage);
@@ -860,6 +978,10 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
   if (!p) return -1;
   if (!p->streamed) return sipg_plan_kernels_per_apply(p);
   int k = 0;
+  if (p->h3) {
+    for (int i = 0; i < p->n_chunks; ++i) k += (int)(p->h3->st_pub[i].size() + p->h3->st_comp[i].size());
+    return k;
+  }
   for (int i = 0; i < p->n_chunks; ++i) k += (int)(p->pub[i].size() + p->comp[i].size());
   return k;
 }
@@ -875,6 +997,7 @@ int sipg_plan_destroy(sipg_plan* p) {
     for (void* b : p->h3->bufs)
       if (b) cudaFree(b);
     if (p->h3->pub) cudaFree(p->h3->pub);
+    if (p->h3->rows_d) cudaFree(p->h3->rows_d);
     delete p->h3;
     p->h3 = nullptr;
   }
