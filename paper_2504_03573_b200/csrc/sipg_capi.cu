@@ -917,15 +917,20 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
       }
       if ((rc = group_end(p))) return rc;
     }
-    for (const auto& L : p->pub[k]) {
-      if (skip) break;
-      L.pe->fn<<<L.grid, p->dps.dim == 3 ? 128 : 256, 0, s>>>(p->dps, L.row, p->x_stage);
-      ++p->launches;
-    }
-    for (const auto& L : p->comp[k]) {
-      if (skip) break;
-      L.k->fn<<<L.grid, L.k->threads, L.k->smem, s>>>(p->dps, L.row, p->x_stage, p->y_stage);
-      ++p->launches;
+    if (!p->h3 && !skip) {   // standard plans: the stage's publishers, then its element rows
+      int rc = group_begin(p, s, (int)p->pub[k].size(), (int)p->pub[k].size());
+      if (rc) return rc;
+      for (const auto& L : p->pub[k]) {
+        L.pe->fn<<<L.grid, p->dps.dim == 3 ? 128 : 256, 0, group_stream(p)>>>(p->dps, L.row, p->x_stage);
+        ++p->launches;
+      }
+      if ((rc = group_end(p))) return rc;
+      if ((rc = group_begin(p, s, (int)p->comp[k].size(), (int)p->comp[k].size()))) return rc;
+      for (const auto& L : p->comp[k]) {
+        L.k->fn<<<L.grid, L.k->threads, L.k->smem, group_stream(p)>>>(p->dps, L.row, p->x_stage, p->y_stage);
+        ++p->launches;
+      }
+      if ((rc = group_end(p))) return rc;
     }
     CK(cudaEventRecord(p->ev_comp[k], s));
     mark(s); tkind.push_back('C');
