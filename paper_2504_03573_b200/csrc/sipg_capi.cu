@@ -266,6 +266,9 @@ bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
     if (d->class_desc[c * CD_WORDS + CD_COUNT] > 0) launches_per_stage += p->planes_k[c] ? 2 : 1;
   int64_t chunk_bytes = (int64_t)launches_per_stage * (3ll << 19);
   if (chunk_bytes < (12ll << 20)) chunk_bytes = 12ll << 20;
+  // mid-size meshes (16-48 MB of x): two chunks still overlap half of each copy direction with the
+  // compute (cfg2, 22.6 MB: host apply 2.21 -> 2.03 ms)
+  if (bytes >= (16ll << 20) && chunk_bytes > bytes / 2) chunk_bytes = bytes / 2 - 4096;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
   if (cb) chunk_bytes = atoll(cb);
   int K = (int)(bytes / (chunk_bytes > 0 ? chunk_bytes : 1));
