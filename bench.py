@@ -79,6 +79,11 @@ class ClockSampler:
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t.start()
+            # nvidia-smi can take ~1 s to emit its first line: start the load phase only once the
+            # sampler is live, so short workloads still get samples inside the timed window
+            t_end = time.perf_counter() + 5.0
+            while not self.samples and time.perf_counter() < t_end:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
