@@ -335,23 +335,32 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
   }
   __syncthreads();
   // stage 2: group sums with the B rows (prism: B on eta2, s1 over eta1; tet: B on eta1, s1 over eta2)
-  // (g, ko) pencils over kb: prism kb = k2, ko = k1; tet kb = k1, ko = k2
-  for (int it = t; it < NG * Q; it += NT) {
-    const int g = it / Q, ko = it % Q;
-    double out[Q];
+  // (g, ko, part) pencils over a part of kb: prism kb = k2, ko = k1; tet kb = k1, ko = k2 (the kb
+  // range is split so that every thread has work)
+  {
+    constexpr int KS = (NT / (NG * Q)) < 1 ? 1 : ((NT / (NG * Q)) > Q ? Q : NT / (NG * Q));
+    constexpr int KP = (Q + KS - 1) / KS;
+    for (int it = t; it < NG * Q * KS; it += NT) {
+      const int part = it % KS, go = it / KS;
+      const int g = go / Q, ko = go % Q;
+      const int kb0 = part * KP;
+      double out[KP];
 #pragma unroll
-    for (int k = 0; k < Q; ++k) out[k] = 0.0;
-    for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
-      const int m = gmem[q];
-      const double sv = s1[m * Q + ko];
-      const double* Br = B + m * Q;
+      for (int k = 0; k < KP; ++k) out[k] = 0.0;
+      for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
+        const int m = gmem[q];
+        const double sv = s1[m * Q + ko];
+        const double* Br = B + m * Q + kb0;
 #pragma unroll
-      for (int k = 0; k < Q; ++k) out[k] = fma(Br[k], sv, out[k]);
-    }
+        for (int k = 0; k < KP; ++k)
+          if (kb0 + k < Q) out[k] = fma(Br[k], sv, out[k]);
+      }
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {
-      if (S == H3_PRISM) s2[(g * Q + ko) * Q + k] = out[k];
-      else s2[(g * Q + k) * Q + ko] = out[k];
+      for (int k = 0; k < KP; ++k) {
+        if (kb0 + k >= Q) break;
+        if (S == H3_PRISM) s2[(g * Q + ko) * Q + kb0 + k] = out[k];
+        else s2[(g * Q + kb0 + k) * Q + ko] = out[k];
+      }
     }
   }
   __syncthreads();
