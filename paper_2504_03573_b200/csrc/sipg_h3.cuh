@@ -212,20 +212,60 @@ __device__ __forceinline__ void cmatT(const Tab& M, int off, const double (&in)[
   }
 }
 
+// rows [R0, R0 + KR) of out = M in  /  columns [C0, C0 + KC) of out = M^T in
+template <int R0, int KR, int J, typename Tab>
+__device__ __forceinline__ void cmat_rows(const Tab& M, int off, const double (&in)[J], double* out) {
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) a = fma(M[off + (R0 + k) * J + j], in[j], a);
+    out[k] = a;
+  }
+}
+template <int C0, int KC, int K, int J, typename Tab>
+__device__ __forceinline__ void cmatT_cols(const Tab& M, int off, const double (&in)[K], double* out) {
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) a = fma(M[off + k * J + C0 + j], in[k], a);
+    out[j] = a;
+  }
+}
+
+// Pencil work is split in two halves of the output line when Q^2 pencils would leave half of the
+// threads idle (2 Q^2 <= NT): part = item / Q^2 (warp-uniform for q = 8)
+template <int S, int Q>
+constexpr int pencil_split() { return (S != H3_TET && 2 * Q * Q <= nthreads<Q>()) ? 2 : 1; }   // tets: measured slower
+
 // du_a = D_a u along each eta axis: Q^2 pencils per axis (one compile-time axis per loop: a runtime
 // axis switch over three unrolled constant-operand contractions makes ptxas spill)
 template <int S, int N, int A>
 __device__ __forceinline__ void pencil_deriv_axis(const double* __restrict__ u, double* __restrict__ du) {
-  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>();
+  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int KP = (Q + 1) / 2;
   constexpr int st = A == 0 ? Q2 : (A == 1 ? Q : 1);
-  for (int r = threadIdx.x; r < Q2; r += NT) {
+  for (int it = threadIdx.x; it < KS * Q2; it += NT) {
+    const int r = it % Q2, part = it / Q2;
     const int base = A == 0 ? r : (A == 1 ? (r / Q) * Q2 + r % Q : r * Q);
     double col[Q], out[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) col[j] = u[base + j * st];
-    cmat<Q, Q>(c3D<S, N>, A * Q2, col, out);
+    double* d = du + A * Q3 + base;
+    if (KS == 1) {
+      cmat_rows<0, Q, Q>(c3D<S, N>, A * Q2, col, out);
 #pragma unroll
-    for (int k = 0; k < Q; ++k) du[A * Q3 + base + k * st] = out[k];
+      for (int k = 0; k < Q; ++k) d[k * st] = out[k];
+    } else if (part == 0) {
+      cmat_rows<0, KP, Q>(c3D<S, N>, A * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) d[k * st] = out[k];
+    } else {
+      cmat_rows<KP, Q - KP, Q>(c3D<S, N>, A * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < Q - KP; ++k) d[(KP + k) * st] = out[k];
+    }
   }
 }
 template <int S, int N>
@@ -236,50 +276,92 @@ __device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ 
 }
 
 // T = W0 + sum_a D_a^T W_a, in place into W0 (three passes, one per axis)
+template <int S, int N, int A>
+__device__ __forceinline__ void pencil_dt_axis(double* __restrict__ W0, const double* __restrict__ W) {
+  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int KP = (Q + 1) / 2;
+  constexpr int st = A == 0 ? Q2 : (A == 1 ? Q : 1);
+  for (int it = threadIdx.x; it < KS * Q2; it += NT) {
+    const int r = it % Q2, part = it / Q2;
+    const int base = A == 0 ? r : (A == 1 ? (r / Q) * Q2 + r % Q : r * Q);
+    double col[Q], out[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) col[j] = W[A * Q3 + base + j * st];
+    double* w0 = W0 + base;
+    if (KS == 1) {
+      cmatT_cols<0, Q, Q, Q>(c3D<S, N>, A * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) w0[k * st] += out[k];
+    } else if (part == 0) {
+      cmatT_cols<0, KP, Q, Q>(c3D<S, N>, A * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) w0[k * st] += out[k];
+    } else {
+      cmatT_cols<KP, Q - KP, Q, Q>(c3D<S, N>, A * Q2, col, out);
+#pragma unroll
+      for (int k = 0; k < Q - KP; ++k) w0[(KP + k) * st] += out[k];
+    }
+  }
+}
 template <int S, int N>
 __device__ void pencil_dt(double* __restrict__ W0, const double* __restrict__ W) {
-  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>();
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    for (int r = threadIdx.x; r < Q2; r += NT) {
-      const int base = a == 0 ? r : (a == 1 ? (r / Q) * Q2 + r % Q : r * Q);
-      const int st = a == 0 ? Q2 : (a == 1 ? Q : 1);
-      double col[Q], out[Q];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) col[j] = W[a * Q3 + base + j * st];
-      cmatT<Q, Q>(c3D<S, N>, a * Q2, col, out);
-#pragma unroll
-      for (int k = 0; k < Q; ++k) W0[base + k * st] += out[k];
-    }
-    __syncthreads();
-  }
+  pencil_dt_axis<S, N, 0>(W0, W);
+  __syncthreads();
+  pencil_dt_axis<S, N, 1>(W0, W);
+  __syncthreads();
+  pencil_dt_axis<S, N, 2>(W0, W);
+  __syncthreads();
 }
 
 // u[k0][k12] = sum_g A[k0][g] s2[g][k12]   (outermost BwdTrans stage, all shapes)
 template <int S, int N>
 __device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict__ u) {
-  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>();
-  for (int r = threadIdx.x; r < Q2; r += NT) {
+  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int KP = (Q + 1) / 2;
+  for (int it = threadIdx.x; it < KS * Q2; it += NT) {
+    const int r = it % Q2, part = it / Q2;
     double col[NA], out[Q];
 #pragma unroll
     for (int g = 0; g < NA; ++g) col[g] = s2[g * Q2 + r];
-    cmat<Q, NA>(c3A<S, N>, 0, col, out);
+    if (KS == 1) {
+      cmat_rows<0, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-    for (int k = 0; k < Q; ++k) u[k * Q2 + r] = out[k];
+      for (int k = 0; k < Q; ++k) u[k * Q2 + r] = out[k];
+    } else if (part == 0) {
+      cmat_rows<0, KP, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) u[k * Q2 + r] = out[k];
+    } else {
+      cmat_rows<KP, Q - KP, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int k = 0; k < Q - KP; ++k) u[(KP + k) * Q2 + r] = out[k];
+    }
   }
 }
 
 // s2[g][k12] = sum_k0 A[k0][g] T[k0][k12]   (its transpose)
 template <int S, int N>
 __device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restrict__ s2) {
-  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>();
-  for (int r = threadIdx.x; r < Q2; r += NT) {
+  constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int GP = (NA + 1) / 2;
+  for (int it = threadIdx.x; it < KS * Q2; it += NT) {
+    const int r = it % Q2, part = it / Q2;
     double col[Q], out[NA];
 #pragma unroll
     for (int k = 0; k < Q; ++k) col[k] = T[k * Q2 + r];
-    cmatT<Q, NA>(c3A<S, N>, 0, col, out);
+    if (KS == 1) {
+      cmatT_cols<0, NA, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-    for (int g = 0; g < NA; ++g) s2[g * Q2 + r] = out[g];
+      for (int g = 0; g < NA; ++g) s2[g * Q2 + r] = out[g];
+    } else if (part == 0) {
+      cmatT_cols<0, GP, Q, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int g = 0; g < GP; ++g) s2[g * Q2 + r] = out[g];
+    } else {
+      cmatT_cols<GP, NA - GP, Q, NA>(c3A<S, N>, 0, col, out);
+#pragma unroll
+      for (int g = 0; g < NA - GP; ++g) s2[(GP + g) * Q2 + r] = out[g];
+    }
   }
 }
 
