@@ -371,7 +371,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
                     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                     const int* gstart, const int* gmem, const int* coff) {
   using C = Cfg<S, N>;
-  constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NG = C::NG, NT = nthreads<Q>();
+  constexpr int Q = C::Q, NG = C::NG, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
     for (int r = t; r < N * N; r += NT) {        // (i0, i1) pencils: i2 -> k2
@@ -456,7 +456,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
                       const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                       const int* gof, const int* mofr) {
   using C = Cfg<S, N>;
-  constexpr int Q = C::Q, Q2 = C::Q2, NG = C::NG, NT = nthreads<Q>();
+  constexpr int Q = C::Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
     pencil_stage_a_t<S, N>(T, s2);             // k0 -> i0
@@ -868,11 +868,11 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
     for (int r = t; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
     __pipeline_commit();
   };
-  int64_t dof = 0, sb = 0, dof1 = 0, sb1 = 0;
-  int ns = 0, ns1 = 0;
-  scalars(blockIdx.x, dof, sb, ns);
-  if ((int)blockIdx.x < count) issue(0, dof, sb, ns);
-  scalars(blockIdx.x + G, dof1, sb1, ns1);
+  int64_t dof_n = 0, sb_n = 0, dof_nn = 0, sb_nn = 0;   // next and next-but-one element
+  int ns_n = 0, ns_nn = 0;
+  scalars(blockIdx.x, dof_n, sb_n, ns_n);
+  if ((int)blockIdx.x < count) issue(0, dof_n, sb_n, ns_n);
+  scalars(blockIdx.x + G, dof_nn, sb_nn, ns_nn);
   int it_el = 0;
   for (int i = blockIdx.x; i < count; i += G, ++it_el) {
     const int bsel = it_el & 1;
@@ -880,18 +880,14 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
     __syncthreads();
     L.c = L.cbuf + bsel * C::NCP;
     L.hdr = L.hbuf + bsel * C::NSMAX * C::SLOTD;
-    if (i + G < count) issue(bsel ^ 1, dof1, sb1, ns1);
-    const int64_t cur_dof = dof;
-    dof = dof1;
-    sb = sb1;
-    const int cur_ns = ns;
-    ns = ns1;
-    scalars(i + 2 * G, dof1, sb1, ns1);
+    const int64_t dof = dof_n;
+    const int ns = ns_n;
+    if (i + G < count) issue(bsel ^ 1, dof_nn, sb_nn, ns_nn);
+    dof_n = dof_nn;
+    sb_n = sb_nn;
+    ns_n = ns_nn;
+    scalars(i + 2 * G, dof_nn, sb_nn, ns_nn);
     const int e = __ldg(ce + i);
-    (void)sb;
-    {
-      const int64_t dof = cur_dof;
-      const int ns = cur_ns;
     bwd<S, N>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
     if (PUB) {
       // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
@@ -1049,7 +1045,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
     pencil_dt<S, N>(L.u, L.du);
     bwd_t<S, N>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
     __syncthreads();
-    }
   }
 }
 

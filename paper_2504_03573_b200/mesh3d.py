@@ -85,16 +85,12 @@ def generate_hybrid3d(nx, rng: np.random.Generator, extent=(0.0, 1.0),
 
     def vid(i, j, k):
         return (i * my + j) * mz + k
-    u = np.empty(int(np.prod(nxs)))
     els = []
     perms = list(itertools.permutations(range(3)))
-    t = 0
     for i in range(nxs[0]):
         for j in range(nxs[1]):
             for k in range(nxs[2]):
                 r = rng.uniform()
-                u[t] = r
-                t += 1
                 c = [[[vid(i + a, j + b, k + cc) for cc in (0, 1)] for b in (0, 1)] for a in (0, 1)]
                 if r < p_hex:
                     els.append(Element(Shape.HEX, (c[0][0][0], c[1][0][0], c[1][1][0], c[0][1][0],

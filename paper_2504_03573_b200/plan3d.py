@@ -315,7 +315,6 @@ class Plan3DBuilder:
             off += ids.size
         self.class_desc = cd
         self.class_elems = np.concatenate(elems).astype(np.int32)
-        self.ct_of_elem = lambda e: self.ct[self.class_of[e]]
 
     # -- faces ------------------------------------------------------------------------------------
     def _face_frame(self, elems, f):
