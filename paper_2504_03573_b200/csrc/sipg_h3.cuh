@@ -1003,7 +1003,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
       // (G n)_k fd on the face grid) through their endpoint rows; the slot decode is hoisted into
       // registers (the batch has at most SB = 4 slots)
       {
-        int fxs[C::SB];
+        // per slot: kf = k . mk (one-hot on the fixed axis), a = k . ma (face-grid index)
+        int mk0[C::SB], mk1[C::SB], mk2[C::SB], ma0[C::SB], ma1[C::SB], ma2[C::SB];
         const double* Es[C::SB];
         const double* Fs[C::SB];
         const double* Gs[C::SB];
@@ -1011,23 +1012,27 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 4 : 5) k_h3(
         for (int j = 0; j < C::SB; ++j) {
           const int sj = j < nb ? b0 + j : b0;
           const int face = slot_hdr(L.hdr, sj).face;
-          fxs[j] = c_faces[S][face][0];
-          Es[j] = Et + (fxs[j] * 2 + (c_faces[S][face][1] > 0)) * Q;
+          const int fx = c_faces[S][face][0];
+          mk0[j] = fx == 0;
+          mk1[j] = fx == 1;
+          mk2[j] = fx == 2;
+          ma0[j] = fx == 0 ? 0 : Q;
+          ma1[j] = fx == 0 ? Q : (fx == 1 ? 0 : 1);
+          ma2[j] = fx == 2 ? 0 : 1;
+          Es[j] = Et + (fx * 2 + (c_faces[S][face][1] > 0)) * Q;
           Fs[j] = L.F + sj * 2 * Q2;
           Gs[j] = L.tb + j * 4 * TMAX;
         }
         for (int o = t; o < Q3; o += NT) {
           const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
-          const int a0 = k1 * Q + k2, a1 = k0 * Q + k2, a2 = k0 * Q + k1;   // face point, fixed axis 0/1/2
           double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
           for (int j = 0; j < C::SB; ++j) {
             if (j >= nb) break;
-            const int fx = fxs[j];
-            const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
-            const int a = fx == 0 ? a0 : (fx == 1 ? a1 : a2);
+            const int kf = k0 * mk0[j] + k1 * mk1[j] + k2 * mk2[j];
+            const int a = k0 * ma0[j] + k1 * ma1[j] + k2 * ma2[j];
             const double ek = Es[j][kf];
-            if (ek == 0.0) continue;
+            if (S != H3_TET && ek == 0.0) continue;   // GLL endpoint rows are one-hot
             w0 = fma(ek, Fs[j][a], w0);
             w1 = fma(ek, Gs[j][a], w1);
             w2 = fma(ek, Gs[j][Q2 + a], w2);
