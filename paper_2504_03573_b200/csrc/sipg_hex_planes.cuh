@@ -52,22 +52,27 @@ k_planes(const DevPlan P, const int cls, const double* __restrict__ x) {
   }
 }
 
-// Shared-trace scratch layout (doubles, from SHX): tables E0, E1 (QT x NMAX), I0, I1 (QT x QMAX),
-// weights (2 QT), T (2 QT NMAX), UO (2 QT^2), SI (2 QT QMAX), SS (2 QT^2), FL (2 QT^2), G (2 QMAX QT)
+// Shared-trace scratch layout (doubles, from SHX): tables E0, E1 (QM x NM), I0, I1 (QM x QM),
+// weights (2 QM), T (2 QM NM), UO (2 QM^2), SI (2 QM^2), SS (2 QM^2), FL (2 QM^2), G (2 QM^2)
+// QM / NM: the instantiation's largest trace size / neighbour order (sizes the scratch: a class of
+// order N only takes fast shared faces with neighbours of order <= N + SIPG_SF_RANGE, plan.py)
+template <int QM, int NM>
 struct ShScr {
+  static constexpr int QMX = QM, NMX = NM;
   double* base;
   __device__ double* tE0() const { return base; }
-  __device__ double* tE1() const { return base + QMAX * NMAX; }
-  __device__ double* tI0() const { return base + 2 * QMAX * NMAX; }
-  __device__ double* tI1() const { return base + 2 * QMAX * NMAX + QMAX * QMAX; }
-  __device__ double* tw0() const { return base + 2 * QMAX * NMAX + 2 * QMAX * QMAX; }
-  __device__ double* tw1() const { return tw0() + 2 * QMAX; }
-  __device__ double* sT() const { return tw1() + 2 * QMAX; }
-  __device__ double* sUO() const { return sT() + 2 * QMAX * NMAX; }
-  __device__ double* sSI() const { return sUO() + 2 * QMAX * QMAX; }
-  __device__ double* sSS() const { return sSI() + 2 * QMAX * QMAX; }
-  __device__ double* sFL() const { return sSS() + 2 * QMAX * QMAX; }
-  __device__ double* sG() const { return sFL() + 2 * QMAX * QMAX; }
+  __device__ double* tE1() const { return base + QM * NM; }
+  __device__ double* tI0() const { return base + 2 * QM * NM; }
+  __device__ double* tI1() const { return base + 2 * QM * NM + QM * QM; }
+  __device__ double* tw0() const { return base + 2 * QM * NM + 2 * QM * QM; }
+  __device__ double* tw1() const { return tw0() + 2 * QM; }
+  __device__ double* sT() const { return tw1() + 2 * QM; }
+  __device__ double* sUO() const { return sT() + 2 * QM * NM; }
+  __device__ double* sSI() const { return sUO() + 2 * QM * QM; }
+  __device__ double* sSS() const { return sSI() + 2 * QM * QM; }
+  __device__ double* sFL() const { return sSS() + 2 * QM * QM; }
+  __device__ double* sG() const { return sFL() + 2 * QM * QM; }
+  static constexpr int doubles() { return 4 * QM * NM + 12 * QM * QM + 4 * QM + 16; }
 };
 
 // One fast shared-trace face (F_FAST_SHARED): the neighbour's published planes evaluated at the
@@ -75,11 +80,11 @@ struct ShScr {
 // grid (self normal n, other -n, one metric: reference sipg.py:640-650) and the transposed
 // interpolation back to the own face grid.  NO / QT > 0: compile-time neighbour order and trace
 // size (the common cases, fully unrolled); 0: runtime sizes.  Called by every thread of the CTA.
-template <int N, int Q, int NO, int QT>
+template <int N, int Q, int NO, int QT, class SC>
 __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const int t, const int f,
                                          const FaceRec& r, const int64_t e01, const double* pl,
                                          const double* __restrict__ T, const double* OWN, double* FVD,
-                                         const ShScr sc) {
+                                         const SC sc) {
   constexpr int NT = Q * Q, QQ = Q * Q;
   const int no = NO ? NO : no_rt, qt = QT ? QT : qt_rt;
   double *tE0 = sc.tE0(), *tE1 = sc.tE1(), *tI0 = sc.tI0(), *tI1 = sc.tI1(), *tw0 = sc.tw0(), *tw1 = sc.tw1();
@@ -99,7 +104,7 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
     const int plx = it / (qt * no), r0 = it - plx * qt * no, p0 = r0 / no, i1 = r0 - p0 * no;
     double s = 0.0;
 #pragma unroll
-    for (int i0 = 0; i0 < (NO ? NO : NMAX); ++i0)
+    for (int i0 = 0; i0 < (NO ? NO : SC::NMX); ++i0)
       if (NO || i0 < no) s = fma(tE0[p0 * no + i0], pl[plx * nno + i0 * no + i1], s);
     sT[it] = s;
   }
@@ -121,7 +126,7 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
     const int plx = it / (qt * qt), r0 = it - plx * qt * qt, p0 = r0 / qt, p1 = r0 - p0 * qt;
     double s = 0.0;
 #pragma unroll
-    for (int i1 = 0; i1 < (NO ? NO : NMAX); ++i1)
+    for (int i1 = 0; i1 < (NO ? NO : SC::NMX); ++i1)
       if (NO || i1 < no) s = fma(tE1[p1 * no + i1], sT[plx * qt * no + p0 * no + i1], s);
     sUO[it] = s;
     if (!sid) {
@@ -158,7 +163,7 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
       const int plx = it / (Q * qt), r0 = it - plx * Q * qt, q0 = r0 / qt, p1 = r0 - q0 * qt;
       double s = 0.0;
 #pragma unroll
-      for (int p0 = 0; p0 < (QT ? QT : QMAX); ++p0)
+      for (int p0 = 0; p0 < (QT ? QT : SC::QMX); ++p0)
         if (QT || p0 < qt) s = fma(tI0[p0 * Q + q0], sFL[plx * qt * qt + p0 * qt + p1], s);
       sG[it] = s;
     }
@@ -167,7 +172,7 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
       const int plx = it / QQ, r0 = it - plx * QQ, q0 = r0 / Q, q1 = r0 - q0 * Q;
       double s = 0.0;
 #pragma unroll
-      for (int p1 = 0; p1 < (QT ? QT : QMAX); ++p1)
+      for (int p1 = 0; p1 < (QT ? QT : SC::QMX); ++p1)
         if (QT || p1 < qt) s = fma(tI1[p1 * Q + q1], sG[plx * Q * qt + q0 * qt + p1], s);
       FVD[f * 2 * QQ + it] = s;
     }
@@ -180,10 +185,10 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
 #endif
 // compile-time dispatch over the neighbour order NO in [LO, HI] (trace size max(Q, NO + 1),
 // the GLL / GLL case F_FAST_SHARED covers); anything else takes the runtime-size variant
-template <int N, int Q, int LO, int HI>
+template <int N, int Q, int LO, int HI, class SC>
 __device__ __forceinline__ void sf_dispatch(const int no, const int qt, const int t, const int f, const FaceRec& r,
                                             const int64_t e01, const double* pl, const double* T,
-                                            const double* OWN, double* FVD, const ShScr sc) {
+                                            const double* OWN, double* FVD, const SC sc) {
   if constexpr (LO > HI) {
     shared_face<N, Q, 0, 0>(no, qt, t, f, r, e01, pl, T, OWN, FVD, sc);
   } else {
@@ -204,14 +209,16 @@ struct HexPlanes {
   static constexpr int N3 = N * N * N;
   static constexpr int QQ = Q * Q;
   static constexpr int BLK = (N3 + 2 + 1) & ~1;
-  static constexpr int NNX = NMAX * NMAX + 2;          // one plane slot (any neighbour order)
+  // neighbour orders of the fast faces: <= N + SIPG_SF_RANGE (F_FAST_SHARED is set only then, plan.py)
+  static constexpr int NM = N + SIPG_SF_RANGE < NMAX ? N + SIPG_SF_RANGE : NMAX;
+  static constexpr int QM0 = Q > NM + 1 ? Q : NM + 1;
+  static constexpr int QM = QM0 < QMAX ? QM0 : QMAX;
+  static constexpr int NNX = NM * NM + 2;              // one plane slot
   static constexpr int RECW = 96 + 12;                 // 6 records + 6 x 2 ext words (doubles)
   // face-phase scratch: U2 (6 x 2 x QQ), OWN (6 x 2 x QQ), FVD (6 x 2 x QQ), T1 (12 Q N)
   static constexpr int FACE = 36 * QQ + 12 * Q * N;
   // shared-trace scratch (SH): tables, T, UO, SI, SS, FL, G
-  static constexpr int QT = QMAX;
-  static constexpr int SHS = SH ? (2 * QT * NMAX + 2 * QT * QMAX + 4 * QT + 2 * QT * NMAX + 8 * QT * QT +
-                                   2 * QMAX * QT + 16) : 0;   // ShScr
+  static constexpr int SHS = SH ? ShScr<QM, NM>::doubles() : 0;
   static constexpr int S0 = 3 * BUF > FACE + SHS ? 3 * BUF : FACE + SHS;
   static constexpr int SCR = (S0 + 1) & ~1;
   // dynamic shared memory (doubles): REC[2] | CO[2] | NBP[6] | S
@@ -412,7 +419,7 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
         if (sk[f] != 3) continue;
         __syncthreads();
         const FaceRec& r = srec[f];
-        ShScr sc{SHX};
+        ShScr<H::QM, H::NM> sc{SHX};
         sf_dispatch<N, Q, (N - SIPG_SF_RANGE > 2 ? N - SIPG_SF_RANGE : 2),
                     (N + SIPG_SF_RANGE < NMAX ? N + SIPG_SF_RANGE : NMAX)>(
             sno[f], r.nt0, t, f, r, sext[2 * f + 1], NBP + f * 2 * NNX, T, OWN, FVD, sc);

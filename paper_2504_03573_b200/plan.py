@@ -18,6 +18,10 @@ import numpy as np
 
 from . import layout as L
 from .mesh import as_shape
+
+# k_hexp sizes its shared-trace scratch for neighbour orders <= own order + SF_RANGE
+# (SIPG_SF_RANGE in csrc/sipg_hex_planes.cuh); farther neighbours take the generic face path
+SF_RANGE = 3
 from .polylib import (BasisKind, QuadKind, as_basis_kind, as_quad_kind, eval_basis_1d,
                       lagrange_interp_matrix, quad_rule)
 from .stdregions import DEFAULT_RULES, DIM, FACES, class_tables
@@ -673,7 +677,8 @@ class PlanBuilder:
             if (d == 3 and not sws and not swo and c_o.kind.value == "modified_modal"
                     and c_s.kind.value == "modified_modal"
                     and all(c_.axis[a]["gll"] for c_ in (c_o, c_s) for a in range(3))
-                    and c_o.n <= 9 and rules[0].n <= 11 and rules[1].n <= 11):
+                    and c_o.n <= 9 and rules[0].n <= 11 and rules[1].n <= 11
+                    and c_o.n <= c_s.n + SF_RANGE):
                 code_o = code if self_is_left else 0
                 sign = [-1.0 if (code_o >> 1) & 1 else 1.0, -1.0 if code_o & 1 else 1.0]
                 E = [eval_basis_1d(c_o.kind, c_o.n, sign[k] * t_axes[k])[0] for k in range(2)]
