@@ -7,8 +7,8 @@ namespace {
 template <int S, int N>
 H3Entry entry() {
   using C = h3::Cfg<S, N>;
-  return H3Entry{S, N, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(),
-                 C::smem_bytes(), &h3::h3_upload<S, N>};
+  return H3Entry{S, N, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(true),
+                 C::smem_bytes(false), &h3::h3_upload<S, N>};
 }
 template <int S>
 void add(std::vector<H3Entry>& v) {

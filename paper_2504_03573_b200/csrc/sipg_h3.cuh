@@ -84,8 +84,11 @@ struct Cfg {
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
   // coefficients and slot headers are double-buffered: the next element's arrive (cp.async) while
   // the current one computes
-  static constexpr int doubles() { return TABD + 2 * NCP + 4 * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + SCR; }
-  static constexpr size_t smem_bytes() { return sizeof(double) * doubles() + sizeof(int) * NI; }
+  // the publish kernel has no derivative arrays (3 Q^3 doubles less: more CTAs per SM)
+  static constexpr int doubles(bool pub) {
+    return TABD + 2 * NCP + (pub ? 1 : 4) * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + SCR;
+  }
+  static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
 };
 
 // (fixed axis, side, run axis 0, run axis 1) per shape and local face (plan3d.FACES)
@@ -526,7 +529,7 @@ struct Lay {
   double *c, *u, *du, *s1, *s2, *F, *hdr, *tb, *cbuf, *hbuf;
   double *pts, *R, *D, *W, *E, *ED, *B, *Ct;
   int *gstart, *gmem, *gof, *coff, *mofr;
-  __device__ Lay(double* sm) {
+  __device__ Lay(double* sm, bool pub) {
     constexpr int Q = C::Q, Q2 = C::Q2;
     pts = sm;
     R = pts + 3 * Q;
@@ -540,7 +543,7 @@ struct Lay {
     c = cbuf;
     u = cbuf + 2 * C::NCP;
     du = u + C::Q3;
-    F = du + 3 * C::Q3;                  // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    F = du + (pub ? 0 : 3 * C::Q3);      // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
     hdr = hbuf;
     tb = hbuf + 2 * C::NSMAX * C::SLOTD; // [SB][4][TMAX]: trace values / flux / map temporaries,
@@ -820,7 +823,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 5 : 12) k_h3
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
   extern __shared__ double sm[];
-  Lay<S, N> L(sm);
+  Lay<S, N> L(sm, PUB);
   const int t = threadIdx.x;
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
