@@ -818,7 +818,7 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
 }
 
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 5 : 12) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? (PUB ? 6 : 5) : 12) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
