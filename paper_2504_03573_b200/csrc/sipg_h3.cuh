@@ -80,7 +80,7 @@ struct Cfg {
   static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
   // small 1-D tables + the ragged triangle-group rows B (and the tet C rows) in shared memory;
   // A / D / prism psi are __constant__ (register pencils)
-  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB + (S == H3_TET ? TC : 0);
+  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB;   // tet C rows: global (L1)
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
   // coefficients and slot headers are double-buffered: the next element's arrive (cp.async) while
   // the current one computes
@@ -818,7 +818,7 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
 }
 
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? (PUB ? 6 : 5) : 12) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
@@ -839,7 +839,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? (PUB ? 6 : 5
     cp(L.E, CD3_T_E, 6 * Q);
     cp(L.ED, CD3_T_ED, 6 * Q);
     if (S != H3_HEX) cp(L.B, CD3_T_B, C::TB);
-    if (S == H3_TET) cp(L.Ct, CD3_T_C, C::TC);
   }
   const double* pts = L.pts;
   const double* Rt = L.R;
@@ -849,7 +848,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? (PUB ? 6 : 5
   const double* EDt = L.ED;
   const double* At = P.tab + cd[CD3_T_A];
   const double* Bt = S == H3_HEX ? At : L.B;
-  const double* Ct = S == H3_TET ? L.Ct : At;
+  const double* Ct = S == H3_TET ? P.tab + cd[CD3_T_C] : At;
   if (S != H3_HEX) build_int_tables<S, N>(L.gstart, L.gmem, L.gof, L.coff, L.mofr);
   // element pipeline: scalars (element id, DoF and slot offsets) two elements ahead in registers,
   // coefficients + slot headers one element ahead by cp.async into the other buffer
