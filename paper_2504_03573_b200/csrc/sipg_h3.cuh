@@ -748,9 +748,11 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
         tv[3 * TMAX + it] = a1;
         continue;
       }
-      for (int r2 = 0; r2 < n2; ++r2) {
-        const double m = __ldg(tab + h.moff2 + r2 * Q + ib);
-        const int p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
+      const double* Yc = tab + h.moff2 + ib;
+      const int pst = sw ? n1 : 1;
+      int p = sw ? r1 : r1 * n2;
+      for (int r2 = 0; r2 < n2; ++r2, p += pst) {
+        const double m = __ldg(Yc + r2 * Q);
         a0 = fma(m, tv[p], a0);
         a1 = fma(m, tv[TMAX + p], a1);
       }
@@ -779,10 +781,13 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
       const int n1 = h.nab & 255, ia = a / Q, ib = a % Q;
       a0 = 0.0;
       a1 = 0.0;
+      const double* Xc = tab + h.moff + ia;
+      const double* t0 = tv + 2 * TMAX + ib;
+#pragma unroll 4
       for (int r1 = 0; r1 < n1; ++r1) {
-        const double m = __ldg(tab + h.moff + r1 * Q + ia);
-        a0 = fma(m, tv[2 * TMAX + r1 * Q + ib], a0);
-        a1 = fma(m, tv[3 * TMAX + r1 * Q + ib], a1);
+        const double m = __ldg(Xc + r1 * Q);
+        a0 = fma(m, t0[r1 * Q], a0);
+        a1 = fma(m, t0[TMAX + r1 * Q], a1);
       }
     } else if (h.mkind == MAP_DENSE) {
       a0 = 0.0;
