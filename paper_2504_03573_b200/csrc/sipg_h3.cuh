@@ -414,7 +414,10 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     for (int o = t; o < C::NPM * Q; o += NT) {
       const int k = o % Q, m = o / Q;
       double a = 0.0;
-      for (int r = coff[m]; r < coff[m + 1]; ++r) a = fma(Ct[r * Q + k], c[r], a);
+      const int r0 = coff[m], cnt = coff[m + 1] - r0;   // <= N - 1 modes per triangle mode
+#pragma unroll
+      for (int kk = 0; kk < N - 1; ++kk)
+        if (kk < cnt) a = fma(Ct[(r0 + kk) * Q + k], c[r0 + kk], a);
       s1[o] = a;
     }
   }
