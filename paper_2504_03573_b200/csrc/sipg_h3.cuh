@@ -435,8 +435,12 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       double out[KP];
 #pragma unroll
       for (int k = 0; k < KP; ++k) out[k] = 0.0;
-      for (int q = gstart[g]; q < gstart[g + 1]; ++q) {
-        const int m = gmem[q];
+      constexpr int GMAX = N - 1 > 2 ? N - 1 : 2;   // members per group (tet n = 2: vertex + apex)
+      const int q0 = gstart[g], cntg = gstart[g + 1] - q0;
+#pragma unroll
+      for (int qq = 0; qq < GMAX; ++qq) {
+        if (qq >= cntg) break;
+        const int m = gmem[q0 + qq];
         const double sv = s1[m * Q + ko];
         const double* Br = B + m * Q + kb0;
 #pragma unroll
