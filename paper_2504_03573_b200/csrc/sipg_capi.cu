@@ -666,6 +666,9 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(SIPG_ERR_NO_DEVICE, "no CUDA device available (the SIP apply has no CPU fallback)");
+  if (d->n_classes <= 0 || d->n_elements <= 0 || !d->class_desc || !d->class_elems || !d->dof_off ||
+      !d->elem_geom || !d->slot_off || !d->slots || !d->tables)
+    return fail(SIPG_ERR_ARG, "hybrid plan descriptor: missing arrays");
   static const std::vector<H3Entry> table = [] {
     std::vector<H3Entry> v;
     sipg_register_h3(v);

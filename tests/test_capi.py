@@ -72,3 +72,25 @@ def test_python_mirror_rejects_bad_arguments():
             pass
         else:
             raise AssertionError(kw)
+
+
+def test_h3_layout_and_error_paths():
+    """Config-4 plan descriptor: layout constants agree with the library, bad descriptors are
+    rejected with an error code (no crash), and no plan is created without a GPU."""
+    import torch
+    from paper_2504_03573_b200.plan3d import CD3_WORDS, H3_ABI_VERSION, SLOT
+    lib = _native.load()
+    assert SLOT.itemsize == 96 and CD3_WORDS == 16
+    h = ctypes.c_void_p()
+    d = _native.H3Desc()
+    d.abi_version = H3_ABI_VERSION + 99
+    assert lib.sipg_h3_plan_create(ctypes.byref(d), ctypes.byref(h)) == -1      # SIPG_ERR_ARG
+    assert "ABI" in _native.last_error()
+    d.abi_version, d.slot_bytes, d.class_words = H3_ABI_VERSION, 95, CD3_WORDS
+    assert lib.sipg_h3_plan_create(ctypes.byref(d), ctypes.byref(h)) == -1
+    d.slot_bytes = 96
+    rc = lib.sipg_h3_plan_create(ctypes.byref(d), ctypes.byref(h))
+    if not torch.cuda.is_available():
+        assert rc == -3 and not h.value                                          # SIPG_ERR_NO_DEVICE
+    else:
+        assert rc == -1 and not h.value                                          # null arrays
