@@ -78,6 +78,13 @@ typedef struct sipg_h3_desc {
   const double* tables;        /* basis tables, trace weights, trace maps */
 } sipg_h3_desc;
 int sipg_h3_plan_create(const sipg_h3_desc* desc, sipg_plan** plan);
+/* The apply kernels of a hybrid plan reading `traces` (device, sipg_h3_trace_len doubles, the
+ * published-trace layout: per slot (u, n.grad u) per trace point) instead of publishing: with
+ * x = 0 and the Dirichlet data as the boundary slots' traces this is the boundary lift of the
+ * reference's rhs_assemble (sipg.py:707-717). */
+int sipg_h3_apply_traces(sipg_plan* plan, const double* x_dev, const double* traces_dev, double* y_dev,
+                         void* stream);
+int64_t sipg_h3_trace_len(const sipg_plan* plan);
 
 /* Build the device-resident plan (uploads all tables). */
 int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);

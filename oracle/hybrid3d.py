@@ -590,3 +590,60 @@ class HybridOracle3D:
         for k in range(3):
             contrib += (fd * gn[k]) @ D[k]
         np.add.at(out, dofs, contrib)
+
+
+# --- right-hand side and error (reference sipg.py:697-741, restated on the hybrid machinery) -----
+def _rhs_l2_methods():
+    def phys_points(self, e, ex):
+        """Physical coordinates (3, n_pts) of an expansion's volume points in element e."""
+        return (self.x0[e][:, None] + self.F[e] @ (ex.xi.T + 1.0))
+
+    def rhs_assemble(self, case, bcs):
+        """b = -(v, f) plus the Dirichlet lift of the mirror ghost state (sipg.py:697-718): volume
+        IProduct of the forcing, and on boundary faces the absorb of jump = -2 g, average 0 with
+        sign -1 (TraceIProduct branch)."""
+        b = np.zeros(self.n_dofs)
+        for (s, n, q), ids in self.classes.items():
+            ex = self.exps[ids[0]]
+            ids = np.asarray(ids)
+            xs = np.stack([phys_points(self, e, ex) for e in ids], axis=-1)            # (3, p, W)
+            f = case.forcing(xs)
+            jw = ex.ref_w[:, None] * self.detJ[ids][None, :]
+            dof = self.dof_off[ids][None, :] + np.arange(ex.n_coeffs)[:, None]
+            b[dof] = -ex.iprod(f * jw)
+        for g in self.groups:
+            if g["key"][0] != "b":
+                continue
+            gfun = bcs["dirichlet"]
+            el = g["el"]
+            exl = self.exps[int(el[0])]
+            prm, _ = exl.face_grid(g["key"][2])
+            eta = face_to_eta(exl.faces[g["key"][2]], prm)
+            xi = xi_of_eta(exl.shape, eta)
+            gv = np.stack([gfun(self.x0[e][:, None] + self.F[e] @ (xi.T + 1.0)) for e in el])   # (W, nf)
+            jump, avg, sign = -2.0 * gv, 0.0 * gv, -1.0
+            fv = (g["tau"] * jump - avg) * g["swj"] * sign
+            fd = (-0.5 * sign) * jump * g["swj"]
+            contrib = fv @ g["B_l"]
+            for k in range(3):
+                contrib += (fd * g["gn_l"][k]) @ g["D_l"][k]
+            np.add.at(b, g["dofs_l"], contrib)
+        return b
+
+    def l2_error(self, x, exact):
+        """sqrt(sum_e int (u_h - u)^2 J) on rules with 2 extra points per direction (sipg.py:720-741)."""
+        err2 = 0.0
+        for (s, n, q), ids in self.classes.items():
+            fine = expansion3(s, n, q + 2)
+            ids = np.asarray(ids)
+            dof = self.dof_off[ids][None, :] + np.arange(fine.n_coeffs)[:, None]
+            uh = fine.bwd(np.asarray(x)[dof])
+            xs = np.stack([phys_points(self, e, fine) for e in ids], axis=-1)
+            diff = uh - exact(xs)
+            err2 += float((diff * diff * fine.ref_w[:, None] * self.detJ[ids][None, :]).sum())
+        return math.sqrt(err2)
+
+    return rhs_assemble, l2_error
+
+
+HybridOracle3D.rhs_assemble, HybridOracle3D.l2_error = _rhs_l2_methods()

@@ -21,7 +21,7 @@ EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destr
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
            "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply", "sipg_plan_n_dofs", "sipg_cg",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
-           "sipg_apply_role", "sipg_h3_plan_create"]
+           "sipg_apply_role", "sipg_h3_plan_create", "sipg_h3_apply_traces", "sipg_h3_trace_len"]
 
 
 class SolveReportC(ctypes.Structure):
@@ -72,6 +72,9 @@ def load() -> ctypes.CDLL:
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.sipg_plan_create.argtypes = [ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)]
     lib.sipg_h3_plan_create.argtypes = [ctypes.POINTER(H3Desc), ctypes.POINTER(vp)]
+    lib.sipg_h3_apply_traces.argtypes = [vp, vp, vp, vp, vp]
+    lib.sipg_h3_trace_len.argtypes = [vp]
+    lib.sipg_h3_trace_len.restype = ctypes.c_int64
     lib.sipg_plan_create.restype = ctypes.c_int
     lib.sipg_apply.argtypes = [vp, vp, vp, vp]
     lib.sipg_apply.restype = ctypes.c_int
@@ -188,6 +191,16 @@ class NativePlan:
         self.n_dofs = pb.n_dofs
         self.n_classes = 2 * int(keep[0].shape[0])   # launch units: publish kernels, then apply kernels
         self._keep = None
+
+    def apply_traces(self, x_ptr: int, traces_ptr: int, y_ptr: int, stream: int = 0) -> None:
+        """Hybrid plans: the apply kernels on a caller-provided trace buffer (sipg_h3_apply_traces)."""
+        check(self._lib.sipg_h3_apply_traces(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(traces_ptr),
+                                             ctypes.c_void_p(y_ptr), ctypes.c_void_p(stream)),
+              "sipg_h3_apply_traces")
+
+    @property
+    def trace_len(self) -> int:
+        return int(self._lib.sipg_h3_trace_len(self.handle))
 
     def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
         check(self._lib.sipg_apply(self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),

@@ -125,6 +125,7 @@ struct H3State {
   H3Plan hps{};
   void* bufs[7] = {};
   double* pub = nullptr;
+  int64_t n_pub = 0;
 };
 
 // Independent class launches (the publishers of a phase, then the element classes) are spread over
@@ -657,6 +658,28 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
   return true;
 }
 
+// RHS lift of hybrid plans: the apply kernels alone, reading a caller-provided
+// trace buffer instead of the published one (same layout: slot pub_self offsets, (u, n.grad u)
+// per trace point).  With x = 0 and the Dirichlet data as the boundary slots' own traces this is
+// exactly the reference's boundary lift (rhs_assemble, sipg.py:707-717).
+int sipg_h3_apply_traces(sipg_plan* p, const double* x_dev, const double* traces_dev, double* y_dev, void* stream) {
+  if (!p || !p->h3 || !x_dev || !traces_dev || !y_dev) return fail(SIPG_ERR_ARG, "bad argument");
+  H3State* h = p->h3;
+  H3Plan hp = h->hp;
+  hp.pub = const_cast<double*>(traces_dev);
+  for (int c = 0; c < p->n_cls; ++c) {
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    if (count == 0 || h->cd[c * CD3_WORDS + CD3_ROLE] == 2) continue;
+    const H3Entry* k = h->kern[c];
+    k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, (cudaStream_t)stream>>>(hp, c, x_dev, y_dev);
+    ++p->launches;
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int64_t sipg_h3_trace_len(const sipg_plan* p) { return p && p->h3 ? p->h3->n_pub : -1; }
+
 int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   if (!d || !out) return fail(SIPG_ERR_ARG, "null argument");
   *out = nullptr;
@@ -715,6 +738,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   }
   void* b[7] = {cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d};
   memcpy(h->bufs, b, sizeof(b));
+  h->n_pub = d->n_pub;
   if (d->n_pub > 0) {
     cudaError_t e = cudaMalloc((void**)&h->pub, sizeof(double) * d->n_pub);
     if (e != cudaSuccess) {

@@ -148,3 +148,37 @@ def test_oracle_matches_frozen_cfg4_fixtures(path):
     x = case.draw_x(op.n_dofs)
     assert np.array_equal(x, g["x"])
     assert rel_maxnorm(op(x), g["y"]) <= 1e-14
+
+
+# ---- rhs_assemble / l2_error, pinned by the real reference on an all-hex mesh
+def _sin_case(k, lam=1.0):
+    """The reference's sinusoidal manufactured case (sipg.py:88-100), restated."""
+    def exact(x):
+        return np.sin(k * x[0]) * np.sin(k * x[1]) * np.sin(k * x[2])
+
+    def forcing(x):
+        return -(lam + 3 * k * k) * exact(x)
+    return exact, forcing
+
+
+def test_rhs_and_l2_match_reference_fixture():
+    from pathlib import Path
+    d = np.load(Path(__file__).resolve().parent / "golden" / "oracle_cfg4" / "ref_rhs_hex.npz")
+    P = d["P"]
+    ref = h.HybridOracle3D(["hex"] * len(P), d["elem_verts"], d["verts"], P + 1, P + 2)
+    exact, forcing = _sin_case(float(d["k"]))
+    case = type("Case", (), {"exact": staticmethod(exact), "forcing": staticmethod(forcing)})
+    b = ref.rhs_assemble(case, {"dirichlet": exact})
+    assert rel_maxnorm(b, d["b"]) <= 1e-13
+    assert abs(ref.l2_error(d["x"], exact) - float(d["err"])) <= 1e-13 * float(d["err"])
+
+
+@pytest.mark.parametrize("shape", ["hex", "prism", "tet"])
+@pytest.mark.parametrize("n,dq", [(2, 1), (5, 1), (7, 3)])
+def test_rhs3d_dense_phi_matches_oracle_basis(shape, n, dq):
+    """The product's dense class table (built from the plan's staged BwdTrans tables) is the
+    oracle's basis at the volume points."""
+    from paper_2504_03573_b200.plan3d import ClassTables3
+    from paper_2504_03573_b200.rhs3d import dense_phi
+    ex = h.Expansion3(shape, n, n + dq)
+    assert np.abs(dense_phi(ClassTables3(shape, n, n + dq)) - ex.Phi).max() <= 1e-14
