@@ -89,19 +89,21 @@ class HelmholtzOperator:
         self.timers["setup"] = time.perf_counter() - t0
 
     def rhs_assemble(self, case, bcs):
-        """b = -(v, f) + Dirichlet lift (reference sipg.py:697-718): on the GPU for hybrid 3-D
-        plans (rhs3d.py); the standard plans do not carry it yet."""
-        if not getattr(self.plan, "is_h3", False):
-            raise NotImplementedError("rhs_assemble: hybrid 3-D plans only in this build")
-        from .rhs3d import rhs_assemble
+        """b = -(v, f) + Dirichlet lift (reference sipg.py:697-718), on the GPU: rhs.py for the
+        standard plans, rhs3d.py (lift through the apply kernels) for hybrid 3-D plans."""
+        if getattr(self.plan, "is_h3", False):
+            from .rhs3d import rhs_assemble
+        else:
+            from .rhs import rhs_assemble
         return rhs_assemble(self, case, bcs)
 
     def l2_error(self, x, exact) -> float:
         """sqrt(sum_e int (u_h - u)^2 J) with 2 extra points per direction (reference
-        sipg.py:720-741); hybrid 3-D plans."""
-        if not getattr(self.plan, "is_h3", False):
-            raise NotImplementedError("l2_error: hybrid 3-D plans only in this build")
-        from .rhs3d import l2_error
+        sipg.py:720-741), on the GPU."""
+        if getattr(self.plan, "is_h3", False):
+            from .rhs3d import l2_error
+        else:
+            from .rhs import l2_error
         return l2_error(self, x, exact)
 
     def dof_slice(self, e: int) -> slice:

@@ -1,0 +1,71 @@
+"""SURVEY §8f row f2 on the standard plans: rhs_assemble / l2_error on the GPU against the REAL
+reference's outputs (tests/golden/rhs_*.npz, made by tests/golden/make_rhs_golden.py) for the
+reference's sinusoidal and Gaussian-pulse manufactured cases (sipg.py:88-121, restated here), on
+configs 0-3 (conforming / perturbed p-nonconforming quads, hybrid quad / tri, hex), patched and
+unpatched penalties. Bar: 1e-12 relative max-norm."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_maxnorm
+
+pytestmark = pytest.mark.gpu
+FILES = sorted(GOLDEN.glob("rhs_cfg*.npz"))
+
+
+def manufactured(d, k, a, lam=1.0):
+    """(sinusoidal, pulse) cases as (exact, forcing) pairs."""
+    def s_ex(x):
+        return np.prod([np.sin(k * x[i]) for i in range(d)], axis=0)
+
+    def g_ex(x):
+        return np.exp(-sum(x[i] ** 2 for i in range(d)) / (a * a))
+    sin = (s_ex, lambda x: -(lam + d * k * k) * s_ex(x))
+    pulse = (g_ex, lambda x: (4.0 * sum(x[i] ** 2 for i in range(d)) / a ** 4 - 2.0 * d / (a * a) - lam) * g_ex(x))
+    return [type("Case", (), {"exact": staticmethod(e), "forcing": staticmethod(f)}) for e, f in (sin, pulse)]
+
+
+def _op(g):
+    from paper_2504_03573_b200 import configs
+    from paper_2504_03573_b200.sipg import HelmholtzOperator
+    case = configs.build_case(str(g["config"]), int(g["nx"]), int(g["seed"]))
+    patched = bool(g["patched"])
+    return HelmholtzOperator(case.mesh, case.order_map, basis_kind="modified_modal",
+                             tau_rule="baseline" if patched else "reference",
+                             shared_rule="patched" if patched else "reference")
+
+
+@pytest.mark.parametrize("path", FILES, ids=[p.stem for p in FILES])
+def test_rhs_and_l2_match_reference(path):
+    g = np.load(path)
+    op = _op(g)
+    sin, pulse = manufactured(op.mesh.dim, float(g["k"]), float(g["a"]))
+    assert rel_maxnorm(op.rhs_assemble(sin, {"dirichlet": sin.exact}), g["b_sin"]) <= 1e-12
+    assert rel_maxnorm(op.rhs_assemble(pulse, {"dirichlet": pulse.exact}), g["b_pulse"]) <= 1e-12
+    err = float(g["err"])
+    assert abs(op.l2_error(g["x"], sin.exact) - err) <= 1e-12 * err
+
+
+def test_missing_boundary_tag_raises():
+    g = np.load(FILES[0])
+    op = _op(g)
+    sin, _ = manufactured(op.mesh.dim, 2.0, 0.3)
+    with pytest.raises(KeyError):
+        op.rhs_assemble(sin, {"neumann": sin.exact})
+
+
+def test_manufactured_solve_converges_2d():
+    """rhs -> CG over the GPU apply -> l2_error, conforming quads: spectral in P."""
+    from scipy.sparse.linalg import LinearOperator, cg
+    from paper_2504_03573_b200.mesh import OrderMap, Shape, generate_box
+    from paper_2504_03573_b200.sipg import HelmholtzOperator
+    m = generate_box(2, 4, Shape.QUAD, (0.0, 1.0))
+    sin, _ = manufactured(2, 2.0, 0.3)
+    errs = []
+    for P in (2, 4, 6):
+        op = HelmholtzOperator(m, OrderMap(np.full(m.n_elements, P + 1), np.full(m.n_elements, P + 2)),
+                               basis_kind="modified_modal", tau_rule="baseline")
+        b = op.rhs_assemble(sin, {"dirichlet": sin.exact})
+        x, info = cg(LinearOperator((op.n_dofs,) * 2, matvec=op.lhs_eval), b, rtol=1e-12, maxiter=20000)
+        assert info == 0
+        errs.append(op.l2_error(x, sin.exact))
+    assert errs[1] < 0.05 * errs[0] and errs[2] < 0.05 * errs[1], errs

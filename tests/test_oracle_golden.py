@@ -27,3 +27,37 @@ def test_oracle_rejects_wrong_length():
     op = OracleOperator(case.mesh, case.order_map)
     with pytest.raises(ValueError):
         op.lhs_eval(np.zeros(op.n_dofs + 1))
+
+
+def test_rhs_fixtures_present_and_consistent():
+    """The reference rhs / l2 fixtures (tests/golden/make_rhs_golden.py) carry what test_gpu_rhs.py
+    needs, and their DoF counts match the plans this package builds for the same cases."""
+    from conftest import GOLDEN
+    from paper_2504_03573_b200 import configs
+    from paper_2504_03573_b200.plan import PlanBuilder
+    files = sorted(GOLDEN.glob("rhs_cfg*.npz"))
+    assert len(files) >= 5
+    for p in files:
+        g = np.load(p)
+        case = configs.build_case(str(g["config"]), int(g["nx"]), int(g["seed"]))
+        pb = PlanBuilder(case.mesh, case.order_map, basis_kind="modified_modal").build()
+        assert g["b_sin"].shape == g["b_pulse"].shape == g["x"].shape == (pb.n_dofs,)
+        assert np.isfinite(g["b_sin"]).all() and float(g["err"]) > 0
+
+
+def test_rhs_volume_basis_matches_oracle_expansion():
+    """rhs.volume_basis (the dense class table of the GPU rhs / l2) equals the oracle's BwdTrans of
+    unit coefficient vectors."""
+    from oracle.elements import expansion
+    from paper_2504_03573_b200.rhs import volume_basis
+    from paper_2504_03573_b200.stdregions import DEFAULT_RULES, class_tables
+    for shape, n, q in (("quad", 5, 6), ("tri", 4, 6), ("hex", 4, 5), ("tri", 7, 9)):
+        kinds = tuple(k.value for k in DEFAULT_RULES[shape])
+        ct = class_tables(shape, "modified_modal", n, (q,) * ct_dim(shape), kinds)
+        ex = expansion(shape, "modified_modal", n, (q,) * ct_dim(shape), kinds)
+        ref = ex.bwd(np.eye(ct.n_coeffs))
+        assert np.abs(volume_basis(ct) - ref).max() <= 1e-13
+
+
+def ct_dim(shape):
+    return 3 if shape == "hex" else 2
