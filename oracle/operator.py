@@ -178,7 +178,7 @@ class OracleOperator:
         for key, items in buckets.items():
             if key[0] == "b":
                 e0, f0 = items[0].left
-                g = {"kind": "boundary", "tau": np.array([[self._tau(t)] for t in items])}
+                g = {"kind": "boundary", "tau": np.array([[self._tau(t)] for t in items]), "tag": key[3]}
                 g["left"] = self._own_side(self.exps[e0], f0, [t.left[0] for t in items])
                 self.groups.append(g)
             else:
@@ -321,7 +321,7 @@ class OracleOperator:
         """sipg.py:663-677."""
         fv = (tau * jump - avg) * s.swj * sign
         fd = (-0.5 * sign) * jump * s.swj
-        if s.pv is not None:
+        if s.pv is not None and pacc is not None:
             cls = self.cls_of[int(s.elems[0])]
             cols = self.col[s.elems]
             p = pacc[cls]
@@ -344,3 +344,40 @@ class OracleOperator:
                 terms += ex.iprod_d(k, blk[1 + k])
             dof_idx = (self.dof_off[np.asarray(ids)][None, :] + np.arange(ex.n_coeffs)[:, None])
             out[dof_idx] += terms
+
+    # -- right-hand side and error ----------------------------------------
+
+    def rhs_assemble(self, case, bcs):
+        """sipg.py:697-718: b = -(v, f) per class, then on every boundary group the absorb of the
+        mirror ghost's jump = -2 g and average 0 with sign -1, straight into b (no final sweep)."""
+        b = np.zeros(self.n_dofs)
+        for cid, ids in self.classes.items():
+            ex = self.exps[ids[0]]
+            ids_a = np.asarray(ids)
+            xs = self.efac[cid]["x"].transpose(2, 1, 0)               # (d, n_phys, W)
+            dof_idx = self.dof_off[ids_a][None, :] + np.arange(ex.n_coeffs)[:, None]
+            b[dof_idx] = -ex.iprod(case.forcing(xs) * self.efac[cid]["jw"].T)
+        for g in self.groups:
+            if g["kind"] != "boundary":
+                continue
+            if g["tag"] not in bcs:
+                raise KeyError(f"no boundary condition for tag {g['tag']!r}")
+            L = g["left"]
+            xf = [self._fac(int(e), L.f)["x"] for e in L.elems]           # (nf, d) each
+            gv = np.stack([bcs[g["tag"]](x.T) for x in xf])
+            self._absorb(L, g["tau"], -2.0 * gv, 0.0 * gv, b, None, -1.0)
+        return b
+
+    def l2_error(self, x, exact):
+        """sipg.py:720-741: per element on rules with 2 extra points per direction."""
+        x = np.asarray(x, dtype=float)
+        err2 = 0.0
+        for cid, ids in self.classes.items():
+            ex = self.exps[ids[0]]
+            fine = expansion(ex.shape, ex.kind, ex.n, tuple(q + 2 for q in ex.nq), ex.kinds)
+            ids_a = np.asarray(ids)
+            ef = geo.element_factors(ex.shape, np.stack([self.ev[e] for e in ids]), fine)
+            dof_idx = self.dof_off[ids_a][None, :] + np.arange(ex.n_coeffs)[:, None]
+            diff = fine.bwd(x[dof_idx]) - exact(ef["x"].transpose(2, 1, 0))
+            err2 += float((diff * diff * ef["jw"].T).sum())
+        return float(np.sqrt(err2))

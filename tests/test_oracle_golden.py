@@ -61,3 +61,32 @@ def test_rhs_volume_basis_matches_oracle_expansion():
 
 def ct_dim(shape):
     return 3 if shape == "hex" else 2
+
+
+@pytest.mark.parametrize("tag", ["rhs_cfg0_n3", "rhs_cfg1_n4", "rhs_cfg1_n4_unpatched", "rhs_cfg2_n5",
+                                 "rhs_cfg3b_n2"])
+def test_oracle_rhs_and_l2_match_reference(tag):
+    """The oracle's restatement of rhs_assemble / l2_error (sipg.py:697-741) against the real
+    reference's outputs (tests/golden/make_rhs_golden.py)."""
+    from conftest import GOLDEN
+    from oracle import OracleOperator
+    from paper_2504_03573_b200 import configs
+    g = np.load(GOLDEN / f"{tag}.npz")
+    case = configs.build_case(str(g["config"]), int(g["nx"]), int(g["seed"]))
+    patched = bool(g["patched"])
+    ref = OracleOperator(case.mesh, case.order_map, basis_kind="modified_modal",
+                         tau_rule="baseline" if patched else "reference",
+                         shared_rule="patched" if patched else "reference")
+    d, k, a = case.mesh.dim, float(g["k"]), float(g["a"])
+
+    def s_ex(x):
+        return np.prod([np.sin(k * x[i]) for i in range(d)], axis=0)
+
+    def g_ex(x):
+        return np.exp(-sum(x[i] ** 2 for i in range(d)) / (a * a))
+    sin = type("C", (), {"exact": staticmethod(s_ex), "forcing": staticmethod(lambda x: -(1 + d * k * k) * s_ex(x))})
+    pulse = type("C", (), {"exact": staticmethod(g_ex), "forcing": staticmethod(
+        lambda x: (4.0 * sum(x[i] ** 2 for i in range(d)) / a ** 4 - 2.0 * d / (a * a) - 1.0) * g_ex(x))})
+    assert rel_maxnorm(ref.rhs_assemble(sin, {"dirichlet": s_ex}), g["b_sin"]) <= 1e-13
+    assert rel_maxnorm(ref.rhs_assemble(pulse, {"dirichlet": g_ex}), g["b_pulse"]) <= 1e-13
+    assert abs(ref.l2_error(g["x"], s_ex) - float(g["err"])) <= 1e-13 * float(g["err"])
