@@ -158,6 +158,11 @@ struct sipg_plan {
   void* bufs[11];
   double* x_stage = nullptr;
   double* y_stage = nullptr;
+  // solver workspace (sipg_cg): device vectors + reduction scratch and pinned scalars, kept across
+  // solves (allocated on first use, grown on demand, freed with the plan)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  double* ws_host = nullptr;
   int64_t launches = 0;
   std::vector<int> per_sm;               // resident CTAs per SM of each class's kernel
   int sms = 148;
@@ -1047,7 +1052,26 @@ int sipg_plan_destroy(sipg_plan* p) {
   for (cudaEvent_t e : p->ev_comp) cudaEventDestroy(e);
   if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->y_stage) cudaFree(p->y_stage);
+  if (p->ws) cudaFree(p->ws);
+  if (p->ws_host) cudaFreeHost(p->ws_host);
   delete p;
+  return 0;
+}
+
+// Internal (sipg_krylov.cu): the plan's cached solver workspace of at least `bytes` device bytes and
+// `host_doubles` <= 64 pinned host doubles.  One solve per plan at a time (like the staging buffers).
+int sipg__workspace(sipg_plan* p, size_t bytes, void** dev, double** host) {
+  if (!p || !dev || !host) return SIPG_ERR_ARG;
+  if (bytes > p->ws_bytes) {
+    if (p->ws) cudaFree(p->ws);
+    p->ws = nullptr;
+    p->ws_bytes = 0;
+    if (cudaMalloc(&p->ws, bytes) != cudaSuccess) return SIPG_ERR_CUDA;
+    p->ws_bytes = bytes;
+  }
+  if (!p->ws_host && cudaMallocHost((void**)&p->ws_host, 64 * sizeof(double)) != cudaSuccess) return SIPG_ERR_CUDA;
+  *dev = p->ws;
+  *host = p->ws_host;
   return 0;
 }
 

@@ -127,6 +127,8 @@ int fetch(Ctx& c) {
 
 }  // namespace
 
+extern "C" int sipg__workspace(sipg_plan* p, size_t bytes, void** dev, double** host);   // sipg_capi.cu
+
 extern "C" int sipg_cg(sipg_plan* plan, const double* b, double* x, int64_t n, double tol, int64_t maxiter,
                        sipg_solve_report* rep, void* stream) {
   if (!plan || !b || !x || !rep || n <= 0 || n != sipg_plan_n_dofs(plan)) {
@@ -137,16 +139,20 @@ extern "C" int sipg_cg(sipg_plan* plan, const double* b, double* x, int64_t n, d
   Ctx c{(cudaStream_t)stream, nullptr, nullptr, nullptr};
   double *r = nullptr, *p = nullptr, *ap = nullptr;
   int rc = 0;
-  auto cleanup = [&]() {
-    cudaFree(r); cudaFree(p); cudaFree(ap); cudaFree(c.part); cudaFree(c.sc);
-    if (c.host) cudaFreeHost(c.host);
-  };
-  if (cudaMalloc((void**)&r, sizeof(double) * n) != cudaSuccess || cudaMalloc((void**)&p, sizeof(double) * n) ||
-      cudaMalloc((void**)&ap, sizeof(double) * n) || cudaMalloc((void**)&c.part, sizeof(double) * RB) ||
-      cudaMalloc((void**)&c.sc, sizeof(double) * S_N) || cudaMallocHost((void**)&c.host, sizeof(double) * S_N)) {
-    cleanup();
-    sipg_set_error("sipg_cg: device allocation failed");
-    return SIPG_ERR_CUDA;
+  auto cleanup = [&]() {};   // the workspace belongs to the plan (reused by the next solve)
+  {
+    // r, p, Ap, reduction partials, device scalars: one cached block (sipg__workspace)
+    const size_t nn = ((size_t)n + 31) & ~(size_t)31;   // 256-byte aligned vectors
+    void* ws = nullptr;
+    if (sipg__workspace(plan, sizeof(double) * (3 * nn + RB + S_N + 8), &ws, &c.host) != 0) {
+      sipg_set_error("sipg_cg: device allocation failed");
+      return SIPG_ERR_CUDA;
+    }
+    r = static_cast<double*>(ws);
+    p = r + nn;
+    ap = p + nn;
+    c.part = ap + nn;
+    c.sc = c.part + RB;
   }
   // nb = ||b||; x = 0
   cudaMemsetAsync(x, 0, sizeof(double) * n, c.s);
