@@ -47,11 +47,24 @@ def _fine(ct):
                         tuple(r.kind.value for r in ct.rules))
 
 
-def _volume(pb, ct, verts):
-    """Physical points (d, p, W) and jw (p, W) of elements with vertex coords `verts` (W, nv, d)."""
-    x, F = jacobians(ct.shape, verts, ct.xi)
-    J = np.linalg.det(F)                                           # (W, p)
-    return np.ascontiguousarray(x.transpose(2, 1, 0)), (J * ct.ref_w[None, :]).T
+def _volume(pb, i, ct, ids, verts):
+    """Physical points (d, p, W) as numpy (for the user's callbacks) and jw (p, W) on the device, of
+    the class-i elements `ids` (vertex coords `verts` (W, nv, d)) at the volume points of `ct`.
+    The vertex-map products run on the GPU; affine elements take the plan's constant Jacobian
+    (ElemGeo.J0), the others det F per point (batched on the device)."""
+    import torch
+    from .plan import vertex_maps
+    N, dN = vertex_maps(ct.shape, ct.xi)
+    vd = _dev(verts)                                                          # (W, nv, d)
+    x = torch.einsum("pv,evi->ipe", _dev(N), vd)
+    g = pb.geo[i]
+    pos = pb.exp_pos[ids]
+    J = _dev(np.broadcast_to(g.J0[pos][None, :], (ct.n_phys, ids.size)))
+    nr = np.flatnonzero(~g.regular[pos])
+    if nr.size:
+        F = torch.einsum("pvj,evi->epij", _dev(dN), vd[torch.from_numpy(nr).cuda()])
+        J[:, torch.from_numpy(nr).cuda()] = torch.linalg.det(F).T
+    return x.cpu().numpy(), J * _dev(ct.ref_w)[:, None]
 
 
 def _dev(a):
@@ -70,9 +83,9 @@ def rhs_assemble(op, case, bcs):
         if ids.size == 0:
             continue
         ct = pb.exp_list[i]
-        xs, jw = _volume(pb, ct, X[ev[ids, :NV[ct.shape]]])
-        f = np.asarray(case.forcing(xs), dtype=float)
-        contrib = -(_dev(volume_basis(ct)).T @ _dev(f * jw))       # (nc, W)
+        xs, jw = _volume(pb, i, ct, ids, X[ev[ids, :NV[ct.shape]]])
+        f = _dev(np.asarray(case.forcing(xs), dtype=float))
+        contrib = -(_dev(volume_basis(ct)).T @ (f * jw))           # (nc, W)
         dof = pb.dof_off[ids][None, :] + np.arange(ct.n_coeffs)[:, None]
         b.index_copy_(0, torch.from_numpy(dof.reshape(-1)).cuda(), contrib.reshape(-1))
     # boundary faces grouped by (class, face, tag)
@@ -116,8 +129,8 @@ def l2_error(op, x, exact) -> float:
         if ids.size == 0:
             continue
         fine = _fine(pb.exp_list[i])
-        xs, jw = _volume(pb, fine, X[ev[ids, :NV[fine.shape]]])
+        xs, jw = _volume(pb, i, fine, ids, X[ev[ids, :NV[fine.shape]]])
         dof = torch.from_numpy(pb.dof_off[ids][None, :] + np.arange(fine.n_coeffs)[:, None]).cuda()
         d = _dev(volume_basis(fine)) @ xd[dof] - _dev(np.asarray(exact(xs), dtype=float))
-        err2 += (d * d * _dev(jw)).sum()
+        err2 += (d * d * jw).sum()
     return math.sqrt(float(err2))
