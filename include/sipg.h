@@ -118,7 +118,9 @@ int sipg_plan_destroy(sipg_plan* plan);
  * the reference: stop on p.Ap <= 0 ("indefinite direction", x not updated), on
  * ||r||/||b|| <= tol after verifying the true residual (<= 10 tol, else
  * "residual drift"), on 250 iterations without a 0.1 % improvement
- * ("stagnation"), or at maxiter. */
+ * ("stagnation"), or at maxiter.  The solver's vectors (r, p, Ap) live in a workspace owned by
+ * the plan (allocated by the first solve, reused, freed by sipg_plan_destroy): one solve per plan
+ * at a time, like sipg_apply_host's staging buffers. */
 typedef struct sipg_solve_report {
   int32_t converged;   /* 1 / 0 */
   int32_t reason;      /* 0 converged, 1 indefinite direction, 2 residual drift, 3 stagnation, 4 maxiter */
