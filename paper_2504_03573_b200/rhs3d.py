@@ -25,7 +25,6 @@ import numpy as np
 
 from .plan3d import FACES, CD3_COUNT, CD3_ELEM_OFF, ClassTables3, xi_of_eta
 
-NAMES = {0: "hex", 1: "prism", 2: "tet"}
 
 
 def _tri_groups(n, tet):
