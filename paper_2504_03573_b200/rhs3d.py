@@ -26,7 +26,6 @@ import numpy as np
 from .plan3d import FACES, CD3_COUNT, CD3_ELEM_OFF, ClassTables3, xi_of_eta
 
 
-
 def _tri_groups(n, tet):
     gof = []
     for i in range(n):
