@@ -35,6 +35,10 @@ void sipg_register_hex(std::vector<KernelEntry>& v);
 
 #include <cuda_runtime.h>
 #ifdef __CUDACC__
+// warps (elements in flight) per CTA of the 2-D warp-per-element kernels
+#ifndef SIPG_WPC
+#define SIPG_WPC 8
+#endif
 template <int SHAPE, int N, int Q, int GEOM>
 KernelEntry sipg_entry();
 #define SIPG_DEFINE_ENTRY                                                                    \
@@ -44,8 +48,8 @@ KernelEntry sipg_entry();
     if (SHAPE == SHAPE_HEX)                                                                  \
       return KernelEntry{SHAPE, N, Q, GEOM, 0, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,     \
                          sizeof(double) * (size_t)C::TOTAL, nullptr};                        \
-    return KernelEntry{SHAPE, N, Q, GEOM, 5, &sipg::k_apply_w<SHAPE, N, Q, GEOM, 8>, 256,    \
-                       sizeof(double) * (size_t)(C::TABP + 8 * C::ESZ), nullptr};            \
+    return KernelEntry{SHAPE, N, Q, GEOM, 5, &sipg::k_apply_w<SHAPE, N, Q, GEOM, SIPG_WPC>,      \
+                       32 * SIPG_WPC, sizeof(double) * (size_t)(C::TABP + SIPG_WPC * C::ESZ), nullptr};            \
   }
 #define SIPG_ENTRIES_NQ(S, N)                                                                \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_REGULAR>());                                      \
