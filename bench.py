@@ -1,16 +1,20 @@
 """Benchmark of the B200 SIP-Helmholtz apply (one JSON line on rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3a] [--impl native|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl native|reference]
 
 A step is one apply y = (lambda M + L_SIP) x over the whole synthetic workload
-(BASELINE.json config; default cfg3a = unit cube, 32^3 hex, P = 6,
-modified-modal basis, GLL q = P+2, lambda = 1, tau = (P+1)^2/h, x ~ U[-1,1]).
+(BASELINE.json config; default cfg4 — the largest single-GPU configuration:
+unit cube on 48^3 cubes, each a hex / 2 prisms / 6 tets, P in {3..6},
+modified-modal bases, q = P+2 (GLL on hex axes, Gauss-Legendre + Duffy on
+collapsed axes), lambda = 1, tau = (P+1)^2/h, x ~ U[-1,1]).
 `value` is GDoF/s with x resident in HBM (device-timed with CUDA events,
 L2 flushed between steps); `e2e` is the same metric through the public C-ABI
 host entry point (sipg_apply_host) from pinned host buffers, H2D + apply + D2H
 inside the timed region.  Multi-GPU: weak scaling, one x-slab of the config
 per rank; `--impl reference` times the CPU oracle port on the
-host cores (rank 0 only).
+host cores (rank 0 only): the unmodified reference (`baseline/_ref`, patched
+from outside for the BASELINE penalty / shared rule) on configs 0-3b, the
+oracle port on config 4 (the reference has no prism / tet).
 """
 from __future__ import annotations
 
@@ -34,7 +38,7 @@ HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.js
 OP_KW = dict(basis_kind="modified_modal", tau_rule="baseline", shared_rule="patched")
 
 
-KERNEL_NAMES = {0: "k_apply", 1: "k_hexw", 2: "k_hex_mma", 3: "k_hex_mma", 4: "k_hex", 5: "k_apply_w",
+KERNEL_NAMES = {0: "k_apply", 2: "k_hex(generic faces)", 4: "k_hex", 5: "k_apply_w",
                 6: "k_hexp", 7: "k_hexp", 8: "k_h3_publish", 9: "k_h3_apply"}
 
 
@@ -118,10 +122,9 @@ def build_workload(name, nx, seed, rank=0, world=1):
     return case
 
 
-def _cpu_sample(name):
-    """Oracle port on a bounded sample of the workload: for the 3D configs the
-    first x-slab holding 1/8 of the elements (same orders / geometry), else the
-    full mesh."""
+def _port_sample(name):
+    """Oracle port on a bounded sample of the workload (config 4, which the reference cannot run:
+    the cfg4 recipe on a 12^3 cube grid; elsewhere the fallback when baseline/_ref is missing)."""
     from oracle import OracleOperator
     from paper_2504_03573_b200 import configs
     from paper_2504_03573_b200.mesh import OrderMap, Shape, generate_box
@@ -133,7 +136,7 @@ def _cpu_sample(name):
         t0 = time.perf_counter()
         op = HybridOracle3D(m.shapes, [el.verts for el in m.elements], m.vertices, om.n_modes, om.n_quad)
         sample = (f"cfg4 recipe on a 12^3 cube grid ({m.n_elements} of {case.mesh.n_elements} elements), "
-                  f"oracle/hybrid3d numpy restatement (setup {time.perf_counter() - t0:.1f}s)")
+                  f"oracle/hybrid3d numpy port (setup {time.perf_counter() - t0:.1f}s)")
         x = np.random.default_rng(0).uniform(-1.0, 1.0, op.n_dofs)
         return op, x, sample
     if name in ("cfg3a", "cfg3b"):
@@ -147,7 +150,7 @@ def _cpu_sample(name):
         sample = f"{name} full mesh"
     t0 = time.perf_counter()
     op = OracleOperator(m, om, **OP_KW)
-    sample += f", oracle/ numpy restatement (setup {time.perf_counter() - t0:.1f}s)"
+    sample += f", oracle/ numpy port (setup {time.perf_counter() - t0:.1f}s)"
     x = np.random.default_rng(0).uniform(-1.0, 1.0, op.n_dofs)
     return op, x, sample
 
@@ -156,46 +159,109 @@ def _threads():
     return int(os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count())
 
 
-def cpu_baseline(name, seconds_hint=20.0):
-    op, x, sample = _cpu_sample(name)
-    op.lhs_eval(x)
+def cpu_measure(name, steps, warmup):
+    """The CPU leg: the reference's own lhs_eval (configs 0-3b; batch widths 64 and 4) or the
+    oracle port (config 4), on a bounded sample, all host threads.  Returns the cpu_baseline dict
+    (value in GDoF/s = sample DoFs / mean apply time)."""
+    from oracle import reference_arm
+    base = {"unit": "GDoF/s", "cores": _threads(), "cpu_model": reference_arm.cpu_model(),
+            "host_cpus": os.cpu_count()}
+    if name != "cfg4":
+        try:
+            r = reference_arm.time_reference(name, steps, warmup)
+        except Exception as exc:   # reported; falls back to the port
+            r = {"error": repr(exc)}
+        if r and "by_width" in r:
+            w64, w4 = r["by_width"][64], r["by_width"][4]
+            return dict(base, value=w64["n_dofs"] / w64["mean_s"] / 1e9, kind="reference",
+                        sample=(f"{r['sample']}; unmodified reference dgsipg from {r['path']} (patches P1/P2 "
+                                f"applied from outside), batch_width=64 (its fastest, bit-identical output); "
+                                f"mean of {steps} applies"),
+                        reference_batch_width_4={"value": w4["n_dofs"] / w4["mean_s"] / 1e9,
+                                                 "note": "the reference's default batch_width"})
+        base["reference_error"] = (r or {}).get("error", "baseline/_ref not installed")
+    op, x, sample = _port_sample(name)
+    for _ in range(max(1, warmup)):
+        op.lhs_eval(x)
     ts = []
-    t_end = time.perf_counter() + seconds_hint
-    while len(ts) < 3 or (time.perf_counter() < t_end and len(ts) < 20):
+    for _ in range(steps):
         t1 = time.perf_counter()
         op.lhs_eval(x)
         ts.append(time.perf_counter() - t1)
-    t = float(np.median(ts))
-    return {"value": op.n_dofs / t / 1e9, "unit": "GDoF/s", "cores": _threads(), "kind": "port",
-            "sample": sample + f", median of {len(ts)} applies"}
+    t = float(np.mean(ts))
+    return dict(base, value=op.n_dofs / t / 1e9, kind="port",
+                sample=sample + f", mean of {steps} applies" +
+                ("; the reference has no prism / tet (SURVEY a18)" if name == "cfg4" else ""))
 
 
 def run_reference(args):
-    """The reference arm: the CPU oracle port (the Python reference cannot travel
-    to the GPU box), all host threads, rank 0 only; one step = one apply of the
-    bounded sample."""
+    """The reference arm: rank 0 only, all host threads, one step = one apply of the bounded
+    sample (cpu_measure)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-    op, x, sample = _cpu_sample(args.config)
-    for _ in range(args.warmup):
-        op.lhs_eval(x)
-    ts = []
-    for _ in range(args.steps):
-        t1 = time.perf_counter()
-        op.lhs_eval(x)
-        ts.append(time.perf_counter() - t1)
-    t = float(np.sum(ts)) / args.steps
-    v = op.n_dofs / t / 1e9
-    cb = {"value": v, "unit": "GDoF/s", "cores": _threads(), "kind": "port", "sample": sample}
+    t0 = time.perf_counter()
+    cb = cpu_measure(args.config, args.steps, args.warmup)
+    v = cb["value"]
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GDoF/s", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+           "data": "synthetic", "config": {"workload": args.config, "sample": cb["sample"]},
            "cpu_baseline": cb, "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0,
-                                       "d2h_bytes_per_step": 0}}
+                                       "d2h_bytes_per_step": 0},
+           "wall_s": time.perf_counter() - t0}
     print(json.dumps(out))
+
+
+def traffic_child(args):
+    """Runs under ncu (spawned by measure_traffic): one launch of launch unit `args.traffic_child`."""
+    import torch
+    from paper_2504_03573_b200 import configs
+    from paper_2504_03573_b200.sipg import HelmholtzOperator
+    case = build_workload(args.config, args.nx, args.seed)
+    op = HelmholtzOperator(case.mesh, case.order_map, **OP_KW)
+    x = torch.from_numpy(case.draw_x(op.n_dofs)).cuda()
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    op.native.apply_class(args.traffic_child, x.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+
+
+def measure_traffic(args, unit):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one launch of the dominant
+    kernel, measured in this run by ncu on a child process (the bench's own timings never run
+    under a profiler).  Returns (bytes | None, note)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "--kernel-name-base", "function", "-k", "regex:^k_", "-c", "1", "--csv",
+           sys.executable, str(ROOT / "bench.py"), "--config", args.config, "--seed", str(args.seed),
+           "--traffic-child", str(unit)] + (["--nx", str(args.nx)] if args.nx else [])
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=args.traffic_timeout)
+    except Exception as exc:
+        return None, f"ncu child failed: {exc!r}"
+    import csv
+    import io
+    vals, kname = {}, None
+    rows = [r for r in csv.reader(io.StringIO(res.stdout)) if len(r) > 10]
+    if rows:
+        h = rows[0]
+        try:
+            mi, vi, ui, ki = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit"), h.index("Kernel Name")
+        except ValueError:
+            return None, f"ncu output not parsed (rc={res.returncode})"
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+        for r in rows[1:]:
+            if r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                vals[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+                kname = r[ki]
+    if len(vals) != 2:
+        return None, f"ncu gave no DRAM counters (rc={res.returncode}): {res.stderr[-200:]!r}"
+    return int(round(sum(vals.values()))), f"ncu dram__bytes_read.sum + dram__bytes_write.sum of one {kname} launch in a child process of this run (cold L2)"
 
 
 def main():
@@ -203,13 +269,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg3a")
+    ap.add_argument("--config", default="cfg4")
     ap.add_argument("--nx", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=9)
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic child")
+    ap.add_argument("--traffic-timeout", type=float, default=300.0)
+    ap.add_argument("--traffic-child", type=int, default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_child is not None:
+        traffic_child(args)
+        return
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
@@ -398,13 +470,15 @@ def main():
         peak, peak_kind = hbm_peak()
         ach_gbs = rd["bytes"] / (cls_ms[dom] * 1e-3) / 1e9
         ach_tf = rd["flops"] / (cls_ms[dom] * 1e-3) / 1e12
-        traffic = None
-        tp = ROOT / "profiles" / "traffic.json"
-        if tp.exists():
-            try:
-                traffic = json.loads(tp.read_text()).get(args.config)
-            except Exception:
-                traffic = None
+        hbm_frac, fp_frac = ach_gbs / peak, ach_tf / FP64_PEAK_TFLOPS
+        traffic, traffic_note = (None, "skipped (--no-traffic)")
+        if world == 1 and not args.no_traffic:
+            traffic, traffic_note = measure_traffic(args, dom)
+        hbm_block = {"achieved": ach_gbs, "peak": peak, "unit": "GB/s", "frac": hbm_frac,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+        fp_block = {"achieved": ach_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": fp_frac,
+                    "peak_source": "measured DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak.log)"}
+        bound = fp_block if fp_frac >= hbm_frac else hbm_block
         clocks = clk.summary()
         out = {
             "metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
@@ -417,19 +491,18 @@ def main():
                        "parallelism": (f"x-slab dp{world}: {world} config boxes stacked in x, one slab + "
                                        "ghost layer per GPU, NCCL halo exchange overlapped with interior "
                                        "elements") if world > 1 else "single GPU"},
-            "roofline": {"bound": "hbm", "achieved": ach_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": ach_gbs / peak, "traffic": traffic,
-                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "kernel": kernel_label(op.native.class_info(dom), rd),
-                         "kernel_ms": float(cls_ms[dom]), "kernel_share": float(cls_ms[dom] / cls_ms.sum()),
-                         "algorithmic_bytes_per_launch": rd["bytes"]},
-            "roofline_fp64": {"achieved": ach_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                              "frac": ach_tf / FP64_PEAK_TFLOPS,
-                              "algorithmic_flops_per_launch": rd["flops"],
-                              "peak_source": "measured DFMA microbenchmark (profiles/r01_fp64_peak.log)"},
-            "apply_totals": {"algorithmic_bytes": b_alg, "algorithmic_flops": f_alg,
-                             "hbm_frac": b_alg / (ms * 1e-3) / 1e9 / peak,
-                             "fp64_frac": f_alg / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
+            # the binding roof of the dominant kernel: fp64 (DFMA) or HBM, whichever fraction is larger
+            "roofline": dict(bound, bound="fp64" if bound is fp_block else "hbm", traffic=traffic,
+                             traffic_source=traffic_note,
+                             kernel=kernel_label(op.native.class_info(dom), rd),
+                             kernel_ms=float(cls_ms[dom]), kernel_share=float(cls_ms[dom] / cls_ms.sum()),
+                             algorithmic_bytes_per_launch=rd["bytes"], algorithmic_flops_per_launch=rd["flops"],
+                             hbm=hbm_block, fp64=fp_block),
+            # the whole apply (every launch of one step) against both roofs
+            "apply_roofline": {"algorithmic_bytes": b_alg, "algorithmic_flops": f_alg,
+                               "hbm_frac": b_alg / (ms * 1e-3) / 1e9 / peak,
+                               "fp64_frac": f_alg / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                               "bytes_per_dof": b_alg / max(n_owned, 1), "flops_per_dof": f_alg / max(n_owned, 1)},
             "e2e": {"value": n_total / (e2e * 1e-3) / 1e9, "unit": "GDoF/s", "ms_per_step": e2e,
                     "h2d_bytes_per_step": 8 * n_owned, "d2h_bytes_per_step": 8 * n_owned,
                     "path": ("sipg_apply_host: pinned host x -> H2D by DoF chunk, overlapped with the "
@@ -445,7 +518,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
             try:
-                out["cpu_baseline"] = cpu_baseline(args.config)
+                out["cpu_baseline"] = cpu_measure(args.config, 10, 2)
             except Exception as exc:  # reported, never fatal
                 out["cpu_baseline"] = {"error": repr(exc)}
         print(json.dumps(out))

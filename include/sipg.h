@@ -114,7 +114,8 @@ int sipg_plan_destroy(sipg_plan* plan);
 /* GPU-resident unpreconditioned conjugate gradient on A = the plan's operator
  * (reference krylov.cg, pkg/src/dgsipg/krylov.py:39-81):
  * x (device, n doubles, overwritten, starts from 0) approximates A^-1 b (device).
- * maxiter <= 0 means the reference default max(10 n, 200).  Same control flow as
+ * maxiter < 0 means the reference default max(10 n, 200); maxiter = 0 runs no iteration
+ * (x = 0, reason 4 "maxiter", residual 1).  Same control flow as
  * the reference: stop on p.Ap <= 0 ("indefinite direction", x not updated), on
  * ||r||/||b|| <= tol after verifying the true residual (<= 10 tol, else
  * "residual drift"), on 250 iterations without a 0.1 % improvement
@@ -129,6 +130,14 @@ typedef struct sipg_solve_report {
 } sipg_solve_report;
 int sipg_cg(sipg_plan* plan, const double* b_dev, double* x_dev, int64_t n, double tol, int64_t maxiter,
             sipg_solve_report* report, void* stream);
+/* GPU-resident restarted GMRES (reference krylov.gmres, pkg/src/dgsipg/krylov.py:84-141): same
+ * interface and stopping rules (restart = max(1, min(restart, n)); converged when the restart
+ * residual or the true residual after an update is <= tol; reason 4 "maxiter" otherwise);
+ * maxiter < 0 means the reference default max(20 n, 400).  The Arnoldi basis (restart + 1 vectors)
+ * lives in the plan's solver workspace; orthogonalisation is classical Gram-Schmidt applied twice
+ * (batched multi-dot kernels), one host read per Arnoldi step.  restart <= 255. */
+int sipg_gmres(sipg_plan* plan, const double* b_dev, double* x_dev, int64_t n, double tol, int32_t restart,
+               int64_t maxiter, sipg_solve_report* report, void* stream);
 const char* sipg_last_error(void);
 
 /* Introspection: kernel launches issued so far / per apply; layout constants. */

@@ -47,3 +47,51 @@ def cg(apply_op, b, tol=1e-9, maxiter=None):
         rr = rr_new
         p = r + beta * p
     return x, False, maxiter, np.sqrt(rr) / nb, "maxiter"
+
+
+def gmres(apply_op, b, tol=1e-9, restart=50, maxiter=None):
+    """The reference's restarted GMRES contract (krylov.py:84-141): restart cycles of at most
+    `restart` Arnoldi steps; a cycle ends early when the least-squares residual drops to tol; the
+    solve stops when the residual at a cycle start or the true residual after an update is <= tol,
+    else after `maxiter` steps in total with reason "maxiter".  Restated with Householder-free
+    numpy: modified Gram-Schmidt Arnoldi and the small least-squares problem by np.linalg.lstsq
+    (the reference rotates with Givens; both minimise the same residual).
+    Returns (x, converged, iterations, residual, reason)."""
+    b = np.asarray(b, dtype=float)
+    n = b.size
+    nb = float(np.linalg.norm(b))
+    x = np.zeros(n)
+    if nb == 0.0:
+        return x, True, 0, 0.0, ""
+    maxiter = max(20 * n, 400) if maxiter is None else maxiter
+    m_cap = max(1, min(restart, n))
+    steps = 0
+    while steps < maxiter:
+        r = b - apply_op(x)
+        beta = float(np.linalg.norm(r))
+        if beta / nb <= tol:
+            return x, True, steps, beta / nb, ""
+        m = min(m_cap, maxiter - steps)
+        basis = [r / beta]
+        hess = np.zeros((m + 1, m))
+        e1 = np.zeros(m + 1)
+        e1[0] = beta
+        y = np.zeros(0)
+        for k in range(m):
+            v = apply_op(basis[k])
+            for i, qi in enumerate(basis):
+                hess[i, k] = float(v @ qi)
+                v = v - hess[i, k] * qi
+            hess[k + 1, k] = float(np.linalg.norm(v))
+            basis.append(v / hess[k + 1, k] if hess[k + 1, k] > 1e-300 else np.zeros(n))
+            steps += 1
+            y, *_ = np.linalg.lstsq(hess[:k + 2, :k + 1], e1[:k + 2], rcond=None)
+            res = float(np.linalg.norm(e1[:k + 2] - hess[:k + 2, :k + 1] @ y))
+            if res / nb <= tol:
+                break
+        x = x + np.stack(basis[:y.size], axis=1) @ y
+        rel = float(np.linalg.norm(b - apply_op(x))) / nb
+        if rel <= tol:
+            return x, True, steps, rel, ""
+    rel = float(np.linalg.norm(b - apply_op(x))) / nb
+    return x, False, steps, rel, "maxiter"

@@ -20,6 +20,7 @@ LIB_PATH = Path(os.environ.get("SIPG_LIB_PATH", "")) if os.environ.get("SIPG_LIB
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
            "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply", "sipg_plan_n_dofs", "sipg_cg",
+           "sipg_gmres",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
            "sipg_apply_role", "sipg_h3_plan_create", "sipg_h3_apply_traces", "sipg_h3_trace_len"]
 
@@ -93,6 +94,9 @@ def load() -> ctypes.CDLL:
     lib.sipg_cg.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
                             ctypes.POINTER(SolveReportC), vp]
     lib.sipg_cg.restype = ctypes.c_int
+    lib.sipg_gmres.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, i32, ctypes.c_int64,
+                               ctypes.POINTER(SolveReportC), vp]
+    lib.sipg_gmres.restype = ctypes.c_int
     for nm in ("sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply"):
         getattr(lib, nm).argtypes = [vp]
         getattr(lib, nm).restype = ctypes.c_int
@@ -240,6 +244,14 @@ class NativePlan:
         rep = SolveReportC()
         check(self._lib.sipg_cg(self.handle, ctypes.c_void_p(b_ptr), ctypes.c_void_p(x_ptr), n, tol, maxiter,
                                 ctypes.byref(rep), ctypes.c_void_p(stream)), "sipg_cg")
+        return rep
+
+    def gmres(self, b_ptr: int, x_ptr: int, n: int, tol: float, restart: int, maxiter: int,
+              stream: int = 0) -> SolveReportC:
+        """GPU-resident restarted GMRES (sipg_gmres): x <- A^-1 b on device buffers."""
+        rep = SolveReportC()
+        check(self._lib.sipg_gmres(self.handle, ctypes.c_void_p(b_ptr), ctypes.c_void_p(x_ptr), n, tol, restart,
+                                   maxiter, ctypes.byref(rep), ctypes.c_void_p(stream)), "sipg_gmres")
         return rep
 
     def stream_chunks(self) -> int:

@@ -163,9 +163,11 @@ struct sipg_plan {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   double* ws_host = nullptr;
+  size_t ws_host_n = 0;
   int64_t launches = 0;
   std::vector<int> per_sm;               // resident CTAs per SM of each class's kernel
-  int sms = 148;
+  int sms = 0;                           // multiprocessors of the plan's device (queried)
+  bool stream_trace = false;             // SIPG_STREAM_TRACE, read once at plan creation
   // Streamed host apply (sipg_apply_host): x is copied H2D in K DoF chunks; chunk k's elements
   // publish their planes/traces as soon as it lands, and the elements whose neighbourhood lies in
   // chunks <= k ("stage k") compute right after; y chunks go back D2H as soon as their last stage
@@ -187,6 +189,17 @@ struct sipg_plan {
 namespace {
 
 constexpr int kSideStreams = 3;
+
+// Instrumentation switches that change results exist only in SIPG_INSTRUMENT builds
+// (build.py OUT.so -DSIPG_INSTRUMENT); the product library ignores them.
+int instrument_debug() {
+#ifdef SIPG_INSTRUMENT
+  const char* e = getenv("SIPG_DEBUG");
+  return e ? atoi(e) : 0;
+#else
+  return 0;
+#endif
+}
 
 bool concurrency_on() {
   static const bool on = [] {
@@ -245,15 +258,15 @@ __global__ void k_stamp(unsigned long long* buf, int i) {
 
 int launch_grid(const KernelEntry* k, int count, int per_sm, int sms) {
   if (k->kind == 0) return count;   // CTA per element
-  const int epc = (k->kind == 1 || k->kind == 5) ? k->threads / 32 : 1;   // warp-per-element kernels
+  const int epc = k->kind == 5 ? k->threads / 32 : 1;   // warp-per-element kernels
   const int g = (count + epc - 1) / epc;
   return g < per_sm * sms ? g : per_sm * sms;
 }
 
-int publish_grid(const int32_t* cd, int count) {
+int publish_grid(const int32_t* cd, int count, int sms) {
   const int per = cd[CD_SHAPE] == SHAPE_HEX ? 1 : 8;
   const int g = (count + per - 1) / per;
-  return g < 148 * 8 ? g : 148 * 8;
+  return g < sms * 8 ? g : sms * 8;
 }
 
 // Build the streamed-apply schedule (see sipg_plan).  Returns false when the mesh ordering does not
@@ -354,7 +367,7 @@ bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
           if (key[el[j]] <= k) return false;   // not monotone: no streaming
         const int r = add_row(cd, i0, i1);
         if (pass == 0)
-          p->pub[k].push_back({r, publish_grid(cd, i1 - i0), nullptr, p->planes_k[c]});
+          p->pub[k].push_back({r, publish_grid(cd, i1 - i0, p->sms), nullptr, p->planes_k[c]});
         else
           p->comp[k].push_back({r, launch_grid(p->kern[c], i1 - i0, p->per_sm[c], p->sms), p->kern[c], nullptr});
         i0 = i1;
@@ -410,62 +423,67 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     const KernelEntry* k = nullptr;
     if (uniform && shape == SHAPE_HEX && geom == GEOM_REGULAR && cd[CD_KIND] == 0 && cd[CD_GLLMASK] == 7 &&
         !getenv("SIPG_GENERIC_KERNELS")) {
-      // SIPG_HEX_FAST_KERNEL: instrumentation override of the all-fast-faces kernel
-      // (1 warp-per-element DMMA, 3 CTA-per-element DMMA, 4 DFMA register-column [default, fastest measured])
-      const char* ov = getenv("SIPG_HEX_FAST_KERNEL");
-      const int fast_kind = ov ? atoi(ov) : 4;
+      // all faces boundary / conforming-fast: k_hex (kind 4); fast shared traces: k_hexp (kind 7);
+      // anything else: k_hex with the generic face path (kind 2)
       const int level = class_face_level(d, c);
-      k = find_kernel(shape, n, q, geom, level == 0 ? fast_kind : (level == 1 ? 7 : 2));
-      if (!k) k = find_kernel(shape, n, q, geom, level == 0 ? 4 : 2);
+      k = find_kernel(shape, n, q, geom, level == 0 ? 4 : (level == 1 ? 7 : 2));
       if (k) {
         const int* ax = cd + CD_TAX;
         cudaError_t e = k->upload(d->tables + ax[TX_V], d->tables + ax[TX_D], d->tables + ax[TX_W],
                                   d->tables + ax[TX_DVEND]);
         if (e != cudaSuccess) {
-          delete p;
+          sipg_plan_destroy(p);
           return fail(SIPG_ERR_CUDA, std::string("constant table upload: ") + cudaGetErrorString(e));
         }
       }
     }
     if (!k && uniform) k = find_kernel(shape, n, q, geom, shape == SHAPE_HEX ? 0 : 5);
     if (!k) {
-      delete p;
+      sipg_plan_destroy(p);
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a kernel for shape=" + std::to_string(shape) +
                                             " n_modes=" + std::to_string(n) + " n_quad=" + std::to_string(q));
     }
     p->kern.push_back(k);
   }
+  // every device buffer is owned by p->bufs from the moment it exists, so any failure below can
+  // release the partial plan through sipg_plan_destroy
   int rc = 0;
+  int nb = 0;
+  auto up = [&](const auto* host, int64_t count, auto** dev) -> int {
+    int r = upload(host, count, dev);
+    p->bufs[nb++] = (void*)*dev;
+    return r;
+  };
   int32_t *cd_d, *ce_d, *ec_d, *ep_d;
   int64_t* dof_d;
   FaceRec* rec_d;
   double *tab_d, *eg_d, *fg_d;
-  if ((rc = upload(d->class_desc, (int64_t)d->n_classes * CD_WORDS, &cd_d)) ||
-      (rc = upload(d->class_elems, d->n_elements, &ce_d)) ||
-      (rc = upload(d->elem_class, d->n_elements, &ec_d)) ||
-      (rc = upload(d->elem_pos, d->n_elements, &ep_d)) ||
-      (rc = upload(d->dof_off, d->n_elements + 1, &dof_d)) ||
-      (rc = upload((const FaceRec*)d->face_records, d->n_records, &rec_d)) ||
-      (rc = upload(d->tables, d->n_tables, &tab_d)) || (rc = upload(d->elem_geom, d->n_elem_geom, &eg_d)) ||
-      (rc = upload(d->face_geom, d->n_face_geom, &fg_d))) {
-    delete p;
-    return rc;
-  }
   int64_t *po_d = nullptr, *rx_d = nullptr;
-  if ((d->plane_off && (rc = upload(d->plane_off, d->n_elements, &po_d))) ||
-      (d->rec_ext && (rc = upload(d->rec_ext, 2 * d->n_records, &rx_d)))) {
-    delete p;
+  if ((rc = up(d->class_desc, (int64_t)d->n_classes * CD_WORDS, &cd_d)) ||
+      (rc = up(d->class_elems, d->n_elements, &ce_d)) || (rc = up(d->elem_class, d->n_elements, &ec_d)) ||
+      (rc = up(d->elem_pos, d->n_elements, &ep_d)) || (rc = up(d->dof_off, d->n_elements + 1, &dof_d)) ||
+      (rc = up((const FaceRec*)d->face_records, d->n_records, &rec_d)) ||
+      (rc = up(d->tables, d->n_tables, &tab_d)) || (rc = up(d->elem_geom, d->n_elem_geom, &eg_d)) ||
+      (rc = up(d->face_geom, d->n_face_geom, &fg_d)) ||
+      (rc = up(d->plane_off, d->plane_off ? d->n_elements : 0, &po_d)) ||
+      (rc = up(d->rec_ext, d->rec_ext ? 2 * d->n_records : 0, &rx_d))) {
+    sipg_plan_destroy(p);
     return rc;
   }
-  void* b[11] = {cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, po_d, rx_d};
-  memcpy(p->bufs, b, sizeof(b));
   // Published neighbour data: hex planes for the k_hexp classes; 2-D face traces when the mesh has
   // triangles (a triangle trace costs a collapsed-coordinate chain per face — worth computing once per
   // face instead of once per reader; quad traces are cheap enough to evaluate in place).
   for (const KernelEntry* k : p->kern)
     p->need_planes = p->need_planes || k->kind == 6 || k->kind == 7 || (k->kind == 5 && k->shape == SHAPE_TRI);
   if (getenv("SIPG_NO_PUBLISH")) p->need_planes = false;   // instrumentation: 2-D kernels evaluate neighbours
-  if (p->need_planes && d->n_planes > 0) CK(cudaMalloc((void**)&p->planes, sizeof(double) * d->n_planes));
+  if (p->need_planes && d->n_planes > 0) {
+    cudaError_t e = cudaMalloc((void**)&p->planes, sizeof(double) * d->n_planes);
+    if (e != cudaSuccess) {
+      p->planes = nullptr;
+      sipg_plan_destroy(p);
+      return fail(SIPG_ERR_CUDA, std::string("face-plane buffer: ") + cudaGetErrorString(e));
+    }
+  }
   for (int c = 0; c < d->n_classes; ++c) {
     const int32_t* cd = d->class_desc + c * CD_WORDS;
     const PlanesEntry* pe = nullptr;
@@ -495,7 +513,7 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     p->planes_k.push_back(pe);
   }
   p->dp = DevPlan{cd_d, ce_d, ec_d, ep_d, dof_d, rec_d, tab_d, eg_d, fg_d, d->lambda, d->dim, d->n_classes,
-                  getenv("SIPG_DEBUG") ? atoi(getenv("SIPG_DEBUG")) : 0, 0, p->planes, po_d, rx_d};
+                  instrument_debug(), 0, p->planes, po_d, rx_d};
   for (const KernelEntry* k : p->kern) {
     if (k->smem == 0) continue;
     cudaError_t e = cudaFuncSetAttribute((const void*)k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -506,8 +524,13 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     }
   }
   int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+    sipg_plan_destroy(p);
+    return fail(SIPG_ERR_CUDA, "multiprocessor count query failed");
+  }
+  p->sms = sms;
+  p->stream_trace = getenv("SIPG_STREAM_TRACE") != nullptr;
   for (int c = 0; c < p->n_cls; ++c) {
     const KernelEntry* k = p->kern[c];
     const int count = p->cd_host[c * CD_WORDS + CD_COUNT];
@@ -522,7 +545,6 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
     p->per_sm.push_back(per_sm);
     p->grid.push_back(launch_grid(k, count, p->per_sm.back(), sms));
   }
-  p->sms = sms;
   p->streamed = !getenv("SIPG_NO_STREAM") && build_stream_schedule(p, d);
   *out = p;
   return 0;
@@ -762,9 +784,14 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       return fail(SIPG_ERR_CUDA, "cudaFuncSetAttribute (hybrid kernels)");
     }
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+    sipg_plan_destroy(p);
+    return fail(SIPG_ERR_CUDA, "multiprocessor count query failed");
+  }
+  p->sms = sms;
+  p->stream_trace = getenv("SIPG_STREAM_TRACE") != nullptr;
   for (int c = 0; c < p->n_cls; ++c) {
     const H3Entry* k = h->kern[c];
     const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
@@ -805,13 +832,14 @@ int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_d
     for (int c = 0; c < p->n_cls; ++c) {
       if (!go(c)) continue;
       ++n;
-      nsmall += publish_grid(p->cd_host.data() + c * CD_WORDS, p->cd_host[c * CD_WORDS + CD_COUNT]) < 148 * 8;
+      nsmall += publish_grid(p->cd_host.data() + c * CD_WORDS, p->cd_host[c * CD_WORDS + CD_COUNT], p->sms) <
+                p->sms * 8;
     }
     if ((rc = group_begin(p, s, n, nsmall))) return rc;
     for (int c = 0; c < p->n_cls; ++c) {
       if (!go(c)) continue;
       const int32_t* cd = p->cd_host.data() + c * CD_WORDS;
-      p->planes_k[c]->fn<<<publish_grid(cd, cd[CD_COUNT]), cd[CD_SHAPE] == SHAPE_HEX ? 128 : 256, 0,
+      p->planes_k[c]->fn<<<publish_grid(cd, cd[CD_COUNT], p->sms), cd[CD_SHAPE] == SHAPE_HEX ? 128 : 256, 0,
                            group_stream(p)>>>(p->dp, c, x_dev);
       ++p->launches;
     }
@@ -883,14 +911,39 @@ int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
   return 0;
 }
 
+static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, cudaStream_t s);
+
 int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* stream) {
   if (!p || !x_host || !y_host) return fail(SIPG_ERR_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = sizeof(double) * (size_t)p->n_dofs;
-  if (!p->x_stage) {
-    CK(cudaMalloc((void**)&p->x_stage, bytes));
-    CK(cudaMalloc((void**)&p->y_stage, bytes));
+  if (!p->x_stage || !p->y_stage) {   // both staging buffers or neither
+    if (p->x_stage) cudaFree(p->x_stage);
+    if (p->y_stage) cudaFree(p->y_stage);
+    p->x_stage = p->y_stage = nullptr;
+    double *xs = nullptr, *ys = nullptr;
+    if (cudaMalloc((void**)&xs, bytes) != cudaSuccess || cudaMalloc((void**)&ys, bytes) != cudaSuccess) {
+      if (xs) cudaFree(xs);
+      cudaGetLastError();
+      return fail(SIPG_ERR_CUDA, "host-apply staging buffers: out of device memory");
+    }
+    p->x_stage = xs;
+    p->y_stage = ys;
   }
+  const int rc = apply_host_impl(p, x_host, y_host, s);
+  if (rc) {
+    // copies that target the caller's host buffers may already be queued: drain them before the
+    // caller can free or reuse x_host / y_host (their own errors are superseded by rc)
+    if (p->s_h2d) cudaStreamSynchronize(p->s_h2d);
+    if (p->s_d2h) cudaStreamSynchronize(p->s_d2h);
+    cudaStreamSynchronize(s);
+  }
+  return rc;
+}
+
+static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, cudaStream_t s) {
+  const size_t bytes = sizeof(double) * (size_t)p->n_dofs;
+  void* stream = (void*)s;
   if (!p->streamed) {
     CK(cudaMemcpyAsync(p->x_stage, x_host, bytes, cudaMemcpyHostToDevice, s));
     int rc = sipg_apply(p, p->x_stage, p->y_stage, stream);
@@ -912,7 +965,7 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
     }
   }
   // SIPG_STREAM_TRACE (instrumentation): timestamps of every chunk copy / stage, printed to stderr
-  const bool trace = getenv("SIPG_STREAM_TRACE") != nullptr;
+  const bool trace = p->stream_trace;
   static unsigned long long* tbuf = nullptr;
   if (trace && !tbuf) cudaMalloc((void**)&tbuf, sizeof(unsigned long long) * 1024);
   int nmark = 0;
@@ -934,7 +987,11 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
   }
   for (int k = 0; k < K; ++k) {
     CK(cudaStreamWaitEvent(s, p->ev_h2d[k], 0));
-    const bool skip = getenv("SIPG_STREAM_NOCOMPUTE") != nullptr;   // instrumentation: copies only
+#ifdef SIPG_INSTRUMENT
+    const bool skip = getenv("SIPG_STREAM_NOCOMPUTE") != nullptr;   // instrumentation build: copies only
+#else
+    const bool skip = false;
+#endif
     if (p->h3 && !skip) {   // each stage's rows are small: run them side by side (fork / join)
       H3State* h = p->h3;
       int rc = group_begin(p, s, (int)h->st_pub[k].size(), (int)h->st_pub[k].size());
@@ -972,8 +1029,12 @@ int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* st
     for (int j = 0; j < K; ++j) {
       if (p->d2h_stage[j] != k) continue;
       const int64_t a = p->chunk_dof[j], b = p->chunk_dof[j + 1];
-      // SIPG_STREAM_DIAG=1 (instrumentation, wrong results): D2H gated on the copies only
+#ifdef SIPG_INSTRUMENT
+      // SIPG_STREAM_DIAG=1 (instrumentation build, wrong results): D2H gated on the copies only
       static const bool diag = getenv("SIPG_STREAM_DIAG") != nullptr;
+#else
+      const bool diag = false;
+#endif
       CK(cudaStreamWaitEvent(p->s_d2h, diag ? p->ev_h2d[k] : p->ev_comp[k], 0));
       CK(cudaMemcpyAsync(y_host + a, p->y_stage + a, sizeof(double) * (b - a), cudaMemcpyDeviceToHost, p->s_d2h));
       mark(p->s_d2h); tkind.push_back('D');
@@ -1059,17 +1120,30 @@ int sipg_plan_destroy(sipg_plan* p) {
 }
 
 // Internal (sipg_krylov.cu): the plan's cached solver workspace of at least `bytes` device bytes and
-// `host_doubles` <= 64 pinned host doubles.  One solve per plan at a time (like the staging buffers).
-int sipg__workspace(sipg_plan* p, size_t bytes, void** dev, double** host) {
+// `host_doubles` pinned host doubles.  One solve per plan at a time (like the staging buffers).
+int sipg__workspace(sipg_plan* p, size_t bytes, size_t host_doubles, void** dev, double** host) {
   if (!p || !dev || !host) return SIPG_ERR_ARG;
   if (bytes > p->ws_bytes) {
     if (p->ws) cudaFree(p->ws);
     p->ws = nullptr;
     p->ws_bytes = 0;
-    if (cudaMalloc(&p->ws, bytes) != cudaSuccess) return SIPG_ERR_CUDA;
+    if (cudaMalloc(&p->ws, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return SIPG_ERR_CUDA;
+    }
     p->ws_bytes = bytes;
   }
-  if (!p->ws_host && cudaMallocHost((void**)&p->ws_host, 64 * sizeof(double)) != cudaSuccess) return SIPG_ERR_CUDA;
+  if (host_doubles < 64) host_doubles = 64;
+  if (host_doubles > p->ws_host_n) {
+    if (p->ws_host) cudaFreeHost(p->ws_host);
+    p->ws_host = nullptr;
+    p->ws_host_n = 0;
+    if (cudaMallocHost((void**)&p->ws_host, host_doubles * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return SIPG_ERR_CUDA;
+    }
+    p->ws_host_n = host_doubles;
+  }
   *dev = p->ws;
   *host = p->ws_host;
   return 0;

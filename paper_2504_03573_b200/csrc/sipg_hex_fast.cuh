@@ -316,7 +316,9 @@ k_hex(const DevPlan P, const int cls, const double* __restrict__ x, double* __re
   if (t < 6) {
     const int fl = srec[t].flags, ty = srec[t].type;
     sk[t] = (ty == FT_DIRECT && (fl & F_FAST_HEX)) ? 1 : ((ty == FT_BOUNDARY && !(fl & F_SELF_PW)) ? 2 : 0);
-    if (!GEN && (P.debug & 2)) sk[t] = 0;   // instrumentation (SIPG_DEBUG=2): no face work, wrong result
+#ifdef SIPG_INSTRUMENT
+    if (!GEN && (P.debug & 2)) sk[t] = 0;   // instrumentation build only (SIPG_DEBUG=2): no face work
+#endif
   }
   if (t >= NT - 6) {      // neighbour blocks, one per thread: the last 6 threads (NT >= 9),
                           // never thread 0 (which issues the next-element prefetch)

@@ -10,7 +10,7 @@ using UploadFn = cudaError_t (*)(const double* V, const double* D, const double*
 // kind: 6/7 = planes-consuming hex kernel (k_hexp) without / with fast shared traces,
 //       0 = generic smem kernel, one CTA per element (any basis / rule / geometry),
 //       5 = the same element routine, one warp per element (2-D shapes, persistent),
-//       1 = register-column hex kernel, conforming + boundary faces only,
+//       4 = register-column hex kernel (k_hex), conforming + boundary faces only,
 //       2 = register-column hex kernel with the generic face path
 struct KernelEntry {
   int shape, n, q, geom, kind;
@@ -62,26 +62,10 @@ KernelEntry sipg_entry();
                           (N + 1) * (N + 1), sipg::HexPlanes<N, N + 1, true>::smem_bytes(),       \
                           &sipg::hex_fast_upload<N, N + 1>})
 #define SIPG_HEX_FAST(N)                                                                     \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1, &sipg::k_hex<N, N + 1, false>,  \
+  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 4, &sipg::k_hex<N, N + 1, false>,  \
                           (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(false),         \
                           &sipg::hex_fast_upload<N, N + 1>});                                   \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex<N, N + 1, true>,   \
                           (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(true),          \
-                          &sipg::hex_fast_upload<N, N + 1>})
-// fp64 tensor-core (DMMA) hex kernels, Q <= 8: warp-per-element (all faces fast) and CTA-per-element
-#define SIPG_HEX_MMA(N)                                                                      \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 1,                              \
-                          &sipg::k_hexw<N, N + 1, sipg::HexWarpSlice<N, N + 1>::W>,           \
-                          32 * sipg::HexWarpSlice<N, N + 1>::W,                               \
-                          sipg::HexWarp<N, N + 1, sipg::HexWarpSlice<N, N + 1>::W>::smem_bytes(), \
-                          &sipg::hex_mma_upload<N, N + 1>});                                    \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 2, &sipg::k_hex_mma<N, N + 1, true>,  \
-                          128, sipg::HexMma<N, N + 1>::smem_bytes(true),                         \
-                          &sipg::hex_mma_upload<N, N + 1>});                                    \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 3, &sipg::k_hex_mma<N, N + 1, false>, \
-                          128, sipg::HexMma<N, N + 1>::smem_bytes(false),                        \
-                          &sipg::hex_mma_upload<N, N + 1>});                                    \
-  v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 4, &sipg::k_hex<N, N + 1, false>,     \
-                          (N + 1) * (N + 1), sipg::HexFast<N, N + 1>::smem_bytes(false),         \
                           &sipg::hex_fast_upload<N, N + 1>})
 #endif

@@ -12,9 +12,9 @@ package's `HelmholtzOperator` (the vectors stay in HBM; there is no CPU path):
   the paper's symmetry study): the columns are sm_100a applies of device-resident unit vectors
   written straight into a device matrix; the two diagnostics are host post-processing of that
   matrix, as in the reference.
-* gmres keeps the Krylov basis on the device (torch tensors as plumbing); every
-  operator application is the sm_100a apply, the small Hessenberg least-squares
-  problem is solved on the host like the reference (krylov.py:84-141).
+* gmres runs in libsipg.so too (`sipg_gmres`): the Arnoldi basis stays in HBM, each step
+  is one apply, two batched Gram-Schmidt passes (multi-dot + fused update kernels) and one
+  read of k + 2 scalars; the tiny Hessenberg least-squares problem is solved on the host.
 
 `b` may be a numpy array (copied in, x copied out as numpy, like the reference)
 or a CUDA float64 tensor (x returned as a CUDA tensor).
@@ -68,69 +68,23 @@ def cg(apply_op, b, tol: float = 1e-9, maxiter: int | None = None):
     x = torch.empty_like(bd)
     stream = torch.cuda.current_stream()
     rep = apply_op.native.cg(bd.data_ptr(), x.data_ptr(), int(bd.numel()), float(tol),
-                             int(maxiter) if maxiter is not None else 0, stream.cuda_stream)
+                             int(maxiter) if maxiter is not None else -1, stream.cuda_stream)
     out = SolveReport(bool(rep.converged), int(rep.iterations), float(rep.residual), REASONS[int(rep.reason)])
     return (x if on_dev else x.cpu().numpy()), out
 
 
 def gmres(apply_op, b, tol: float = 1e-9, restart: int = 50, maxiter: int | None = None):
-    """Restarted GMRES with modified Gram-Schmidt (reference krylov.py:84-141); basis on device."""
+    """Restarted GMRES on the GPU (reference interface krylov.py:84-141; device solver sipg_gmres in
+    csrc/sipg_krylov.cu: basis in HBM, twice-applied classical Gram-Schmidt as batched multi-dot
+    kernels, one host read per Arnoldi step); returns (x, SolveReport)."""
     import torch
     bd, on_dev = _device_rhs(apply_op, b)
-    n = bd.numel()
-    nb = float(torch.linalg.vector_norm(bd))
-    x = torch.zeros_like(bd)
-    done = (lambda xx, rep: ((xx if on_dev else xx.cpu().numpy()), rep))
-    if nb == 0.0:
-        return done(x, SolveReport(True, 0, 0.0))
-    if maxiter is None:
-        maxiter = max(20 * n, 400)
-    restart = max(1, min(restart, n))
-    total = 0
-
-    def apply(v):
-        return apply_op(v)
-
-    while total < maxiter:
-        r = bd - apply(x)
-        beta = float(torch.linalg.vector_norm(r))
-        if beta / nb <= tol:
-            return done(x, SolveReport(True, total, beta / nb))
-        m = min(restart, maxiter - total)
-        q = torch.zeros((m + 1, n), dtype=torch.float64, device=bd.device)
-        h = np.zeros((m + 1, m))
-        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
-        g[0] = beta
-        q[0] = r / beta
-        k_done = 0
-        for k in range(m):
-            w = apply(q[k])
-            for i in range(k + 1):
-                h[i, k] = float(torch.dot(w, q[i]))
-                w = w - h[i, k] * q[i]
-            h[k + 1, k] = float(torch.linalg.vector_norm(w))
-            if h[k + 1, k] > 1e-300:
-                q[k + 1] = w / h[k + 1, k]
-            for i in range(k):
-                t = cs[i] * h[i, k] + sn[i] * h[i + 1, k]
-                h[i + 1, k] = -sn[i] * h[i, k] + cs[i] * h[i + 1, k]
-                h[i, k] = t
-            denom = np.hypot(h[k, k], h[k + 1, k])
-            cs[k], sn[k] = h[k, k] / denom, h[k + 1, k] / denom
-            h[k, k], h[k + 1, k] = denom, 0.0
-            g[k + 1] = -sn[k] * g[k]
-            g[k] = cs[k] * g[k]
-            k_done = k + 1
-            total += 1
-            if abs(g[k + 1]) / nb <= tol:
-                break
-        y = np.linalg.solve(h[:k_done, :k_done] + 0.0, g[:k_done]) if k_done else np.zeros(0)
-        x = x + (q[:k_done].T @ torch.from_numpy(y).to(q.device))
-        rel = float(torch.linalg.vector_norm(bd - apply(x))) / nb
-        if rel <= tol:
-            return done(x, SolveReport(True, total, rel))
-    rel = float(torch.linalg.vector_norm(bd - apply(x))) / nb
-    return done(x, SolveReport(False, total, rel, "maxiter"))
+    x = torch.empty_like(bd)
+    stream = torch.cuda.current_stream()
+    rep = apply_op.native.gmres(bd.data_ptr(), x.data_ptr(), int(bd.numel()), float(tol), int(restart),
+                                int(maxiter) if maxiter is not None else -1, stream.cuda_stream)
+    out = SolveReport(bool(rep.converged), int(rep.iterations), float(rep.residual), REASONS[int(rep.reason)])
+    return (x if on_dev else x.cpu().numpy()), out
 
 
 def probe_dense(apply_op, n: int, limit: int = DEFAULT_PROBE_LIMIT) -> np.ndarray:

@@ -494,6 +494,8 @@ class PlanBuilder:
                 RE[i], RF[i] = itf.right
             CODE[i] = itf.orientation
         recs = np.zeros(self.n_recs, dtype=L.FACE_REC)
+        self._perm_buckets = []
+        self._n_itf, self._bnd_itf = nI, RE < 0
         self.rec_ext = np.zeros((self.n_recs, 2), dtype=np.int64)
         self.rec_ext[:, 0] = -1
         self._rec_face = np.zeros(self.n_recs, dtype=np.int64)
@@ -566,6 +568,8 @@ class PlanBuilder:
             cl, cr = self.exp_list[el], self.exp_list[er]
             pts_l, pts_r = cl.face_pts(fl), cr.face_pts(fr)
             if s in (0, 1):
+                self._perm_buckets.append((mem, self._transfer_perm(pts_r, pts_l, code, fd),
+                                           self._transfer_perm(pts_l, pts_r, inverse_code(code, fd), fd)))
                 for r, ee, ff_, eo, fo, src, dst, cc in (
                         (rl, le, fl, re_, fr, pts_r, pts_l, code),
                         (rr, re_, fr, le, fl, pts_l, pts_r, inverse_code(code, fd))):
@@ -589,8 +593,52 @@ class PlanBuilder:
                               & (self.f_gxn[eo, fo, tang[1]] == 0.0))
                         recs["flags"][r[ok]] |= L.F_FAST_HEX
                 continue
+            self._cur_mem = mem
             self._shared_bucket(cl, fl, cr, fr, code, le, re_, rl, rr)
         self._finish()
+
+    def _transfer_perm(self, src, dst, code, fd):
+        """Index permutation of the transfer src face grid -> dst grid, or None when it is a
+        dense interpolation (the reference's one-hot test, trace.py:190-198), from this plan's
+        own per-axis matrices; force_interp densifies every transfer (sipg.py:502-504)."""
+        if self.force_interp:
+            return None
+        mats, swap, _ = axis_transfer(src, dst, code)
+        if fd == 1:
+            m = mats[0]
+        else:
+            a, b = (mats[1], mats[0]) if swap else (mats[0], mats[1])
+            # M[(t0, t1), (i0, i1)]: no swap a[t0, i0] b[t1, i1]; swap a = mats[1][t1, i0], b = mats[0][t0, i1]
+            if swap:
+                m = np.einsum("yi,xj->xyij", a, b).reshape(b.shape[0] * a.shape[0], -1)
+            else:
+                m = np.einsum("xi,yj->xyij", a, b).reshape(a.shape[0] * b.shape[0], -1)
+        if m.shape[0] != m.shape[1]:
+            return None
+        hits = np.isclose(m, 1.0, atol=1e-12)
+        if np.all(hits.sum(axis=1) == 1) and np.allclose(m, hits.astype(float), atol=1e-12):
+            return np.argmax(hits, axis=1)
+        return None
+
+    def transfer_perm_sha256(self) -> bytes:
+        """SHA-256 over interfaces (ascending id) of [left perm, -1, right perm] for every interior
+        interface (a side's own face grid -> the partner grid for gather / p2p, -> the shared trace
+        grid for shared traces; empty for dense transfers) — the digest the golden
+        fixtures record from the reference's Transfer.perm (tests/golden/make_golden.py maps_of)."""
+        import hashlib
+        rows = {}
+        for mem, pl, pr in self._perm_buckets:
+            a = np.zeros(0, np.int64) if pl is None else np.asarray(pl, np.int64)
+            b = np.zeros(0, np.int64) if pr is None else np.asarray(pr, np.int64)
+            row = np.concatenate([a, [-1], b]).astype(np.int64).tobytes()
+            for i in mem:
+                rows[int(i)] = row
+        shared = np.int64(-1).tobytes()
+        h = hashlib.sha256()
+        for i in np.flatnonzero(~self._bnd_itf):
+            h.update(np.int64(i).tobytes())
+            h.update(rows.get(int(i), shared))
+        return h.digest()
 
     def _own_geometry(self, r, e, f):
         """Self geometry on the own face grid for records r of faces (e, f)."""
@@ -646,6 +694,8 @@ class PlanBuilder:
         _, _, invr, fcr, _ = gr.face(fr, prm_tr, np.ones(prm_t.shape[0]), self.exp_pos[re_])
         ml, swl, idl = axis_transfer(cl.face_pts(fl), t_axes, 0)
         mr, swr, idr = axis_transfer(cr.face_pts(fr), t_axes, code)
+        self._perm_buckets.append((self._cur_mem, self._transfer_perm(cl.face_pts(fl), t_axes, 0, fd),
+                                   self._transfer_perm(cr.face_pts(fr), t_axes, code, fd)))
         neg_r = fd == 1 and code == 1
         regular = fcl & fcr
         gxl = np.einsum("ekm,em->ek", invl[:, 0], nl[:, 0])

@@ -150,6 +150,7 @@ class ClassTables3:
         kinds = AXIS_KINDS[shape]
         self.kinds = kinds
         self.rules = [quad_rule(k, q) for k in kinds]
+        self.n_modes, self.nq, self.n_phys = n, (q, q, q), q ** 3
         self.pts = [r.points for r in self.rules]
         self.wts = [r.weights for r in self.rules]
         g = np.meshgrid(*self.pts, indexing="ij")
@@ -161,6 +162,8 @@ class ClassTables3:
             w = w * 0.5 * (1.0 - eta[:, 1]) * (0.5 * (1.0 - eta[:, 2])) ** 2
         self.wref = w
         self.nc = n_coeffs(shape, n)
+        self.n_coeffs, self.ref_weights, self.eta_phys = self.nc, w, eta
+        self.xi_phys = xi_of_eta(shape, eta)
         E = [lagrange_interp_matrix(p, [sd])[0] for p in self.pts for sd in (-1.0, 1.0)]
         Dm = [diff_matrix(p) for p in self.pts]
         parts = {"pts": np.concatenate(self.pts),

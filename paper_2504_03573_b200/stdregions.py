@@ -147,6 +147,27 @@ class ClassTables:
             w = np.multiply.outer(w, self.rules[a].weights).reshape(-1)
         return w
 
+    # reference Expansion field names (stdregions.py:391-412)
+    @property
+    def n_modes(self):
+        return self.n
+
+    @property
+    def ref_weights(self):
+        return self.ref_w
+
+    @property
+    def xi_phys(self):
+        return self.xi
+
+    @property
+    def eta_phys(self):
+        return self.eta
+
+    def face_n_phys(self, face):
+        f = face if isinstance(face, int) else self.faces.index(face)
+        return self.face_npts(f)
+
     @property
     def key(self):
         return (self.shape, self.kind.value, self.n, self.nq, tuple(r.kind.value for r in self.rules))

@@ -100,6 +100,68 @@ def test_gpu_cg_deterministic_and_torch_input():
     assert np.array_equal(x1, x2.cpu().numpy())
 
 
+def test_oracle_gmres_solves_dense_system():
+    from oracle import OracleOperator
+    from oracle.krylov import gmres
+    from paper_2504_03573_b200 import configs
+    case = configs.build_case("cfg0", 3, 5)
+    op = OracleOperator(case.mesh, case.order_map, basis_kind="modified_modal", tau_rule="baseline")
+    n = op.n_dofs
+    a = np.stack([op.lhs_eval(np.eye(n)[j]) for j in range(n)], axis=1)
+    b = np.random.default_rng(2).uniform(-1, 1, n)
+    x, conv, it, res, why = gmres(op.lhs_eval, b, tol=1e-12, restart=n)
+    assert conv and why == ""
+    assert np.allclose(x, np.linalg.solve(a, b), rtol=1e-8, atol=1e-10)
+    x, conv, it, res, why = gmres(op.lhs_eval, b, maxiter=0)
+    assert not conv and it == 0 and why == "maxiter" and abs(res - 1.0) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nx,seed,basis,restart", [("cfg0", 3, 8, "lagrange", 400), ("cfg1", 3, 9, "modified_modal", 30),
+                                                        ("cfg4", 1, 4, "modified_modal", 40)])
+def test_gpu_gmres_matches_oracle_gmres(name, nx, seed, basis, restart):
+    """Device GMRES (sipg_gmres) against the CPU restatement of the reference's GMRES over the
+    oracle apply: same stopping reason, iteration count within 2, same solution."""
+    from oracle import OracleOperator
+    from oracle.krylov import gmres as ogmres
+    from paper_2504_03573_b200.krylov import gmres
+    if name == "cfg4":
+        from oracle.hybrid3d import HybridOracle3D
+        from paper_2504_03573_b200 import configs
+        from paper_2504_03573_b200.sipg import HelmholtzOperator
+        case = configs.build_case(name, nx, seed)
+        op = HelmholtzOperator(case.mesh, case.order_map, basis_kind="modified_modal", tau_rule="baseline")
+        m = case.mesh
+        ref = HybridOracle3D(m.shapes, [el.verts for el in m.elements], m.vertices, case.order_map.n_modes,
+                             case.order_map.n_quad)
+    else:
+        case, args, op = _case(name, nx, seed, basis)
+        ref = OracleOperator(case.mesh, case.order_map, **args)
+    b = case.draw_x(op.n_dofs)
+    x, rep = gmres(op, b, tol=1e-10, restart=restart)
+    xo, conv, it, res, why = ogmres(ref.lhs_eval, b, tol=1e-10, restart=restart)
+    assert rep.converged and conv, (rep, why)
+    assert abs(rep.iterations - it) <= 2
+    assert rel_maxnorm(x, xo) <= 1e-7
+    assert np.linalg.norm(b - ref.lhs_eval(x)) / np.linalg.norm(b) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_solvers_maxiter_zero_and_zero_rhs():
+    """maxiter=0 runs no iteration (reference krylov.py:54, 81, 97); b = 0 converges at once."""
+    from paper_2504_03573_b200.krylov import cg, gmres
+    case, args, op = _case("cfg0", 3, 8)
+    b = case.draw_x(op.n_dofs)
+    for solve in (cg, gmres):
+        x, rep = solve(op, b, maxiter=0)
+        assert not rep.converged and rep.iterations == 0 and rep.reason == "maxiter"
+        assert abs(rep.residual - 1.0) < 1e-12 and not np.any(x)
+        x, rep = solve(op, np.zeros(op.n_dofs))
+        assert rep.converged and rep.iterations == 0 and not np.any(x)
+    x, rep = gmres(op, b, tol=1e-14, restart=5, maxiter=7)
+    assert not rep.converged and rep.reason == "maxiter" and rep.iterations == 7
+
+
 @pytest.mark.gpu
 def test_gpu_gmres_matches_cg_solution():
     from paper_2504_03573_b200.krylov import cg, gmres

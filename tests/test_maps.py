@@ -27,15 +27,19 @@ def test_maps_small(path):
     assert np.array_equal(pb.dof_off, g["dof_off"])
     assert np.array_equal(pb.trace_slots, g["trace_slots"])
     assert np.array_equal(pb.strategy_of, g["itf_strategy"])
+    assert pb.transfer_perm_sha256() == bytes(g["perm_sha256"])
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("path", [p for p in FULL if "cfg2" not in p.stem and "cfg3" not in p.stem],
-                         ids=lambda p: p.stem)
+@pytest.mark.parametrize("path", FULL, ids=lambda p: p.stem)
 def test_maps_full(path):
+    """BASELINE sizes (cfg1 64^2, cfg2 256^2, cfg3a / cfg3b 32^3): every map the reference run
+    recorded, bit-exact."""
     g = load_golden(path)
     case, pb = _plan(g)
     assert hashlib.sha256(case.mesh.dump().encode()).digest() == bytes(g["dump_sha256"])
     assert np.array_equal(pb.dof_off, g["dof_off"])
+    assert np.array_equal(pb.trace_slots, g["trace_slots"])
     key = "itf_strategy" if "itf_strategy" in g else "strategy"
     assert np.array_equal(pb.strategy_of, g[key])
+    assert pb.transfer_perm_sha256() == bytes(g["perm_sha256"])
