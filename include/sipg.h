@@ -29,6 +29,7 @@ extern "C" {
 #define SIPG_ERR_CUDA (-2)
 #define SIPG_ERR_NO_DEVICE (-3)
 #define SIPG_ERR_UNSUPPORTED (-4)
+#define SIPG_ERR_COMM (-5)
 
 typedef struct sipg_plan sipg_plan;
 
@@ -86,6 +87,28 @@ int sipg_h3_apply_traces(sipg_plan* plan, const double* x_dev, const double* tra
                          void* stream);
 int64_t sipg_h3_trace_len(const sipg_plan* plan);
 
+/* Multi-GPU slab partitions (the paper's trace-only exchange; the
+ * reference's stand-in is the in-memory double buffer of sipg.py:565-567 between phase 1 and phase 2).
+ * A rank's plan holds its owned elements only; the published traces (u, n.grad u per trace point,
+ * sipg.py:585-592) of its partition-face slots are contiguous per neighbour rank (send ranges) and
+ * the partner traces arrive in contiguous receive ranges that the slots read directly
+ * (paper_2504_03573_b200/halo3d.py builds both orders).  Offsets and counts are in doubles of the
+ * published-trace buffer. */
+int sipg_h3_set_halo(sipg_plan* plan, int32_t rank, int32_t nranks, int32_t n_nbr, const int32_t* nbr_rank,
+                     const int64_t* send_off, const int64_t* send_cnt, const int64_t* recv_off,
+                     const int64_t* recv_cnt);
+/* NCCL communicator of the partition (ncclCommInitRank with a 128-byte ncclUniqueId that rank 0
+ * made with sipg_nccl_unique_id and the caller broadcast): sipg_apply then publishes the
+ * boundary-layer traces first, exchanges them with ncclSend / ncclRecv on a high-priority comm
+ * stream while the interior elements publish and apply, and applies the boundary layer after the
+ * receive.  libnccl.so.2 is resolved at run time (the one torch loaded, if any).  Every element runs
+ * the one-GPU arithmetic on the same data, so the owned y is bitwise identical for any rank count. */
+int sipg_nccl_unique_id(void* out128);
+int sipg_comm_init(sipg_plan* plan, const void* nccl_unique_id, int32_t rank, int32_t nranks);
+/* Loop-back transport (tests, one GPU): copy `src`'s send range for dst's rank into dst's receive
+ * range for src's rank. */
+int sipg_h3_halo_copy(sipg_plan* dst, const sipg_plan* src, void* stream);
+
 /* Build the device-resident plan (uploads all tables). */
 int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);
 
@@ -94,8 +117,10 @@ int sipg_plan_create(const sipg_plan_desc* desc, sipg_plan** plan);
 int sipg_apply(sipg_plan* plan, const double* x_dev, double* y_dev, void* stream);
 
 /* Only the element classes of one launch role (0: elements whose neighbours are
- * all local, 1: elements touching a ghost element, i.e. after the halo
- * exchange; -1: both).  Multi-GPU slabs: role 0, exchange, role 1. */
+ * all local, 1: elements touching a ghost element / a partition face, i.e. after
+ * the halo exchange; -1: both).  Multi-GPU slabs: role 0, exchange, role 1.
+ * Hybrid plans: role 0 publishes every class and applies the interior, role 1
+ * applies the boundary layer. */
 int sipg_apply_role(sipg_plan* plan, int32_t role, const double* x_dev, double* y_dev, void* stream);
 
 /* One element class only (instrumentation: per-kernel timing).  Classes are

@@ -1,5 +1,7 @@
-"""CPU emulation of the config-4 kernels (csrc/sipg_h3.cuh) on a plan3d plan: same stages, same
-tables, per element in numpy.  Debug aid: separates plan-builder bugs from kernel bugs."""
+"""ORACLE (test infrastructure only) — CPU emulation of the config-4 kernels (csrc/sipg_h3.cuh) on a
+flattened plan3d / halo3d plan: same stages, same tables, same published-trace layout, per element
+in numpy.  Separates plan-builder bugs from kernel bugs, and lets the multi-rank trace-halo path run
+on CPU (tests/test_partition3d.py: publish, exchange over gloo, apply)."""
 import numpy as np
 
 from paper_2504_03573_b200.plan3d import (CD3_ELEM_OFF, CD3_COUNT, CD3_N, CD3_NC, CD3_Q, CD3_SHAPE, CD3_T_A,
@@ -95,10 +97,12 @@ def phi_matrix(pb, c):
     return out.reshape(Q ** 3, NC)
 
 
-def emulate(pb, x, skip_faces=False, skip_volume=False):
+def emulate(pb, x, skip_faces=False, skip_volume=False, pub=None, phases=(0, 1)):
+    """Phase 0 publishes every element's slot traces into `pub`, phase 1 applies (y returned)."""
     y = np.zeros(pb.n_dofs)
     T = pb.tables
-    pub = np.zeros(max(pb.n_pub, 1))
+    if pub is None:
+        pub = np.zeros(max(pb.n_pub, 1))
     S_ = pb.slots
     ctx = {}
     for c in range(pb.class_desc.shape[0]):
@@ -146,7 +150,7 @@ def emulate(pb, x, skip_faces=False, skip_volume=False):
         du = [np.moveaxis(np.tensordot(D[a], u, axes=(1, a)), 0, a) for a in range(3)]
         return u, du
 
-    for phase in (0, 1):
+    for phase in phases:
         for c in range(pb.class_desc.shape[0]):
             cd = pb.class_desc[c]
             S, N, Q, Phi, pts, D, Wr, E = ctx[c]

@@ -20,7 +20,7 @@ LIB_PATH = Path(os.environ.get("SIPG_LIB_PATH", "")) if os.environ.get("SIPG_LIB
 EXPORTS = ["sipg_plan_create", "sipg_apply", "sipg_apply_host", "sipg_plan_destroy",
            "sipg_last_error", "sipg_plan_launches", "sipg_plan_kernels_per_apply",
            "sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply", "sipg_plan_n_dofs", "sipg_cg",
-           "sipg_gmres",
+           "sipg_gmres", "sipg_h3_set_halo", "sipg_nccl_unique_id", "sipg_comm_init", "sipg_h3_halo_copy",
            "sipg_abi_layout", "sipg_supported", "sipg_apply_class", "sipg_plan_class_info",
            "sipg_apply_role", "sipg_h3_plan_create", "sipg_h3_apply_traces", "sipg_h3_trace_len"]
 
@@ -97,6 +97,14 @@ def load() -> ctypes.CDLL:
     lib.sipg_gmres.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_double, i32, ctypes.c_int64,
                                ctypes.POINTER(SolveReportC), vp]
     lib.sipg_gmres.restype = ctypes.c_int
+    lib.sipg_h3_set_halo.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp]
+    lib.sipg_h3_set_halo.restype = ctypes.c_int
+    lib.sipg_nccl_unique_id.argtypes = [vp]
+    lib.sipg_nccl_unique_id.restype = ctypes.c_int
+    lib.sipg_comm_init.argtypes = [vp, vp, i32, i32]
+    lib.sipg_comm_init.restype = ctypes.c_int
+    lib.sipg_h3_halo_copy.argtypes = [vp, vp, vp]
+    lib.sipg_h3_halo_copy.restype = ctypes.c_int
     for nm in ("sipg_plan_stream_chunks", "sipg_plan_host_launches_per_apply"):
         getattr(lib, nm).argtypes = [vp]
         getattr(lib, nm).restype = ctypes.c_int
@@ -121,6 +129,14 @@ def last_error() -> str:
 def check(rc: int, what: str) -> None:
     if rc != 0:
         raise RuntimeError(f"{what} failed ({rc}): {last_error()}")
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 makes it; the caller broadcasts it)."""
+    lib = load()
+    buf = ctypes.create_string_buffer(128)
+    check(lib.sipg_nccl_unique_id(buf), "sipg_nccl_unique_id")
+    return buf.raw
 
 
 def abi_layout() -> list:
@@ -195,6 +211,21 @@ class NativePlan:
         self.n_dofs = pb.n_dofs
         self.n_classes = 2 * int(keep[0].shape[0])   # launch units: publish kernels, then apply kernels
         self._keep = None
+
+    def set_halo(self, part) -> None:
+        """Trace halo of a slab partition (halo3d.PartitionPlan) -> sipg_h3_set_halo."""
+        arrs = [np.ascontiguousarray(part.nbr, dtype=np.int32)] + \
+            [np.ascontiguousarray(a, dtype=np.int64) for a in (part.send_off, part.send_cnt, part.recv_off, part.recv_cnt)]
+        check(self._lib.sipg_h3_set_halo(self.handle, part.rank, part.world, int(arrs[0].size),
+                                         *[a.ctypes.data for a in arrs]), "sipg_h3_set_halo")
+
+    def comm_init(self, uid: bytes, rank: int, world: int) -> None:
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(self._lib.sipg_comm_init(self.handle, buf, rank, world), "sipg_comm_init")
+
+    def halo_copy_from(self, src: "NativePlan", stream: int = 0) -> None:
+        """Loop-back transport (one GPU): src's send range for this rank -> this receive range."""
+        check(self._lib.sipg_h3_halo_copy(self.handle, src.handle, ctypes.c_void_p(stream)), "sipg_h3_halo_copy")
 
     def apply_traces(self, x_ptr: int, traces_ptr: int, y_ptr: int, stream: int = 0) -> None:
         """Hybrid plans: the apply kernels on a caller-provided trace buffer (sipg_h3_apply_traces)."""

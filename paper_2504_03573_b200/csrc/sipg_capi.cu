@@ -1,6 +1,8 @@
 // C-ABI of libsipg.so (declared in include/sipg.h).  Plain pointers and sizes:
 // no torch types cross this boundary.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: libnccl is resolved at run time by sipg_comm_init (dlopen)
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -126,6 +128,15 @@ struct H3State {
   void* bufs[7] = {};
   double* pub = nullptr;
   int64_t n_pub = 0;
+  // trace halo of a slab partition (sipg_h3_set_halo): per neighbour rank the published-trace
+  // ranges (doubles) this rank sends and the ones it receives; NCCL point-to-point over NVLink on
+  // a dedicated stream (sipg_comm_init)
+  int rank = -1, nranks = 0;
+  std::vector<int32_t> nbr;
+  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
+  ncclComm_t comm = nullptr;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_pub1 = nullptr, ev_comm = nullptr;
 };
 
 // Independent class launches (the publishers of a phase, then the element classes) are spread over
@@ -550,41 +561,135 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   return 0;
 }
 
-// role -1: publish every class, apply roles 0 and 1; role 0: publish the owned classes (roles 0, 1),
-// apply role 0; role 1 (after the halo exchange): publish the ghost classes (role 2), apply role 1
+// ---------------------------------------------------------------------------------------------
+// NCCL, resolved at run time (the library loads without it; torch's own libnccl.so.2 is reused
+// when already loaded in the process)
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    const char* env = getenv("SIPG_NCCL_LIB");
+    if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = "libnccl.so.2 not found (import torch first, or set SIPG_NCCL_LIB)";
+      return a;
+    }
+    auto sym = [&](auto& fp, const char* name) { fp = reinterpret_cast<std::decay_t<decltype(fp)>>(dlsym(h, name)); };
+    sym(a.getUniqueId, "ncclGetUniqueId");
+    sym(a.commInitRank, "ncclCommInitRank");
+    sym(a.commDestroy, "ncclCommDestroy");
+    sym(a.commGetAsyncError, "ncclCommGetAsyncError");
+    sym(a.send, "ncclSend");
+    sym(a.recv, "ncclRecv");
+    sym(a.groupStart, "ncclGroupStart");
+    sym(a.groupEnd, "ncclGroupEnd");
+    sym(a.errorString, "ncclGetErrorString");
+    a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.commGetAsyncError && a.send && a.recv &&
+           a.groupStart && a.groupEnd && a.errorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+#define NCK(call)                                                                                   \
+  do {                                                                                              \
+    ncclResult_t _r = (call);                                                                       \
+    if (_r != ncclSuccess) return fail(SIPG_ERR_COMM, std::string(#call) + ": " + nccl().errorString(_r)); \
+  } while (0)
+
+// launch the classes of one pass (0 publish, 1 apply) whose role is selected by `want` (-1: all)
+int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_dev, cudaStream_t s) {
+  H3State* h = p->h3;
+  auto go = [&](int c) {
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    const int crole = h->cd[c * CD3_WORDS + CD3_ROLE];
+    return count > 0 && (want < 0 || crole == want);
+  };
+  int n = 0, nsmall = 0;
+  for (int c = 0; c < p->n_cls; ++c) {
+    if (!go(c)) continue;
+    ++n;
+    nsmall += (pass == 0 ? h->grid_pub[c] < h->cap_pub[c] : h->grid_apply[c] < h->cap_apply[c]);
+  }
+  int rc = group_begin(p, s, n, nsmall);
+  if (rc) return rc;
+  for (int c = 0; c < p->n_cls; ++c) {
+    if (!go(c)) continue;
+    const H3Entry* k = h->kern[c];
+    cudaStream_t st = group_stream(p);
+    if (pass == 0)
+      k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, st>>>(h->hp, c, x_dev, y_dev);
+    else
+      k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, st>>>(h->hp, c, x_dev, y_dev);
+    ++p->launches;
+  }
+  return group_end(p);
+}
+
+// Trace-halo exchange of a partitioned plan on the comm stream: every neighbour's send range of the
+// published traces goes out and its range arrives in this rank's receive region, one NCCL group.
+int h3_exchange(sipg_plan* p) {
+  H3State* h = p->h3;
+  const NcclApi& a = nccl();
+  NCK(a.groupStart());
+  for (size_t i = 0; i < h->nbr.size(); ++i) {
+    if (h->send_cnt[i] > 0)
+      NCK(a.send(h->pub + h->send_off[i], (size_t)h->send_cnt[i], ncclFloat64, h->nbr[i], h->comm, h->s_comm));
+    if (h->recv_cnt[i] > 0)
+      NCK(a.recv(h->pub + h->recv_off[i], (size_t)h->recv_cnt[i], ncclFloat64, h->nbr[i], h->comm, h->s_comm));
+  }
+  NCK(a.groupEnd());
+  return 0;
+}
+
+// The apply of a hybrid plan.  Whole plan (role -1): publish the boundary-layer classes (role 1)
+// first; with a trace halo and a communicator, their traces leave on the comm stream while the
+// interior classes (role 0) publish and apply; the boundary-layer classes apply once the partner
+// traces have arrived.  role 0 / 1 (a caller-driven exchange between them): 0 publishes every class
+// and applies the interior, 1 applies the boundary layer.
 int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
-  for (int pass = 0; pass < 2; ++pass) {   // publish traces, then apply
-    auto go = [&](int c) {
-      const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
-      const int crole = h->cd[c * CD3_WORDS + CD3_ROLE];
-      if (count == 0) return false;
-      if (pass == 0 && role == 0 && crole == 2) return false;
-      if (pass == 0 && role == 1 && crole != 2) return false;
-      if (pass == 1 && (crole == 2 || (role >= 0 && crole != role))) return false;
-      return true;
-    };
-    int n = 0, nsmall = 0;
-    for (int c = 0; c < p->n_cls; ++c) {
-      if (!go(c)) continue;
-      ++n;
-      const int g = pass == 0 ? h->grid_pub[c] : h->grid_apply[c];
-      const int cap = pass == 0 ? h->cap_pub[c] : h->cap_apply[c];
-      nsmall += g < cap;
-    }
-    int rc = group_begin(p, s, n, nsmall);
-    if (rc) return rc;
-    for (int c = 0; c < p->n_cls; ++c) {
-      if (!go(c)) continue;
-      const H3Entry* k = h->kern[c];
-      cudaStream_t st = group_stream(p);
-      if (pass == 0)
-        k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, st>>>(h->hp, c, x_dev, y_dev);
-      else
-        k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, st>>>(h->hp, c, x_dev, y_dev);
-      ++p->launches;
-    }
-    if ((rc = group_end(p))) return rc;
+  int rc = 0;
+  if (role == 1) {
+    if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
+    CK(cudaGetLastError());
+    return 0;
+  }
+  const bool halo = h->nranks > 1 && !h->nbr.empty();
+  if (role < 0 && halo && !h->comm)
+    return fail(SIPG_ERR_ARG, "partitioned plan without a communicator: call sipg_comm_init, or drive the "
+                              "exchange with sipg_apply_role 0 / 1");
+  if ((rc = h3_launch(p, 0, 1, x_dev, y_dev, s))) return rc;     // boundary layer publishes first
+  if (role < 0 && halo) {
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().commGetAsyncError(h->comm, &ae) != ncclSuccess || ae != ncclSuccess)
+      return fail(SIPG_ERR_COMM, std::string("NCCL asynchronous error: ") + nccl().errorString(ae));
+    CK(cudaEventRecord(h->ev_pub1, s));
+    CK(cudaStreamWaitEvent(h->s_comm, h->ev_pub1, 0));
+    if ((rc = h3_exchange(p))) return rc;
+    CK(cudaEventRecord(h->ev_comm, h->s_comm));
+  }
+  if ((rc = h3_launch(p, 0, 0, x_dev, y_dev, s))) return rc;
+  if ((rc = h3_launch(p, 1, 0, x_dev, y_dev, s))) return rc;
+  if (role < 0) {
+    if (halo) CK(cudaStreamWaitEvent(s, h->ev_comm, 0));
+    if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
   }
   CK(cudaGetLastError());
   return 0;
@@ -706,6 +811,84 @@ int sipg_h3_apply_traces(sipg_plan* p, const double* x_dev, const double* traces
 }
 
 int64_t sipg_h3_trace_len(const sipg_plan* p) { return p && p->h3 ? p->h3->n_pub : -1; }
+
+int sipg_h3_set_halo(sipg_plan* p, int32_t rank, int32_t nranks, int32_t n_nbr, const int32_t* nbr_rank,
+                     const int64_t* send_off, const int64_t* send_cnt, const int64_t* recv_off,
+                     const int64_t* recv_cnt) {
+  if (!p || !p->h3 || rank < 0 || nranks < 1 || rank >= nranks || n_nbr < 0 ||
+      (n_nbr > 0 && (!nbr_rank || !send_off || !send_cnt || !recv_off || !recv_cnt)))
+    return fail(SIPG_ERR_ARG, "sipg_h3_set_halo: bad argument");
+  H3State* h = p->h3;
+  for (int i = 0; i < n_nbr; ++i) {
+    if (nbr_rank[i] < 0 || nbr_rank[i] >= nranks || nbr_rank[i] == rank || send_cnt[i] < 0 || recv_cnt[i] < 0 ||
+        send_off[i] < 0 || recv_off[i] < 0 || send_off[i] + send_cnt[i] > h->n_pub ||
+        recv_off[i] + recv_cnt[i] > h->n_pub)
+      return fail(SIPG_ERR_ARG, "sipg_h3_set_halo: neighbour range outside the published-trace buffer");
+  }
+  h->rank = rank;
+  h->nranks = nranks;
+  h->nbr.assign(nbr_rank, nbr_rank + n_nbr);
+  h->send_off.assign(send_off, send_off + n_nbr);
+  h->send_cnt.assign(send_cnt, send_cnt + n_nbr);
+  h->recv_off.assign(recv_off, recv_off + n_nbr);
+  h->recv_cnt.assign(recv_cnt, recv_cnt + n_nbr);
+  // the receive regions are written only by the exchange: zero them once so that an element
+  // applied before the first exchange reads defined data
+  for (int i = 0; i < n_nbr; ++i)
+    if (recv_cnt[i] > 0) CK(cudaMemset(h->pub + recv_off[i], 0, sizeof(double) * recv_cnt[i]));
+  return 0;
+}
+
+int sipg_nccl_unique_id(void* out128) {
+  if (!out128) return fail(SIPG_ERR_ARG, "null argument");
+  const NcclApi& a = nccl();
+  if (!a.ok) return fail(SIPG_ERR_COMM, a.err);
+  ncclUniqueId id;
+  NCK(a.getUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int sipg_comm_init(sipg_plan* p, const void* nccl_unique_id, int32_t rank, int32_t nranks) {
+  if (!p || !nccl_unique_id || rank < 0 || rank >= nranks) return fail(SIPG_ERR_ARG, "sipg_comm_init: bad argument");
+  if (!p->h3) return fail(SIPG_ERR_UNSUPPORTED, "sipg_comm_init: trace-halo exchange is implemented for hybrid plans");
+  H3State* h = p->h3;
+  if (h->nranks != nranks || h->rank != rank)
+    return fail(SIPG_ERR_ARG, "sipg_comm_init: rank / nranks differ from sipg_h3_set_halo");
+  const NcclApi& a = nccl();
+  if (!a.ok) return fail(SIPG_ERR_COMM, a.err);
+  if (h->comm) {
+    a.commDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  NCK(a.commInitRank(&h->comm, nranks, id, rank));
+  if (!h->s_comm) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CK(cudaStreamCreateWithPriority(&h->s_comm, cudaStreamNonBlocking, hi));   // exchange ahead of compute
+    CK(cudaEventCreateWithFlags(&h->ev_pub1, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+  }
+  return 0;
+}
+
+int sipg_h3_halo_copy(sipg_plan* dst, const sipg_plan* src, void* stream) {
+  if (!dst || !src || !dst->h3 || !src->h3) return fail(SIPG_ERR_ARG, "sipg_h3_halo_copy: bad argument");
+  const H3State *d = dst->h3, *s = src->h3;
+  for (size_t i = 0; i < d->nbr.size(); ++i) {
+    if (d->nbr[i] != s->rank) continue;
+    for (size_t j = 0; j < s->nbr.size(); ++j) {
+      if (s->nbr[j] != d->rank) continue;
+      if (s->send_cnt[j] != d->recv_cnt[i]) return fail(SIPG_ERR_ARG, "sipg_h3_halo_copy: halo sizes differ");
+      if (d->recv_cnt[i] > 0)
+        CK(cudaMemcpyAsync(d->pub + d->recv_off[i], s->pub + s->send_off[j], sizeof(double) * d->recv_cnt[i],
+                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    }
+  }
+  return 0;
+}
 
 int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   if (!d || !out) return fail(SIPG_ERR_ARG, "null argument");
@@ -1095,6 +1278,10 @@ int sipg_plan_destroy(sipg_plan* p) {
     if (e) cudaEventDestroy(e);
   if (p->fork.ev_fork) cudaEventDestroy(p->fork.ev_fork);
   if (p->h3) {
+    if (p->h3->comm) nccl().commDestroy(p->h3->comm);
+    if (p->h3->s_comm) cudaStreamDestroy(p->h3->s_comm);
+    if (p->h3->ev_pub1) cudaEventDestroy(p->h3->ev_pub1);
+    if (p->h3->ev_comm) cudaEventDestroy(p->h3->ev_comm);
     for (void* b : p->h3->bufs)
       if (b) cudaFree(b);
     if (p->h3->pub) cudaFree(p->h3->pub);

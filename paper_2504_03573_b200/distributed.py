@@ -1,6 +1,10 @@
-"""Multi-GPU apply: one process per GPU, x-slab partition, ghost-layer halo
-exchange over torch.distributed (NCCL on NVLink / NVSwitch between GPUs; gloo
-in the CPU tests), overlapped with the elements that do not touch a ghost.
+"""Multi-GPU apply for the quad / tri / hex plans (configs 0-3b): one process per GPU, x-slab
+partition of the configuration, ghost-layer halo exchange over torch.distributed (NCCL on NVLink /
+NVSwitch between GPUs; gloo in the CPU tests), overlapped with the elements that do not touch a
+ghost.  These plans' kernels evaluate a neighbour's trace from its coefficient block in registers
+(k_hex) or from its published planes, so the halo they need is the ghost layer's coefficients —
+2.7x the bytes of the paper's trace-only exchange, which config 4 implements (halo3d.py,
+distributed3d.py).
 
 Per apply:  pack/send owned boundary-layer coefficients to the slab
 neighbours and receive the ghost layer (one P2P batch); meanwhile launch the
@@ -41,14 +45,26 @@ class HaloExchange:
             self.recvs.append((src, torch.as_tensor(ldofs, device=device), contiguous, int(ldofs[0]), ldofs.size))
 
     def start(self, x_local):
-        """Post sends of owned coefficients and receives into the ghost slots."""
+        """Post sends of owned coefficients and receives into the ghost slots (receive / pack
+        buffers of non-contiguous ranges are allocated once per x_local storage)."""
         import torch
+        key = (x_local.data_ptr(), x_local.device)
+        if getattr(self, "_key", None) != key:
+            self._key = key
+            self._sbuf = [None if c else torch.empty(n, dtype=x_local.dtype, device=x_local.device)
+                          for _, _, c, _, n in self.sends]
+            self._rbuf = [None if c else torch.empty(n, dtype=x_local.dtype, device=x_local.device)
+                          for _, _, c, _, n in self.recvs]
         ops, self._unpack = [], []
-        for dst, idx, contig, start, n in self.sends:
-            buf = x_local[start:start + n] if contig else x_local.index_select(0, idx)
+        for (dst, idx, contig, start, n), sb in zip(self.sends, self._sbuf):
+            if contig:
+                buf = x_local[start:start + n]
+            else:
+                torch.index_select(x_local, 0, idx, out=sb)
+                buf = sb
             ops.append(self.dist.P2POp(self.dist.isend, buf, dst))
-        for src, idx, contig, start, n in self.recvs:
-            buf = x_local[start:start + n] if contig else torch.empty(n, dtype=x_local.dtype, device=x_local.device)
+        for (src, idx, contig, start, n), rb in zip(self.recvs, self._rbuf):
+            buf = x_local[start:start + n] if contig else rb
             ops.append(self.dist.P2POp(self.dist.irecv, buf, src))
             if not contig:
                 self._unpack.append((idx, buf))

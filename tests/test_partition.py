@@ -44,7 +44,12 @@ def _worker(rank, world, port, name, nx, q):
     try:
         from oracle import OracleOperator
         from paper_2504_03573_b200.distributed import HaloExchange
-        m, om, rng = stack_box_config(name, world, nx=nx, seed=3)
+        if name == "cfg2":      # strong scaling: the hybrid quad / tri config itself is cut into x-slabs
+            from paper_2504_03573_b200 import configs
+            case = configs.build_case(name, nx, 3)
+            m, om, rng = case.mesh, case.order_map, case.rng
+        else:
+            m, om, rng = stack_box_config(name, world, nx=nx, seed=3)
         ref = OracleOperator(m, om, **OP_KW)
         x = rng.uniform(-1.0, 1.0, ref.n_dofs)
         r = slab_ranges(m, om, world)
@@ -68,7 +73,7 @@ def _worker(rank, world, port, name, nx, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,nx", [("cfg3b", 3), ("cfg1", 5)])
+@pytest.mark.parametrize("name,nx", [("cfg3b", 3), ("cfg1", 5), ("cfg2", 6)])
 def test_gloo_two_ranks_match_global(name, nx):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

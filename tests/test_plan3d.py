@@ -1,5 +1,5 @@
 """Config-4 host logic without a GPU: the plan3d tables reproduce the oracle's bases, and a numpy
-emulation of the kernels' algorithm (tools/h3_emulate.py) on the flattened plan reproduces the
+emulation of the kernels' algorithm (oracle/h3_emulate.py) on the flattened plan reproduces the
 oracle apply — so a GPU mismatch can only be a kernel bug."""
 import sys
 from pathlib import Path
@@ -12,8 +12,7 @@ from oracle import hybrid3d as h
 from paper_2504_03573_b200 import configs
 from paper_2504_03573_b200.plan3d import SLOT, Plan3DBuilder
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
-from h3_emulate import emulate, phi_matrix  # noqa: E402
+from oracle.h3_emulate import emulate, phi_matrix  # noqa: E402
 
 
 def _ref(case):
