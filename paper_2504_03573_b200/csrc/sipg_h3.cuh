@@ -80,13 +80,13 @@ struct Cfg {
   static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
   // small 1-D tables + the ragged triangle-group rows B (and the tet C rows) in shared memory;
   // A / D / prism psi are __constant__ (register pencils)
-  static constexpr int TABD = 6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB;   // tet C rows: global (L1)
+  static constexpr int TABD = (6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB + 1) & ~1;   // even: 16-B cp.async after it; tet C rows: global (L1)
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
   // coefficients and slot headers are double-buffered: the next element's arrive (cp.async) while
   // the current one computes
   // the publish kernel has no derivative arrays (3 Q^3 doubles less: more CTAs per SM)
   static constexpr int doubles(bool pub) {
-    return TABD + 2 * NCP + (pub ? 1 : 4) * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + SCR;
+    return TABD + 2 * NCP + (pub ? 1 : 4) * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + 2 * H3_EGEO + SCR;
   }
   static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
 };
@@ -533,7 +533,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
 template <int S, int N>
 struct Lay {
   using C = Cfg<S, N>;
-  double *c, *u, *du, *s1, *s2, *F, *hdr, *tb, *cbuf, *hbuf;
+  double *c, *u, *du, *s1, *s2, *F, *hdr, *tb, *cbuf, *hbuf, *ebuf;
   double *pts, *R, *D, *W, *E, *ED, *B, *Ct;
   int *gstart, *gmem, *gof, *coff, *mofr;
   __device__ Lay(double* sm, bool pub) {
@@ -553,7 +553,8 @@ struct Lay {
     F = du + (pub ? 0 : 3 * C::Q3);      // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
     hdr = hbuf;
-    tb = hbuf + 2 * C::NSMAX * C::SLOTD; // [SB][4][TMAX]: trace values / flux / map temporaries,
+    ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;   // [2][H3_EGEO]: element geometry, double-buffered
+    tb = ebuf + 2 * H3_EGEO;             // [SB][4][TMAX]: trace values / flux / map temporaries,
     s1 = tb;                             // shared with the BwdTrans stages (never live together)
     s2 = s1 + C::S1;
     gstart = (int*)(tb + C::SCR);
@@ -866,27 +867,30 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
   // coefficients + slot headers one element ahead by cp.async into the other buffer
   const int G = gridDim.x;
   const int32_t* ce = P.class_elems + cd[CD3_ELEM_OFF];
-  auto scalars = [&](int i, int64_t& dof, int64_t& sb, int& ns) {
+  auto scalars = [&](int i, int& e, int64_t& dof, int64_t& sb, int& ns) {
     if (i < count) {
-      const int e = __ldg(ce + i);
+      e = __ldg(ce + i);
       dof = __ldg(P.dof_off + e);
       sb = __ldg(P.slot_off + e);
       ns = (int)(__ldg(P.slot_off + e + 1) - sb);
     }
   };
-  auto issue = [&](int buf, int64_t dof, int64_t sb, int ns) {
+  // coefficients, slot headers and (apply) the element geometry of the next element, by cp.async
+  auto issue = [&](int buf, int e, int64_t dof, int64_t sb, int ns) {
     double* cd_ = L.cbuf + buf * C::NCP;
     double* hd_ = L.hbuf + buf * C::NSMAX * C::SLOTD;
     for (int r = t; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
     const double* src = reinterpret_cast<const double*>(P.slots + sb);
     for (int r = t; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
+    if (!PUB && t < H3_EGEO / 2)
+      __pipeline_memcpy_async(L.ebuf + buf * H3_EGEO + 2 * t, P.egeo + (int64_t)e * H3_EGEO + 2 * t, 2 * sizeof(double));
     __pipeline_commit();
   };
   int64_t dof_n = 0, sb_n = 0, dof_nn = 0, sb_nn = 0;   // next and next-but-one element
-  int ns_n = 0, ns_nn = 0;
-  scalars(blockIdx.x, dof_n, sb_n, ns_n);
-  if ((int)blockIdx.x < count) issue(0, dof_n, sb_n, ns_n);
-  scalars(blockIdx.x + G, dof_nn, sb_nn, ns_nn);
+  int ns_n = 0, ns_nn = 0, e_n = 0, e_nn = 0;
+  scalars(blockIdx.x, e_n, dof_n, sb_n, ns_n);
+  if ((int)blockIdx.x < count) issue(0, e_n, dof_n, sb_n, ns_n);
+  scalars(blockIdx.x + G, e_nn, dof_nn, sb_nn, ns_nn);
   int it_el = 0;
   for (int i = blockIdx.x; i < count; i += G, ++it_el) {
     const int bsel = it_el & 1;
@@ -894,14 +898,15 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
     __syncthreads();
     L.c = L.cbuf + bsel * C::NCP;
     L.hdr = L.hbuf + bsel * C::NSMAX * C::SLOTD;
+    const double* eg = L.ebuf + bsel * H3_EGEO;
     const int64_t dof = dof_n;
     const int ns = ns_n;
-    if (i + G < count) issue(bsel ^ 1, dof_nn, sb_nn, ns_nn);
+    if (i + G < count) issue(bsel ^ 1, e_nn, dof_nn, sb_nn, ns_nn);
     dof_n = dof_nn;
     sb_n = sb_nn;
     ns_n = ns_nn;
-    scalars(i + 2 * G, dof_nn, sb_nn, ns_nn);
-    const int e = __ldg(ce + i);
+    e_n = e_nn;
+    scalars(i + 2 * G, e_nn, dof_nn, sb_nn, ns_nn);
     bwd<S, N>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
     if (PUB) {
       // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
@@ -955,14 +960,27 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
         map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, false);
       continue;
     }
+    // the published own / partner traces of the first slot batch land in the trace scratch (free
+    // once BwdTrans is done) while PhysDeriv and the volume terms run: per slot j, own (u, g)
+    // interleaved at tb[j][0, 2 TMAX), partner at tb[j][2 TMAX, 4 TMAX)
+    {
+      const int nb0 = ns < C::SB ? ns : C::SB;
+      for (int j = 0; j < nb0; ++j) {
+        const H3Slot& h = slot_hdr(L.hdr, j);
+        double* dst = L.tb + j * 4 * TMAX;
+        for (int r = t; r < h.nt; r += NT) {
+          __pipeline_memcpy_async(dst + 2 * r, P.pub + h.pub_self + 2 * r, 2 * sizeof(double));
+          if (h.kind) __pipeline_memcpy_async(dst + 2 * TMAX + 2 * r, P.pub + h.pub_other + 2 * r, 2 * sizeof(double));
+        }
+      }
+      __pipeline_commit();
+    }
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
     pencil_deriv<S, N>(L.u, L.du);
     __syncthreads();
     // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du)
     {
-      const double* eg = P.egeo + (int64_t)e * H3_EGEO;
-      const double dJ = __ldg(eg), S00 = __ldg(eg + 1), S01 = __ldg(eg + 2), S02 = __ldg(eg + 3),
-                   S11 = __ldg(eg + 4), S12 = __ldg(eg + 5), S22 = __ldg(eg + 6);
+      const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
       const double lam = P.lam;
       for (int o = t; o < Q3; o += NT) {
         const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
@@ -988,26 +1006,53 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
       {
         auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
         const Batch BF(b0, nb, cnt);
-        for (int it0 = t; it0 < BF.tot; it0 += NT) {
+        constexpr int PER = (C::SB * TMAX + NT - 1) / NT;   // flux items per thread
+        double fvr[PER], fdr[PER];
+        if (b0 == 0) __pipeline_wait_prior(0);              // the prefetched first batch
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int it0 = t + k * NT;
+          if (it0 >= BF.tot) break;
           int p = it0;
           const int s = BF.slot(p);
           const H3Slot& h = slot_hdr(L.hdr, s);
-          double* tv = L.tb + (s - b0) * 4 * TMAX;
-          const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
-          const double ut = own.x, gt = own.y;
-          double un, gn;
-          if (h.kind) {
-            const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
-            un = nbv.x;
-            gn = nbv.y;
+          double ut, gt, un, gn;
+          if (b0 == 0) {
+            const double* tv = L.tb + s * 4 * TMAX;
+            ut = tv[2 * p];
+            gt = tv[2 * p + 1];
+            un = tv[2 * TMAX + 2 * p];
+            gn = tv[2 * TMAX + 2 * p + 1];
           } else {
+            const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+            ut = own.x;
+            gt = own.y;
+            if (h.kind) {
+              const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+              un = nbv.x;
+              gn = nbv.y;
+            }
+          }
+          if (!h.kind) {
             un = -ut;
             gn = -gt;
           }
           const double j = ut - un, cc = 0.5 * (gt - gn);
           const double w = h.sJ * __ldg(P.tab + h.wtoff + p);
-          tv[p] = (h.tau * j - cc) * w;
-          tv[TMAX + p] = -0.5 * j * w;
+          fvr[k] = (h.tau * j - cc) * w;
+          fdr[k] = -0.5 * j * w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int it0 = t + k * NT;
+          if (it0 >= BF.tot) break;
+          int p = it0;
+          const int s = BF.slot(p);
+          double* tv = L.tb + (s - b0) * 4 * TMAX;
+          tv[p] = fvr[k];
+          tv[TMAX + p] = fdr[k];
         }
       }
       __syncthreads();
