@@ -177,6 +177,10 @@ struct sipg_plan {
   size_t ws_host_n = 0;
   int64_t launches = 0;
   std::vector<int> per_sm;               // resident CTAs per SM of each class's kernel
+  struct Graph { const double* x; double* y; cudaGraphExec_t exec; int64_t kernels; };
+  std::vector<Graph> graphs;             // captured whole applies (sipg_apply)
+  bool use_graphs = true;
+  cudaStream_t cap_stream = nullptr;
   int sms = 0;                           // multiprocessors of the plan's device (queried)
   bool stream_trace = false;             // SIPG_STREAM_TRACE, read once at plan creation
   // Streamed host apply (sipg_apply_host): x is copied H2D in K DoF chunks; chunk k's elements
@@ -542,6 +546,7 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
   }
   p->sms = sms;
   p->stream_trace = getenv("SIPG_STREAM_TRACE") != nullptr;
+  p->use_graphs = !getenv("SIPG_NO_GRAPH");
   for (int c = 0; c < p->n_cls; ++c) {
     const KernelEntry* k = p->kern[c];
     const int count = p->cd_host[c * CD_WORDS + CD_COUNT];
@@ -975,6 +980,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   }
   p->sms = sms;
   p->stream_trace = getenv("SIPG_STREAM_TRACE") != nullptr;
+  p->use_graphs = !getenv("SIPG_NO_GRAPH");
   for (int c = 0; c < p->n_cls; ++c) {
     const H3Entry* k = h->kern[c];
     const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
@@ -1050,8 +1056,53 @@ int sipg_apply_role(sipg_plan* p, int32_t role, const double* x_dev, double* y_d
   return 0;
 }
 
+// Whole applies are replayed as CUDA graphs: the launch sequence (publishers, element classes, the
+// fork / join over side streams) is captured once per (x, y) pair on a private stream and relaunched
+// with one cudaGraphLaunch (configs 0 / 1 are launch-latency bound: 6-48 kernels of a few us).
+// Distributed plans (an NCCL exchange inside the apply) run eagerly.  SIPG_NO_GRAPH=1 disables it.
 int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
-  return sipg_apply_role(p, -1, x_dev, y_dev, stream);
+  if (!p || !x_dev || !y_dev) return fail(SIPG_ERR_ARG, "null argument");
+  const bool dist = p->h3 && p->h3->nranks > 1;
+  if (!p->use_graphs || dist) return sipg_apply_role(p, -1, x_dev, y_dev, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (auto& g : p->graphs)
+    if (g.x == x_dev && g.y == y_dev) {
+      CK(cudaGraphLaunch(g.exec, s));
+      p->launches += g.kernels;
+      return 0;
+    }
+  if (!p->cap_stream) CK(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+  const int64_t l0 = p->launches;
+  CK(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = sipg_apply_role(p, -1, x_dev, y_dev, p->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+  if (rc || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    p->launches = l0;
+    if (rc) return rc;
+    p->use_graphs = false;      // capture unsupported here: eager from now on
+    return sipg_apply_role(p, -1, x_dev, y_dev, stream);
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    p->launches = l0;
+    p->use_graphs = false;
+    return sipg_apply_role(p, -1, x_dev, y_dev, stream);
+  }
+  if (p->graphs.size() >= 8) {   // small cache: solvers cycle through a few (x, y) pairs
+    cudaGraphExecDestroy(p->graphs.front().exec);
+    p->graphs.erase(p->graphs.begin());
+  }
+  p->graphs.push_back({x_dev, y_dev, exec, p->launches - l0});
+  p->launches = l0;
+  CK(cudaGraphLaunch(exec, s));
+  p->launches += p->graphs.back().kernels;
+  return 0;
 }
 
 int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
@@ -1272,6 +1323,8 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
 
 int sipg_plan_destroy(sipg_plan* p) {
   if (!p) return 0;
+  for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   for (cudaStream_t st : p->fork.side)
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t e : p->fork.ev_join)

@@ -24,6 +24,13 @@
 #include <stdint.h>
 
 #define SIPG_H3_ABI_VERSION 1
+// build knobs (measured variants; the defaults are the fastest measured)
+#ifndef SIPG_H3_PREFETCH_TRACES
+#define SIPG_H3_PREFETCH_TRACES 0   // first slot batch's published traces by cp.async during the volume work
+#endif
+#ifndef SIPG_H3_PUB_DIRECT
+#define SIPG_H3_PUB_DIRECT 1        // identity-map slots publish straight from the face-grid pass
+#endif
 
 enum { H3_HEX = 0, H3_PRISM = 1, H3_TET = 2 };
 #define CD3_WORDS 16
@@ -602,10 +609,13 @@ __device__ __forceinline__ void unpack_nab(int nab, int& n1, int& n2, int& swap)
 // batch; with `pub`, the trace values go straight to the published buffer instead
 template <int Q>
 __device__ void map_forward(const double* hdr, const double* F, double* tb, int b0, int nb, const double* tab,
-                            double* pub, bool only_interior) {
+                            double* pub, bool only_interior, bool skip_identity = false) {
   constexpr int Q2 = Q * Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
-  auto active = [&](int s) { return !only_interior || slot_hdr(hdr, s).kind == 1; };
+  auto active = [&](int s) {
+    const H3Slot& h = slot_hdr(hdr, s);
+    return (!only_interior || h.kind == 1) && !(skip_identity && h.mkind == MAP_ID);
+  };
   // stage 1: tensor X contraction over own axis 0; dense and identity complete here
   auto c1 = [&](int s) -> int {
     if (!active(s)) return 0;
@@ -953,17 +963,25 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
         const double gf = fx == 0 ? g0 : (fx == 1 ? g1 : g2);
         const double ga = ra == 0 ? g0 : (ra == 1 ? g1 : g2);
         const double gb = rb == 0 ? g0 : (rb == 1 ? g1 : g2);
-        L.F[s * 2 * Q2 + Q2 + a] = gf * fu[Q2 + a] + ga * da + gb * db;
+        const double gv = gf * fu[Q2 + a] + ga * da + gb * db;
+        if (SIPG_H3_PUB_DIRECT && h.mkind == MAP_ID)   // own face grid = trace grid: straight to the published buffer
+          reinterpret_cast<double2*>(P.pub + h.pub_self)[a] = make_double2(fu[a], gv);
+        else
+          L.F[s * 2 * Q2 + Q2 + a] = gv;
       }
-      __syncthreads();
-      for (int b0 = 0; b0 < ns; b0 += C::SB)
-        map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, false);
+      bool mapped = false;
+      for (int j = 0; j < ns; ++j) mapped |= !SIPG_H3_PUB_DIRECT || slot_hdr(L.hdr, j).mkind != MAP_ID;
+      if (mapped) {
+        __syncthreads();
+        for (int b0 = 0; b0 < ns; b0 += C::SB)
+          map_forward<Q>(L.hdr, L.F, L.tb, b0, min(C::SB, ns - b0), P.tab, P.pub, false, SIPG_H3_PUB_DIRECT);
+      }
       continue;
     }
     // the published own / partner traces of the first slot batch land in the trace scratch (free
     // once BwdTrans is done) while PhysDeriv and the volume terms run: per slot j, own (u, g)
     // interleaved at tb[j][0, 2 TMAX), partner at tb[j][2 TMAX, 4 TMAX)
-    {
+    if (SIPG_H3_PREFETCH_TRACES) {
       const int nb0 = ns < C::SB ? ns : C::SB;
       for (int j = 0; j < nb0; ++j) {
         const H3Slot& h = slot_hdr(L.hdr, j);
@@ -1008,8 +1026,11 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
         const Batch BF(b0, nb, cnt);
         constexpr int PER = (C::SB * TMAX + NT - 1) / NT;   // flux items per thread
         double fvr[PER], fdr[PER];
-        if (b0 == 0) __pipeline_wait_prior(0);              // the prefetched first batch
-        __syncthreads();
+        constexpr bool PF = SIPG_H3_PREFETCH_TRACES;
+        if (PF && b0 == 0) {
+          __pipeline_wait_prior(0);                         // the prefetched first batch
+          __syncthreads();
+        }
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           const int it0 = t + k * NT;
@@ -1018,7 +1039,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
           const int s = BF.slot(p);
           const H3Slot& h = slot_hdr(L.hdr, s);
           double ut, gt, un, gn;
-          if (b0 == 0) {
+          if (PF && b0 == 0) {
             const double* tv = L.tb + s * 4 * TMAX;
             ut = tv[2 * p];
             gt = tv[2 * p + 1];
@@ -1043,7 +1064,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3
           fvr[k] = (h.tau * j - cc) * w;
           fdr[k] = -0.5 * j * w;
         }
-        __syncthreads();
+        if (PF && b0 == 0) __syncthreads();   // the flux overwrites the prefetched traces
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           const int it0 = t + k * NT;
