@@ -840,8 +840,20 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
   __syncthreads();
 }
 
+// resident CTAs per SM the register allocation must allow (q >= 7: 128 threads, else 64)
+#ifndef SIPG_H3_PUB_MINB_HI
+#define SIPG_H3_PUB_MINB_HI 6
+#endif
+#ifndef SIPG_H3_PUB_MINB_LO
+#define SIPG_H3_PUB_MINB_LO 12
+#endif
+template <bool PUB, int Q>
+constexpr int h3_minb() {
+  return PUB ? (Q >= 7 ? SIPG_H3_PUB_MINB_HI : SIPG_H3_PUB_MINB_LO) : (Q >= 7 ? 6 : 12);
+}
+
 template <int S, int N, bool PUB>
-__global__ void __launch_bounds__(nthreads<N + 1>(), (N + 1) >= 7 ? 6 : 12) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
+__global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3(const H3Plan P, const int cls, const double* __restrict__ x,
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
