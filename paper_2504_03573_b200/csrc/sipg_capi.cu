@@ -205,6 +205,15 @@ namespace {
 
 constexpr int kSideStreams = 3;
 
+// element count below which a 2-D class runs CTA-per-element (SIPG_SMALL_CLASS overrides)
+int small_class_elems() {
+  static const int v = [] {
+    const char* e = getenv("SIPG_SMALL_CLASS");
+    return e ? atoi(e) : 2048;
+  }();
+  return v;
+}
+
 // Instrumentation switches that change results exist only in SIPG_INSTRUMENT builds
 // (build.py OUT.so -DSIPG_INSTRUMENT); the product library ignores them.
 int instrument_debug() {
@@ -453,6 +462,12 @@ int sipg_plan_create(const sipg_plan_desc* d, sipg_plan** out) {
       }
     }
     if (!k && uniform) k = find_kernel(shape, n, q, geom, shape == SHAPE_HEX ? 0 : 5);
+    // 2-D classes too small to fill the GPU with warp-per-element pipelines: one CTA per element
+    // (every element in flight at once; the per-element latency, not throughput, is the cost)
+    if (k && k->kind == 5 && cd[CD_COUNT] <= small_class_elems()) {
+      const KernelEntry* kc = find_kernel(shape, n, q, geom, 0);
+      if (kc) k = kc;
+    }
     if (!k) {
       sipg_plan_destroy(p);
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a kernel for shape=" + std::to_string(shape) +

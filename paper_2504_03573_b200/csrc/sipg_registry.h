@@ -50,10 +50,22 @@ KernelEntry sipg_entry();
                          sizeof(double) * (size_t)C::TOTAL, nullptr};                        \
     return KernelEntry{SHAPE, N, Q, GEOM, 5, &sipg::k_apply_w<SHAPE, N, Q, GEOM, SIPG_WPC>,      \
                        32 * SIPG_WPC, sizeof(double) * (size_t)(C::TABP + SIPG_WPC * C::ESZ), nullptr};            \
+  }                                                                                          \
+  /* 2-D shapes also get the CTA-per-element kernel (kind 0): small classes (configs 0 / 1) */  \
+  /* are latency-bound and run every element at once, 64 threads each instead of one warp */   \
+  template <int SHAPE, int N, int Q, int GEOM>                                               \
+  KernelEntry sipg_entry_cta() {                                                             \
+    using C = sipg::Cfg<SHAPE, N, Q>;                                                        \
+    return KernelEntry{SHAPE, N, Q, GEOM, 0, &sipg::k_apply<SHAPE, N, Q, GEOM>, C::NT,       \
+                       sizeof(double) * (size_t)C::TOTAL, nullptr};                          \
   }
 #define SIPG_ENTRIES_NQ(S, N)                                                                \
   v.push_back(sipg_entry<S, N, N + 1, GEOM_REGULAR>());                                      \
-  v.push_back(sipg_entry<S, N, N + 1, GEOM_POINTWISE>())
+  v.push_back(sipg_entry<S, N, N + 1, GEOM_POINTWISE>());                                    \
+  if (S != SHAPE_HEX) {                                                                      \
+    v.push_back(sipg_entry_cta<S, N, N + 1, GEOM_REGULAR>());                                \
+    v.push_back(sipg_entry_cta<S, N, N + 1, GEOM_POINTWISE>());                              \
+  }
 #define SIPG_HEX_PLANES(N)                                                                   \
   v.push_back(KernelEntry{SHAPE_HEX, N, N + 1, GEOM_REGULAR, 6, &sipg::k_hexp<N, N + 1, false>,    \
                           (N + 1) * (N + 1), sipg::HexPlanes<N, N + 1, false>::smem_bytes(),      \
