@@ -47,7 +47,7 @@ def _fine(ct):
                         tuple(r.kind.value for r in ct.rules))
 
 
-def _volume(pb, i, ct, ids, verts):
+def _volume(pb, i, ct, ids, verts, on_dev=False):
     """Physical points (d, p, W) as numpy (for the user's callbacks) and jw (p, W) on the device, of
     the class-i elements `ids` (vertex coords `verts` (W, nv, d)) at the volume points of `ct`.
     The vertex-map products run on the GPU; affine elements take the plan's constant Jacobian
@@ -64,7 +64,7 @@ def _volume(pb, i, ct, ids, verts):
     if nr.size:
         F = torch.einsum("pvj,evi->epij", _dev(dN), vd[torch.from_numpy(nr).cuda()])
         J[:, torch.from_numpy(nr).cuda()] = torch.linalg.det(F).T
-    return x.cpu().numpy(), J * _dev(ct.ref_w)[:, None]
+    return (x if on_dev else x.cpu().numpy()), J * _dev(ct.ref_w)[:, None]
 
 
 def _dev(a):
@@ -73,18 +73,22 @@ def _dev(a):
 
 
 def rhs_assemble(op, case, bcs):
+    """With device-capable callables (cases.py) the points stay on the GPU and the callables run
+    there; otherwise they get host points like the reference's."""
     import torch
+    from .cases import device_callable
     pb = op.plan
     mesh = op.mesh
     ev = element_vertex_array(mesh)
     X = np.asarray(mesh.vertices, dtype=float)
+    on_dev = device_callable(case.forcing, mesh.dim)
     b = torch.zeros(pb.n_dofs, dtype=torch.float64, device="cuda")
     for i, ids in enumerate(pb.exp_members):
         if ids.size == 0:
             continue
         ct = pb.exp_list[i]
-        xs, jw = _volume(pb, i, ct, ids, X[ev[ids, :NV[ct.shape]]])
-        f = _dev(np.asarray(case.forcing(xs), dtype=float))
+        xs, jw = _volume(pb, i, ct, ids, X[ev[ids, :NV[ct.shape]]], on_dev)
+        f = case.forcing(xs) if on_dev else _dev(np.asarray(case.forcing(xs), dtype=float))
         contrib = -(_dev(volume_basis(ct)).T @ (f * jw))           # (nc, W)
         dof = pb.dof_off[ids][None, :] + np.arange(ct.n_coeffs)[:, None]
         b.index_copy_(0, torch.from_numpy(dof.reshape(-1)).cuda(), contrib.reshape(-1))
@@ -104,14 +108,21 @@ def rhs_assemble(op, case, bcs):
         swj, nrm, inv, _, _ = pb.geo[i].face(f, prm, ct.face_weights(f), elems=pb.exp_pos[el])
         gn = gn_at(ct, f, inv, nrm, prm)                            # (W, p, d)
         xi = np.asarray(face.center) + prm @ np.asarray(face.tangents)
-        xf, _ = jacobians(ct.shape, X[ev[el, :NV[ct.shape]]], xi)   # (W, p, d)
-        gv = np.stack([np.asarray(gfun(xf[w].T), dtype=float) for w in range(el.size)])   # (W, p)
+        if device_callable(gfun, mesh.dim):        # pointwise data: the whole group in one call
+            from .plan import vertex_maps
+            Nf, _ = vertex_maps(ct.shape, xi)
+            xf = torch.einsum("pv,evi->ipe", _dev(Nf), _dev(X[ev[el, :NV[ct.shape]]]))   # (d, p, W)
+            gv = gfun(xf).T                                                               # (W, p)
+        else:                                      # the reference's pattern: one face at a time
+            xf, _ = jacobians(ct.shape, X[ev[el, :NV[ct.shape]]], xi)   # (W, p, d)
+            gv = _dev(np.stack([np.asarray(gfun(xf[w].T), dtype=float) for w in range(el.size)]))   # (W, p)
         tau = pb._tau(el, np.full(el.size, f))
-        fv = 2.0 * tau[:, None] * gv * swj
-        fd = -gv * swj
-        contrib = _dev(fv) @ _dev(face_basis(ct, f, prm))
+        swj_d = _dev(swj)
+        fv = 2.0 * _dev(tau)[:, None] * gv * swj_d
+        fd = -gv * swj_d
+        contrib = fv @ _dev(face_basis(ct, f, prm))
         for k in range(ct.dim):
-            contrib += _dev(fd * gn[:, :, k]) @ _dev(face_basis(ct, f, prm, deriv=k))
+            contrib += (fd * _dev(gn[:, :, k])) @ _dev(face_basis(ct, f, prm, deriv=k))
         dof = pb.dof_off[el][:, None] + np.arange(ct.n_coeffs)[None, :]
         b.index_add_(0, torch.from_numpy(dof.reshape(-1)).cuda(), contrib.reshape(-1))
     return b.cpu().numpy()
@@ -123,14 +134,17 @@ def l2_error(op, x, exact) -> float:
     mesh = op.mesh
     ev = element_vertex_array(mesh)
     X = np.asarray(mesh.vertices, dtype=float)
+    from .cases import device_callable
     xd = x if (hasattr(x, "is_cuda") and x.is_cuda) else _dev(np.asarray(x, dtype=float))
+    on_dev = device_callable(exact, mesh.dim)
     err2 = torch.zeros((), dtype=torch.float64, device="cuda")
     for i, ids in enumerate(pb.exp_members):
         if ids.size == 0:
             continue
         fine = _fine(pb.exp_list[i])
-        xs, jw = _volume(pb, i, fine, ids, X[ev[ids, :NV[fine.shape]]])
+        xs, jw = _volume(pb, i, fine, ids, X[ev[ids, :NV[fine.shape]]], on_dev)
         dof = torch.from_numpy(pb.dof_off[ids][None, :] + np.arange(fine.n_coeffs)[:, None]).cuda()
-        d = _dev(volume_basis(fine)) @ xd[dof] - _dev(np.asarray(exact(xs), dtype=float))
+        u = exact(xs) if on_dev else _dev(np.asarray(exact(xs), dtype=float))
+        d = _dev(volume_basis(fine)) @ xd[dof] - u
         err2 += (d * d * jw).sum()
     return math.sqrt(float(err2))

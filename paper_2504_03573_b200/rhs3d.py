@@ -79,25 +79,52 @@ def _classes(pb):
             yield c, pb.ct[c], ids
 
 
-def rhs_assemble(op, case, bcs, tag: str = "dirichlet"):
-    """b = -(v, f) + Dirichlet lift, a numpy vector (reference sipg.py:697-718)."""
+def _geo_dev(op):
+    """Element maps x = x0 + F (xi + 1) on the device (cached on the operator)."""
     import torch
+    if getattr(op, "_geo_dev_cache", None) is None:
+        op._geo_dev_cache = (torch.from_numpy(np.ascontiguousarray(op.plan.x0)).cuda(),
+                             torch.from_numpy(np.ascontiguousarray(op.plan.F)).cuda())
+    return op._geo_dev_cache
+
+
+def _phys_dev(op, elems, xi):
+    """Physical points (3, n_points, W) on the device."""
+    import torch
+    x0, F = _geo_dev(op)
+    e = torch.from_numpy(np.asarray(elems, dtype=np.int64)).cuda()
+    xr = torch.from_numpy(np.ascontiguousarray(xi + 1.0)).cuda()
+    return (x0[e][:, :, None] + torch.einsum("eij,pj->eip", F[e], xr)).permute(1, 2, 0)
+
+
+def rhs_assemble(op, case, bcs, tag: str = "dirichlet"):
+    """b = -(v, f) + Dirichlet lift, a numpy vector (reference sipg.py:697-718).  With
+    device-capable callables (cases.py) every step stays on the GPU; otherwise the callables get
+    host points like the reference's."""
+    import torch
+    from .cases import device_callable
     pb = op.plan
     if tag not in bcs:
         raise KeyError(f"no boundary condition for tag {tag!r}")
     dev = torch.device("cuda")
+    on_dev = device_callable(case.forcing, 3)
     b = torch.zeros(pb.n_dofs, dtype=torch.float64, device=dev)
     for c, ct, ids in _classes(pb):
         xi = xi_of_eta(ct.shape, _eta_grid(ct))
-        f = np.asarray(case.forcing(_phys(pb, ids, xi)), dtype=float)                   # (p, W)
-        jw = ct.wref[:, None] * pb.detJ[ids][None, :]
+        if on_dev:
+            f = case.forcing(_phys_dev(op, ids, xi))                                     # (p, W)
+        else:
+            f = torch.from_numpy(np.asarray(case.forcing(_phys(pb, ids, xi)), dtype=float)).to(dev)
+        jw = torch.from_numpy(ct.wref[:, None] * pb.detJ[ids][None, :]).to(dev)
         phi = torch.from_numpy(dense_phi(ct)).to(dev)
-        contrib = -(phi.T @ torch.from_numpy(f * jw).to(dev))                           # (n_c, W)
+        contrib = -(phi.T @ (f * jw))                                                    # (n_c, W)
         dof = torch.from_numpy((pb.dof_off[ids][None, :] + np.arange(ct.nc)[:, None]).reshape(-1)).to(dev)
         b.index_copy_(0, dof, contrib.reshape(-1))
     # boundary lift: the apply kernels on x = 0 with g as the boundary slots' own traces
     gfun = bcs[tag]
+    g_dev = device_callable(gfun, 3)
     traces = np.zeros(max(op.native.trace_len, 1))
+    tr = torch.zeros(max(op.native.trace_len, 1), dtype=torch.float64, device=dev) if g_dev else None
     S = pb.slots
     bnd = np.flatnonzero(S["kind"] == 0)
     for key in np.unique(np.stack([pb.class_of[S["elem"][bnd]], S["face"][bnd]], axis=1), axis=0):
@@ -110,11 +137,16 @@ def rhs_assemble(op, case, bcs, tag: str = "dirichlet"):
         eta[:, fixed] = side
         eta[:, run[0]] = g[0].reshape(-1)
         eta[:, run[1]] = g[1].reshape(-1)
-        xs = _phys(pb, S["elem"][sel].astype(np.int64), xi_of_eta(ct.shape, eta))          # (3, nf, W)
-        gv = np.stack([np.asarray(gfun(xs[:, :, w]), dtype=float) for w in range(len(sel))])   # (W, nf)
-        off = S["pub_self"][sel][:, None] + 2 * np.arange(gv.shape[1])[None, :]
-        traces[off] = gv
-    tr = torch.from_numpy(traces).to(dev)
+        off = S["pub_self"][sel][:, None] + 2 * np.arange(eta.shape[0])[None, :]
+        if g_dev:      # pointwise data: all faces of the group in one call
+            xs = _phys_dev(op, S["elem"][sel].astype(np.int64), xi_of_eta(ct.shape, eta))  # (3, nf, W)
+            tr[torch.from_numpy(off.reshape(-1)).cuda()] = gfun(xs).T.reshape(-1)
+        else:          # the reference's call pattern: one boundary face at a time, host points
+            xs = _phys(pb, S["elem"][sel].astype(np.int64), xi_of_eta(ct.shape, eta))      # (3, nf, W)
+            gv = np.stack([np.asarray(gfun(xs[:, :, w]), dtype=float) for w in range(len(sel))])   # (W, nf)
+            traces[off] = gv
+    if tr is None:
+        tr = torch.from_numpy(traces).to(dev)
     x0 = torch.zeros(pb.n_dofs, dtype=torch.float64, device=dev)
     lift = torch.empty_like(x0)
     stream = torch.cuda.current_stream().cuda_stream
@@ -129,13 +161,18 @@ def l2_error(op, x, exact) -> float:
     dev = torch.device("cuda")
     xd = torch.as_tensor(np.asarray(x, dtype=float)).to(dev) if not hasattr(x, "is_cuda") else x
     err2 = torch.zeros((), dtype=torch.float64, device=dev)
+    from .cases import device_callable
+    on_dev = device_callable(exact, 3)
     for c, ct, ids in _classes(pb):
         fine = ClassTables3(ct.shape, ct.n, ct.q + 2)
         xi = xi_of_eta(ct.shape, _eta_grid(fine))
-        u = np.asarray(exact(_phys(pb, ids, xi)), dtype=float)                           # (p, W)
+        if on_dev:
+            u = exact(_phys_dev(op, ids, xi))                                           # (p, W)
+        else:
+            u = torch.from_numpy(np.asarray(exact(_phys(pb, ids, xi)), dtype=float)).to(dev)
         dof = torch.from_numpy(pb.dof_off[ids][None, :] + np.arange(ct.nc)[:, None]).to(dev)
         uh = torch.from_numpy(dense_phi(fine)).to(dev) @ xd[dof]                        # (p, W)
         jw = torch.from_numpy(fine.wref[:, None] * pb.detJ[ids][None, :]).to(dev)
-        d = uh - torch.from_numpy(u).to(dev)
+        d = uh - u
         err2 += (d * d * jw).sum()
     return math.sqrt(float(err2))

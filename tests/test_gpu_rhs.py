@@ -88,3 +88,35 @@ def test_rhs_and_l2_match_oracle_seeded(name, nx, seed):
     x = case.draw_x(op.n_dofs)
     e = ref.l2_error(x, pulse.exact)
     assert abs(op.l2_error(x, pulse.exact) - e) <= 1e-12 * e
+
+
+@pytest.mark.parametrize("path", FILES[:4], ids=[p.stem for p in FILES[:4]])
+def test_device_cases_match_reference(path):
+    """The device-capable manufactured cases (cases.py) keep rhs / l2 on the GPU (points, callables,
+    products); same reference fixtures, same bar."""
+    from paper_2504_03573_b200.cases import gaussian_pulse_case, sinusoidal_case
+    g = np.load(path)
+    op = _op(g)
+    d = op.mesh.dim
+    sin, pulse = sinusoidal_case(float(g["k"]), d), gaussian_pulse_case(float(g["a"]), d)
+    assert rel_maxnorm(op.rhs_assemble(sin, {"dirichlet": sin.exact}), g["b_sin"]) <= 1e-12
+    assert rel_maxnorm(op.rhs_assemble(pulse, {"dirichlet": pulse.exact}), g["b_pulse"]) <= 1e-12
+    err = float(g["err"])
+    assert abs(op.l2_error(g["x"], sin.exact) - err) <= 1e-12 * err
+
+
+def test_device_cases_hybrid3d_match_host_path():
+    """Config 4: device callables and the reference-style host callables give the same rhs / l2."""
+    from paper_2504_03573_b200 import configs
+    from paper_2504_03573_b200.cases import sinusoidal_case
+    from paper_2504_03573_b200.sipg import HelmholtzOperator
+    case = configs.build_case("cfg4", 3, 2)
+    op = HelmholtzOperator(case.mesh, case.order_map, basis_kind="modified_modal", tau_rule="baseline")
+    dev = sinusoidal_case(3.0, 3)
+    host = manufactured(3, 3.0, 0.3)[0]
+    b_dev = op.rhs_assemble(dev, {"dirichlet": dev.exact})
+    b_host = op.rhs_assemble(host, {"dirichlet": host.exact})
+    assert rel_maxnorm(b_dev, b_host) <= 1e-13
+    x = case.draw_x(op.n_dofs)
+    e_dev, e_host = op.l2_error(x, dev.exact), op.l2_error(x, host.exact)
+    assert abs(e_dev - e_host) <= 1e-12 * e_host
