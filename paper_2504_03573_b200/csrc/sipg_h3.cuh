@@ -31,6 +31,9 @@
 #ifndef SIPG_H3_PUB_DIRECT
 #define SIPG_H3_PUB_DIRECT 1        // identity-map slots publish straight from the face-grid pass
 #endif
+#ifndef SIPG_H3_EO
+#define SIPG_H3_EO 1                // even-odd factorised PhysDeriv / PhysDeriv^T pencils
+#endif
 
 enum { H3_HEX = 0, H3_PRISM = 1, H3_TET = 2 };
 #define CD3_WORDS 16
@@ -62,6 +65,12 @@ struct H3Plan {
 
 namespace h3 {
 
+#ifndef SIPG_H3_PAD
+#define SIPG_H3_PAD 1
+#endif
+template <int Q>
+constexpr int H3_SJ() { return (SIPG_H3_PAD && !(Q & 1)) ? Q + 1 : Q; }
+
 // threads per CTA: 256 for q >= 8 (512 volume points), else 128
 template <int Q>
 constexpr int nthreads() { return Q <= 6 ? 64 : 128; }
@@ -70,12 +79,16 @@ constexpr int TMAX = 64;   // trace points per coupling: q_t = max(q_L, q_R) <= 
 template <int S, int N>
 struct Cfg {
   static constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q;
+  // padded volume layout (k0, k1, k2) -> k0 SI + k1 SJ + k2: odd row stride, so the pencils along
+  // every axis hit distinct shared-memory banks (ncu: the h3 kernels are bound by the LSU data pipe,
+  // a quarter to a third of whose wavefronts were bank-conflict replays with the dense layout)
+  static constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
   static constexpr int NTRI = N * (N + 1) / 2;
   static constexpr int NG = N + 1;                                   // triangle direction-1 groups
   static constexpr int NPM = NTRI + (S == H3_TET ? 1 : 0);           // + tet apex pseudo-mode
   static constexpr int NC = S == H3_HEX ? N * N * N : (S == H3_PRISM ? N * NTRI : N * (N + 1) * (N + 2) / 6);
   static constexpr int S1 = S == H3_HEX ? N * N * Q : NPM * Q;
-  static constexpr int S2 = S == H3_HEX ? N * Q2 : NG * Q2;
+  static constexpr int S2 = S == H3_HEX ? N * SI : NG * SI;
   static constexpr int NCP = (NC + 1) & ~1;
   static constexpr int NI = 4 * NPM + 4 + NC + 16;                   // int tables + batch offsets
   static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);   // slots per element
@@ -93,7 +106,7 @@ struct Cfg {
   // the current one computes
   // the publish kernel has no derivative arrays (3 Q^3 doubles less: more CTAs per SM)
   static constexpr int doubles(bool pub) {
-    return TABD + 2 * NCP + (pub ? 1 : 4) * Q3 + NSMAX * (2 * Q2 + 2 * SLOTD) + 2 * H3_EGEO + SCR;
+    return TABD + 2 * NCP + (pub ? 1 : 4) * V3 + NSMAX * (2 * Q2 + 2 * SLOTD) + 2 * H3_EGEO + SCR;
   }
   static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
 };
@@ -190,13 +203,117 @@ template <int S, int N> __constant__ double c3D[3 * (N + 1) * (N + 1)];         
 template <int S, int N> __constant__ double c3A[(N + 1) * (S == H3_HEX ? N : N + 1)];   // A[k][g] / V[k][i]
 template <int S, int N> __constant__ double c3P[(N + 1) * N];                           // prism psi[k][l]
 
+// Even-odd (parity) factorisation of the collocation derivatives.  GL and GLL points are symmetric,
+// so D[Q-1-k][Q-1-j] = -D[k][j] (and the same for D^T): with s_j = in_j + in_{Q-1-j},
+// d_j = in_j - in_{Q-1-j} (j < H = Q/2) and, for odd Q, the middle value in_H,
+//   E_k = sum_j Pe[k][j] s_j + mc[k] in_H,   O_k = sum_j Po[k][j] d_j,
+//   out_k = E_k + O_k,   out_{Q-1-k} = O_k - E_k,   out_H = sum_j mr[j] d_j,
+// with Pe = (D[k][j] + D[k][Q-1-j]) / 2, Po = (D[k][j] - D[k][Q-1-j]) / 2, mc[k] = D[k][H],
+// mr[j] = D[H][j]: 2 H^2 (+2H) FMAs per line instead of Q^2.  Per (operator t: 0 = D, 1 = D^T,
+// axis a) a block of EO doubles: Pe | Po | mc | mr.
+template <int Q>
+constexpr int eo_size() { return 2 * (Q / 2) * (Q / 2) + 2 * (Q / 2); }
+template <int S, int N> __constant__ double c3E[6 * eo_size<N + 1>()];
+
+// out_k for k in [K0, K0 + KN) (and their mirrors), plus the middle row when MID
+template <int Q, int K0, int KN, bool MID, typename Tab>
+__device__ __forceinline__ void eo_lines(const Tab& T, int off, const double (&in)[Q], double* out) {
+  constexpr int H = Q / 2;
+  double sm[H], df[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    sm[j] = in[j] + in[Q - 1 - j];
+    df[j] = in[j] - in[Q - 1 - j];
+  }
+#pragma unroll
+  for (int kk = 0; kk < KN; ++kk) {
+    const int k = K0 + kk;
+    double e = 0.0, o = 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      e = fma(T[off + k * H + j], sm[j], e);
+      o = fma(T[off + H * H + k * H + j], df[j], o);
+    }
+    if (Q & 1) e = fma(T[off + 2 * H * H + k], in[H], e);
+    out[k] = e + o;
+    out[Q - 1 - k] = o - e;
+  }
+  if ((Q & 1) && MID) {
+    double m = 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) m = fma(T[off + 2 * H * H + H + j], df[j], m);
+    out[H] = m;
+  }
+}
+
+// the lines eo_lines produced, stored (ACC: accumulated) at stride st
+template <int Q, int K0, int KN, bool MID, bool ACC>
+__device__ __forceinline__ void eo_store(const double* out, double* d, int st) {
+#pragma unroll
+  for (int kk = 0; kk < KN; ++kk) {
+    const int k = K0 + kk;
+    if (ACC) {
+      d[k * st] += out[k];
+      d[(Q - 1 - k) * st] += out[Q - 1 - k];
+    } else {
+      d[k * st] = out[k];
+      d[(Q - 1 - k) * st] = out[Q - 1 - k];
+    }
+  }
+  if ((Q & 1) && MID) {
+    if (ACC) d[(Q / 2) * st] += out[Q / 2];
+    else d[(Q / 2) * st] = out[Q / 2];
+  }
+}
+
+// one pencil line through the even-odd operator block `blk`, part `part` of KS
+template <int S, int N, int KS, bool ACC>
+__device__ __forceinline__ void eo_pencil(int blk, int part, const double (&col)[N + 1], double* dst, int st) {
+  constexpr int Q = N + 1, H = Q / 2, KA = KS == 1 ? H : (H + 1) / 2;
+  double out[Q];
+  if (KS == 1) {
+    eo_lines<Q, 0, H, true>(c3E<S, N>, blk * eo_size<Q>(), col, out);
+    eo_store<Q, 0, H, true, ACC>(out, dst, st);
+  } else if (part == 0) {
+    eo_lines<Q, 0, KA, false>(c3E<S, N>, blk * eo_size<Q>(), col, out);
+    eo_store<Q, 0, KA, false, ACC>(out, dst, st);
+  } else {
+    eo_lines<Q, KA, H - KA, true>(c3E<S, N>, blk * eo_size<Q>(), col, out);
+    eo_store<Q, KA, H - KA, true, ACC>(out, dst, st);
+  }
+}
+
 template <int S, int N>
 cudaError_t h3_upload(const double* D, const double* A, const double* psi) {
-  constexpr int Q = N + 1, NA = S == H3_HEX ? N : N + 1;
+  constexpr int Q = N + 1, NA = S == H3_HEX ? N : N + 1, H = Q / 2, EO = eo_size<Q>();
   cudaError_t e = cudaMemcpyToSymbol(c3D<S, N>, D, sizeof(double) * 3 * Q * Q);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c3A<S, N>, A, sizeof(double) * Q * NA);
   if (e == cudaSuccess && S == H3_PRISM) e = cudaMemcpyToSymbol(c3P<S, N>, psi, sizeof(double) * Q * N);
-  return e;
+  if (e != cudaSuccess) return e;
+  double eo[6 * EO];
+  for (int t = 0; t < 2; ++t)
+    for (int a = 0; a < 3; ++a) {
+      const double* Da = D + a * Q * Q;
+      auto M = [&](int k, int j) { return t == 0 ? Da[k * Q + j] : Da[j * Q + k]; };   // D or D^T
+      double* o = eo + (t * 3 + a) * EO;
+      double scale = 0.0, asym = 0.0;
+      for (int k = 0; k < Q; ++k)
+        for (int j = 0; j < Q; ++j) {
+          scale = fmax(scale, fabs(M(k, j)));
+          asym = fmax(asym, fabs(M(Q - 1 - k, Q - 1 - j) + M(k, j)));
+        }
+      if (asym > 1e-12 * scale) return cudaErrorInvalidValue;   // points not symmetric: no parity split
+      for (int k = 0; k < H; ++k)
+        for (int j = 0; j < H; ++j) {
+          o[k * H + j] = 0.5 * (M(k, j) + M(k, Q - 1 - j));
+          o[H * H + k * H + j] = 0.5 * (M(k, j) - M(k, Q - 1 - j));
+        }
+      for (int k = 0; k < H; ++k) {
+        o[2 * H * H + k] = (Q & 1) ? M(k, H) : 0.0;
+        o[2 * H * H + H + k] = (Q & 1) ? M(H, k) : 0.0;
+      }
+    }
+  return cudaMemcpyToSymbol(c3E<S, N>, eo, sizeof(double) * 6 * EO);
 }
 
 // out[k] = sum_j M[k][j] in[j]  (M row-major K x J in constant memory at compile-time offset)
@@ -253,17 +370,21 @@ constexpr int pencil_split() { return (S != H3_TET && 2 * Q * Q <= nthreads<Q>()
 // axis switch over three unrolled constant-operand contractions makes ptxas spill)
 template <int S, int N, int A>
 __device__ __forceinline__ void pencil_deriv_axis(const double* __restrict__ u, double* __restrict__ du) {
-  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int Q = N + 1, Q2 = Q * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
   constexpr int KP = (Q + 1) / 2;
-  constexpr int st = A == 0 ? Q2 : (A == 1 ? Q : 1);
+  constexpr int st = A == 0 ? SI : (A == 1 ? SJ : 1);
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
     const int r = it % Q2, part = it / Q2;
-    const int base = A == 0 ? r : (A == 1 ? (r / Q) * Q2 + r % Q : r * Q);
+    const int ra = r / Q, rb = r % Q;
+    const int base = A == 0 ? ra * SJ + rb : (A == 1 ? ra * SI + rb : ra * SI + rb * SJ);
     double col[Q], out[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) col[j] = u[base + j * st];
-    double* d = du + A * Q3 + base;
-    if (KS == 1) {
+    double* d = du + A * V3 + base;
+    if (SIPG_H3_EO) {      // even-odd: parts split the mirrored output pairs
+      eo_pencil<S, N, KS, false>(A, part, col, d, st);
+    } else if (KS == 1) {
       cmat_rows<0, Q, Q>(c3D<S, N>, A * Q2, col, out);
 #pragma unroll
       for (int k = 0; k < Q; ++k) d[k * st] = out[k];
@@ -288,17 +409,21 @@ __device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ 
 // T = W0 + sum_a D_a^T W_a, in place into W0 (three passes, one per axis)
 template <int S, int N, int A>
 __device__ __forceinline__ void pencil_dt_axis(double* __restrict__ W0, const double* __restrict__ W) {
-  constexpr int Q = N + 1, Q2 = Q * Q, Q3 = Q2 * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int Q = N + 1, Q2 = Q * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
   constexpr int KP = (Q + 1) / 2;
-  constexpr int st = A == 0 ? Q2 : (A == 1 ? Q : 1);
+  constexpr int st = A == 0 ? SI : (A == 1 ? SJ : 1);
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
     const int r = it % Q2, part = it / Q2;
-    const int base = A == 0 ? r : (A == 1 ? (r / Q) * Q2 + r % Q : r * Q);
+    const int ra = r / Q, rb = r % Q;
+    const int base = A == 0 ? ra * SJ + rb : (A == 1 ? ra * SI + rb : ra * SI + rb * SJ);
     double col[Q], out[Q];
 #pragma unroll
-    for (int j = 0; j < Q; ++j) col[j] = W[A * Q3 + base + j * st];
+    for (int j = 0; j < Q; ++j) col[j] = W[A * V3 + base + j * st];
     double* w0 = W0 + base;
-    if (KS == 1) {
+    if (SIPG_H3_EO) {      // even-odd with the D^T blocks
+      eo_pencil<S, N, KS, true>(3 + A, part, col, w0, st);
+    } else if (KS == 1) {
       cmatT_cols<0, Q, Q, Q>(c3D<S, N>, A * Q2, col, out);
 #pragma unroll
       for (int k = 0; k < Q; ++k) w0[k * st] += out[k];
@@ -327,24 +452,26 @@ __device__ void pencil_dt(double* __restrict__ W0, const double* __restrict__ W)
 template <int S, int N>
 __device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict__ u) {
   constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ;
   constexpr int KP = (Q + 1) / 2;
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
-    const int r = it % Q2, part = it / Q2;
+    const int r0 = it % Q2, part = it / Q2;
+    const int r = (r0 / Q) * SJ + r0 % Q;
     double col[NA], out[Q];
 #pragma unroll
-    for (int g = 0; g < NA; ++g) col[g] = s2[g * Q2 + r];
+    for (int g = 0; g < NA; ++g) col[g] = s2[g * SI + r];
     if (KS == 1) {
       cmat_rows<0, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k = 0; k < Q; ++k) u[k * Q2 + r] = out[k];
+      for (int k = 0; k < Q; ++k) u[k * SI + r] = out[k];
     } else if (part == 0) {
       cmat_rows<0, KP, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k = 0; k < KP; ++k) u[k * Q2 + r] = out[k];
+      for (int k = 0; k < KP; ++k) u[k * SI + r] = out[k];
     } else {
       cmat_rows<KP, Q - KP, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k = 0; k < Q - KP; ++k) u[(KP + k) * Q2 + r] = out[k];
+      for (int k = 0; k < Q - KP; ++k) u[(KP + k) * SI + r] = out[k];
     }
   }
 }
@@ -353,24 +480,26 @@ __device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict
 template <int S, int N>
 __device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restrict__ s2) {
   constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
+  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ;
   constexpr int GP = (NA + 1) / 2;
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
-    const int r = it % Q2, part = it / Q2;
+    const int r0 = it % Q2, part = it / Q2;
+    const int r = (r0 / Q) * SJ + r0 % Q;
     double col[Q], out[NA];
 #pragma unroll
-    for (int k = 0; k < Q; ++k) col[k] = T[k * Q2 + r];
+    for (int k = 0; k < Q; ++k) col[k] = T[k * SI + r];
     if (KS == 1) {
       cmatT_cols<0, NA, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int g = 0; g < NA; ++g) s2[g * Q2 + r] = out[g];
+      for (int g = 0; g < NA; ++g) s2[g * SI + r] = out[g];
     } else if (part == 0) {
       cmatT_cols<0, GP, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int g = 0; g < GP; ++g) s2[g * Q2 + r] = out[g];
+      for (int g = 0; g < GP; ++g) s2[g * SI + r] = out[g];
     } else {
       cmatT_cols<GP, NA - GP, Q, NA>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int g = 0; g < NA - GP; ++g) s2[(GP + g) * Q2 + r] = out[g];
+      for (int g = 0; g < NA - GP; ++g) s2[(GP + g) * SI + r] = out[g];
     }
   }
 }
@@ -400,7 +529,7 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       for (int i = 0; i < N; ++i) col[i] = s1[(i0 * N + i) * Q + k2];
       cmat<Q, N>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k = 0; k < Q; ++k) s2[(i0 * Q + k) * Q + k2] = out[k];
+      for (int k = 0; k < Q; ++k) s2[i0 * C::SI + k * C::SJ + k2] = out[k];
     }
     __syncthreads();
     pencil_stage_a<S, N>(s2, u);
@@ -457,8 +586,8 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         if (kb0 + k >= Q) break;
-        if (S == H3_PRISM) s2[(g * Q + ko) * Q + kb0 + k] = out[k];
-        else s2[(g * Q + kb0 + k) * Q + ko] = out[k];
+        if (S == H3_PRISM) s2[g * C::SI + ko * C::SJ + kb0 + k] = out[k];
+        else s2[g * C::SI + (kb0 + k) * C::SJ + ko] = out[k];
       }
     }
   }
@@ -482,7 +611,7 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
       const int i0 = r / Q, k2 = r % Q;
       double col[Q], out[N];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) col[k] = s2[(i0 * Q + k) * Q + k2];
+      for (int k = 0; k < Q; ++k) col[k] = s2[i0 * C::SI + k * C::SJ + k2];
       cmatT<Q, N>(c3A<S, N>, 0, col, out);
 #pragma unroll
       for (int i = 0; i < N; ++i) s1[(i0 * N + i) * Q + k2] = out[i];
@@ -505,10 +634,10 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     double a = 0.0;
     if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(B[m * Q + k2], s2[(g * Q + k) * Q + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(B[m * Q + k2], s2[g * C::SI + k * C::SJ + k2], a);
     } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(B[m * Q + k1], s2[(g * Q + k1) * Q + k], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(B[m * Q + k1], s2[g * C::SI + k1 * C::SJ + k], a);
     }
     s1[o] = a;
   }
@@ -556,8 +685,8 @@ struct Lay {
     cbuf = sm + C::TABD;                 // [2][NCP]
     c = cbuf;
     u = cbuf + 2 * C::NCP;
-    du = u + C::Q3;
-    F = du + (pub ? 0 : 3 * C::Q3);      // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    du = u + C::V3;
+    F = du + (pub ? 0 : 3 * C::V3);      // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
     hdr = hbuf;
     ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;   // [2][H3_EGEO]: element geometry, double-buffered
@@ -938,9 +1067,9 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         const H3Slot& h = slot_hdr(L.hdr, s);
         const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
         const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
-        const int st_f = fx == 0 ? Q2 : (fx == 1 ? Q : 1);
-        const int st_a = ra == 0 ? Q2 : (ra == 1 ? Q : 1);
-        const int st_b = rb == 0 ? Q2 : (rb == 1 ? Q : 1);
+        const int st_f = fx == 0 ? C::SI : (fx == 1 ? C::SJ : 1);
+        const int st_a = ra == 0 ? C::SI : (ra == 1 ? C::SJ : 1);
+        const int st_b = rb == 0 ? C::SI : (rb == 1 ? C::SJ : 1);
         const double* E = Et + (fx * 2 + (sd > 0)) * Q;
         const double* ED = EDt + (fx * 2 + (sd > 0)) * Q;
         const int base = (a / Q) * st_a + (a % Q) * st_b;
@@ -1012,20 +1141,21 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     {
       const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
       const double lam = P.lam;
-      for (int o = t; o < Q3; o += NT) {
-        const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+      for (int o0 = t; o0 < Q3; o0 += NT) {
+        const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
+        const int o = k0 * C::SI + k1 * C::SJ + k2;
         const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
                                     *(Rt + 2 * Q + k2));
         const double jw = dJ * Wr[k0] * Wr[Q + k1 * Q + k2];
-        const double d0 = L.du[o], d1 = L.du[Q3 + o], d2 = L.du[2 * Q3 + o];
+        const double d0 = L.du[o], d1 = L.du[C::V3 + o], d2 = L.du[2 * C::V3 + o];
         const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
         const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
         const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
         L.u[o] *= lam * jw;
         L.du[o] = jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
-        L.du[Q3 + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
-        L.du[2 * Q3 + o] = jw * f2;
+        L.du[C::V3 + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
+        L.du[2 * C::V3 + o] = jw * f2;
       }
     }
     __syncthreads();
@@ -1115,8 +1245,9 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
           Fs[j] = L.F + sj * 2 * Q2;
           Gs[j] = L.tb + j * 4 * TMAX;
         }
-        for (int o = t; o < Q3; o += NT) {
-          const int k0 = o / Q2, k1 = (o / Q) % Q, k2 = o % Q;
+        for (int o0 = t; o0 < Q3; o0 += NT) {
+          const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
+          const int o = k0 * C::SI + k1 * C::SJ + k2;
           double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
           for (int j = 0; j < C::SB; ++j) {
@@ -1132,8 +1263,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
           }
           L.u[o] += w0;
           L.du[o] += w1;
-          L.du[Q3 + o] += w2;
-          L.du[2 * Q3 + o] += w3;
+          L.du[C::V3 + o] += w2;
+          L.du[2 * C::V3 + o] += w3;
         }
       }
       __syncthreads();

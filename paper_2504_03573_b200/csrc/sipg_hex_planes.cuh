@@ -183,13 +183,17 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
 #ifndef SIPG_SF_RANGE
 #define SIPG_SF_RANGE 3
 #endif
+// 0: every shared face takes the runtime-size variant (one copy of the code: instruction cache)
+#ifndef SIPG_SF_COMPILED
+#define SIPG_SF_COMPILED 1
+#endif
 // compile-time dispatch over the neighbour order NO in [LO, HI] (trace size max(Q, NO + 1),
 // the GLL / GLL case F_FAST_SHARED covers); anything else takes the runtime-size variant
 template <int N, int Q, int LO, int HI, class SC>
 __device__ __forceinline__ void sf_dispatch(const int no, const int qt, const int t, const int f, const FaceRec& r,
                                             const int64_t e01, const double* pl, const double* T,
                                             const double* OWN, double* FVD, const SC sc) {
-  if constexpr (LO > HI) {
+  if constexpr (LO > HI || !SIPG_SF_COMPILED) {
     shared_face<N, Q, 0, 0>(no, qt, t, f, r, e01, pl, T, OWN, FVD, sc);
   } else {
     constexpr int QTV = Q > LO + 1 ? Q : LO + 1;
