@@ -65,11 +65,18 @@ struct H3Plan {
 
 namespace h3 {
 
-#ifndef SIPG_H3_PAD
-#define SIPG_H3_PAD 1
+// padded volume layout per kernel kind (measured: the publish kernels gain, the apply kernels lose
+// the occupancy the larger arrays cost)
+#ifndef SIPG_H3_PAD_PUB
+#define SIPG_H3_PAD_PUB 1
 #endif
-template <int Q>
-constexpr int H3_SJ() { return (SIPG_H3_PAD && !(Q & 1)) ? Q + 1 : Q; }
+#ifndef SIPG_H3_PAD_APPLY
+#define SIPG_H3_PAD_APPLY 0
+#endif
+template <bool PUB>
+constexpr bool h3_pad() { return PUB ? SIPG_H3_PAD_PUB : SIPG_H3_PAD_APPLY; }
+template <int Q, bool PD>
+constexpr int H3_SJ() { return (PD && !(Q & 1)) ? Q + 1 : Q; }
 
 // threads per CTA: 256 for q >= 8 (512 volume points), else 128
 template <int Q>
@@ -82,13 +89,16 @@ struct Cfg {
   // padded volume layout (k0, k1, k2) -> k0 SI + k1 SJ + k2: odd row stride, so the pencils along
   // every axis hit distinct shared-memory banks (ncu: the h3 kernels are bound by the LSU data pipe,
   // a quarter to a third of whose wavefronts were bank-conflict replays with the dense layout)
-  static constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
+  template <bool PD>
+  static constexpr int sj() { return H3_SJ<Q, PD>(); }
+  template <bool PD>
+  static constexpr int v3() { return Q * Q * H3_SJ<Q, PD>(); }
   static constexpr int NTRI = N * (N + 1) / 2;
   static constexpr int NG = N + 1;                                   // triangle direction-1 groups
   static constexpr int NPM = NTRI + (S == H3_TET ? 1 : 0);           // + tet apex pseudo-mode
   static constexpr int NC = S == H3_HEX ? N * N * N : (S == H3_PRISM ? N * NTRI : N * (N + 1) * (N + 2) / 6);
   static constexpr int S1 = S == H3_HEX ? N * N * Q : NPM * Q;
-  static constexpr int S2 = S == H3_HEX ? N * SI : NG * SI;
+  static constexpr int S2 = (S == H3_HEX ? N : NG) * Q * H3_SJ<Q, true>();   // sized for the padded layout
   static constexpr int NCP = (NC + 1) & ~1;
   static constexpr int NI = 4 * NPM + 4 + NC + 16;                   // int tables + batch offsets
   static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);   // slots per element
@@ -106,7 +116,8 @@ struct Cfg {
   // the current one computes
   // the publish kernel has no derivative arrays (3 Q^3 doubles less: more CTAs per SM)
   static constexpr int doubles(bool pub) {
-    return TABD + 2 * NCP + (pub ? 1 : 4) * V3 + NSMAX * (2 * Q2 + 2 * SLOTD) + 2 * H3_EGEO + SCR;
+    return TABD + 2 * NCP + (pub ? v3<h3_pad<true>()>() : 4 * v3<h3_pad<false>()>()) + NSMAX * (2 * Q2 + 2 * SLOTD) +
+           2 * H3_EGEO + SCR;
   }
   static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
 };
@@ -368,10 +379,10 @@ constexpr int pencil_split() { return (S != H3_TET && 2 * Q * Q <= nthreads<Q>()
 
 // du_a = D_a u along each eta axis: Q^2 pencils per axis (one compile-time axis per loop: a runtime
 // axis switch over three unrolled constant-operand contractions makes ptxas spill)
-template <int S, int N, int A>
+template <int S, int N, int A, bool PD>
 __device__ __forceinline__ void pencil_deriv_axis(const double* __restrict__ u, double* __restrict__ du) {
   constexpr int Q = N + 1, Q2 = Q * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
-  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
+  constexpr int SJ = H3_SJ<Q, PD>(), SI = Q * SJ, V3 = Q * SI;
   constexpr int KP = (Q + 1) / 2;
   constexpr int st = A == 0 ? SI : (A == 1 ? SJ : 1);
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
@@ -399,18 +410,18 @@ __device__ __forceinline__ void pencil_deriv_axis(const double* __restrict__ u, 
     }
   }
 }
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void pencil_deriv(const double* __restrict__ u, double* __restrict__ du) {
-  pencil_deriv_axis<S, N, 0>(u, du);
-  pencil_deriv_axis<S, N, 1>(u, du);
-  pencil_deriv_axis<S, N, 2>(u, du);
+  pencil_deriv_axis<S, N, 0, PD>(u, du);
+  pencil_deriv_axis<S, N, 1, PD>(u, du);
+  pencil_deriv_axis<S, N, 2, PD>(u, du);
 }
 
 // T = W0 + sum_a D_a^T W_a, in place into W0 (three passes, one per axis)
-template <int S, int N, int A>
+template <int S, int N, int A, bool PD>
 __device__ __forceinline__ void pencil_dt_axis(double* __restrict__ W0, const double* __restrict__ W) {
   constexpr int Q = N + 1, Q2 = Q * Q, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
-  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ, V3 = Q * SI;
+  constexpr int SJ = H3_SJ<Q, PD>(), SI = Q * SJ, V3 = Q * SI;
   constexpr int KP = (Q + 1) / 2;
   constexpr int st = A == 0 ? SI : (A == 1 ? SJ : 1);
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
@@ -438,21 +449,21 @@ __device__ __forceinline__ void pencil_dt_axis(double* __restrict__ W0, const do
     }
   }
 }
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void pencil_dt(double* __restrict__ W0, const double* __restrict__ W) {
-  pencil_dt_axis<S, N, 0>(W0, W);
+  pencil_dt_axis<S, N, 0, PD>(W0, W);
   __syncthreads();
-  pencil_dt_axis<S, N, 1>(W0, W);
+  pencil_dt_axis<S, N, 1, PD>(W0, W);
   __syncthreads();
-  pencil_dt_axis<S, N, 2>(W0, W);
+  pencil_dt_axis<S, N, 2, PD>(W0, W);
   __syncthreads();
 }
 
 // u[k0][k12] = sum_g A[k0][g] s2[g][k12]   (outermost BwdTrans stage, all shapes)
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict__ u) {
   constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
-  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ;
+  constexpr int SJ = H3_SJ<Q, PD>(), SI = Q * SJ;
   constexpr int KP = (Q + 1) / 2;
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
     const int r0 = it % Q2, part = it / Q2;
@@ -477,10 +488,10 @@ __device__ void pencil_stage_a(const double* __restrict__ s2, double* __restrict
 }
 
 // s2[g][k12] = sum_k0 A[k0][g] T[k0][k12]   (its transpose)
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restrict__ s2) {
   constexpr int Q = N + 1, Q2 = Q * Q, NA = S == H3_HEX ? N : N + 1, NT = nthreads<Q>(), KS = pencil_split<S, Q>();
-  constexpr int SJ = H3_SJ<Q>(), SI = Q * SJ;
+  constexpr int SJ = H3_SJ<Q, PD>(), SI = Q * SJ;
   constexpr int GP = (NA + 1) / 2;
   for (int it = threadIdx.x; it < KS * Q2; it += NT) {
     const int r0 = it % Q2, part = it / Q2;
@@ -505,7 +516,7 @@ __device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restric
 }
 
 // u = Phi c on the q^3 grid (generalised tensor product; stages as plan3d.ClassTables3 tables)
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double* s1, double* s2,
                     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                     const int* gstart, const int* gmem, const int* coff) {
@@ -529,10 +540,10 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       for (int i = 0; i < N; ++i) col[i] = s1[(i0 * N + i) * Q + k2];
       cmat<Q, N>(c3A<S, N>, 0, col, out);
 #pragma unroll
-      for (int k = 0; k < Q; ++k) s2[i0 * C::SI + k * C::SJ + k2] = out[k];
+      for (int k = 0; k < Q; ++k) s2[i0 * C::template sj<PD>() * Q + k * C::template sj<PD>() + k2] = out[k];
     }
     __syncthreads();
-    pencil_stage_a<S, N>(s2, u);
+    pencil_stage_a<S, N, PD>(s2, u);
     __syncthreads();
     return;
   }
@@ -586,18 +597,18 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         if (kb0 + k >= Q) break;
-        if (S == H3_PRISM) s2[g * C::SI + ko * C::SJ + kb0 + k] = out[k];
-        else s2[g * C::SI + (kb0 + k) * C::SJ + ko] = out[k];
+        if (S == H3_PRISM) s2[g * C::template sj<PD>() * Q + ko * C::template sj<PD>() + kb0 + k] = out[k];
+        else s2[g * C::template sj<PD>() * Q + (kb0 + k) * C::template sj<PD>() + ko] = out[k];
       }
     }
   }
   __syncthreads();
-  pencil_stage_a<S, N>(s2, u);
+  pencil_stage_a<S, N, PD>(s2, u);
   __syncthreads();
 }
 
 // y = Phi^T T (transposed stages), written to global
-template <int S, int N>
+template <int S, int N, bool PD>
 __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, double* s1, double* s2,
                       const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                       const int* gof, const int* mofr) {
@@ -605,13 +616,13 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
   constexpr int Q = C::Q, NT = nthreads<Q>();
   const int t = threadIdx.x;
   if (S == H3_HEX) {
-    pencil_stage_a_t<S, N>(T, s2);             // k0 -> i0
+    pencil_stage_a_t<S, N, PD>(T, s2);             // k0 -> i0
     __syncthreads();
     for (int r = t; r < N * Q; r += NT) {        // (i0, k2) pencils: k1 -> i1
       const int i0 = r / Q, k2 = r % Q;
       double col[Q], out[N];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) col[k] = s2[i0 * C::SI + k * C::SJ + k2];
+      for (int k = 0; k < Q; ++k) col[k] = s2[i0 * C::template sj<PD>() * Q + k * C::template sj<PD>() + k2];
       cmatT<Q, N>(c3A<S, N>, 0, col, out);
 #pragma unroll
       for (int i = 0; i < N; ++i) s1[(i0 * N + i) * Q + k2] = out[i];
@@ -627,17 +638,17 @@ __device__ void bwd_t(const double* __restrict__ T, double* __restrict__ y, doub
     }
     return;
   }
-  pencil_stage_a_t<S, N>(T, s2);
+  pencil_stage_a_t<S, N, PD>(T, s2);
   __syncthreads();
   for (int o = t; o < C::NPM * Q; o += NT) {
     const int k = o % Q, m = o / Q, g = gof[m];
     double a = 0.0;
     if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a = fma(B[m * Q + k2], s2[g * C::SI + k * C::SJ + k2], a);
+      for (int k2 = 0; k2 < Q; ++k2) a = fma(B[m * Q + k2], s2[g * C::template sj<PD>() * Q + k * C::template sj<PD>() + k2], a);
     } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
 #pragma unroll
-      for (int k1 = 0; k1 < Q; ++k1) a = fma(B[m * Q + k1], s2[g * C::SI + k1 * C::SJ + k], a);
+      for (int k1 = 0; k1 < Q; ++k1) a = fma(B[m * Q + k1], s2[g * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k], a);
     }
     s1[o] = a;
   }
@@ -685,8 +696,8 @@ struct Lay {
     cbuf = sm + C::TABD;                 // [2][NCP]
     c = cbuf;
     u = cbuf + 2 * C::NCP;
-    du = u + C::V3;
-    F = du + (pub ? 0 : 3 * C::V3);      // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    du = u + (pub ? C::template v3<h3_pad<true>()>() : C::template v3<h3_pad<false>()>());
+    F = du + (pub ? 0 : 3 * C::template v3<h3_pad<false>()>());   // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
     hdr = hbuf;
     ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;   // [2][H3_EGEO]: element geometry, double-buffered
@@ -986,6 +997,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
+  constexpr bool PD = h3_pad<PUB>();   // volume layout of this kernel kind
   extern __shared__ double sm[];
   Lay<S, N> L(sm, PUB);
   const int t = threadIdx.x;
@@ -1058,7 +1070,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     ns_n = ns_nn;
     e_n = e_nn;
     scalars(i + 2 * G, e_nn, dof_nn, sb_nn, ns_nn);
-    bwd<S, N>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
+    bwd<S, N, PD>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
     if (PUB) {
       // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
       // d/d eta_fixed (E D), collocation on the face grid for the two tangential derivatives
@@ -1067,9 +1079,9 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         const H3Slot& h = slot_hdr(L.hdr, s);
         const int fx = c_faces[S][h.face][0], sd = c_faces[S][h.face][1];
         const int ra = c_faces[S][h.face][2], rb = c_faces[S][h.face][3];
-        const int st_f = fx == 0 ? C::SI : (fx == 1 ? C::SJ : 1);
-        const int st_a = ra == 0 ? C::SI : (ra == 1 ? C::SJ : 1);
-        const int st_b = rb == 0 ? C::SI : (rb == 1 ? C::SJ : 1);
+        const int st_f = fx == 0 ? C::template sj<PD>() * Q : (fx == 1 ? C::template sj<PD>() : 1);
+        const int st_a = ra == 0 ? C::template sj<PD>() * Q : (ra == 1 ? C::template sj<PD>() : 1);
+        const int st_b = rb == 0 ? C::template sj<PD>() * Q : (rb == 1 ? C::template sj<PD>() : 1);
         const double* E = Et + (fx * 2 + (sd > 0)) * Q;
         const double* ED = EDt + (fx * 2 + (sd > 0)) * Q;
         const int base = (a / Q) * st_a + (a % Q) * st_b;
@@ -1135,7 +1147,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
       __pipeline_commit();
     }
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
-    pencil_deriv<S, N>(L.u, L.du);
+    pencil_deriv<S, N, PD>(L.u, L.du);
     __syncthreads();
     // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du)
     {
@@ -1143,19 +1155,19 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
       const double lam = P.lam;
       for (int o0 = t; o0 < Q3; o0 += NT) {
         const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
-        const int o = k0 * C::SI + k1 * C::SJ + k2;
+        const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
         const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
                                     *(Rt + 2 * Q + k2));
         const double jw = dJ * Wr[k0] * Wr[Q + k1 * Q + k2];
-        const double d0 = L.du[o], d1 = L.du[C::V3 + o], d2 = L.du[2 * C::V3 + o];
+        const double d0 = L.du[o], d1 = L.du[C::template v3<PD>() + o], d2 = L.du[2 * C::template v3<PD>() + o];
         const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
         const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
         const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
         L.u[o] *= lam * jw;
         L.du[o] = jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
-        L.du[C::V3 + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
-        L.du[2 * C::V3 + o] = jw * f2;
+        L.du[C::template v3<PD>() + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
+        L.du[2 * C::template v3<PD>() + o] = jw * f2;
       }
     }
     __syncthreads();
@@ -1247,7 +1259,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         }
         for (int o0 = t; o0 < Q3; o0 += NT) {
           const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
-          const int o = k0 * C::SI + k1 * C::SJ + k2;
+          const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
           double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
 #pragma unroll
           for (int j = 0; j < C::SB; ++j) {
@@ -1263,15 +1275,15 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
           }
           L.u[o] += w0;
           L.du[o] += w1;
-          L.du[C::V3 + o] += w2;
-          L.du[2 * C::V3 + o] += w3;
+          L.du[C::template v3<PD>() + o] += w2;
+          L.du[2 * C::template v3<PD>() + o] += w3;
         }
       }
       __syncthreads();
     }
     // T = W0 + sum_k D_k^T W_k  (in place)
-    pencil_dt<S, N>(L.u, L.du);
-    bwd_t<S, N>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
+    pencil_dt<S, N, PD>(L.u, L.du);
+    bwd_t<S, N, PD>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
     __syncthreads();
   }
 }
