@@ -34,6 +34,9 @@
 #ifndef SIPG_H3_EO
 #define SIPG_H3_EO 1                // even-odd factorised PhysDeriv / PhysDeriv^T pencils
 #endif
+#ifndef SIPG_H3_FUSE_LIFT
+#define SIPG_H3_FUSE_LIFT 0         // first slot batch: flux before PhysDeriv, its lift in the volume-term pass
+#endif
 
 enum { H3_HEX = 0, H3_PRISM = 1, H3_TET = 2 };
 #define CD3_WORDS 16
@@ -1146,14 +1149,121 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
       }
       __pipeline_commit();
     }
+    // SIP flux at the trace points of the slots [b0, b0 + nb) (sipg.py:622-650, 663-677) from the
+    // published own and partner traces (the publish kernel evaluated both; boundary: jump 2u,
+    // average g), then the transposed maps onto the own face grids: fv / fd in F, (G n)_k fd in the
+    // trace scratch.  Needs only the trace scratch, so the first batch runs right after BwdTrans
+    // and its lift rides on the volume-term pass below (SIPG_H3_FUSE_LIFT).
+    auto face_batch = [&](const int b0, const int nb) {
+        // SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and partner
+        // traces (the publish kernel evaluated both); boundary: jump 2u, average g
+        {
+          auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
+          const Batch BF(b0, nb, cnt);
+          constexpr int PER = (C::SB * TMAX + NT - 1) / NT;   // flux items per thread
+          double fvr[PER], fdr[PER];
+          constexpr bool PF = SIPG_H3_PREFETCH_TRACES;
+          if (PF && b0 == 0) {
+            __pipeline_wait_prior(0);                         // the prefetched first batch
+            __syncthreads();
+          }
+  #pragma unroll
+          for (int k = 0; k < PER; ++k) {
+            const int it0 = t + k * NT;
+            if (it0 >= BF.tot) break;
+            int p = it0;
+            const int s = BF.slot(p);
+            const H3Slot& h = slot_hdr(L.hdr, s);
+            double ut, gt, un, gn;
+            if (PF && b0 == 0) {
+              const double* tv = L.tb + s * 4 * TMAX;
+              ut = tv[2 * p];
+              gt = tv[2 * p + 1];
+              un = tv[2 * TMAX + 2 * p];
+              gn = tv[2 * TMAX + 2 * p + 1];
+            } else {
+              const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+              ut = own.x;
+              gt = own.y;
+              if (h.kind) {
+                const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+                un = nbv.x;
+                gn = nbv.y;
+              }
+            }
+            if (!h.kind) {
+              un = -ut;
+              gn = -gt;
+            }
+            const double j = ut - un, cc = 0.5 * (gt - gn);
+            const double w = h.sJ * __ldg(P.tab + h.wtoff + p);
+            fvr[k] = (h.tau * j - cc) * w;
+            fdr[k] = -0.5 * j * w;
+          }
+          if (PF && b0 == 0) __syncthreads();   // the flux overwrites the prefetched traces
+  #pragma unroll
+          for (int k = 0; k < PER; ++k) {
+            const int it0 = t + k * NT;
+            if (it0 >= BF.tot) break;
+            int p = it0;
+            const int s = BF.slot(p);
+            double* tv = L.tb + (s - b0) * 4 * TMAX;
+            tv[p] = fvr[k];
+            tv[TMAX + p] = fdr[k];
+          }
+        }
+        __syncthreads();
+        map_transpose<S, Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, pts, Rt);
+    };
+    // the lift of a batch's faces at one volume point: the transposed endpoint rows of fv and of the
+    // (G n)_k fd arrays (the reference's scatter + final sweep)
+    // a batch's face geometry packed into registers: per slot 3 bits (fixed axis * 2 + side)
+    struct Lift {
+      int pack, nb, b0;
+    };
+    auto lift_setup = [&](Lift& lf, const int b0, const int nb) {
+      lf.nb = nb;
+      lf.b0 = b0;
+      lf.pack = 0;
+#pragma unroll
+      for (int j = 0; j < C::SB; ++j) {
+        const int face = slot_hdr(L.hdr, j < nb ? b0 + j : b0).face;
+        lf.pack |= (c_faces[S][face][0] * 2 + (c_faces[S][face][1] > 0)) << (3 * j);
+      }
+    };
+    auto lift_at = [&](const Lift& lf, int k0, int k1, int k2, double& w0, double& w1, double& w2, double& w3) {
+#pragma unroll
+      for (int j = 0; j < C::SB; ++j) {
+        if (j >= lf.nb) break;
+        const int code = (lf.pack >> (3 * j)) & 7, fx = code >> 1;
+        const int kf = fx == 0 ? k0 : (fx == 1 ? k1 : k2);
+        const int a = fx == 0 ? k1 * Q + k2 : (fx == 1 ? k0 * Q + k2 : k0 * Q + k1);
+        const double ek = Et[code * Q + kf];
+        if (S != H3_TET && ek == 0.0) continue;   // GLL endpoint rows are one-hot
+        const double* Fs = L.F + (lf.b0 + j) * 2 * Q2;
+        const double* Gs = L.tb + j * 4 * TMAX;
+        w0 = fma(ek, Fs[a], w0);
+        w1 = fma(ek, Gs[a], w1);
+        w2 = fma(ek, Gs[Q2 + a], w2);
+        w3 = fma(ek, Gs[2 * Q2 + a], w3);
+      }
+    };
+    constexpr bool FUSE = SIPG_H3_FUSE_LIFT;
+    const int nb0 = ns < C::SB ? ns : C::SB;
+    if (FUSE && nb0 > 0) face_batch(0, nb0);
     // PhysDeriv: collocation along each eta axis (stdregions.py:658-674)
     pencil_deriv<S, N, PD>(L.u, L.du);
     __syncthreads();
-    // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du)
+    // volume terms (sipg.py:575-582), in place: W0 = lambda jw u (u), W_k = jw (G G^T grad u)_k (du),
+    // plus the first face batch's lift
     {
-      const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
+      Lift lf0;
+      lift_setup(lf0, 0, FUSE ? nb0 : 0);
       const double lam = P.lam;
       for (int o0 = t; o0 < Q3; o0 += NT) {
+        // the metric from shared memory inside the loop (broadcast reads): with the fused lift the
+        // loop would otherwise spill
+        const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
         const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
         const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
         const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
@@ -1164,115 +1274,26 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
         const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
         const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
-        L.u[o] *= lam * jw;
-        L.du[o] = jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
-        L.du[C::template v3<PD>() + o] = jw * (ch.c11 * f1 + ch.c12 * f2);
-        L.du[2 * C::template v3<PD>() + o] = jw * f2;
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+        if (FUSE) lift_at(lf0, k0, k1, k2, w0, w1, w2, w3);
+        L.u[o] = fma(lam * jw, L.u[o], w0);
+        L.du[o] = fma(jw, ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2, w1);
+        L.du[C::template v3<PD>() + o] = fma(jw, ch.c11 * f1 + ch.c12 * f2, w2);
+        L.du[2 * C::template v3<PD>() + o] = fma(jw, f2, w3);
       }
     }
     __syncthreads();
-    for (int b0 = 0; b0 < ns; b0 += C::SB) {
+    for (int b0 = FUSE ? C::SB : 0; b0 < ns; b0 += C::SB) {
       const int nb = min(C::SB, ns - b0);
-      // SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and partner
-      // traces (the publish kernel evaluated both); boundary: jump 2u, average g
+      face_batch(b0, nb);
       {
-        auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
-        const Batch BF(b0, nb, cnt);
-        constexpr int PER = (C::SB * TMAX + NT - 1) / NT;   // flux items per thread
-        double fvr[PER], fdr[PER];
-        constexpr bool PF = SIPG_H3_PREFETCH_TRACES;
-        if (PF && b0 == 0) {
-          __pipeline_wait_prior(0);                         // the prefetched first batch
-          __syncthreads();
-        }
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int it0 = t + k * NT;
-          if (it0 >= BF.tot) break;
-          int p = it0;
-          const int s = BF.slot(p);
-          const H3Slot& h = slot_hdr(L.hdr, s);
-          double ut, gt, un, gn;
-          if (PF && b0 == 0) {
-            const double* tv = L.tb + s * 4 * TMAX;
-            ut = tv[2 * p];
-            gt = tv[2 * p + 1];
-            un = tv[2 * TMAX + 2 * p];
-            gn = tv[2 * TMAX + 2 * p + 1];
-          } else {
-            const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
-            ut = own.x;
-            gt = own.y;
-            if (h.kind) {
-              const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
-              un = nbv.x;
-              gn = nbv.y;
-            }
-          }
-          if (!h.kind) {
-            un = -ut;
-            gn = -gt;
-          }
-          const double j = ut - un, cc = 0.5 * (gt - gn);
-          const double w = h.sJ * __ldg(P.tab + h.wtoff + p);
-          fvr[k] = (h.tau * j - cc) * w;
-          fdr[k] = -0.5 * j * w;
-        }
-        if (PF && b0 == 0) __syncthreads();   // the flux overwrites the prefetched traces
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int it0 = t + k * NT;
-          if (it0 >= BF.tot) break;
-          int p = it0;
-          const int s = BF.slot(p);
-          double* tv = L.tb + (s - b0) * 4 * TMAX;
-          tv[p] = fvr[k];
-          tv[TMAX + p] = fdr[k];
-        }
-      }
-      __syncthreads();
-      map_transpose<S, Q>(L.hdr, L.F, L.tb, b0, nb, P.tab, pts, Rt);
-      // transposed endpoint rows into the volume accumulators (the reference's scatter + final sweep):
-      // per owned volume point, the contributions of the batch's faces (fv and the precomputed
-      // (G n)_k fd on the face grid) through their endpoint rows; the slot decode is hoisted into
-      // registers (the batch has at most SB = 4 slots)
-      {
-        // per slot: kf = k . mk (one-hot on the fixed axis), a = k . ma (face-grid index)
-        int mk0[C::SB], mk1[C::SB], mk2[C::SB], ma0[C::SB], ma1[C::SB], ma2[C::SB];
-        const double* Es[C::SB];
-        const double* Fs[C::SB];
-        const double* Gs[C::SB];
-#pragma unroll
-        for (int j = 0; j < C::SB; ++j) {
-          const int sj = j < nb ? b0 + j : b0;
-          const int face = slot_hdr(L.hdr, sj).face;
-          const int fx = c_faces[S][face][0];
-          mk0[j] = fx == 0;
-          mk1[j] = fx == 1;
-          mk2[j] = fx == 2;
-          ma0[j] = fx == 0 ? 0 : Q;
-          ma1[j] = fx == 0 ? Q : (fx == 1 ? 0 : 1);
-          ma2[j] = fx == 2 ? 0 : 1;
-          Es[j] = Et + (fx * 2 + (c_faces[S][face][1] > 0)) * Q;
-          Fs[j] = L.F + sj * 2 * Q2;
-          Gs[j] = L.tb + j * 4 * TMAX;
-        }
+        Lift lf;
+        lift_setup(lf, b0, nb);
         for (int o0 = t; o0 < Q3; o0 += NT) {
           const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
           const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
           double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-#pragma unroll
-          for (int j = 0; j < C::SB; ++j) {
-            if (j >= nb) break;
-            const int kf = k0 * mk0[j] + k1 * mk1[j] + k2 * mk2[j];
-            const int a = k0 * ma0[j] + k1 * ma1[j] + k2 * ma2[j];
-            const double ek = Es[j][kf];
-            if (S != H3_TET && ek == 0.0) continue;   // GLL endpoint rows are one-hot
-            w0 = fma(ek, Fs[j][a], w0);
-            w1 = fma(ek, Gs[j][a], w1);
-            w2 = fma(ek, Gs[j][Q2 + a], w2);
-            w3 = fma(ek, Gs[j][2 * Q2 + a], w3);
-          }
+          lift_at(lf, k0, k1, k2, w0, w1, w2, w3);
           L.u[o] += w0;
           L.du[o] += w1;
           L.du[C::template v3<PD>() + o] += w2;
