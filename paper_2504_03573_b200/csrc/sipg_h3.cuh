@@ -74,10 +74,10 @@ namespace h3 {
 #define SIPG_H3_PAD_PUB 1
 #endif
 #ifndef SIPG_H3_PAD_APPLY
-#define SIPG_H3_PAD_APPLY (1 << 8)  // bit q set: the apply kernels of q pad (q = 8: the extra 2 KB keep 6 CTAs/SM)
+#define SIPG_H3_PAD_APPLY 0
 #endif
-template <bool PUB, int Q>
-constexpr bool h3_pad() { return PUB ? SIPG_H3_PAD_PUB : ((SIPG_H3_PAD_APPLY >> Q) & 1) != 0; }
+template <bool PUB>
+constexpr bool h3_pad() { return PUB ? SIPG_H3_PAD_PUB : SIPG_H3_PAD_APPLY; }
 template <int Q, bool PD>
 constexpr int H3_SJ() { return (PD && !(Q & 1)) ? Q + 1 : Q; }
 
@@ -113,16 +113,14 @@ struct Cfg {
   static constexpr int TC = S == H3_HEX ? 0 : (S == H3_PRISM ? Q * N : NC * Q);
   // small 1-D tables + the ragged triangle-group rows B (and the tet C rows) in shared memory;
   // A / D / prism psi are __constant__ (register pencils)
-  // pts, R, E, ED, B rows [, D, W: publish kernels only; the apply reads W through L1 and D from
-  // __constant__]; even: 16-B cp.async after it; tet C rows: global (L1)
-  static constexpr int tabd(bool pub) { return (6 * Q + 12 * Q + TB + (pub ? 3 * Q2 + Q + Q2 : 0) + 1) & ~1; }
+  static constexpr int TABD = (6 * Q + 3 * Q2 + (Q + Q2) + 12 * Q + TB + 1) & ~1;   // even: 16-B cp.async after it; tet C rows: global (L1)
   static constexpr int SCR = (S1 + S2) > SB * 4 * TMAX ? (S1 + S2) : SB * 4 * TMAX;   // BwdTrans | traces
   // coefficients and slot headers are double-buffered: the next element's arrive (cp.async) while
   // the current one computes
   // the publish kernel has no derivative arrays (3 Q^3 doubles less: more CTAs per SM)
   static constexpr int doubles(bool pub) {
-    return tabd(pub) + 2 * NCP + (pub ? v3<h3_pad<true, Q>()>() : 4 * v3<h3_pad<false, Q>()>()) +
-           NSMAX * (2 * Q2 + 2 * SLOTD) + 2 * H3_EGEO + SCR;
+    return TABD + 2 * NCP + (pub ? v3<h3_pad<true>()>() : 4 * v3<h3_pad<false>()>()) + NSMAX * (2 * Q2 + 2 * SLOTD) +
+           2 * H3_EGEO + SCR;
   }
   static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
 };
@@ -692,17 +690,17 @@ struct Lay {
     constexpr int Q = C::Q, Q2 = C::Q2;
     pts = sm;
     R = pts + 3 * Q;
-    E = R + 3 * Q;
+    D = R + 3 * Q;
+    W = D + 3 * Q2;          // w0 (Q) then w1 w2 Duffy (Q2)
+    E = W + Q + Q2;
     ED = E + 6 * Q;
     B = ED + 6 * Q;
-    D = B + C::TB;           // publish only
-    W = D + 3 * Q2;          // publish only: w0 (Q) then w1 w2 Duffy (Q2)
-    Ct = nullptr;
-    cbuf = sm + C::tabd(pub);            // [2][NCP]
+    Ct = B + C::TB;
+    cbuf = sm + C::TABD;                 // [2][NCP]
     c = cbuf;
     u = cbuf + 2 * C::NCP;
-    du = u + (pub ? C::template v3<h3_pad<true, Q>()>() : C::template v3<h3_pad<false, Q>()>());
-    F = du + (pub ? 0 : 3 * C::template v3<h3_pad<false, Q>()>());   // [NSMAX][2][Q2]: own-face-grid arrays per slot
+    du = u + (pub ? C::template v3<h3_pad<true>()>() : C::template v3<h3_pad<false>()>());
+    F = du + (pub ? 0 : 3 * C::template v3<h3_pad<false>()>());   // [NSMAX][2][Q2]: own-face-grid arrays per slot
     hbuf = F + C::NSMAX * 2 * C::Q2;     // [2][NSMAX][12]: slot headers
     hdr = hbuf;
     ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;   // [2][H3_EGEO]: element geometry, double-buffered
@@ -1002,7 +1000,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
                                                           double* __restrict__ y) {
   using C = Cfg<S, N>;
   constexpr int Q = C::Q, Q2 = C::Q2, Q3 = C::Q3, NT = nthreads<Q>();
-  constexpr bool PD = h3_pad<PUB, N + 1>();   // volume layout of this kernel kind
+  constexpr bool PD = h3_pad<PUB>();   // volume layout of this kernel kind
   extern __shared__ double sm[];
   Lay<S, N> L(sm, PUB);
   const int t = threadIdx.x;
@@ -1015,10 +1013,8 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     };
     cp(L.pts, CD3_T_PTS, 3 * Q);
     cp(L.R, CD3_T_R, 3 * Q);
-    if (PUB) {
-      cp(L.D, CD3_T_D, 3 * Q2);
-      cp(L.W, CD3_T_W, Q + Q2);
-    }
+    cp(L.D, CD3_T_D, 3 * Q2);
+    cp(L.W, CD3_T_W, Q + Q2);
     cp(L.E, CD3_T_E, 6 * Q);
     cp(L.ED, CD3_T_ED, 6 * Q);
     if (S != H3_HEX) cp(L.B, CD3_T_B, C::TB);
@@ -1026,7 +1022,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
   const double* pts = L.pts;
   const double* Rt = L.R;
   const double* Dt = L.D;
-  const double* Wr = PUB ? L.W : P.tab + cd[CD3_T_W];   // apply: read through L1
+  const double* Wr = L.W;
   const double* Et = L.E;
   const double* EDt = L.ED;
   const double* At = P.tab + cd[CD3_T_A];
@@ -1272,7 +1268,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
         const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
                                     *(Rt + 2 * Q + k2));
-        const double jw = dJ * __ldg(Wr + k0) * __ldg(Wr + Q + k1 * Q + k2);
+        const double jw = dJ * Wr[k0] * Wr[Q + k1 * Q + k2];
         const double d0 = L.du[o], d1 = L.du[C::template v3<PD>() + o], d2 = L.du[2 * C::template v3<PD>() + o];
         const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
         const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
