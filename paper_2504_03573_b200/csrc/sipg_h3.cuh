@@ -25,8 +25,8 @@
 
 #define SIPG_H3_ABI_VERSION 1
 // build knobs (measured variants; the defaults are the fastest measured)
-#ifndef SIPG_H3_PREFETCH_TRACES
-#define SIPG_H3_PREFETCH_TRACES 0   // first slot batch's published traces by cp.async during the volume work
+#ifndef SIPG_H3_EGEO_ASYNC
+#define SIPG_H3_EGEO_ASYNC 1        // element geometry by cp.async with the coefficients (else __ldg in the loop)
 #endif
 #ifndef SIPG_H3_PUB_DIRECT
 #define SIPG_H3_PUB_DIRECT 1        // identity-map slots publish straight from the face-grid pass
@@ -1048,7 +1048,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     for (int r = t; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
     const double* src = reinterpret_cast<const double*>(P.slots + sb);
     for (int r = t; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
-    if (!PUB && t < H3_EGEO / 2)
+    if (!PUB && SIPG_H3_EGEO_ASYNC && t < H3_EGEO / 2)
       __pipeline_memcpy_async(L.ebuf + buf * H3_EGEO + 2 * t, P.egeo + (int64_t)e * H3_EGEO + 2 * t, 2 * sizeof(double));
     __pipeline_commit();
   };
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     __syncthreads();
     L.c = L.cbuf + bsel * C::NCP;
     L.hdr = L.hbuf + bsel * C::NSMAX * C::SLOTD;
-    const double* eg = L.ebuf + bsel * H3_EGEO;
+    const double* eg = SIPG_H3_EGEO_ASYNC ? L.ebuf + bsel * H3_EGEO : P.egeo + (int64_t)__ldg(ce + i) * H3_EGEO;
     const int64_t dof = dof_n;
     const int ns = ns_n;
     if (i + G < count) issue(bsel ^ 1, e_nn, dof_nn, sb_nn, ns_nn);
@@ -1134,21 +1134,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
       }
       continue;
     }
-    // the published own / partner traces of the first slot batch land in the trace scratch (free
-    // once BwdTrans is done) while PhysDeriv and the volume terms run: per slot j, own (u, g)
-    // interleaved at tb[j][0, 2 TMAX), partner at tb[j][2 TMAX, 4 TMAX)
-    if (SIPG_H3_PREFETCH_TRACES) {
-      const int nb0 = ns < C::SB ? ns : C::SB;
-      for (int j = 0; j < nb0; ++j) {
-        const H3Slot& h = slot_hdr(L.hdr, j);
-        double* dst = L.tb + j * 4 * TMAX;
-        for (int r = t; r < h.nt; r += NT) {
-          __pipeline_memcpy_async(dst + 2 * r, P.pub + h.pub_self + 2 * r, 2 * sizeof(double));
-          if (h.kind) __pipeline_memcpy_async(dst + 2 * TMAX + 2 * r, P.pub + h.pub_other + 2 * r, 2 * sizeof(double));
-        }
-      }
-      __pipeline_commit();
-    }
     // SIP flux at the trace points of the slots [b0, b0 + nb) (sipg.py:622-650, 663-677) from the
     // published own and partner traces (the publish kernel evaluated both; boundary: jump 2u,
     // average g), then the transposed maps onto the own face grids: fv / fd in F, (G n)_k fd in the
@@ -1160,56 +1145,26 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         {
           auto cnt = [&](int s) -> int { return slot_hdr(L.hdr, s).nt; };
           const Batch BF(b0, nb, cnt);
-          constexpr int PER = (C::SB * TMAX + NT - 1) / NT;   // flux items per thread
-          double fvr[PER], fdr[PER];
-          constexpr bool PF = SIPG_H3_PREFETCH_TRACES;
-          if (PF && b0 == 0) {
-            __pipeline_wait_prior(0);                         // the prefetched first batch
-            __syncthreads();
-          }
-  #pragma unroll
-          for (int k = 0; k < PER; ++k) {
-            const int it0 = t + k * NT;
-            if (it0 >= BF.tot) break;
+          for (int it0 = t; it0 < BF.tot; it0 += NT) {
             int p = it0;
             const int s = BF.slot(p);
             const H3Slot& h = slot_hdr(L.hdr, s);
-            double ut, gt, un, gn;
-            if (PF && b0 == 0) {
-              const double* tv = L.tb + s * 4 * TMAX;
-              ut = tv[2 * p];
-              gt = tv[2 * p + 1];
-              un = tv[2 * TMAX + 2 * p];
-              gn = tv[2 * TMAX + 2 * p + 1];
+            double* tv = L.tb + (s - b0) * 4 * TMAX;
+            const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+            const double ut = own.x, gt = own.y;
+            double un, gn;
+            if (h.kind) {
+              const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+              un = nbv.x;
+              gn = nbv.y;
             } else {
-              const double2 own = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
-              ut = own.x;
-              gt = own.y;
-              if (h.kind) {
-                const double2 nbv = __ldg(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
-                un = nbv.x;
-                gn = nbv.y;
-              }
-            }
-            if (!h.kind) {
               un = -ut;
               gn = -gt;
             }
             const double j = ut - un, cc = 0.5 * (gt - gn);
             const double w = h.sJ * __ldg(P.tab + h.wtoff + p);
-            fvr[k] = (h.tau * j - cc) * w;
-            fdr[k] = -0.5 * j * w;
-          }
-          if (PF && b0 == 0) __syncthreads();   // the flux overwrites the prefetched traces
-  #pragma unroll
-          for (int k = 0; k < PER; ++k) {
-            const int it0 = t + k * NT;
-            if (it0 >= BF.tot) break;
-            int p = it0;
-            const int s = BF.slot(p);
-            double* tv = L.tb + (s - b0) * 4 * TMAX;
-            tv[p] = fvr[k];
-            tv[TMAX + p] = fdr[k];
+            tv[p] = (h.tau * j - cc) * w;
+            tv[TMAX + p] = -0.5 * j * w;
           }
         }
         __syncthreads();
@@ -1260,10 +1215,13 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
       Lift lf0;
       lift_setup(lf0, 0, FUSE ? nb0 : 0);
       const double lam = P.lam;
+      double mt[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) mt[q] = FUSE ? 0.0 : eg[q];   // hoisted (the fused lift re-reads: spills)
       for (int o0 = t; o0 < Q3; o0 += NT) {
-        // the metric from shared memory inside the loop (broadcast reads): with the fused lift the
-        // loop would otherwise spill
-        const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
+        const double dJ = FUSE ? eg[0] : mt[0], S00 = FUSE ? eg[1] : mt[1], S01 = FUSE ? eg[2] : mt[2],
+                     S02 = FUSE ? eg[3] : mt[3], S11 = FUSE ? eg[4] : mt[4], S12 = FUSE ? eg[5] : mt[5],
+                     S22 = FUSE ? eg[6] : mt[6];
         const int k0 = o0 / Q2, k1 = (o0 / Q) % Q, k2 = o0 % Q;
         const int o = k0 * C::template sj<PD>() * Q + k1 * C::template sj<PD>() + k2;
         const Chain ch = chain_t<S>(1.0 + *(pts + k0), 1.0 + *(pts + Q + k1), *(Rt + Q + k1),
