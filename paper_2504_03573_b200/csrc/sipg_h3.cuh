@@ -25,6 +25,15 @@
 
 #define SIPG_H3_ABI_VERSION 1
 // build knobs (measured variants; the defaults are the fastest measured)
+#ifndef SIPG_H3_NT64_QMAX
+#define SIPG_H3_NT64_QMAX 6         // classes with q <= this run 64-thread CTAs, the others 128
+#endif
+#ifndef SIPG_H3_TET_SPLIT
+#define SIPG_H3_TET_SPLIT 0         // tets: split pencils over two halves of the output line too
+#endif
+#ifndef SIPG_H3_APP_MINB_HI
+#define SIPG_H3_APP_MINB_HI 6       // resident apply CTAs per SM the registers must allow (128-thread classes)
+#endif
 #ifndef SIPG_H3_EGEO_ASYNC
 #define SIPG_H3_EGEO_ASYNC 1        // element geometry by cp.async with the coefficients (else __ldg in the loop)
 #endif
@@ -83,7 +92,7 @@ constexpr int H3_SJ() { return (PD && !(Q & 1)) ? Q + 1 : Q; }
 
 // threads per CTA: 256 for q >= 8 (512 volume points), else 128
 template <int Q>
-constexpr int nthreads() { return Q <= 6 ? 64 : 128; }
+constexpr int nthreads() { return Q <= SIPG_H3_NT64_QMAX ? 64 : 128; }
 constexpr int TMAX = 64;   // trace points per coupling: q_t = max(q_L, q_R) <= 8
 
 template <int S, int N>
@@ -378,7 +387,7 @@ __device__ __forceinline__ void cmatT_cols(const Tab& M, int off, const double (
 // Pencil work is split in two halves of the output line when Q^2 pencils would leave half of the
 // threads idle (2 Q^2 <= NT): part = item / Q^2 (warp-uniform for q = 8)
 template <int S, int Q>
-constexpr int pencil_split() { return (S != H3_TET && 2 * Q * Q <= nthreads<Q>()) ? 2 : 1; }   // tets: measured slower
+constexpr int pencil_split() { return ((S != H3_TET || SIPG_H3_TET_SPLIT) && 2 * Q * Q <= nthreads<Q>()) ? 2 : 1; }
 
 // du_a = D_a u along each eta axis: Q^2 pencils per axis (one compile-time axis per loop: a runtime
 // axis switch over three unrolled constant-operand contractions makes ptxas spill)
@@ -992,7 +1001,8 @@ __device__ void map_transpose(const double* hdr, double* F, double* tb, int b0, 
 #endif
 template <bool PUB, int Q>
 constexpr int h3_minb() {
-  return PUB ? (Q >= 7 ? SIPG_H3_PUB_MINB_HI : SIPG_H3_PUB_MINB_LO) : (Q >= 7 ? 6 : 12);
+  return PUB ? (Q > SIPG_H3_NT64_QMAX ? SIPG_H3_PUB_MINB_HI : SIPG_H3_PUB_MINB_LO)
+             : (Q > SIPG_H3_NT64_QMAX ? SIPG_H3_APP_MINB_HI : 12);
 }
 
 template <int S, int N, bool PUB>
