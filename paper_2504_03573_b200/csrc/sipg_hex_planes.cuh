@@ -183,6 +183,11 @@ __device__ __noinline__ void shared_face(const int no_rt, const int qt_rt, const
 #ifndef SIPG_SF_RANGE
 #define SIPG_SF_RANGE 3
 #endif
+// neighbour orders |NO - N| <= SIPG_SF_CRANGE get a compiled (fully unrolled) variant, the rest the
+// runtime-size one (code size vs instruction cache: ncu shows 35 % no-instruction stalls at 3)
+#ifndef SIPG_SF_CRANGE
+#define SIPG_SF_CRANGE SIPG_SF_RANGE
+#endif
 // 0: every shared face takes the runtime-size variant (one copy of the code: instruction cache)
 #ifndef SIPG_SF_COMPILED
 #define SIPG_SF_COMPILED 1
@@ -424,8 +429,8 @@ k_hexp(const DevPlan P, const int cls, const double* __restrict__ x, double* __r
         __syncthreads();
         const FaceRec& r = srec[f];
         ShScr<H::QM, H::NM> sc{SHX};
-        sf_dispatch<N, Q, (N - SIPG_SF_RANGE > 2 ? N - SIPG_SF_RANGE : 2),
-                    (N + SIPG_SF_RANGE < NMAX ? N + SIPG_SF_RANGE : NMAX)>(
+        sf_dispatch<N, Q, (N - SIPG_SF_CRANGE > 2 ? N - SIPG_SF_CRANGE : 2),
+                    (N + SIPG_SF_CRANGE < NMAX ? N + SIPG_SF_CRANGE : NMAX)>(
             sno[f], r.nt0, t, f, r, sext[2 * f + 1], NBP + f * 2 * NNX, T, OWN, FVD, sc);
       }
     }
