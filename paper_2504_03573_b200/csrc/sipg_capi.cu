@@ -137,6 +137,7 @@ struct H3State {
   ncclComm_t comm = nullptr;
   cudaStream_t s_comm = nullptr;
   cudaEvent_t ev_pub1 = nullptr, ev_comm = nullptr;
+  bool fork_all = false;
 };
 
 // Independent class launches (the publishers of a phase, then the element classes) are spread over
@@ -647,6 +648,7 @@ int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_d
     ++n;
     nsmall += (pass == 0 ? h->grid_pub[c] < h->cap_pub[c] : h->grid_apply[c] < h->cap_apply[c]);
   }
+  if (h->fork_all) nsmall = n;   // SIPG_H3_FORK=1: run even full-size class launches side by side
   int rc = group_begin(p, s, n, nsmall);
   if (rc) return rc;
   for (int c = 0; c < p->n_cls; ++c) {
@@ -977,6 +979,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     }
   }
   h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda};
+  h->fork_all = getenv("SIPG_H3_FORK") && atoi(getenv("SIPG_H3_FORK")) != 0;
   for (const H3Entry* k : h->kern) {
     cudaError_t e1 = cudaFuncSetAttribute((const void*)k->pub, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)k->smem_pub);
