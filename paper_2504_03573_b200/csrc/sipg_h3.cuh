@@ -34,9 +34,6 @@
 #ifndef SIPG_H3_APP_MINB_HI
 #define SIPG_H3_APP_MINB_HI 6       // resident apply CTAs per SM the registers must allow (128-thread classes)
 #endif
-#ifndef SIPG_H3_COLUMN
-#define SIPG_H3_COLUMN 1            // apply: the eta0 point columns of u, d0 u, W0, W1 in registers
-#endif
 #ifndef SIPG_H3_EGEO_ASYNC
 #define SIPG_H3_EGEO_ASYNC 1        // element geometry by cp.async with the coefficients (else __ldg in the loop)
 #endif
@@ -531,7 +528,7 @@ __device__ void pencil_stage_a_t(const double* __restrict__ T, double* __restric
 }
 
 // u = Phi c on the q^3 grid (generalised tensor product; stages as plan3d.ClassTables3 tables)
-template <int S, int N, bool PD, bool STOPA = false>
+template <int S, int N, bool PD>
 __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double* s1, double* s2,
                     const double* __restrict__ A, const double* __restrict__ B, const double* __restrict__ Ct,
                     const int* gstart, const int* gmem, const int* coff) {
@@ -558,7 +555,6 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
       for (int k = 0; k < Q; ++k) s2[i0 * C::template sj<PD>() * Q + k * C::template sj<PD>() + k2] = out[k];
     }
     __syncthreads();
-    if (STOPA) return;   // the caller runs the eta0 stage in registers
     pencil_stage_a<S, N, PD>(s2, u);
     __syncthreads();
     return;
@@ -619,7 +615,6 @@ __device__ void bwd(const double* __restrict__ c, double* __restrict__ u, double
     }
   }
   __syncthreads();
-  if (STOPA) return;
   pencil_stage_a<S, N, PD>(s2, u);
   __syncthreads();
 }
@@ -1088,8 +1083,7 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
     ns_n = ns_nn;
     e_n = e_nn;
     scalars(i + 2 * G, e_nn, dof_nn, sb_nn, ns_nn);
-    constexpr bool COLV = !PUB && SIPG_H3_COLUMN;
-    bwd<S, N, PD, COLV>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
+    bwd<S, N, PD>(L.c, L.u, L.s1, L.s2, At, Bt, Ct, L.gstart, L.gmem, L.coff);
     if (PUB) {
       // own-face-grid u and n.grad u of the interior slots from u alone: endpoint rows for u and
       // d/d eta_fixed (E D), collocation on the face grid for the two tangential derivatives
@@ -1219,97 +1213,6 @@ __global__ void __launch_bounds__(nthreads<N + 1>(), h3_minb<PUB, N + 1>()) k_h3
         w3 = fma(ek, Gs[2 * Q2 + a], w3);
       }
     };
-    if constexpr (COLV) {
-      // Column formulation (thread r < Q^2 owns the eta0 line (k0 = 0..Q-1) at (k1, k2) = (r / Q, r % Q)):
-      // the outermost BwdTrans stage, d/d eta0, the volume terms and the face lift of W0 / W1, and
-      // W0 + D0^T W1 stay in registers; only the eta1 / eta2 derivative passes go through shared
-      // memory (the LSU data pipe is what bounds these kernels)
-      constexpr int NA = S == H3_HEX ? N : N + 1, H = Q / 2;
-      constexpr int SJ = C::template sj<PD>(), SI = Q * SJ, V3 = Q * SI;
-      const bool colt = t < Q2;
-      const int k1c = colt ? t / Q : 0, k2c = colt ? t % Q : 0;
-      const int rc = k1c * SJ + k2c;
-      double uc[Q], dc[Q];
-      if (colt) {
-        double cg[NA];
-#pragma unroll
-        for (int g = 0; g < NA; ++g) cg[g] = L.s2[g * SI + rc];
-        cmat_rows<0, Q, NA>(c3A<S, N>, 0, cg, uc);
-#pragma unroll
-        for (int k0 = 0; k0 < Q; ++k0) L.u[k0 * SI + rc] = uc[k0];
-        if (SIPG_H3_EO) eo_lines<Q, 0, H, true>(c3E<S, N>, 0, uc, dc);
-        else cmat_rows<0, Q, Q>(c3D<S, N>, 0, uc, dc);
-      }
-      __syncthreads();   // u in shared memory for the eta1 / eta2 passes; the BwdTrans scratch is free
-      const int nbc = ns < C::SB ? ns : C::SB;
-      if (nbc > 0) face_batch(0, nbc);
-      pencil_deriv_axis<S, N, 1, PD>(L.u, L.du);
-      pencil_deriv_axis<S, N, 2, PD>(L.u, L.du);
-      __syncthreads();
-      {
-        Lift lf0;
-        lift_setup(lf0, 0, nbc);
-        if (colt) {
-          const double lam = P.lam;
-          const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
-          const double p1 = 1.0 + pts[Q + k1c], r1 = Rt[Q + k1c], r2 = Rt[2 * Q + k2c];
-          const double w12 = dJ * Wr[Q + k1c * Q + k2c];
-#pragma unroll
-          for (int k0 = 0; k0 < Q; ++k0) {
-            const int o = k0 * SI + rc;
-            const Chain ch = chain_t<S>(1.0 + pts[k0], p1, r1, r2);
-            const double jw = w12 * Wr[k0];
-            const double d0 = dc[k0], d1 = L.du[V3 + o], d2 = L.du[2 * V3 + o];
-            const double x0 = ch.c00 * d0, x1 = ch.c01 * d0 + ch.c11 * d1, x2 = ch.c02 * d0 + ch.c12 * d1 + d2;
-            const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
-            const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
-            const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
-            double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-            lift_at(lf0, k0, k1c, k2c, w0, w1, w2, w3);
-            uc[k0] = fma(lam * jw, uc[k0], w0);
-            dc[k0] = fma(jw, ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2, w1);
-            L.du[V3 + o] = fma(jw, ch.c11 * f1 + ch.c12 * f2, w2);
-            L.du[2 * V3 + o] = fma(jw, f2, w3);
-          }
-        }
-      }
-      __syncthreads();
-      for (int b0 = C::SB; b0 < ns; b0 += C::SB) {   // hex / prism: further slot batches
-        const int nb = min(C::SB, ns - b0);
-        face_batch(b0, nb);
-        Lift lf;
-        lift_setup(lf, b0, nb);
-        if (colt) {
-#pragma unroll
-          for (int k0 = 0; k0 < Q; ++k0) {
-            const int o = k0 * SI + rc;
-            double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-            lift_at(lf, k0, k1c, k2c, w0, w1, w2, w3);
-            uc[k0] += w0;
-            dc[k0] += w1;
-            L.du[V3 + o] += w2;
-            L.du[2 * V3 + o] += w3;
-          }
-        }
-        __syncthreads();
-      }
-      // T = W0 + D0^T W1 in registers, then + D1^T W2 + D2^T W3 through shared memory
-      if (colt) {
-        double tc[Q];
-        if (SIPG_H3_EO) eo_lines<Q, 0, H, true>(c3E<S, N>, 3 * eo_size<Q>(), dc, tc);
-        else cmatT_cols<0, Q, Q, Q>(c3D<S, N>, 0, dc, tc);
-#pragma unroll
-        for (int k0 = 0; k0 < Q; ++k0) L.u[k0 * SI + rc] = uc[k0] + tc[k0];
-      }
-      __syncthreads();
-      pencil_dt_axis<S, N, 1, PD>(L.u, L.du);
-      __syncthreads();
-      pencil_dt_axis<S, N, 2, PD>(L.u, L.du);
-      __syncthreads();
-      bwd_t<S, N, PD>(L.u, y + dof, L.s1, L.s2, At, Bt, Ct, L.gof, L.mofr);
-      __syncthreads();
-      continue;
-    }
     constexpr bool FUSE = SIPG_H3_FUSE_LIFT;
     const int nb0 = ns < C::SB ? ns : C::SB;
     if (FUSE && nb0 > 0) face_batch(0, nb0);
