@@ -180,6 +180,8 @@ struct sipg_plan {
   std::vector<int> per_sm;               // resident CTAs per SM of each class's kernel
   struct Graph { const double* x; double* y; cudaGraphExec_t exec; int64_t kernels; };
   std::vector<Graph> graphs;             // captured whole applies (sipg_apply)
+  struct HostGraph { const double* x; double* y; cudaGraphExec_t exec; int64_t kernels; };
+  std::vector<HostGraph> host_graphs;    // captured streamed host applies (sipg_apply_host)
   bool use_graphs = true;
   cudaStream_t cap_stream = nullptr;
   int sms = 0;                           // multiprocessors of the plan's device (queried)
@@ -199,7 +201,7 @@ struct sipg_plan {
   int32_t* cds_d = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev_h2d, ev_comp;
-  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
 };
 
 namespace {
@@ -235,12 +237,8 @@ bool concurrency_on() {
 }
 
 // begin a group of independent launches on s; returns the stream for launch i via group_stream
-int group_begin(sipg_plan* p, cudaStream_t s, int nlaunch, int nsmall) {
+int fork_create(sipg_plan* p) {
   Fork& f = p->fork;
-  f.s = s;
-  f.next = 0;
-  f.used = 0;
-  if (nlaunch <= 1 || nsmall < 2 || !concurrency_on()) return 0;
   if (f.side.empty()) {
     f.side.resize(kSideStreams);
     f.ev_join.resize(kSideStreams);
@@ -252,6 +250,16 @@ int group_begin(sipg_plan* p, cudaStream_t s, int nlaunch, int nsmall) {
     if (cudaEventCreateWithFlags(&f.ev_fork, cudaEventDisableTiming) != cudaSuccess)
       return fail(SIPG_ERR_CUDA, "fork event creation");
   }
+  return 0;
+}
+
+int group_begin(sipg_plan* p, cudaStream_t s, int nlaunch, int nsmall) {
+  Fork& f = p->fork;
+  f.s = s;
+  f.next = 0;
+  f.used = 0;
+  if (nlaunch <= 1 || nsmall < 2 || !concurrency_on()) return 0;
+  if (int rc = fork_create(p)) return rc;
   f.used = nlaunch - 1 < kSideStreams ? nlaunch - 1 : kSideStreams;
   CK(cudaEventRecord(f.ev_fork, s));
   for (int j = 0; j < f.used; ++j) CK(cudaStreamWaitEvent(f.side[j], f.ev_fork, 0));
@@ -735,11 +743,37 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
   int64_t chunk_bytes = 24ll << 20;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
   if (cb) chunk_bytes = atoll(cb);
-  int K = (int)(ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1));
+  // Graduated chunks: quarter- and half-size chunks at both ends (1 2 4 4 ... 4 2 1), so that the
+  // compute starts after a short first copy and the copies of the y chunks the last stage completes
+  // are short (measured on cfg4 with uniform 24 MB chunks: 0.5 ms before the first stage, 0.9 ms of
+  // D2H after the last one)
+  std::vector<double> w;
+  {
+    const double units = (double)ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1) * 4.0;
+    if (getenv("SIPG_STREAM_UNIFORM") || units < 16) {
+      const int Ku = (int)(units / 4);
+      for (int k = 0; k < Ku; ++k) w.push_back(1.0);
+    } else {
+      const int mid = (int)((units - 6) / 4 + 0.5);
+      w = {1, 2};
+      for (int k = 0; k < mid; ++k) w.push_back(4);
+      w.push_back(2);
+      w.push_back(1);
+    }
+  }
+  int K = (int)w.size();
   if (K > 64) K = 64;
   if (K < 2) return false;
+  w.resize(K);
   p->chunk_dof.assign(K + 1, 0);
-  for (int k = 1; k < K; ++k) p->chunk_dof[k] = (ndof * k / K) & ~(int64_t)511;
+  {
+    double tot = 0.0, acc = 0.0;
+    for (double v : w) tot += v;
+    for (int k = 1; k < K; ++k) {
+      acc += w[k - 1];
+      p->chunk_dof[k] = (int64_t)((double)ndof * acc / tot) & ~(int64_t)511;
+    }
+  }
   p->chunk_dof[K] = ndof;
   for (int k = 0; k < K; ++k)
     if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return false;
@@ -1090,6 +1124,7 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
       return 0;
     }
   if (!p->cap_stream) CK(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+  if (int rcf = fork_create(p)) return rcf;   // no resource creation inside the capture
   const int64_t l0 = p->launches;
   CK(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
   int rc = sipg_apply_role(p, -1, x_dev, y_dev, p->cap_stream);
@@ -1164,6 +1199,7 @@ int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
 }
 
 static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, cudaStream_t s);
+static int enqueue_streamed(sipg_plan* p, const double* x_host, double* y_host, cudaStream_t s);
 
 int sipg_apply_host(sipg_plan* p, const double* x_host, double* y_host, void* stream) {
   if (!p || !x_host || !y_host) return fail(SIPG_ERR_ARG, "null argument");
@@ -1209,6 +1245,7 @@ static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, c
     CK(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     p->ev_h2d.resize(K);
     p->ev_comp.resize(K);
     for (int k = 0; k < K; ++k) {
@@ -1216,6 +1253,58 @@ static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, c
       CK(cudaEventCreateWithFlags(&p->ev_comp[k], cudaEventDisableTiming));
     }
   }
+  // Replay as a CUDA graph (copies, stage launches and their fork / join captured once per pinned
+  // (x_host, y_host) pair): ~400 small launches per host apply on config 4.  Pageable host buffers
+  // and the timeline instrumentation run eagerly.
+  if (p->use_graphs && !p->stream_trace) {
+    cudaPointerAttributes ax{}, ay{};
+    const bool pinned = cudaPointerGetAttributes(&ax, x_host) == cudaSuccess &&
+                        cudaPointerGetAttributes(&ay, y_host) == cudaSuccess && ax.type == cudaMemoryTypeHost &&
+                        ay.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (pinned) {
+      for (auto& g : p->host_graphs)
+        if (g.x == x_host && g.y == y_host) {
+          CK(cudaGraphLaunch(g.exec, s));
+          p->launches += g.kernels;
+          CK(cudaStreamSynchronize(s));
+          return 0;
+        }
+      if (!p->cap_stream) CK(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+      if (int rcf = fork_create(p)) return rcf;   // no resource creation inside the capture
+      const int64_t l0 = p->launches;
+      CK(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_streamed(p, x_host, y_host, p->cap_stream);
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(p->cap_stream, &graph);
+      cudaGraphExec_t exec = nullptr;
+      if (!rc && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (rc) return rc;
+      if (e == cudaSuccess) {
+        if (p->host_graphs.size() >= 4) {
+          cudaGraphExecDestroy(p->host_graphs.front().exec);
+          p->host_graphs.erase(p->host_graphs.begin());
+        }
+        p->host_graphs.push_back({x_host, y_host, exec, p->launches - l0});
+        CK(cudaGraphLaunch(exec, s));
+        CK(cudaStreamSynchronize(s));
+        return 0;
+      }
+      cudaGetLastError();   // capture unsupported here: eager from now on
+      p->launches = l0;
+      p->use_graphs = false;
+    }
+  }
+  int rc = enqueue_streamed(p, x_host, y_host, s);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+// The streamed host apply's work, enqueued on `s` (ends with `s` joined to the copy streams).
+static int enqueue_streamed(sipg_plan* p, const double* x_host, double* y_host, cudaStream_t s) {
+  const int K = p->n_chunks;
   // SIPG_STREAM_TRACE (instrumentation): timestamps of every chunk copy / stage, printed to stderr
   const bool trace = p->stream_trace;
   static unsigned long long* tbuf = nullptr;
@@ -1293,9 +1382,10 @@ static int apply_host_impl(sipg_plan* p, const double* x_host, double* y_host, c
     }
   }
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(p->s_d2h));
-  CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(p->ev_done, p->s_d2h));   // join the copy streams back into s
+  CK(cudaStreamWaitEvent(s, p->ev_done, 0));
   if (trace) {
+    CK(cudaStreamSynchronize(s));
     std::vector<unsigned long long> t(nmark);
     cudaMemcpy(t.data(), tbuf, sizeof(unsigned long long) * nmark, cudaMemcpyDeviceToHost);
     for (int i = 0; i < nmark; ++i) fprintf(stderr, "%c%.3f ", tkind[i], (double)(t[i] - t[0]) * 1e-6);
@@ -1342,6 +1432,7 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
 int sipg_plan_destroy(sipg_plan* p) {
   if (!p) return 0;
   for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
+  for (auto& g : p->host_graphs) cudaGraphExecDestroy(g.exec);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   for (cudaStream_t st : p->fork.side)
     if (st) cudaStreamDestroy(st);
@@ -1370,6 +1461,7 @@ int sipg_plan_destroy(sipg_plan* p) {
   for (cudaEvent_t e : p->ev_h2d) cudaEventDestroy(e);
   for (cudaEvent_t e : p->ev_comp) cudaEventDestroy(e);
   if (p->ev_start) cudaEventDestroy(p->ev_start);
+  if (p->ev_done) cudaEventDestroy(p->ev_done);
   if (p->y_stage) cudaFree(p->y_stage);
   if (p->ws) cudaFree(p->ws);
   if (p->ws_host) cudaFreeHost(p->ws_host);
