@@ -302,6 +302,42 @@ int publish_grid(const int32_t* cd, int count, int sms) {
   return g < sms * 8 ? g : sms * 8;
 }
 
+// DoF chunk boundaries of the streamed host apply (4 KB-aligned).  Graduated chunks: quarter- and
+// half-size chunks at both ends (1 2 4 4 ... 4 2 1 in units of chunk_bytes / 4), so that the compute
+// starts after a short first copy and the copies of the y chunks the last stage completes are short
+// (measured on cfg4 with uniform 24 MB chunks: 0.5 ms before the first stage, 0.9 ms of D2H after
+// the last one; host apply 9.0 -> 8.1 ms with the graduated chunks and graph replay).
+// SIPG_STREAM_UNIFORM=1 keeps uniform chunks.  Returns K (0: too small to stream).
+int make_chunks(sipg_plan* p, int64_t ndof, int64_t chunk_bytes) {
+  std::vector<double> w;
+  const double units = (double)ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1) * 4.0;
+  if (getenv("SIPG_STREAM_UNIFORM") || units < 16) {
+    const int Ku = (int)(units / 4);
+    for (int k = 0; k < Ku; ++k) w.push_back(1.0);
+  } else {
+    const int mid = (int)((units - 6) / 4 + 0.5);
+    w = {1, 2};
+    for (int k = 0; k < mid; ++k) w.push_back(4);
+    w.push_back(2);
+    w.push_back(1);
+  }
+  int K = (int)w.size();
+  if (K > 64) K = 64;
+  if (K < 2) return 0;
+  w.resize(K);
+  p->chunk_dof.assign(K + 1, 0);
+  double tot = 0.0, acc = 0.0;
+  for (double v : w) tot += v;
+  for (int k = 1; k < K; ++k) {
+    acc += w[k - 1];
+    p->chunk_dof[k] = (int64_t)((double)ndof * acc / tot) & ~(int64_t)511;
+  }
+  p->chunk_dof[K] = ndof;
+  for (int k = 0; k < K; ++k)
+    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return 0;
+  return K;
+}
+
 // Build the streamed-apply schedule (see sipg_plan).  Returns false when the mesh ordering does not
 // allow it (a class whose element list is not monotone in stage) — the host apply then runs
 // copy -> apply -> copy.
@@ -323,19 +359,13 @@ bool build_stream_schedule(sipg_plan* p, const sipg_plan_desc* d) {
   if (bytes >= (16ll << 20) && chunk_bytes > bytes / 2) chunk_bytes = bytes / 2 - 4096;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
   if (cb) chunk_bytes = atoll(cb);
-  int K = (int)(bytes / (chunk_bytes > 0 ? chunk_bytes : 1));
-  if (K > 64) K = 64;
-  if (K < 2) return false;
   for (int c = 0; c < d->n_classes; ++c)
     if (d->class_desc[c * CD_WORDS + CD_ROLE] != 0) return false;   // distributed local plans: no
-  std::vector<int32_t> chunk(nel), stage(nel);
   // copy chunks: 4 KB-aligned DoF ranges (DMA runs markedly slower on unaligned host ranges when
   // both directions are busy); an element belongs to the chunk in which its last DoF arrives
-  p->chunk_dof.assign(K + 1, 0);
-  for (int k = 1; k < K; ++k) p->chunk_dof[k] = (ndof * k / K) & ~(int64_t)511;
-  p->chunk_dof[K] = ndof;
-  for (int k = 0; k < K; ++k)
-    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return false;
+  const int K = make_chunks(p, ndof, chunk_bytes);
+  if (K < 2) return false;
+  std::vector<int32_t> chunk(nel), stage(nel);
   {
     int k = 0;
     for (int64_t e = 0; e < nel; ++e) {
@@ -743,40 +773,8 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
   int64_t chunk_bytes = 24ll << 20;
   const char* cb = getenv("SIPG_STREAM_CHUNK_BYTES");
   if (cb) chunk_bytes = atoll(cb);
-  // Graduated chunks: quarter- and half-size chunks at both ends (1 2 4 4 ... 4 2 1), so that the
-  // compute starts after a short first copy and the copies of the y chunks the last stage completes
-  // are short (measured on cfg4 with uniform 24 MB chunks: 0.5 ms before the first stage, 0.9 ms of
-  // D2H after the last one)
-  std::vector<double> w;
-  {
-    const double units = (double)ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1) * 4.0;
-    if (getenv("SIPG_STREAM_UNIFORM") || units < 16) {
-      const int Ku = (int)(units / 4);
-      for (int k = 0; k < Ku; ++k) w.push_back(1.0);
-    } else {
-      const int mid = (int)((units - 6) / 4 + 0.5);
-      w = {1, 2};
-      for (int k = 0; k < mid; ++k) w.push_back(4);
-      w.push_back(2);
-      w.push_back(1);
-    }
-  }
-  int K = (int)w.size();
-  if (K > 64) K = 64;
+  const int K = make_chunks(p, ndof, chunk_bytes);
   if (K < 2) return false;
-  w.resize(K);
-  p->chunk_dof.assign(K + 1, 0);
-  {
-    double tot = 0.0, acc = 0.0;
-    for (double v : w) tot += v;
-    for (int k = 1; k < K; ++k) {
-      acc += w[k - 1];
-      p->chunk_dof[k] = (int64_t)((double)ndof * acc / tot) & ~(int64_t)511;
-    }
-  }
-  p->chunk_dof[K] = ndof;
-  for (int k = 0; k < K; ++k)
-    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return false;
   std::vector<int32_t> chunk(nel), stage(nel);
   {
     int k = 0;
