@@ -968,11 +968,13 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   p->n_cls = d->n_classes;
   p->n_dofs = d->n_dofs;
   h->cd.assign(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD3_WORDS);
+  // SIPG_H3_GEN=0: the first-generation kernels (same results to rounding; kept for A/B timing)
+  const int gen = getenv("SIPG_H3_GEN") ? atoi(getenv("SIPG_H3_GEN")) : 1;
   for (int c = 0; c < d->n_classes; ++c) {
     const int32_t* cd = d->class_desc + c * CD3_WORDS;
     const H3Entry* k = nullptr;
     for (const auto& e : table)
-      if (e.shape == cd[CD3_SHAPE] && e.n == cd[CD3_N] && cd[CD3_Q] == e.n + 1) k = &e;
+      if (e.gen == gen && e.shape == cd[CD3_SHAPE] && e.n == cd[CD3_N] && cd[CD3_Q] == e.n + 1) k = &e;
     if (!k) {
       sipg_plan_destroy(p);
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a hybrid kernel for shape=" + std::to_string(cd[CD3_SHAPE]) +
@@ -981,7 +983,8 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     h->kern.push_back(k);
     // __constant__ 1-D tables (one (shape, n) class per instantiation; role-split classes share them)
     const double* tab = d->tables;
-    cudaError_t e = k->upload(tab + cd[CD3_T_D], tab + cd[CD3_T_A], cd[CD3_SHAPE] == 1 ? tab + cd[CD3_T_C] : nullptr);
+    cudaError_t e = k->upload(tab + cd[CD3_T_D], tab + cd[CD3_T_A], cd[CD3_SHAPE] == 1 ? tab + cd[CD3_T_C] : nullptr,
+                              tab + cd[CD3_T_E], tab + cd[CD3_T_ED], tab + cd[CD3_T_PTS], tab + cd[CD3_T_W]);
     if (e != cudaSuccess) {
       sipg_plan_destroy(p);
       return fail(SIPG_ERR_CUDA, std::string("hybrid constant tables: ") + cudaGetErrorString(e));

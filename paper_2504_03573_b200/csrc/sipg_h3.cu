@@ -1,23 +1,42 @@
-// Instantiations of the config-4 hybrid hex / prism / tet kernels (sipg_h3.cuh), n_modes 2..7.
+// Instantiations of the config-4 hybrid hex / prism / tet kernels, n_modes 2..7: the register-column
+// kernels (sipg_h3c.cuh, generation 1, default) and the first-generation kernels (sipg_h3.cuh,
+// generation 0).
 #include <vector>
-#include "sipg_h3.cuh"
+#include "sipg_h3c.cuh"
 #include "sipg_h3_registry.h"
 
 namespace {
 template <int S, int N>
-H3Entry entry() {
+cudaError_t upload0(const double* D, const double* A, const double* psi, const double*, const double*, const double*,
+                    const double*) {
+  return h3::h3_upload<S, N>(D, A, psi);
+}
+template <int S, int N>
+H3Entry entry0() {
   using C = h3::Cfg<S, N>;
-  return H3Entry{S, N, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(true),
-                 C::smem_bytes(false), &h3::h3_upload<S, N>};
+  return H3Entry{S, N, 0, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(true),
+                 C::smem_bytes(false), &upload0<S, N>};
+}
+template <int S, int N>
+H3Entry entry1() {
+  using C = h3c::CfgC<S, N>;
+  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, true>, &h3c::k_h3c<S, N, false>, C::NT, C::smem_bytes(true),
+                 C::smem_bytes(false), &h3c::h3c_upload<S, N>};
 }
 template <int S>
 void add(std::vector<H3Entry>& v) {
-  v.push_back(entry<S, 2>());
-  v.push_back(entry<S, 3>());
-  v.push_back(entry<S, 4>());
-  v.push_back(entry<S, 5>());
-  v.push_back(entry<S, 6>());
-  v.push_back(entry<S, 7>());
+  v.push_back(entry0<S, 2>());
+  v.push_back(entry0<S, 3>());
+  v.push_back(entry0<S, 4>());
+  v.push_back(entry0<S, 5>());
+  v.push_back(entry0<S, 6>());
+  v.push_back(entry0<S, 7>());
+  v.push_back(entry1<S, 2>());
+  v.push_back(entry1<S, 3>());
+  v.push_back(entry1<S, 4>());
+  v.push_back(entry1<S, 5>());
+  v.push_back(entry1<S, 6>());
+  v.push_back(entry1<S, 7>());
 }
 }  // namespace
 

@@ -5,12 +5,15 @@
 #include "sipg_h3.cuh"
 
 using H3Fn = void (*)(const H3Plan, const int, const double*, double*);
-using H3UploadFn = cudaError_t (*)(const double* D, const double* A, const double* psi);
+// __constant__ tables of a (shape, n) instantiation: D, A, psi, E, ED, pts, W (plan3d.ClassTables3 parts)
+using H3UploadFn = cudaError_t (*)(const double* D, const double* A, const double* psi, const double* E,
+                                   const double* ED, const double* pts, const double* W);
 struct H3Entry {
   int shape, n;
+  int gen;             // 1: register-column kernels (sipg_h3c.cuh); 0: first generation (sipg_h3.cuh)
   H3Fn pub, apply;
   int threads;
   size_t smem_pub, smem_apply;
-  H3UploadFn upload;   // __constant__ tables of this (shape, n) instantiation
+  H3UploadFn upload;
 };
 void sipg_register_h3(std::vector<H3Entry>& v);

@@ -1,0 +1,1048 @@
+// Config 4, register-column kernels: the SIP-Helmholtz apply on 3-D hybrid hex / prism / tet meshes
+// (sm_100a, fp64).  Same algorithm, plan layout and published-trace format as sipg_h3.cuh (the
+// reference's two-phase apply, pkg/src/dgsipg/sipg.py:558-602, on the shared-trace route
+// sipg.py:513-554, 653-677, extended to prisms and tets as restated in oracle/hybrid3d.py); what
+// changes is the mapping onto the machine.  ncu showed the first-generation kernels bound by the
+// shared-memory data pipe (85 % of its wavefront peak; every pointwise phase went through four q^3
+// arrays in shared memory), so here
+//   * one CTA of q^2 threads per element; thread (k1, k2) owns the q points (., k1, k2) along eta0 in
+//     REGISTERS: the last BwdTrans stage, PhysDeriv along eta0, the volume terms, every face lift,
+//     D0^T and the first IProduct stage never touch shared memory;
+//   * eta1 / eta2 derivatives are one line per thread through two (bank-padded) q^3 buffers,
+//     even-odd factorised with __constant__ operands;
+//   * faces are compile-time unrolled (fixed axis, side, run axes are constants of the shape): the
+//     fluxes of all couplings are evaluated first (they need the published traces only), folded per
+//     local face into four own-face-grid arrays, and lifted straight into the register columns
+//     (one-hot GLL endpoint rows touch the boundary columns only);
+//   * the publish kernel takes u and d/d eta_fixed on the faces from the register columns (eta0
+//     faces) or from one line read per thread (eta1 / eta2 faces) and the tangential derivatives as
+//     even-odd lines on the face grids.
+// The element body is written against a tiny execution abstraction (par / sync) so that the very
+// same code runs on the host, thread after thread, in the CPU test of the kernel logic
+// (tests/emu, -DH3C_HOST_EMU; test infrastructure, not part of libsipg.so).
+#pragma once
+#include <type_traits>
+#include "sipg_h3.cuh"
+
+#ifdef H3C_HOST_EMU
+#define H3C_HD __host__ __device__ __forceinline__
+#else
+#define H3C_HD __device__ __forceinline__
+#endif
+#if defined(__CUDA_ARCH__)
+#define H3C_LDG(p) __ldg(p)
+#else
+#define H3C_LDG(p) (*(p))
+#endif
+
+#ifndef SIPG_H3C_MINB8
+#define SIPG_H3C_MINB8 7            // resident CTAs per SM the registers must allow, q = 8 (64 threads)
+#endif
+
+namespace h3c {
+using h3::Chain;
+using h3::TMAX;
+
+// E | ED endpoint rows (6 q each, row (axis * 2 + (side > 0))), 1 + eta0 points, eta0 weights
+template <int S, int N> __constant__ double c3X[14 * (N + 1)];
+
+#ifdef H3C_HOST_EMU
+template <int S, int N>
+struct HostTabs {
+  static double A[(N + 1) * (N + 1)], P[(N + 1) * N], E[6 * h3::eo_size<N + 1>()], X[14 * (N + 1)];
+};
+template <int S, int N> double HostTabs<S, N>::A[(N + 1) * (N + 1)];
+template <int S, int N> double HostTabs<S, N>::P[(N + 1) * N];
+template <int S, int N> double HostTabs<S, N>::E[6 * h3::eo_size<N + 1>()];
+template <int S, int N> double HostTabs<S, N>::X[14 * (N + 1)];
+#endif
+#if defined(__CUDA_ARCH__) || !defined(H3C_HOST_EMU)
+#define H3C_TA (h3::c3A<S, N>)
+#define H3C_TP (h3::c3P<S, N>)
+#define H3C_TE (h3::c3E<S, N>)
+#define H3C_TX (c3X<S, N>)
+#else
+#define H3C_TA (HostTabs<S, N>::A)
+#define H3C_TP (HostTabs<S, N>::P)
+#define H3C_TE (HostTabs<S, N>::E)
+#define H3C_TX (HostTabs<S, N>::X)
+#endif
+
+// (fixed axis, side, run axis 0, run axis 1) per shape and local face (plan3d.FACES)
+H3C_HD constexpr int fc(int S, int f, int w) {
+  constexpr int T[3][6][4] = {
+      {{0, -1, 1, 2}, {0, 1, 1, 2}, {1, -1, 0, 2}, {1, 1, 0, 2}, {2, -1, 0, 1}, {2, 1, 0, 1}},
+      {{2, -1, 0, 1}, {1, -1, 0, 2}, {0, 1, 1, 2}, {1, 1, 0, 2}, {0, -1, 1, 2}, {0, 0, 0, 0}},
+      {{2, -1, 0, 1}, {1, -1, 0, 2}, {0, 1, 1, 2}, {0, -1, 1, 2}, {0, 0, 0, 0}, {0, 0, 0, 0}},
+  };
+  return T[S][f][w];
+}
+// the same for a run-time face: the __constant__ copy on the device (no per-thread table)
+H3C_HD int fcr(int S, int f, int w) {
+#if defined(__CUDA_ARCH__)
+  return h3::c_faces[S][f][w];
+#else
+  return fc(S, f, w);
+#endif
+}
+// GLL axes (endpoint rows one-hot): hex all, prism eta1 (plan3d.AXIS_KINDS)
+H3C_HD constexpr bool gll_axis(int S, int a) { return S == H3_HEX || (S == H3_PRISM && a == 1); }
+
+template <int S>
+H3C_HD Chain chain_t(double p0, double p1, double r1, double r2) {
+  Chain c{1.0, 0.0, 0.0, 1.0, 0.0};
+  if (S == H3_PRISM) {
+    c.c00 = 2.0 * r2;
+    c.c02 = p0 * r2;
+  } else if (S == H3_TET) {
+    const double r12 = r1 * r2;
+    c.c00 = 4.0 * r12;
+    c.c01 = c.c02 = 2.0 * p0 * r12;
+    c.c11 = 2.0 * r2;
+    c.c12 = p1 * r2;
+  }
+  return c;
+}
+// chain at own-face-grid point (ia, ib) of a face (h3::face_chain)
+template <int S>
+H3C_HD Chain face_chain(const double* pts, const double* R, int Q, int fx, int sd, int ra, int rb, int ia, int ib) {
+  if (S == H3_HEX) return Chain{1.0, 0.0, 0.0, 1.0, 0.0};
+  const double ea = *(pts + ra * Q + ia), eb = *(pts + rb * Q + ib);
+  const double rra = *(R + ra * Q + ia), rrb = *(R + rb * Q + ib);
+  const double es = (double)sd, rs = sd < 0 ? 0.5 : 0.0;
+  const double e0 = fx == 0 ? es : (ra == 0 ? ea : eb);
+  const double e1 = fx == 1 ? es : (ra == 1 ? ea : eb);
+  const double r1 = fx == 1 ? rs : (ra == 1 ? rra : rrb);
+  const double r2 = fx == 2 ? rs : (ra == 2 ? rra : rrb);
+  return chain_t<S>(1.0 + e0, 1.0 + e1, r1, r2);
+}
+
+H3C_HD const H3Slot& slot_hdr(const double* hdr, int s) { return *reinterpret_cast<const H3Slot*>(hdr + 12 * s); }
+
+// items of a batch of <= 4 slots (h3::Batch)
+struct Batch {
+  int b0, o1, o2, o3, tot;
+  template <typename CountFn>
+  H3C_HD Batch(int b0_, int nb, CountFn cnt) : b0(b0_) {
+    const int c0 = nb > 0 ? cnt(b0) : 0;
+    const int c1 = nb > 1 ? cnt(b0 + 1) : 0;
+    const int c2 = nb > 2 ? cnt(b0 + 2) : 0;
+    const int c3 = nb > 3 ? cnt(b0 + 3) : 0;
+    o1 = c0;
+    o2 = o1 + c1;
+    o3 = o2 + c2;
+    tot = o3 + c3;
+  }
+  H3C_HD int slot(int& it) const {
+    const int j = (it >= o1) + (it >= o2) + (it >= o3);
+    it -= j == 0 ? 0 : (j == 1 ? o1 : (j == 2 ? o2 : o3));
+    return b0 + j;
+  }
+};
+
+// full even-odd line: out = M in for the operator block at T[off] (Pe | Po | mc | mr, sipg_h3.cuh)
+template <int Q, typename Tab>
+H3C_HD void eo_full(const Tab& T, const int off, const double (&in)[Q], double (&out)[Q]) {
+  constexpr int H = Q / 2;
+  double sm[H > 0 ? H : 1], df[H > 0 ? H : 1];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    sm[j] = in[j] + in[Q - 1 - j];
+    df[j] = in[j] - in[Q - 1 - j];
+  }
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    double e = 0.0, o = 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      e = fma(T[off + k * H + j], sm[j], e);
+      o = fma(T[off + H * H + k * H + j], df[j], o);
+    }
+    if (Q & 1) e = fma(T[off + 2 * H * H + k], in[H], e);
+    out[k] = e + o;
+    out[Q - 1 - k] = o - e;
+  }
+  if (Q & 1) {
+    double m = 0.0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) m = fma(T[off + 2 * H * H + H + j], df[j], m);
+    out[H] = m;
+  }
+}
+
+template <int K, int J, typename Tab>
+H3C_HD void cmat(const Tab& M, const int off, const double (&in)[J], double (&out)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) a = fma(M[off + k * J + j], in[j], a);
+    out[k] = a;
+  }
+}
+template <int K, int J, typename Tab>
+H3C_HD void cmatT(const Tab& M, const int off, const double (&in)[K], double (&out)[J]) {
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) a = fma(M[off + k * J + j], in[k], a);
+    out[j] = a;
+  }
+}
+
+template <int S, int N>
+struct CfgC {
+  static constexpr int Q = N + 1, Q2 = Q * Q, NT = Q2;
+  static constexpr int SJ = (Q & 1) ? Q : Q + 1, SI = Q * SJ, BUF = Q * SI;   // odd row stride
+  static constexpr int NF = S == H3_HEX ? 6 : (S == H3_PRISM ? 5 : 4);
+  static constexpr int NTRI = N * (N + 1) / 2, NG = N + 1;
+  static constexpr int NPM = NTRI + (S == H3_TET ? 1 : 0);
+  static constexpr int NA = S == H3_HEX ? N : N + 1;
+  static constexpr int NC = S == H3_HEX ? N * N * N : (S == H3_PRISM ? N * NTRI : N * (N + 1) * (N + 2) / 6);
+  static constexpr int NCP = (NC + 1) & ~1;
+  static constexpr int S1 = S == H3_HEX ? N * N * Q : NPM * Q;
+  static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);
+  static constexpr int SLOTD = 12;
+  static constexpr int SB = Q >= 8 ? 4 : 2;                                   // slots per map batch
+  static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
+  static constexpr int TABD = (3 * Q + 3 * Q + Q2 + 6 * Q + TB + 1) & ~1;     // pts R W12 E B
+  static constexpr int imax(int a, int b) { return a > b ? a : b; }
+  static constexpr int SCR_A = (imax(2 * BUF, SB * 4 * TMAX) + 1) & ~1;
+  static constexpr int SCR_P = (imax(BUF + S1, SB * 4 * TMAX) + 1) & ~1;
+  static constexpr int NI = 4 * NPM + 4 + NC + 16;
+  static constexpr int doubles(bool pub) {
+    return TABD + 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + NF * 4 * Q2 + (pub ? SCR_P : SCR_A);
+  }
+  static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
+};
+
+// triangle-mode groups and tet mode offsets (h3::build_int_tables), by one thread
+template <int S, int N>
+H3C_HD void build_int_tables(int* gstart, int* gmem, int* gof, int* coff, int* mofr) {
+  using C = CfgC<S, N>;
+  int cnt[C::NG + 1];
+  for (int g = 0; g <= C::NG; ++g) cnt[g] = 0;
+  int m = 0;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N - i; ++j, ++m) {
+      const int g = i == 0 ? (j == 1 ? 1 : 0) : (i == 1 ? 2 : i + 1);
+      gof[m] = g;
+      ++cnt[g];
+    }
+  if (S == H3_TET) {
+    gof[C::NTRI] = 1;
+    ++cnt[1];
+  }
+  gstart[0] = 0;
+  for (int g = 0; g < C::NG; ++g) gstart[g + 1] = gstart[g] + cnt[g];
+  int fill[C::NG];
+  for (int g = 0; g < C::NG; ++g) fill[g] = gstart[g];
+  for (int mm = 0; mm < C::NPM; ++mm) gmem[fill[gof[mm]]++] = mm;
+  if (S == H3_TET) {
+    int r = 0, mm = 0;
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N - i; ++j, ++mm) {
+        const int d = (i + j) > 1 ? i + j : 1;
+        coff[mm] = r;
+        for (int k = 0; k < N - d; ++k) mofr[r++] = mm;
+      }
+    coff[C::NTRI] = r;
+    mofr[r++] = C::NTRI;
+    coff[C::NTRI + 1] = r;
+  }
+}
+
+// compile-time loop over the local faces
+template <int F0, int F1, typename Fn>
+H3C_HD void for_faces(Fn&& fn) {
+  if constexpr (F0 < F1) {
+    fn(std::integral_constant<int, F0>{});
+    for_faces<F0 + 1, F1>(fn);
+  }
+}
+
+template <int S, int N, bool PUB>
+H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, double* __restrict__ y, const int bid,
+                 const int G, double* sm) {
+  using C = CfgC<S, N>;
+  constexpr int Q = C::Q, Q2 = C::Q2, NT = C::NT, SJ = C::SJ, SI = C::SI, BUF = C::BUF, NF = C::NF, SB = C::SB;
+  constexpr int EOS = h3::eo_size<Q>(), NA = C::NA;
+  constexpr int XE = 0, XED = 6 * Q, XP0 = 12 * Q, XW0 = 13 * Q;   // c3X sections
+  // prism: eta1 is GLL, eta0 / eta2 GL (two collocation matrices); hex / tet: one
+  struct TS {
+    double u[Q], d0[Q], d1[Q], d2[Q];
+    double w12, p1, r1, r2;
+  };
+#if defined(__CUDA_ARCH__) || !defined(H3C_HOST_EMU)
+  TS ts_;
+  auto par = [&](auto&& f) { f((int)threadIdx.x, ts_); };
+  auto sync = [&]() { __syncthreads(); };
+#else
+  static thread_local TS tsa[NT];
+  auto par = [&](auto&& f) {
+    for (int lt = 0; lt < NT; ++lt) f(lt, tsa[lt]);
+  };
+  auto sync = [&]() {};
+#endif
+  // ---- shared memory
+  double* pts = sm;
+  double* Rt = pts + 3 * Q;
+  double* W12 = Rt + 3 * Q;
+  double* Et = W12 + Q2;
+  double* Bt = Et + 6 * Q;
+  double* cbuf = sm + C::TABD;                       // [2][NCP] coefficients
+  double* hbuf = cbuf + 2 * C::NCP;                  // [2][NSMAX][12] slot headers
+  double* ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;     // [2][8] element geometry
+  double* FL = ebuf + 2 * H3_EGEO;                   // [NF][4][Q2] own-face-grid arrays per local face
+  double* B0 = FL + NF * 4 * Q2;                     // q^3 buffer (padded); BwdTrans s2; trace scratch
+  double* B1 = B0 + BUF;                             // q^3 buffer (apply); BwdTrans s1
+  double* s2 = B0;
+  double* s1 = B0 + BUF;
+  double* tb = B0;                                   // [SB][4][TMAX]
+  int* gstart = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : C::SCR_A));
+  int* gmem = gstart + C::NPM + 2;
+  int* gof = gmem + C::NPM;
+  int* coff = gof + C::NPM;
+  int* mofr = coff + C::NPM + 2;
+
+  const int32_t* cd = P.cd + cls * CD3_WORDS;
+  const int count = cd[CD3_COUNT];
+  const double* tab = P.tab;
+  const double* Ct = S == H3_TET ? tab + cd[CD3_T_C] : tab;
+  par([&](int lt, TS&) {
+    auto cp = [&](double* dst, const double* src, int n) {
+      for (int r = lt; r < n; r += NT) dst[r] = H3C_LDG(src + r);
+    };
+    cp(pts, tab + cd[CD3_T_PTS], 3 * Q);
+    cp(Rt, tab + cd[CD3_T_R], 3 * Q);
+    cp(W12, tab + cd[CD3_T_W] + Q, Q2);
+    cp(Et, tab + cd[CD3_T_E], 6 * Q);
+    if (S != H3_HEX) cp(Bt, tab + cd[CD3_T_B], C::TB);
+    if (S != H3_HEX && lt == 0) build_int_tables<S, N>(gstart, gmem, gof, coff, mofr);
+  });
+  sync();
+  par([&](int lt, TS& ts) {
+    const int ta = lt / Q, tb_ = lt % Q;
+    ts.w12 = W12[lt];
+    ts.p1 = 1.0 + pts[Q + ta];
+    ts.r1 = Rt[Q + ta];
+    ts.r2 = Rt[2 * Q + tb_];
+  });
+
+  // ---- element pipeline: scalars two elements ahead, coefficients + slot headers + geometry one
+  // element ahead (cp.async into the other buffer)
+  const int32_t* ce = P.class_elems + cd[CD3_ELEM_OFF];
+  auto scalars = [&](int i, int& e, int64_t& dof, int64_t& sb, int& ns) {
+    if (i < count) {
+      e = H3C_LDG(ce + i);
+      dof = H3C_LDG(P.dof_off + e);
+      sb = H3C_LDG(P.slot_off + e);
+      ns = (int)(H3C_LDG(P.slot_off + e + 1) - sb);
+    }
+  };
+  auto issue = [&](int buf, int e, int64_t dof, int64_t sb, int ns) {
+    double* cd_ = cbuf + buf * C::NCP;
+    double* hd_ = hbuf + buf * C::NSMAX * C::SLOTD;
+    const double* src = reinterpret_cast<const double*>(P.slots + sb);
+    par([&](int lt, TS&) {
+#if defined(__CUDA_ARCH__)
+      for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
+      for (int r = lt; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
+      if (!PUB && lt < H3_EGEO / 2)
+        __pipeline_memcpy_async(ebuf + buf * H3_EGEO + 2 * lt, P.egeo + (int64_t)e * H3_EGEO + 2 * lt,
+                                2 * sizeof(double));
+      __pipeline_commit();
+#else
+      for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
+      for (int r = lt; r < ns * C::SLOTD; r += NT) hd_[r] = src[r];
+      if (!PUB && lt < H3_EGEO / 2) {
+        ebuf[buf * H3_EGEO + 2 * lt] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt];
+        ebuf[buf * H3_EGEO + 2 * lt + 1] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt + 1];
+      }
+#endif
+    });
+  };
+  int64_t dof_n = 0, sb_n = 0, dof_nn = 0, sb_nn = 0;
+  int ns_n = 0, ns_nn = 0, e_n = 0, e_nn = 0;
+  scalars(bid, e_n, dof_n, sb_n, ns_n);
+  if (bid < count) issue(0, e_n, dof_n, sb_n, ns_n);
+  scalars(bid + G, e_nn, dof_nn, sb_nn, ns_nn);
+  int it_el = 0;
+  for (int i = bid; i < count; i += G, ++it_el) {
+    const int bsel = it_el & 1;
+#if defined(__CUDA_ARCH__)
+    __pipeline_wait_prior(0);
+#endif
+    sync();
+    const double* c = cbuf + bsel * C::NCP;
+    const double* hdr = hbuf + bsel * C::NSMAX * C::SLOTD;
+    const double* eg = ebuf + bsel * H3_EGEO;
+    const int64_t dof = dof_n;
+    const int ns = ns_n;
+    if (i + G < count) issue(bsel ^ 1, e_nn, dof_nn, sb_nn, ns_nn);
+    dof_n = dof_nn;
+    sb_n = sb_nn;
+    ns_n = ns_nn;
+    e_n = e_nn;
+    scalars(i + 2 * G, e_nn, dof_nn, sb_nn, ns_nn);
+
+    // ================= apply, phase 0: the fluxes of every coupling, folded per local face =========
+    // SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and partner
+    // traces; boundary: jump 2u, average g.  Then the transposed trace maps onto the own face grid,
+    // and per local face FL[f] = (fv, (G n)_0 fd, (G n)_1 fd, (G n)_2 fd) summed over its couplings.
+    int fmask = 0;
+    if (!PUB) {
+      for (int s = 0; s < ns; ++s) fmask |= 1 << slot_hdr(hdr, s).face;
+      for (int b0 = 0; b0 < ns; b0 += SB) {
+        const int nb = ns - b0 < SB ? ns - b0 : SB;
+        bool mapped = false;
+        for (int j = 0; j < nb; ++j) mapped |= slot_hdr(hdr, b0 + j).mkind != MAP_ID;
+        par([&](int lt, TS&) {
+          auto cnt = [&](int s) -> int { return slot_hdr(hdr, s).nt; };
+          const Batch BF(b0, nb, cnt);
+          for (int it0 = lt; it0 < BF.tot; it0 += NT) {
+            int p = it0;
+            const int s = BF.slot(p);
+            const H3Slot& h = slot_hdr(hdr, s);
+            double* tv = tb + (s - b0) * 4 * TMAX;
+            const double2 own = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+            const double ut = own.x, gt = own.y;
+            double un, gn;
+            if (h.kind) {
+              const double2 nbv = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+              un = nbv.x;
+              gn = nbv.y;
+            } else {
+              un = -ut;
+              gn = -gt;
+            }
+            const double j = ut - un, cc = 0.5 * (gt - gn);
+            const double w = h.sJ * H3C_LDG(tab + h.wtoff + p);
+            tv[p] = (h.tau * j - cc) * w;
+            tv[TMAX + p] = -0.5 * j * w;
+          }
+        });
+        sync();
+        if (mapped) {
+          // transposed maps, stage 1: tensor / row first contraction, dense complete -> tv[2], tv[3]
+          par([&](int lt, TS&) {
+            auto c1 = [&](int s) -> int {
+              const H3Slot& h = slot_hdr(hdr, s);
+              if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
+              if (h.mkind == MAP_TENSOR) return (h.nab & 255) * Q;
+              return h.mkind == MAP_DENSE ? Q2 : 0;
+            };
+            const Batch B1_(b0, nb, c1);
+            for (int it0 = lt; it0 < B1_.tot; it0 += NT) {
+              int it = it0;
+              const int s = B1_.slot(it);
+              const H3Slot& h = slot_hdr(hdr, s);
+              const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
+              double* tv = tb + (s - b0) * 4 * TMAX;
+              double a0 = 0.0, a1 = 0.0;
+              if (h.mkind == MAP_ROW) {   // tmp[pb][i_par] = sum_pa X[pb][pa][i_par] g[pa, pb]
+                const int r1 = it / Q, ib = it % Q;
+                for (int pa = 0; pa < n1; ++pa) {
+                  const double m = H3C_LDG(tab + h.moff + (r1 * n1 + pa) * Q + ib);
+                  a0 = fma(m, tv[pa * n2 + r1], a0);
+                  a1 = fma(m, tv[TMAX + pa * n2 + r1], a1);
+                }
+              } else if (h.mkind == MAP_TENSOR) {
+                const int r1 = it / Q, ib = it % Q;
+                const double* Yc = tab + h.moff2 + ib;
+                const int pst = sw ? n1 : 1;
+                int p = sw ? r1 : r1 * n2;
+                for (int r2 = 0; r2 < n2; ++r2, p += pst) {
+                  const double m = H3C_LDG(Yc + r2 * Q);
+                  a0 = fma(m, tv[p], a0);
+                  a1 = fma(m, tv[TMAX + p], a1);
+                }
+              } else {                    // dense: F(a) = sum_p M[p][a] g[p]
+                for (int p = 0; p < h.nt; ++p) {
+                  const double m = H3C_LDG(tab + h.moff + (int64_t)p * Q2 + it);
+                  a0 = fma(m, tv[p], a0);
+                  a1 = fma(m, tv[TMAX + p], a1);
+                }
+              }
+              tv[2 * TMAX + it] = a0;
+              tv[3 * TMAX + it] = a1;
+            }
+          });
+          sync();
+          // stage 2: second contraction onto the own face grid -> tv[0], tv[1]
+          par([&](int lt, TS&) {
+            for (int it0 = lt; it0 < nb * Q2; it0 += NT) {
+              const int j = it0 / Q2, a = it0 % Q2;
+              const H3Slot& h = slot_hdr(hdr, b0 + j);
+              if (h.mkind == MAP_ID) continue;
+              double* tv = tb + j * 4 * TMAX;
+              double a0 = 0.0, a1 = 0.0;
+              if (h.mkind == MAP_ROW) {   // F(i_par, i_perp) = sum_pb Y[pb][i_perp] tmp[pb][i_par]
+                const int n2 = (h.nab >> 8) & 255, perp = (h.nab >> 16) & 1;
+                const int ipar = perp ? a / Q : a % Q, iperp = perp ? a % Q : a / Q;
+                for (int pb = 0; pb < n2; ++pb) {
+                  const double m = H3C_LDG(tab + h.moff2 + pb * Q + iperp);
+                  a0 = fma(m, tv[2 * TMAX + pb * Q + ipar], a0);
+                  a1 = fma(m, tv[3 * TMAX + pb * Q + ipar], a1);
+                }
+              } else if (h.mkind == MAP_TENSOR) {
+                const int n1 = h.nab & 255, ia = a / Q, ib = a % Q;
+                const double* Xc = tab + h.moff + ia;
+                const double* t0 = tv + 2 * TMAX + ib;
+                for (int r1 = 0; r1 < n1; ++r1) {
+                  const double m = H3C_LDG(Xc + r1 * Q);
+                  a0 = fma(m, t0[r1 * Q], a0);
+                  a1 = fma(m, t0[TMAX + r1 * Q], a1);
+                }
+              } else {
+                a0 = tv[2 * TMAX + a];
+                a1 = tv[3 * TMAX + a];
+              }
+              tv[a] = a0;
+              tv[TMAX + a] = a1;
+            }
+          });
+          sync();
+        }
+        // fold into the per-face arrays (a local face carries one or two couplings, adjacent in the
+        // slot order; the first of them in this batch is the leader)
+        par([&](int lt, TS&) {
+          for (int it0 = lt; it0 < nb * Q2; it0 += NT) {
+            const int j = it0 / Q2, a = it0 % Q2, s = b0 + j;
+            const H3Slot& h = slot_hdr(hdr, s);
+            const int f = h.face;
+            const bool follows = s > 0 && slot_hdr(hdr, s - 1).face == f;
+            if (follows && j > 0) continue;
+            const int fx = fcr(S, f, 0), sd = fcr(S, f, 1), ra = fcr(S, f, 2), rb = fcr(S, f, 3);
+            const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, a / Q, a % Q);
+            double l0 = 0.0, l1 = 0.0, l2 = 0.0, l3 = 0.0;
+            auto add = [&](int jj) {
+              const H3Slot& hh = slot_hdr(hdr, b0 + jj);
+              const double* tv = tb + jj * 4 * TMAX;
+              const double fd = tv[TMAX + a];
+              l0 += tv[a];
+              l1 += (ch.c00 * hh.v[0] + ch.c01 * hh.v[1] + ch.c02 * hh.v[2]) * fd;
+              l2 += (ch.c11 * hh.v[1] + ch.c12 * hh.v[2]) * fd;
+              l3 += hh.v[2] * fd;
+            };
+            add(j);
+            if (j + 1 < nb && slot_hdr(hdr, s + 1).face == f) add(j + 1);
+            double* Ff = FL + f * 4 * Q2;
+            if (follows) {
+              Ff[a] += l0;
+              Ff[Q2 + a] += l1;
+              Ff[2 * Q2 + a] += l2;
+              Ff[3 * Q2 + a] += l3;
+            } else {
+              Ff[a] = l0;
+              Ff[Q2 + a] = l1;
+              Ff[2 * Q2 + a] = l2;
+              Ff[3 * Q2 + a] = l3;
+            }
+          }
+        });
+        sync();
+      }
+    }
+
+    // ================= BwdTrans (stdregions.py:575-597): u column in registers ====================
+    if (S == H3_HEX) {
+      par([&](int lt, TS&) {
+        if (lt < N * N) {                      // (i0, i1): i2 -> k2
+          double col[N], out[Q];
+#pragma unroll
+          for (int i = 0; i < N; ++i) col[i] = c[lt * N + i];
+          cmat<Q, N>(H3C_TA, 0, col, out);
+#pragma unroll
+          for (int k = 0; k < Q; ++k) s1[lt * Q + k] = out[k];
+        }
+      });
+      sync();
+      par([&](int lt, TS&) {
+        if (lt < N * Q) {                      // (i0, k2): i1 -> k1
+          const int i0 = lt / Q, k2 = lt % Q;
+          double col[N], out[Q];
+#pragma unroll
+          for (int i = 0; i < N; ++i) col[i] = s1[(i0 * N + i) * Q + k2];
+          cmat<Q, N>(H3C_TA, 0, col, out);
+#pragma unroll
+          for (int k = 0; k < Q; ++k) s2[i0 * SI + k * SJ + k2] = out[k];
+        }
+      });
+      sync();
+    } else {
+      // stage 1: the innermost family (prism: psi on eta1 per triangle mode; tet: C rows on eta2)
+      par([&](int lt, TS&) {
+        if (S == H3_PRISM) {
+          for (int m = lt; m < C::NPM; m += NT) {
+            double col[N], out[Q];
+#pragma unroll
+            for (int l = 0; l < N; ++l) col[l] = c[m * N + l];
+            cmat<Q, N>(H3C_TP, 0, col, out);
+#pragma unroll
+            for (int k = 0; k < Q; ++k) s1[m * Q + k] = out[k];
+          }
+        } else {
+          for (int o = lt; o < C::NPM * Q; o += NT) {
+            const int k = o % Q, m = o / Q;
+            double a = 0.0;
+            const int r0 = coff[m], cn = coff[m + 1] - r0;
+#pragma unroll
+            for (int kk = 0; kk < (N - 1 > 1 ? N - 1 : 1); ++kk)
+              if (kk < cn) a = fma(H3C_LDG(Ct + (r0 + kk) * Q + k), c[r0 + kk], a);
+            s1[o] = a;
+          }
+        }
+      });
+      sync();
+      // stage 2: group sums with the B rows; thread (g, ko) produces the whole kb line
+      // (prism: kb = k2, ko = k1; tet: kb = k1, ko = k2)
+      par([&](int lt, TS&) {
+        const int g = lt / Q, ko = lt % Q;     // NG * Q = NT
+        double out[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) out[k] = 0.0;
+        const int q0 = gstart[g], cntg = gstart[g + 1] - q0;
+        for (int qq = 0; qq < cntg; ++qq) {
+          const int m = gmem[q0 + qq];
+          const double sv = s1[m * Q + ko];
+          const double* Br = Bt + m * Q;
+#pragma unroll
+          for (int k = 0; k < Q; ++k) out[k] = fma(Br[k], sv, out[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          if (S == H3_PRISM) s2[g * SI + ko * SJ + k] = out[k];
+          else s2[g * SI + k * SJ + ko] = out[k];
+        }
+      });
+      sync();
+    }
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+      double col[NA];
+#pragma unroll
+      for (int g = 0; g < NA; ++g) col[g] = s2[g * SI + ta * SJ + tb_];
+      cmat<Q, NA>(H3C_TA, 0, col, ts.u);
+    });
+
+    if (PUB) {
+      // ================= publish: own traces (u, n.grad u) of every coupling =====================
+      // FL[f] = (u, d u / d eta_fixed, d u / d eta_ra, d u / d eta_rb) on the own face grid
+      par([&](int lt, TS& ts) {
+        const int ta = lt / Q, tb_ = lt % Q;
+        for_faces<0, NF>([&](auto Fc) {
+          constexpr int f = decltype(Fc)::value;
+          if constexpr (fc(S, f, 0) == 0) {
+            constexpr int row = fc(S, f, 1) > 0 ? 1 : 0;
+            double uf = 0.0, un = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              uf = fma(H3C_TX[XE + row * Q + k], ts.u[k], uf);
+              un = fma(H3C_TX[XED + row * Q + k], ts.u[k], un);
+            }
+            FL[f * 4 * Q2 + lt] = uf;
+            FL[f * 4 * Q2 + Q2 + lt] = un;
+          }
+        });
+#pragma unroll
+        for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
+      });
+      sync();
+      par([&](int lt, TS&) {
+        const int ta = lt / Q, tb_ = lt % Q;
+        double v[Q], w[Q];
+#pragma unroll
+        for (int m = 0; m < Q; ++m) {
+          v[m] = B0[ta * SI + m * SJ + tb_];   // line along eta1: (k0 = ta, k2 = tb)
+          w[m] = B0[ta * SI + tb_ * SJ + m];   // line along eta2: (k0 = ta, k1 = tb)
+        }
+        for_faces<0, NF>([&](auto Fc) {
+          constexpr int f = decltype(Fc)::value;
+          constexpr int fx = fc(S, f, 0);
+          if constexpr (fx != 0) {
+            constexpr int row = fx * 2 + (fc(S, f, 1) > 0 ? 1 : 0);
+            double uf = 0.0, un = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              const double val = fx == 1 ? v[k] : w[k];
+              uf = fma(H3C_TX[XE + row * Q + k], val, uf);
+              un = fma(H3C_TX[XED + row * Q + k], val, un);
+            }
+            FL[f * 4 * Q2 + lt] = uf;
+            FL[f * 4 * Q2 + Q2 + lt] = un;
+          }
+        });
+      });
+      sync();
+      // tangential derivatives: one face-grid line per task (face, direction, line)
+      par([&](int lt, TS&) {
+        for (int task = lt; task < NF * 2 * Q; task += NT) {
+          const int f = task / (2 * Q), dir = (task / Q) & 1, line = task % Q;
+          const int base = dir ? line * Q : line, st = dir ? 1 : Q;
+          const double* fu = FL + f * 4 * Q2;
+          double in[Q], out[Q];
+#pragma unroll
+          for (int j = 0; j < Q; ++j) in[j] = fu[base + j * st];
+          const int axis = fcr(S, f, dir ? 3 : 2);
+          if (S == H3_PRISM && axis == 1) eo_full<Q>(H3C_TE, 1 * EOS, in, out);
+          else eo_full<Q>(H3C_TE, 0, in, out);
+          double* fo = FL + f * 4 * Q2 + (2 + dir) * Q2;
+#pragma unroll
+          for (int j = 0; j < Q; ++j) fo[base + j * st] = out[j];
+        }
+      });
+      sync();
+      // n.grad u at own face point a = lt of every face; identity-map couplings publish directly
+      par([&](int lt, TS&) {
+        int s = 0;
+        for_faces<0, NF>([&](auto Fc) {
+          constexpr int f = decltype(Fc)::value;
+          constexpr int fx = fc(S, f, 0), sd = fc(S, f, 1), ra = fc(S, f, 2), rb = fc(S, f, 3);
+          if (s < ns && slot_hdr(hdr, s).face == f) {
+            const H3Slot& h = slot_hdr(hdr, s);
+            double* Ff = FL + f * 4 * Q2;
+            const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, lt / Q, lt % Q);
+            const double g0 = ch.c00 * h.v[0] + ch.c01 * h.v[1] + ch.c02 * h.v[2];
+            const double g1 = ch.c11 * h.v[1] + ch.c12 * h.v[2];
+            const double g2 = h.v[2];
+            const double gf = fx == 0 ? g0 : (fx == 1 ? g1 : g2);
+            const double ga = ra == 0 ? g0 : (ra == 1 ? g1 : g2);
+            const double gb = rb == 0 ? g0 : (rb == 1 ? g1 : g2);
+            const double uf = Ff[lt];
+            const double gv = gf * Ff[Q2 + lt] + ga * Ff[2 * Q2 + lt] + gb * Ff[3 * Q2 + lt];
+            Ff[Q2 + lt] = gv;
+            for (; s < ns && slot_hdr(hdr, s).face == f; ++s) {
+              const H3Slot& hs = slot_hdr(hdr, s);
+              if (hs.mkind == MAP_ID) reinterpret_cast<double2*>(P.pub + hs.pub_self)[lt] = make_double2(uf, gv);
+            }
+          }
+        });
+      });
+      bool mapped = false;
+      for (int j = 0; j < ns; ++j) mapped |= slot_hdr(hdr, j).mkind != MAP_ID;
+      if (mapped) {
+        sync();
+        for (int b0 = 0; b0 < ns; b0 += SB) {
+          const int nb = ns - b0 < SB ? ns - b0 : SB;
+          bool bm = false;
+          for (int j = 0; j < nb; ++j) bm |= slot_hdr(hdr, b0 + j).mkind != MAP_ID;
+          if (!bm) continue;
+          // forward maps, stage 1: tensor X / row Y contraction; dense complete
+          par([&](int lt, TS&) {
+            auto c1 = [&](int s) -> int {
+              const H3Slot& h = slot_hdr(hdr, s);
+              if (h.mkind == MAP_TENSOR) return (h.nab & 255) * Q;
+              if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
+              return h.mkind == MAP_DENSE ? h.nt : 0;
+            };
+            const Batch B1_(b0, nb, c1);
+            for (int it0 = lt; it0 < B1_.tot; it0 += NT) {
+              int it = it0;
+              const int s = B1_.slot(it);
+              const H3Slot& h = slot_hdr(hdr, s);
+              const double* fu = FL + h.face * 4 * Q2;
+              const double* fg = fu + Q2;
+              double* tu = tb + (s - b0) * 4 * TMAX;
+              double a0 = 0.0, a1 = 0.0;
+              if (h.mkind == MAP_ROW) {
+                const int pb = it / Q, ipar = it % Q, perp = (h.nab >> 16) & 1;
+                const double* Yr = tab + h.moff2 + pb * Q;
+#pragma unroll
+                for (int ip = 0; ip < Q; ++ip) {
+                  const double m = H3C_LDG(Yr + ip);
+                  const int o = perp ? ipar * Q + ip : ip * Q + ipar;
+                  a0 = fma(m, fu[o], a0);
+                  a1 = fma(m, fg[o], a1);
+                }
+                tu[2 * TMAX + it] = a0;
+                tu[3 * TMAX + it] = a1;
+              } else if (h.mkind == MAP_TENSOR) {
+                const int r1 = it / Q, ib = it % Q;
+                const double* X = tab + h.moff + r1 * Q;
+#pragma unroll
+                for (int ia = 0; ia < Q; ++ia) {
+                  const double m = H3C_LDG(X + ia);
+                  a0 = fma(m, fu[ia * Q + ib], a0);
+                  a1 = fma(m, fg[ia * Q + ib], a1);
+                }
+                tu[2 * TMAX + it] = a0;
+                tu[3 * TMAX + it] = a1;
+              } else {
+                const double* M = tab + h.moff + (int64_t)it * Q2;
+                for (int a = 0; a < Q2; ++a) {
+                  const double m = H3C_LDG(M + a);
+                  a0 = fma(m, fu[a], a0);
+                  a1 = fma(m, fg[a], a1);
+                }
+                reinterpret_cast<double2*>(P.pub + h.pub_self)[it] = make_double2(a0, a1);
+              }
+            }
+          });
+          sync();
+          par([&](int lt, TS&) {
+            auto c2 = [&](int s) -> int {
+              const H3Slot& h = slot_hdr(hdr, s);
+              return (h.mkind == MAP_TENSOR || h.mkind == MAP_ROW) ? h.nt : 0;
+            };
+            const Batch B2(b0, nb, c2);
+            for (int it0 = lt; it0 < B2.tot; it0 += NT) {
+              int it = it0;
+              const int s = B2.slot(it);
+              const H3Slot& h = slot_hdr(hdr, s);
+              const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
+              const double* tu = tb + (s - b0) * 4 * TMAX;
+              int p;
+              const double *Y, *m0, *m1;
+              if (h.mkind == MAP_ROW) {   // t[pa, pb] = sum_i_par X[pb][pa][i_par] tmp[pb][i_par]
+                const int pa = it / n2, pb = it % n2;
+                p = it;
+                Y = tab + h.moff + (pb * n1 + pa) * Q;
+                m0 = tu + 2 * TMAX + pb * Q;
+                m1 = tu + 3 * TMAX + pb * Q;
+              } else {
+                const int r1 = it / n2, r2 = it % n2;
+                p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
+                Y = tab + h.moff2 + r2 * Q;
+                m0 = tu + 2 * TMAX + r1 * Q;
+                m1 = tu + 3 * TMAX + r1 * Q;
+              }
+              double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+              for (int ib = 0; ib < Q; ++ib) {
+                const double m = H3C_LDG(Y + ib);
+                a0 = fma(m, m0[ib], a0);
+                a1 = fma(m, m1[ib], a1);
+              }
+              reinterpret_cast<double2*>(P.pub + h.pub_self)[p] = make_double2(a0, a1);
+            }
+          });
+          sync();
+        }
+      }
+      continue;
+    }
+
+    // ================= apply: PhysDeriv (stdregions.py:658-674) ==================================
+    // eta0 in registers; eta1 / eta2 one line per thread through B0 / B1
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
+      eo_full<Q>(H3C_TE, 0 * EOS, ts.u, ts.d0);
+    });
+    sync();
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+      double v[Q], w[Q];
+#pragma unroll
+      for (int m = 0; m < Q; ++m) {
+        v[m] = B0[ta * SI + m * SJ + tb_];
+        w[m] = B0[ta * SI + tb_ * SJ + m];
+      }
+      eo_full<Q>(H3C_TE, 1 * EOS, v, ts.d1);
+      eo_full<Q>(H3C_TE, 2 * EOS, w, ts.d2);
+#pragma unroll
+      for (int r = 0; r < Q; ++r) B1[ta * SI + r * SJ + tb_] = ts.d1[r];
+    });
+    sync();   // every line of B0 read
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+#pragma unroll
+      for (int r = 0; r < Q; ++r) B0[ta * SI + tb_ * SJ + r] = ts.d2[r];
+    });
+    sync();
+    // ================= volume terms (sipg.py:575-582) + face lifts, in registers ==================
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        ts.d1[k] = B1[k * SI + ta * SJ + tb_];
+        ts.d2[k] = B0[k * SI + ta * SJ + tb_];
+      }
+      const double lam = P.lam;
+      const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
+      const double jw12 = dJ * ts.w12;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const Chain ch = chain_t<S>(H3C_TX[XP0 + k], ts.p1, ts.r1, ts.r2);
+        const double jw = jw12 * H3C_TX[XW0 + k];
+        const double e0 = ts.d0[k], e1 = ts.d1[k], e2 = ts.d2[k];
+        const double x0 = ch.c00 * e0, x1 = ch.c01 * e0 + ch.c11 * e1, x2 = ch.c02 * e0 + ch.c12 * e1 + e2;
+        const double f0 = S00 * x0 + S01 * x1 + S02 * x2;
+        const double f1 = S01 * x0 + S11 * x1 + S12 * x2;
+        const double f2 = S02 * x0 + S12 * x1 + S22 * x2;
+        ts.u[k] = lam * jw * ts.u[k];
+        ts.d0[k] = jw * (ch.c00 * f0 + ch.c01 * f1 + ch.c02 * f2);
+        ts.d1[k] = jw * (ch.c11 * f1 + ch.c12 * f2);
+        ts.d2[k] = jw * f2;
+      }
+      // lift (the reference's scatter + final sweep, sipg.py:663-693): W_c(k0, k1, k2) += E[k_fixed] FL[f][c](a)
+      for_faces<0, NF>([&](auto Fc) {
+        constexpr int f = decltype(Fc)::value;
+        constexpr int fx = fc(S, f, 0), hi = fc(S, f, 1) > 0 ? 1 : 0;
+        constexpr bool onehot = gll_axis(S, fx);
+        constexpr int kend = hi ? Q - 1 : 0;
+        if (!((fmask >> f) & 1)) return;
+        const double* Ff = FL + f * 4 * Q2;
+        if constexpr (fx == 0) {
+          const double l0 = Ff[lt], l1 = Ff[Q2 + lt], l2 = Ff[2 * Q2 + lt], l3 = Ff[3 * Q2 + lt];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            if (onehot && k != kend) continue;
+            const double ek = H3C_TX[XE + hi * Q + k];
+            ts.u[k] = fma(ek, l0, ts.u[k]);
+            ts.d0[k] = fma(ek, l1, ts.d0[k]);
+            ts.d1[k] = fma(ek, l2, ts.d1[k]);
+            ts.d2[k] = fma(ek, l3, ts.d2[k]);
+          }
+        } else {
+          const int kf = fx == 1 ? ta : tb_, ko = fx == 1 ? tb_ : ta;   // own index on the fixed / other axis
+          if (onehot && kf != kend) return;
+          const double ek = Et[(fx * 2 + hi) * Q + kf];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            const int a = k * Q + ko;
+            ts.u[k] = fma(ek, Ff[a], ts.u[k]);
+            ts.d0[k] = fma(ek, Ff[Q2 + a], ts.d0[k]);
+            ts.d1[k] = fma(ek, Ff[2 * Q2 + a], ts.d1[k]);
+            ts.d2[k] = fma(ek, Ff[3 * Q2 + a], ts.d2[k]);
+          }
+        }
+      });
+      // ================= T = W0 + sum_a D_a^T W_a (IProductDeriv, stdregions.py:620-656) ==========
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        B0[k * SI + ta * SJ + tb_] = ts.d1[k];
+        B1[k * SI + ta * SJ + tb_] = ts.d2[k];
+      }
+      double r[Q];
+      eo_full<Q>(H3C_TE, 3 * EOS, ts.d0, r);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) ts.u[k] += r[k];
+    });
+    sync();
+    par([&](int lt, TS&) {
+      const int ta = lt / Q, tb_ = lt % Q;
+      double v[Q], w[Q], r1[Q], r2[Q];
+#pragma unroll
+      for (int m = 0; m < Q; ++m) {
+        v[m] = B0[ta * SI + m * SJ + tb_];
+        w[m] = B1[ta * SI + tb_ * SJ + m];
+      }
+      eo_full<Q>(H3C_TE, 4 * EOS, v, r1);
+      eo_full<Q>(H3C_TE, 5 * EOS, w, r2);
+#pragma unroll
+      for (int m = 0; m < Q; ++m) {
+        B0[ta * SI + m * SJ + tb_] = r1[m];
+        B1[ta * SI + tb_ * SJ + m] = r2[m];
+      }
+    });
+    sync();
+    // ================= IProduct (stdregions.py:599-618): y = Phi^T T ==============================
+    par([&](int lt, TS& ts) {
+      const int ta = lt / Q, tb_ = lt % Q;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) ts.u[k] += B0[k * SI + ta * SJ + tb_] + B1[k * SI + ta * SJ + tb_];
+      double o[NA];
+      cmatT<Q, NA>(H3C_TA, 0, ts.u, o);
+#pragma unroll
+      for (int g = 0; g < NA; ++g) s2[g * SI + ta * SJ + tb_] = o[g];
+    });
+    sync();
+    if (S == H3_HEX) {
+      par([&](int lt, TS&) {
+        if (lt < N * Q) {                      // (i0, k2): k1 -> i1
+          const int i0 = lt / Q, k2 = lt % Q;
+          double col[Q], out[N];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) col[k] = s2[i0 * SI + k * SJ + k2];
+          cmatT<Q, N>(H3C_TA, 0, col, out);
+#pragma unroll
+          for (int i = 0; i < N; ++i) s1[(i0 * N + i) * Q + k2] = out[i];
+        }
+      });
+      sync();
+      par([&](int lt, TS&) {
+        if (lt < N * N) {                      // (i0, i1): k2 -> i2
+          double col[Q], out[N];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) col[k] = s1[lt * Q + k];
+          cmatT<Q, N>(H3C_TA, 0, col, out);
+#pragma unroll
+          for (int i = 0; i < N; ++i) y[dof + lt * N + i] = out[i];
+        }
+      });
+    } else {
+      par([&](int lt, TS&) {
+        for (int o = lt; o < C::NPM * Q; o += NT) {
+          const int k = o % Q, m = o / Q, g = gof[m];
+          const double* Br = Bt + m * Q;
+          double a = 0.0;
+          if (S == H3_PRISM) {   // s1[m][k1] = sum_k2 B[m][k2] s2[g][k1][k2]
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) a = fma(Br[k2], s2[g * SI + k * SJ + k2], a);
+          } else {               // s1[m][k2] = sum_k1 B[m][k1] s2[g][k1][k2]
+#pragma unroll
+            for (int k1 = 0; k1 < Q; ++k1) a = fma(Br[k1], s2[g * SI + k1 * SJ + k], a);
+          }
+          s1[o] = a;
+        }
+      });
+      sync();
+      par([&](int lt, TS&) {
+        if (S == H3_PRISM) {
+          for (int m = lt; m < C::NPM; m += NT) {
+            double col[Q], out[N];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) col[k] = s1[m * Q + k];
+            cmatT<Q, N>(H3C_TP, 0, col, out);
+#pragma unroll
+            for (int l = 0; l < N; ++l) y[dof + m * N + l] = out[l];
+          }
+        } else {
+          for (int r = lt; r < C::NC; r += NT) {
+            const int m = mofr[r];
+            double a = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < Q; ++k2) a = fma(H3C_LDG(Ct + r * Q + k2), s1[m * Q + k2], a);
+            y[dof + r] = a;
+          }
+        }
+      });
+    }
+  }
+}
+
+template <int Q>
+constexpr int h3c_minb() { return Q >= 8 ? SIPG_H3C_MINB8 : (Q == 7 ? 7 : (Q == 6 ? 8 : 16)); }
+
+template <int S, int N, bool PUB>
+__global__ void __launch_bounds__((N + 1) * (N + 1), h3c_minb<N + 1>())
+k_h3c(const H3Plan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(16) double h3c_sm[];
+  body<S, N, PUB>(P, cls, x, y, (int)blockIdx.x, (int)gridDim.x, h3c_sm);
+}
+
+// __constant__ tables of one (shape, n) instantiation: the h3 tables (D, A, psi, even-odd blocks)
+// plus the endpoint rows, 1 + eta0 and the eta0 weights
+template <int S, int N>
+cudaError_t h3c_upload(const double* D, const double* A, const double* psi, const double* E, const double* ED,
+                       const double* pts, const double* W) {
+  constexpr int Q = N + 1;
+  cudaError_t e = h3::h3_upload<S, N>(D, A, psi);
+  if (e != cudaSuccess) return e;
+  double xt[14 * Q];
+  for (int i = 0; i < 6 * Q; ++i) {
+    xt[i] = E[i];
+    xt[6 * Q + i] = ED[i];
+  }
+  for (int k = 0; k < Q; ++k) {
+    xt[12 * Q + k] = 1.0 + pts[k];
+    xt[13 * Q + k] = W[k];
+  }
+  return cudaMemcpyToSymbol(c3X<S, N>, xt, sizeof(double) * 14 * Q);
+}
+
+}  // namespace h3c

@@ -1,0 +1,92 @@
+// TEST INFRASTRUCTURE ONLY (never linked into libsipg.so): runs the element body of the config-4
+// register-column kernels (paper_2504_03573_b200/csrc/sipg_h3c.cuh) on the host, thread after thread
+// between the barriers, on a flattened plan3d plan.  tests/test_h3c_emu.py compares it with the numpy
+// emulation of the plan (oracle/h3_emulate.py) — indexing and phase-order bugs show up on CPU.
+#define H3C_HOST_EMU 1
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include "../../paper_2504_03573_b200/csrc/sipg_h3c.cuh"
+#include "sipg.h"
+
+namespace {
+template <int Q>
+void eo_build(const double* D, double* eo) {
+  constexpr int H = Q / 2, EO = h3::eo_size<Q>();
+  for (int t = 0; t < 2; ++t)
+    for (int a = 0; a < 3; ++a) {
+      const double* Da = D + a * Q * Q;
+      auto M = [&](int k, int j) { return t == 0 ? Da[k * Q + j] : Da[j * Q + k]; };
+      double* o = eo + (t * 3 + a) * EO;
+      for (int k = 0; k < H; ++k)
+        for (int j = 0; j < H; ++j) {
+          o[k * H + j] = 0.5 * (M(k, j) + M(k, Q - 1 - j));
+          o[H * H + k * H + j] = 0.5 * (M(k, j) - M(k, Q - 1 - j));
+        }
+      for (int k = 0; k < H; ++k) {
+        o[2 * H * H + k] = (Q & 1) ? M(k, H) : 0.0;
+        o[2 * H * H + H + k] = (Q & 1) ? M(H, k) : 0.0;
+      }
+    }
+}
+
+template <int S, int N>
+void run_class(const H3Plan& P, const sipg_h3_desc* d, int cls, const double* x, double* y, int phases) {
+  using C = h3c::CfgC<S, N>;
+  using T = h3c::HostTabs<S, N>;
+  constexpr int Q = N + 1;
+  const int32_t* cd = d->class_desc + cls * CD3_WORDS;
+  const double* tab = d->tables;
+  constexpr int NA = S == H3_HEX ? N : N + 1;
+  std::memcpy(T::A, tab + cd[CD3_T_A], sizeof(double) * Q * NA);
+  if (S == H3_PRISM) std::memcpy(T::P, tab + cd[CD3_T_C], sizeof(double) * Q * N);
+  eo_build<Q>(tab + cd[CD3_T_D], T::E);
+  for (int i = 0; i < 6 * Q; ++i) {
+    T::X[i] = tab[cd[CD3_T_E] + i];
+    T::X[6 * Q + i] = tab[cd[CD3_T_ED] + i];
+  }
+  for (int k = 0; k < Q; ++k) {
+    T::X[12 * Q + k] = 1.0 + tab[cd[CD3_T_PTS] + k];
+    T::X[13 * Q + k] = tab[cd[CD3_T_W] + k];
+  }
+  const int G = 3;   // a few "CTAs": exercises the double-buffered element pipeline
+  for (int b = 0; b < G; ++b) {
+    if (phases == 0) {
+      std::vector<double> sm(C::smem_bytes(true) / 8 + 8, NAN);
+      h3c::body<S, N, true>(P, cls, x, y, b, G, sm.data());
+    } else {
+      std::vector<double> sm(C::smem_bytes(false) / 8 + 8, NAN);
+      h3c::body<S, N, false>(P, cls, x, y, b, G, sm.data());
+    }
+  }
+}
+
+template <int S>
+bool dispatch_n(const H3Plan& P, const sipg_h3_desc* d, int cls, int n, const double* x, double* y, int phase) {
+  switch (n) {
+    case 2: run_class<S, 2>(P, d, cls, x, y, phase); return true;
+    case 3: run_class<S, 3>(P, d, cls, x, y, phase); return true;
+    case 4: run_class<S, 4>(P, d, cls, x, y, phase); return true;
+    case 5: run_class<S, 5>(P, d, cls, x, y, phase); return true;
+    case 6: run_class<S, 6>(P, d, cls, x, y, phase); return true;
+    case 7: run_class<S, 7>(P, d, cls, x, y, phase); return true;
+  }
+  return false;
+}
+}  // namespace
+
+// phase 0: publish every class into pub; phase 1: apply every class (reads pub) into y
+extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, double* pub, int phase) {
+  H3Plan P{d->class_desc, d->class_elems, d->dof_off, d->elem_geom, d->slot_off, (const H3Slot*)d->slots,
+           d->tables, pub, d->lambda};
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    if (cd[CD3_COUNT] <= 0) continue;
+    bool ok = false;
+    if (cd[CD3_SHAPE] == H3_HEX) ok = dispatch_n<H3_HEX>(P, d, c, cd[CD3_N], x, y, phase);
+    if (cd[CD3_SHAPE] == H3_PRISM) ok = dispatch_n<H3_PRISM>(P, d, c, cd[CD3_N], x, y, phase);
+    if (cd[CD3_SHAPE] == H3_TET) ok = dispatch_n<H3_TET>(P, d, c, cd[CD3_N], x, y, phase);
+    if (!ok) return 1;
+  }
+  return 0;
+}
