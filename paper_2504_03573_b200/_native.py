@@ -209,7 +209,7 @@ class NativePlan:
         self._lib = lib
         self.handle = h
         self.n_dofs = pb.n_dofs
-        self.n_classes = 2 * int(keep[0].shape[0])   # launch units: publish kernels, then apply kernels
+        self.n_classes = 3 * int(keep[0].shape[0])   # launch units: publish, apply, flux kernels per class
         self._keep = None
 
     def set_halo(self, part) -> None:

@@ -120,8 +120,15 @@ struct H3State {
   std::vector<const H3Entry*> kern;
   std::vector<int> grid_pub, grid_apply;   // persistent grids: min(count, SMs x resident CTAs)
   std::vector<int> cap_pub, cap_apply;     // SMs x resident CTAs
+  // register-column kernels: own-grid fluxes per slot, written by the flux kernel (one warp per slot,
+  // work list cslots = slot ids in class-list order; cslot_off[i] = first entry of class-list position i)
+  bool flux = false;
+  double* fb = nullptr;
+  int64_t* fb_off_d = nullptr;
+  H3FluxRec* frec_d = nullptr;
+  std::vector<int64_t> cslot_off;
   // streamed host apply (see build_stream_schedule_h3): per stage, publish rows and apply rows
-  struct Launch { int row, grid; const H3Entry* k; };
+  struct Launch { int row, grid; const H3Entry* k; int64_t flux_first, flux_count; };
   std::vector<std::vector<Launch>> st_pub, st_comp;
   int32_t* rows_d = nullptr;
   H3Plan hps{};
@@ -672,7 +679,8 @@ const NcclApi& nccl() {
     if (_r != ncclSuccess) return fail(SIPG_ERR_COMM, std::string(#call) + ": " + nccl().errorString(_r)); \
   } while (0)
 
-// launch the classes of one pass (0 publish, 1 apply) whose role is selected by `want` (-1: all)
+// launch the classes of one pass (0 publish, 1 apply, 2 flux: the slots of those classes, adjacent
+// classes merged into one launch) whose role is selected by `want` (-1: all)
 int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
   auto go = [&](int c) {
@@ -680,6 +688,26 @@ int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_d
     const int crole = h->cd[c * CD3_WORDS + CD3_ROLE];
     return count > 0 && (want < 0 || crole == want);
   };
+  if (pass == 2) {
+    if (!h->flux) return 0;
+    int64_t first = -1, last = -1;
+    for (int c = 0; c <= p->n_cls; ++c) {
+      const bool on = c < p->n_cls && go(c);
+      const int64_t a = on ? h->cslot_off[h->cd[c * CD3_WORDS + CD3_ELEM_OFF]] : 0;
+      const int64_t b = on ? h->cslot_off[h->cd[c * CD3_WORDS + CD3_ELEM_OFF] + h->cd[c * CD3_WORDS + CD3_COUNT]] : 0;
+      if (on && first >= 0 && a == last) {
+        last = b;
+        continue;
+      }
+      if (first >= 0 && last > first) {
+        sipg_h3c_flux_launch(h->hp, first, last - first, s);
+        ++p->launches;
+      }
+      first = on ? a : -1;
+      last = on ? b : -1;
+    }
+    return 0;
+  }
   int n = 0, nsmall = 0;
   for (int c = 0; c < p->n_cls; ++c) {
     if (!go(c)) continue;
@@ -726,7 +754,9 @@ int h3_exchange(sipg_plan* p) {
 int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
   int rc = 0;
+  // pass 0 publish, 2 flux (register-column kernels; a no-op for the first generation), 1 apply
   if (role == 1) {
+    if ((rc = h3_launch(p, 2, 1, x_dev, y_dev, s))) return rc;
     if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
     CK(cudaGetLastError());
     return 0;
@@ -746,9 +776,11 @@ int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStr
     CK(cudaEventRecord(h->ev_comm, h->s_comm));
   }
   if ((rc = h3_launch(p, 0, 0, x_dev, y_dev, s))) return rc;
+  if ((rc = h3_launch(p, 2, 0, x_dev, y_dev, s))) return rc;
   if ((rc = h3_launch(p, 1, 0, x_dev, y_dev, s))) return rc;
   if (role < 0) {
     if (halo) CK(cudaStreamWaitEvent(s, h->ev_comm, 0));
+    if ((rc = h3_launch(p, 2, 1, x_dev, y_dev, s))) return rc;
     if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
   }
   CK(cudaGetLastError());
@@ -832,7 +864,8 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
         rows[(int64_t)r * CD3_WORDS + CD3_ELEM_OFF] += i0;
         const int cap = pass == 0 ? h->cap_pub[c] : h->cap_apply[c];
         const int g = (i1 - i0) < cap ? (i1 - i0) : cap;
-        (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c]});
+        const int64_t f0 = h->cslot_off[cd[CD3_ELEM_OFF] + i0], f1 = h->cslot_off[cd[CD3_ELEM_OFF] + i1];
+        (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c], f0, f1 - f0});
         i0 = i1;
       }
     }
@@ -853,6 +886,15 @@ int sipg_h3_apply_traces(sipg_plan* p, const double* x_dev, const double* traces
   H3State* h = p->h3;
   H3Plan hp = h->hp;
   hp.pub = const_cast<double*>(traces_dev);
+  for (int c = 0; c < p->n_cls; ++c) {
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    if (count == 0 || h->cd[c * CD3_WORDS + CD3_ROLE] == 2) continue;
+    if (h->flux) {
+      const int eo = h->cd[c * CD3_WORDS + CD3_ELEM_OFF];
+      sipg_h3c_flux_launch(hp, h->cslot_off[eo], h->cslot_off[eo + count] - h->cslot_off[eo], (cudaStream_t)stream);
+      ++p->launches;
+    }
+  }
   for (int c = 0; c < p->n_cls; ++c) {
     const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
     if (count == 0 || h->cd[c * CD3_WORDS + CD3_ROLE] == 2) continue;
@@ -1013,7 +1055,43 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       return fail(SIPG_ERR_CUDA, std::string("published-trace buffer: ") + cudaGetErrorString(e));
     }
   }
-  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda};
+  {   // own-grid flux buffer: element e's slots from fb_off[e], 2 q^2 doubles each; flux work list
+    std::vector<int64_t> fbo((size_t)d->n_elements + 1, 0);
+    std::vector<int32_t> qe(d->n_elements, 0);
+    std::vector<H3FluxRec> fr((size_t)d->n_slots);
+    h->cslot_off.assign((size_t)d->n_elements + 1, 0);
+    for (int c = 0; c < d->n_classes; ++c) {
+      const int32_t* cd = d->class_desc + c * CD3_WORDS;
+      for (int i = 0; i < cd[CD3_COUNT]; ++i) qe[d->class_elems[cd[CD3_ELEM_OFF] + i]] = cd[CD3_Q];
+    }
+    for (int64_t e = 0; e < d->n_elements; ++e)
+      fbo[e + 1] = fbo[e] + 2ll * qe[e] * qe[e] * (d->slot_off[e + 1] - d->slot_off[e]);
+    const H3Slot* sl = (const H3Slot*)d->slots;
+    int64_t k = 0;
+    for (int64_t i = 0; i < d->n_elements; ++i) {   // class-list order
+      const int32_t e = d->class_elems[i];
+      h->cslot_off[i] = k;
+      for (int64_t q = d->slot_off[e]; q < d->slot_off[e + 1]; ++q, ++k) {
+        const H3Slot& s0 = sl[q];
+        fr[k] = H3FluxRec{s0.pub_self, s0.pub_other, (fbo[e] + 2ll * qe[e] * qe[e] * (q - d->slot_off[e])) * 16 + qe[e],
+                          s0.tau, s0.sJ, s0.nt, s0.mkind | (s0.kind << 8), s0.nab, s0.moff, s0.moff2, s0.wtoff};
+      }
+    }
+    h->cslot_off[d->n_elements] = k;
+    h->flux = gen == 1;
+    if ((rc = upload(fbo.data(), d->n_elements + 1, &h->fb_off_d)) || (rc = upload(fr.data(), d->n_slots, &h->frec_d))) {
+      sipg_plan_destroy(p);
+      return rc;
+    }
+    if (h->flux && fbo[d->n_elements] > 0) {
+      cudaError_t e = cudaMalloc((void**)&h->fb, sizeof(double) * fbo[d->n_elements]);
+      if (e != cudaSuccess) {
+        sipg_plan_destroy(p);
+        return fail(SIPG_ERR_CUDA, std::string("own-grid flux buffer: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda, h->fb, h->fb_off_d, h->frec_d};
   h->fork_all = getenv("SIPG_H3_FORK") && atoi(getenv("SIPG_H3_FORK")) != 0;
   for (const H3Entry* k : h->kern) {
     cudaError_t e1 = cudaFuncSetAttribute((const void*)k->pub, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1161,17 +1239,21 @@ int sipg_apply(sipg_plan* p, const double* x_dev, double* y_dev, void* stream) {
 
 int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_dev, void* stream) {
   if (!p || !x_dev || !y_dev || cls < 0 || (cls >= p->n_cls && !p->h3)) return fail(SIPG_ERR_ARG, "bad argument");
-  if (p->h3) {   // hybrid plans: launch units 0..n-1 = publish kernels, n..2n-1 = apply kernels
-    if (cls >= 2 * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) {   // hybrid plans: launch units 0..n-1 = publish, n..2n-1 = apply, 2n..3n-1 = flux kernels
+    if (cls >= 3 * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
     H3State* h = p->h3;
     const int c = cls % p->n_cls;
     const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
-    if (count == 0) return 0;
     const H3Entry* k = h->kern[c];
+    if (count == 0 || (cls >= 2 * p->n_cls && !h->flux)) return 0;
     if (cls < p->n_cls)
       k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
-    else
+    else if (cls < 2 * p->n_cls)
       k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+    else {
+      const int eo = h->cd[c * CD3_WORDS + CD3_ELEM_OFF];
+      sipg_h3c_flux_launch(h->hp, h->cslot_off[eo], h->cslot_off[eo + count] - h->cslot_off[eo], (cudaStream_t)stream);
+    }
     ++p->launches;
     CK(cudaGetLastError());
     return 0;
@@ -1186,11 +1268,12 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
 }
 
 int sipg_plan_class_info(const sipg_plan* p, int32_t cls, int32_t* out6) {
-  if (!p || cls < 0 || !out6 || cls >= (p->h3 ? 2 : 1) * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
-  if (p->h3) {   // shape codes 3/4/5 = hex/prism/tet of a hybrid plan; kernel kind 8 publish, 9 apply
+  if (!p || cls < 0 || !out6 || cls >= (p->h3 ? 3 : 1) * p->n_cls) return fail(SIPG_ERR_ARG, "bad argument");
+  if (p->h3) {   // shape codes 3/4/5 = hex/prism/tet of a hybrid plan; kernel kind 8 publish, 9 apply, 10 flux
     const int32_t* cd = p->h3->cd.data() + (cls % p->n_cls) * CD3_WORDS;
     out6[0] = 3 + cd[CD3_SHAPE]; out6[1] = cd[CD3_N]; out6[2] = cd[CD3_Q]; out6[3] = 0;
-    out6[4] = cd[CD3_COUNT]; out6[5] = cls < p->n_cls ? 8 : 9;
+    out6[4] = cls >= 2 * p->n_cls && !p->h3->flux ? 0 : cd[CD3_COUNT];
+    out6[5] = cls < p->n_cls ? 8 : (cls < 2 * p->n_cls ? 9 : 10);
     return 0;
   }
   const int32_t* cd = p->cd_host.data() + cls * CD_WORDS;
@@ -1344,9 +1427,13 @@ static int enqueue_streamed(sipg_plan* p, const double* x_host, double* y_host, 
       }
       if ((rc = group_end(p))) return rc;
       if ((rc = group_begin(p, s, (int)h->st_comp[k].size(), (int)h->st_comp[k].size()))) return rc;
-      for (const auto& L : h->st_comp[k]) {
-        L.k->apply<<<L.grid, L.k->threads, L.k->smem_apply, group_stream(p)>>>(h->hps, L.row, p->x_stage,
-                                                                                 p->y_stage);
+      for (const auto& L : h->st_comp[k]) {   // a stage row's flux kernel, then its apply kernel, on one stream
+        cudaStream_t st = group_stream(p);
+        if (h->flux) {
+          sipg_h3c_flux_launch(h->hps, L.flux_first, L.flux_count, st);
+          ++p->launches;
+        }
+        L.k->apply<<<L.grid, L.k->threads, L.k->smem_apply, st>>>(h->hps, L.row, p->x_stage, p->y_stage);
         ++p->launches;
       }
       if ((rc = group_end(p))) return rc;
@@ -1405,7 +1492,7 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
       const int32_t* cd = p->h3->cd.data() + c * CD3_WORDS;
       if (cd[CD3_COUNT] > 0) k += cd[CD3_ROLE] == 2 ? 1 : 2;
     }
-    return k;
+    return k + (p->h3->flux ? 1 : 0);   // + the flux kernel (one launch over every slot)
   }
   for (int c = 0; c < p->n_cls; ++c) {
     if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->cd_host[c * CD_WORDS + CD_ROLE] != 2) ++k;
@@ -1423,7 +1510,10 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
   if (!p->streamed) return sipg_plan_kernels_per_apply(p);
   int k = 0;
   if (p->h3) {
-    for (int i = 0; i < p->n_chunks; ++i) k += (int)(p->h3->st_pub[i].size() + p->h3->st_comp[i].size());
+    for (int i = 0; i < p->n_chunks; ++i) {
+      k += (int)p->h3->st_pub[i].size();
+      k += (int)p->h3->st_comp[i].size() * (p->h3->flux ? 2 : 1);
+    }
     return k;
   }
   for (int i = 0; i < p->n_chunks; ++i) k += (int)(p->pub[i].size() + p->comp[i].size());
@@ -1448,6 +1538,9 @@ int sipg_plan_destroy(sipg_plan* p) {
     for (void* b : p->h3->bufs)
       if (b) cudaFree(b);
     if (p->h3->pub) cudaFree(p->h3->pub);
+    if (p->h3->fb) cudaFree(p->h3->fb);
+    if (p->h3->fb_off_d) cudaFree(p->h3->fb_off_d);
+    if (p->h3->frec_d) cudaFree(p->h3->frec_d);
     if (p->h3->rows_d) cudaFree(p->h3->rows_d);
     delete p->h3;
     p->h3 = nullptr;

@@ -20,8 +20,8 @@ H3Entry entry0() {
 template <int S, int N>
 H3Entry entry1() {
   using C = h3c::CfgC<S, N>;
-  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, true>, &h3c::k_h3c<S, N, false>, C::NT, C::smem_bytes(true),
-                 C::smem_bytes(false), &h3c::h3c_upload<S, N>};
+  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, 1>, &h3c::k_h3c<S, N, 0>, C::NT, C::smem_bytes(1),
+                 C::smem_bytes(0), &h3c::h3c_upload<S, N>};
 }
 template <int S>
 void add(std::vector<H3Entry>& v) {
@@ -44,4 +44,10 @@ void sipg_register_h3(std::vector<H3Entry>& v) {
   add<H3_HEX>(v);
   add<H3_PRISM>(v);
   add<H3_TET>(v);
+}
+
+void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, cudaStream_t stream) {
+  if (count <= 0) return;
+  const int64_t ctas = (count + H3C_FLUX_WPB - 1) / H3C_FLUX_WPB;
+  h3c::k_h3c_flux<<<(unsigned)ctas, 32 * H3C_FLUX_WPB, 0, stream>>>(P, first, count);
 }

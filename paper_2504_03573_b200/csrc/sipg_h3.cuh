@@ -73,7 +73,19 @@ struct H3Plan {
   const double* tab;
   double* pub;
   double lam;
+  // register-column kernels (sipg_h3c.cuh): own-grid fluxes (fv, fd) per slot, written by the flux
+  // kernels; element e's slots are contiguous from fb_off[e], 2 q^2 doubles each
+  double* fb;
+  const int64_t* fb_off;
+  const struct H3FluxRec* frec;   // the flux kernel's work list: one record per slot, class-list order
 };
+// what the flux kernel needs of a slot, 64 bytes, in work-list order (built by sipg_h3_plan_create)
+struct H3FluxRec {
+  int64_t pub_self, pub_other, fb_q;   // fb_q = (offset into fb) * 16 + q of the owning element
+  double tau, sJ;
+  int32_t nt, mk_kind, nab, moff, moff2, wtoff;   // mk_kind = mkind | kind << 8
+};
+static_assert(sizeof(H3FluxRec) == 64, "H3FluxRec layout");
 
 namespace h3 {
 

@@ -17,3 +17,5 @@ struct H3Entry {
   H3UploadFn upload;
 };
 void sipg_register_h3(std::vector<H3Entry>& v);
+// generation 1: the flux kernel (one warp per slot) over cslots[first, first + count), between publish and apply
+void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, cudaStream_t stream);

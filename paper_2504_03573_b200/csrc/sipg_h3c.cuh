@@ -10,10 +10,13 @@
 //     D0^T and the first IProduct stage never touch shared memory;
 //   * eta1 / eta2 derivatives are one line per thread through two (bank-padded) q^3 buffers,
 //     even-odd factorised with __constant__ operands;
-//   * faces are compile-time unrolled (fixed axis, side, run axes are constants of the shape): the
-//     fluxes of all couplings are evaluated first (they need the published traces only), folded per
-//     local face into four own-face-grid arrays, and lifted straight into the register columns
-//     (one-hot GLL endpoint rows touch the boundary columns only);
+//   * three kernels per class.  publish: own traces (u, n.grad u) of every coupling at its trace
+//     points.  flux: the SIP flux of every coupling from the published own and partner traces and
+//     the transposed trace maps back onto the own face grid (the reference's per-interface phase 2,
+//     sipg.py:607-661) -- all the irregular, DRAM-latency-bound work, in a kernel that needs few
+//     registers and runs at full occupancy.  apply: the element-local work; the own-grid fluxes
+//     arrive by cp.async behind BwdTrans / PhysDeriv and are lifted straight into the register
+//     columns, faces compile-time unrolled (one-hot GLL endpoint rows touch the boundary columns only);
 //   * the publish kernel takes u and d/d eta_fixed on the faces from the register columns (eta0
 //     faces) or from one line read per thread (eta1 / eta2 faces) and the tangential derivatives as
 //     even-odd lines on the face grids.
@@ -35,6 +38,23 @@
 #define H3C_LDG(p) (*(p))
 #endif
 
+// build knobs (measured variants, tools/h3c_variants.sh)
+#ifndef H3C_MAP_U8
+#define H3C_MAP_U8 1        // transposed-map contractions: eight predicated, unrolled steps
+#endif
+#ifndef H3C_ITEM_U
+#define H3C_ITEM_U 0        // ragged tet stages: item loops unrolled (measured slower: spills)
+#endif
+#if H3C_MAP_U8
+#define H3C_MAPLOOP(i, n) _Pragma("unroll") for (int i = 0; i < 8; ++i) if (i < (n))
+#else
+#define H3C_MAPLOOP(i, n) for (int i = 0; i < (n); ++i)
+#endif
+#if H3C_ITEM_U
+#define H3C_ITEM_UNROLL _Pragma("unroll")
+#else
+#define H3C_ITEM_UNROLL _Pragma("unroll 1")
+#endif
 #ifndef SIPG_H3C_MINB8
 #define SIPG_H3C_MINB8 7            // resident CTAs per SM the registers must allow, q = 8 (64 threads)
 #endif
@@ -204,17 +224,19 @@ struct CfgC {
   static constexpr int S1 = S == H3_HEX ? N * N * Q : NPM * Q;
   static constexpr int NSMAX = S == H3_HEX ? 12 : (S == H3_PRISM ? 8 : 4);
   static constexpr int SLOTD = 12;
-  static constexpr int SB = Q >= 8 ? 4 : 2;                                   // slots per map batch
+  static constexpr int SB = 4;                                  // slots per map batch
   static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
   static constexpr int TABD = (3 * Q + 3 * Q + Q2 + 6 * Q + TB + 1) & ~1;     // pts R W12 E B
   static constexpr int imax(int a, int b) { return a > b ? a : b; }
-  static constexpr int SCR_A = (imax(2 * BUF, SB * 4 * TMAX) + 1) & ~1;
-  static constexpr int SCR_P = (imax(BUF + S1, SB * 4 * TMAX) + 1) & ~1;
+  static constexpr int SCR_P = (imax(BUF + S1, SB * 4 * TMAX) + 1) & ~1;      // publish: u, s1 | map scratch
+  static constexpr int FBN = NSMAX * 2 * Q2;                                   // own-grid fluxes of an element
   static constexpr int NI = 4 * NPM + 4 + NC + 16;
-  static constexpr int doubles(bool pub) {
-    return TABD + 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + NF * 4 * Q2 + (pub ? SCR_P : SCR_A);
+  // kernel modes: 0 apply, 1 publish
+  static constexpr int doubles(int mode) {
+    return mode == 1 ? 16 + TABD + 2 * NCP + 2 * NSMAX * SLOTD + NF * 4 * Q2 + SCR_P
+                     : 16 + TABD + 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + FBN + 2 * BUF + (BUF & 1);
   }
-  static constexpr size_t smem_bytes(bool pub) { return sizeof(double) * doubles(pub) + sizeof(int) * NI; }
+  static constexpr size_t smem_bytes(int mode) { return sizeof(double) * doubles(mode) + sizeof(int) * NI; }
 };
 
 // triangle-mode groups and tet mode offsets (h3::build_int_tables), by one thread
@@ -262,17 +284,16 @@ H3C_HD void for_faces(Fn&& fn) {
   }
 }
 
-template <int S, int N, bool PUB>
+template <int S, int N, int MODE>
 H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, double* __restrict__ y, const int bid,
                  const int G, double* sm) {
   using C = CfgC<S, N>;
+  constexpr bool PUB = MODE == 1, APP = MODE == 0;
   constexpr int Q = C::Q, Q2 = C::Q2, NT = C::NT, SJ = C::SJ, SI = C::SI, BUF = C::BUF, NF = C::NF, SB = C::SB;
   constexpr int EOS = h3::eo_size<Q>(), NA = C::NA;
   constexpr int XE = 0, XED = 6 * Q, XP0 = 12 * Q, XW0 = 13 * Q;   // c3X sections
-  // prism: eta1 is GLL, eta0 / eta2 GL (two collocation matrices); hex / tet: one
   struct TS {
     double u[Q], d0[Q], d1[Q], d2[Q];
-    double w12, p1, r1, r2;
   };
 #if defined(__CUDA_ARCH__) || !defined(H3C_HOST_EMU)
   TS ts_;
@@ -285,22 +306,24 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   };
   auto sync = [&]() {};
 #endif
-  // ---- shared memory
-  double* pts = sm;
+  // ---- shared memory (CfgC::doubles)
+  long long* ring = reinterpret_cast<long long*>(sm);                  // [3][5] element scalars (e, ns, dof, sb, fbo)
+  double* pts = sm + 16;
   double* Rt = pts + 3 * Q;
   double* W12 = Rt + 3 * Q;
   double* Et = W12 + Q2;
   double* Bt = Et + 6 * Q;
-  double* cbuf = sm + C::TABD;                       // [2][NCP] coefficients
-  double* hbuf = cbuf + 2 * C::NCP;                  // [2][NSMAX][12] slot headers
-  double* ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;     // [2][8] element geometry
-  double* FL = ebuf + 2 * H3_EGEO;                   // [NF][4][Q2] own-face-grid arrays per local face
-  double* B0 = FL + NF * 4 * Q2;                     // q^3 buffer (padded); BwdTrans s2; trace scratch
-  double* B1 = B0 + BUF;                             // q^3 buffer (apply); BwdTrans s1
+  double* cbuf = sm + 16 + C::TABD;                          // [2][NCP] coefficients
+  double* hbuf = cbuf + 2 * C::NCP;                     // [2][NSMAX][12] slot headers
+  double* ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;                    // apply: [2][8] element geometry
+  double* fbuf = ebuf + 2 * H3_EGEO;                                // apply: [ns][2][Q2] own-grid fluxes
+  double* FL = hbuf + 2 * C::NSMAX * C::SLOTD;                      // publish: [NF][4][Q2] face arrays
+  double* B0 = APP ? fbuf + C::FBN : FL + NF * 4 * Q2;        // q^3 buffer (padded); s2; map scratch
+  double* B1 = B0 + BUF;                                            // q^3 buffer (apply); s1
   double* s2 = B0;
   double* s1 = B0 + BUF;
-  double* tb = B0;                                   // [SB][4][TMAX]
-  int* gstart = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : C::SCR_A));
+  double* tb = B0;                                                  // publish / flux: [SB][4][TMAX]
+  int* gstart = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : 2 * BUF + (BUF & 1)));
   int* gmem = gstart + C::NPM + 2;
   int* gof = gmem + C::NPM;
   int* coff = gof + C::NPM;
@@ -310,38 +333,44 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   const int count = cd[CD3_COUNT];
   const double* tab = P.tab;
   const double* Ct = S == H3_TET ? tab + cd[CD3_T_C] : tab;
-  par([&](int lt, TS&) {
-    auto cp = [&](double* dst, const double* src, int n) {
-      for (int r = lt; r < n; r += NT) dst[r] = H3C_LDG(src + r);
-    };
-    cp(pts, tab + cd[CD3_T_PTS], 3 * Q);
-    cp(Rt, tab + cd[CD3_T_R], 3 * Q);
-    cp(W12, tab + cd[CD3_T_W] + Q, Q2);
-    cp(Et, tab + cd[CD3_T_E], 6 * Q);
-    if (S != H3_HEX) cp(Bt, tab + cd[CD3_T_B], C::TB);
-    if (S != H3_HEX && lt == 0) build_int_tables<S, N>(gstart, gmem, gof, coff, mofr);
-  });
-  sync();
-  par([&](int lt, TS& ts) {
-    const int ta = lt / Q, tb_ = lt % Q;
-    ts.w12 = W12[lt];
-    ts.p1 = 1.0 + pts[Q + ta];
-    ts.r1 = Rt[Q + ta];
-    ts.r2 = Rt[2 * Q + tb_];
-  });
+  {
+    par([&](int lt, TS&) {
+      auto cp = [&](double* dst, const double* src, int n) {
+        for (int r = lt; r < n; r += NT) dst[r] = H3C_LDG(src + r);
+      };
+      cp(pts, tab + cd[CD3_T_PTS], 3 * Q);
+      cp(Rt, tab + cd[CD3_T_R], 3 * Q);
+      cp(W12, tab + cd[CD3_T_W] + Q, Q2);
+      cp(Et, tab + cd[CD3_T_E], 6 * Q);
+      if (S != H3_HEX) cp(Bt, tab + cd[CD3_T_B], C::TB);
+      if (S != H3_HEX && lt == 0) build_int_tables<S, N>(gstart, gmem, gof, coff, mofr);
+    });
+  }
 
-  // ---- element pipeline: scalars two elements ahead, coefficients + slot headers + geometry one
-  // element ahead (cp.async into the other buffer)
+  // ---- element pipeline: scalars two elements ahead; coefficients + slot headers + geometry one
+  // element ahead (cp.async into the other buffer); apply: the element's own-grid fluxes (written by
+  // the flux kernel) at the top of the element, consumed after BwdTrans / PhysDeriv
   const int32_t* ce = P.class_elems + cd[CD3_ELEM_OFF];
-  auto scalars = [&](int i, int& e, int64_t& dof, int64_t& sb, int& ns) {
-    if (i < count) {
-      e = H3C_LDG(ce + i);
-      dof = H3C_LDG(P.dof_off + e);
-      sb = H3C_LDG(P.slot_off + e);
-      ns = (int)(H3C_LDG(P.slot_off + e + 1) - sb);
-    }
+  // element scalars through a 3-deep ring in shared memory (one thread loads them two elements ahead;
+  // nothing of the pipeline is carried in registers)
+  auto scalars = [&](int i, int slot) {
+    par([&](int lt, TS&) {
+      if (lt == 0 && i < count) {
+        const int e = H3C_LDG(ce + i);
+        const long long sb = H3C_LDG(P.slot_off + e);
+        long long* r = ring + 5 * slot;
+        r[0] = e;
+        r[1] = H3C_LDG(P.slot_off + e + 1) - sb;
+        r[2] = H3C_LDG(P.dof_off + e);
+        r[3] = sb;
+        r[4] = APP ? H3C_LDG(P.fb_off + e) : 0;
+      }
+    });
   };
-  auto issue = [&](int buf, int e, int64_t dof, int64_t sb, int ns) {
+  auto issue = [&](int buf, int slot) {
+    const long long* r = ring + 5 * slot;
+    const int e = (int)r[0], ns = (int)r[1];
+    const int64_t dof = r[2], sb = r[3];
     double* cd_ = cbuf + buf * C::NCP;
     double* hd_ = hbuf + buf * C::NSMAX * C::SLOTD;
     const double* src = reinterpret_cast<const double*>(P.slots + sb);
@@ -349,28 +378,39 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 #if defined(__CUDA_ARCH__)
       for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
       for (int r = lt; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
-      if (!PUB && lt < H3_EGEO / 2)
+      if (APP && lt < H3_EGEO / 2)
         __pipeline_memcpy_async(ebuf + buf * H3_EGEO + 2 * lt, P.egeo + (int64_t)e * H3_EGEO + 2 * lt,
                                 2 * sizeof(double));
       __pipeline_commit();
 #else
       for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
       for (int r = lt; r < ns * C::SLOTD; r += NT) hd_[r] = src[r];
-      if (!PUB && lt < H3_EGEO / 2) {
+      if (APP && lt < H3_EGEO / 2) {
         ebuf[buf * H3_EGEO + 2 * lt] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt];
         ebuf[buf * H3_EGEO + 2 * lt + 1] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt + 1];
       }
 #endif
     });
   };
-  int64_t dof_n = 0, sb_n = 0, dof_nn = 0, sb_nn = 0;
-  int ns_n = 0, ns_nn = 0, e_n = 0, e_nn = 0;
-  scalars(bid, e_n, dof_n, sb_n, ns_n);
-  if (bid < count) issue(0, e_n, dof_n, sb_n, ns_n);
-  scalars(bid + G, e_nn, dof_nn, sb_nn, ns_nn);
+  auto issue_fb = [&](int64_t fbo, int ns) {   // ns * 2 * Q2 doubles, 16-byte pieces (fb_off is even)
+    const double* src = P.fb + fbo;
+    par([&](int lt, TS&) {
+#if defined(__CUDA_ARCH__)
+      for (int r = lt; r < ns * Q2; r += NT) __pipeline_memcpy_async(fbuf + 2 * r, src + 2 * r, 2 * sizeof(double));
+      __pipeline_commit();
+#else
+      for (int r = lt; r < ns * 2 * Q2; r += NT) fbuf[r] = src[r];
+#endif
+    });
+  };
+  scalars(bid, 0);
+  scalars(bid + G, 1);
+  sync();
+  if (bid < count) issue(0, 0);
   int it_el = 0;
   for (int i = bid; i < count; i += G, ++it_el) {
     const int bsel = it_el & 1;
+    const int slot = it_el % 3, slot_n = (it_el + 1) % 3, slot_nn = (it_el + 2) % 3;
 #if defined(__CUDA_ARCH__)
     __pipeline_wait_prior(0);
 #endif
@@ -378,173 +418,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     const double* c = cbuf + bsel * C::NCP;
     const double* hdr = hbuf + bsel * C::NSMAX * C::SLOTD;
     const double* eg = ebuf + bsel * H3_EGEO;
-    const int64_t dof = dof_n;
-    const int ns = ns_n;
-    if (i + G < count) issue(bsel ^ 1, e_nn, dof_nn, sb_nn, ns_nn);
-    dof_n = dof_nn;
-    sb_n = sb_nn;
-    ns_n = ns_nn;
-    e_n = e_nn;
-    scalars(i + 2 * G, e_nn, dof_nn, sb_nn, ns_nn);
-
-    // ================= apply, phase 0: the fluxes of every coupling, folded per local face =========
-    // SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and partner
-    // traces; boundary: jump 2u, average g.  Then the transposed trace maps onto the own face grid,
-    // and per local face FL[f] = (fv, (G n)_0 fd, (G n)_1 fd, (G n)_2 fd) summed over its couplings.
-    int fmask = 0;
-    if (!PUB) {
-      for (int s = 0; s < ns; ++s) fmask |= 1 << slot_hdr(hdr, s).face;
-      for (int b0 = 0; b0 < ns; b0 += SB) {
-        const int nb = ns - b0 < SB ? ns - b0 : SB;
-        bool mapped = false;
-        for (int j = 0; j < nb; ++j) mapped |= slot_hdr(hdr, b0 + j).mkind != MAP_ID;
-        par([&](int lt, TS&) {
-          auto cnt = [&](int s) -> int { return slot_hdr(hdr, s).nt; };
-          const Batch BF(b0, nb, cnt);
-          for (int it0 = lt; it0 < BF.tot; it0 += NT) {
-            int p = it0;
-            const int s = BF.slot(p);
-            const H3Slot& h = slot_hdr(hdr, s);
-            double* tv = tb + (s - b0) * 4 * TMAX;
-            const double2 own = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
-            const double ut = own.x, gt = own.y;
-            double un, gn;
-            if (h.kind) {
-              const double2 nbv = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
-              un = nbv.x;
-              gn = nbv.y;
-            } else {
-              un = -ut;
-              gn = -gt;
-            }
-            const double j = ut - un, cc = 0.5 * (gt - gn);
-            const double w = h.sJ * H3C_LDG(tab + h.wtoff + p);
-            tv[p] = (h.tau * j - cc) * w;
-            tv[TMAX + p] = -0.5 * j * w;
-          }
-        });
-        sync();
-        if (mapped) {
-          // transposed maps, stage 1: tensor / row first contraction, dense complete -> tv[2], tv[3]
-          par([&](int lt, TS&) {
-            auto c1 = [&](int s) -> int {
-              const H3Slot& h = slot_hdr(hdr, s);
-              if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
-              if (h.mkind == MAP_TENSOR) return (h.nab & 255) * Q;
-              return h.mkind == MAP_DENSE ? Q2 : 0;
-            };
-            const Batch B1_(b0, nb, c1);
-            for (int it0 = lt; it0 < B1_.tot; it0 += NT) {
-              int it = it0;
-              const int s = B1_.slot(it);
-              const H3Slot& h = slot_hdr(hdr, s);
-              const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
-              double* tv = tb + (s - b0) * 4 * TMAX;
-              double a0 = 0.0, a1 = 0.0;
-              if (h.mkind == MAP_ROW) {   // tmp[pb][i_par] = sum_pa X[pb][pa][i_par] g[pa, pb]
-                const int r1 = it / Q, ib = it % Q;
-                for (int pa = 0; pa < n1; ++pa) {
-                  const double m = H3C_LDG(tab + h.moff + (r1 * n1 + pa) * Q + ib);
-                  a0 = fma(m, tv[pa * n2 + r1], a0);
-                  a1 = fma(m, tv[TMAX + pa * n2 + r1], a1);
-                }
-              } else if (h.mkind == MAP_TENSOR) {
-                const int r1 = it / Q, ib = it % Q;
-                const double* Yc = tab + h.moff2 + ib;
-                const int pst = sw ? n1 : 1;
-                int p = sw ? r1 : r1 * n2;
-                for (int r2 = 0; r2 < n2; ++r2, p += pst) {
-                  const double m = H3C_LDG(Yc + r2 * Q);
-                  a0 = fma(m, tv[p], a0);
-                  a1 = fma(m, tv[TMAX + p], a1);
-                }
-              } else {                    // dense: F(a) = sum_p M[p][a] g[p]
-                for (int p = 0; p < h.nt; ++p) {
-                  const double m = H3C_LDG(tab + h.moff + (int64_t)p * Q2 + it);
-                  a0 = fma(m, tv[p], a0);
-                  a1 = fma(m, tv[TMAX + p], a1);
-                }
-              }
-              tv[2 * TMAX + it] = a0;
-              tv[3 * TMAX + it] = a1;
-            }
-          });
-          sync();
-          // stage 2: second contraction onto the own face grid -> tv[0], tv[1]
-          par([&](int lt, TS&) {
-            for (int it0 = lt; it0 < nb * Q2; it0 += NT) {
-              const int j = it0 / Q2, a = it0 % Q2;
-              const H3Slot& h = slot_hdr(hdr, b0 + j);
-              if (h.mkind == MAP_ID) continue;
-              double* tv = tb + j * 4 * TMAX;
-              double a0 = 0.0, a1 = 0.0;
-              if (h.mkind == MAP_ROW) {   // F(i_par, i_perp) = sum_pb Y[pb][i_perp] tmp[pb][i_par]
-                const int n2 = (h.nab >> 8) & 255, perp = (h.nab >> 16) & 1;
-                const int ipar = perp ? a / Q : a % Q, iperp = perp ? a % Q : a / Q;
-                for (int pb = 0; pb < n2; ++pb) {
-                  const double m = H3C_LDG(tab + h.moff2 + pb * Q + iperp);
-                  a0 = fma(m, tv[2 * TMAX + pb * Q + ipar], a0);
-                  a1 = fma(m, tv[3 * TMAX + pb * Q + ipar], a1);
-                }
-              } else if (h.mkind == MAP_TENSOR) {
-                const int n1 = h.nab & 255, ia = a / Q, ib = a % Q;
-                const double* Xc = tab + h.moff + ia;
-                const double* t0 = tv + 2 * TMAX + ib;
-                for (int r1 = 0; r1 < n1; ++r1) {
-                  const double m = H3C_LDG(Xc + r1 * Q);
-                  a0 = fma(m, t0[r1 * Q], a0);
-                  a1 = fma(m, t0[TMAX + r1 * Q], a1);
-                }
-              } else {
-                a0 = tv[2 * TMAX + a];
-                a1 = tv[3 * TMAX + a];
-              }
-              tv[a] = a0;
-              tv[TMAX + a] = a1;
-            }
-          });
-          sync();
-        }
-        // fold into the per-face arrays (a local face carries one or two couplings, adjacent in the
-        // slot order; the first of them in this batch is the leader)
-        par([&](int lt, TS&) {
-          for (int it0 = lt; it0 < nb * Q2; it0 += NT) {
-            const int j = it0 / Q2, a = it0 % Q2, s = b0 + j;
-            const H3Slot& h = slot_hdr(hdr, s);
-            const int f = h.face;
-            const bool follows = s > 0 && slot_hdr(hdr, s - 1).face == f;
-            if (follows && j > 0) continue;
-            const int fx = fcr(S, f, 0), sd = fcr(S, f, 1), ra = fcr(S, f, 2), rb = fcr(S, f, 3);
-            const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, a / Q, a % Q);
-            double l0 = 0.0, l1 = 0.0, l2 = 0.0, l3 = 0.0;
-            auto add = [&](int jj) {
-              const H3Slot& hh = slot_hdr(hdr, b0 + jj);
-              const double* tv = tb + jj * 4 * TMAX;
-              const double fd = tv[TMAX + a];
-              l0 += tv[a];
-              l1 += (ch.c00 * hh.v[0] + ch.c01 * hh.v[1] + ch.c02 * hh.v[2]) * fd;
-              l2 += (ch.c11 * hh.v[1] + ch.c12 * hh.v[2]) * fd;
-              l3 += hh.v[2] * fd;
-            };
-            add(j);
-            if (j + 1 < nb && slot_hdr(hdr, s + 1).face == f) add(j + 1);
-            double* Ff = FL + f * 4 * Q2;
-            if (follows) {
-              Ff[a] += l0;
-              Ff[Q2 + a] += l1;
-              Ff[2 * Q2 + a] += l2;
-              Ff[3 * Q2 + a] += l3;
-            } else {
-              Ff[a] = l0;
-              Ff[Q2 + a] = l1;
-              Ff[2 * Q2 + a] = l2;
-              Ff[3 * Q2 + a] = l3;
-            }
-          }
-        });
-        sync();
-      }
-    }
+    const int ns = (int)ring[5 * slot + 1];
+    const int64_t dof = ring[5 * slot + 2], fbo = ring[5 * slot + 4];
+    if (i + G < count) issue(bsel ^ 1, slot_n);
+    scalars(i + 2 * G, slot_nn);
+    if (APP) issue_fb(fbo, ns);
 
     // ================= BwdTrans (stdregions.py:575-597): u column in registers ====================
     if (S == H3_HEX) {
@@ -584,14 +462,18 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
             for (int k = 0; k < Q; ++k) s1[m * Q + k] = out[k];
           }
         } else {
-          for (int o = lt; o < C::NPM * Q; o += NT) {
-            const int k = o % Q, m = o / Q;
-            double a = 0.0;
-            const int r0 = coff[m], cn = coff[m + 1] - r0;
+          H3C_ITEM_UNROLL
+          for (int rr = 0; rr < (C::NPM * Q + NT - 1) / NT; ++rr) {
+            const int o = lt + rr * NT;
+            if (o < C::NPM * Q) {
+              const int k = o % Q, m = o / Q;
+              double a = 0.0;
+              const int r0 = coff[m], cn = coff[m + 1] - r0;
 #pragma unroll
-            for (int kk = 0; kk < (N - 1 > 1 ? N - 1 : 1); ++kk)
-              if (kk < cn) a = fma(H3C_LDG(Ct + (r0 + kk) * Q + k), c[r0 + kk], a);
-            s1[o] = a;
+              for (int kk = 0; kk < (N - 1 > 1 ? N - 1 : 1); ++kk)
+                if (kk < cn) a = fma(H3C_LDG(Ct + (r0 + kk) * Q + k), c[r0 + kk], a);
+              s1[o] = a;
+            }
           }
         }
       });
@@ -852,8 +734,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 #pragma unroll
       for (int r = 0; r < Q; ++r) B0[ta * SI + tb_ * SJ + r] = ts.d2[r];
     });
-    sync();
     // ================= volume terms (sipg.py:575-582) + face lifts, in registers ==================
+#if defined(__CUDA_ARCH__)
+    __pipeline_wait_prior(0);   // this element's own-grid fluxes (and the next element's prefetch)
+#endif
+    sync();
     par([&](int lt, TS& ts) {
       const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
@@ -862,11 +747,12 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         ts.d2[k] = B0[k * SI + ta * SJ + tb_];
       }
       const double lam = P.lam;
+      const double tp1 = 1.0 + pts[Q + ta], tr1 = Rt[Q + ta], tr2 = Rt[2 * Q + tb_];   // this thread's (eta1, eta2)
       const double dJ = eg[0], S00 = eg[1], S01 = eg[2], S02 = eg[3], S11 = eg[4], S12 = eg[5], S22 = eg[6];
-      const double jw12 = dJ * ts.w12;
+      const double jw12 = dJ * W12[lt];
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
-        const Chain ch = chain_t<S>(H3C_TX[XP0 + k], ts.p1, ts.r1, ts.r2);
+        const Chain ch = chain_t<S>(H3C_TX[XP0 + k], tp1, tr1, tr2);
         const double jw = jw12 * H3C_TX[XW0 + k];
         const double e0 = ts.d0[k], e1 = ts.d1[k], e2 = ts.d2[k];
         const double x0 = ch.c00 * e0, x1 = ch.c01 * e0 + ch.c11 * e1, x2 = ch.c02 * e0 + ch.c12 * e1 + e2;
@@ -878,21 +764,34 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         ts.d1[k] = jw * (ch.c11 * f1 + ch.c12 * f2);
         ts.d2[k] = jw * f2;
       }
-      // lift (the reference's scatter + final sweep, sipg.py:663-693): W_c(k0, k1, k2) += E[k_fixed] FL[f][c](a)
+      // lift (the reference's scatter + final sweep, sipg.py:663-693), per local face f with own-grid
+      // fluxes (fv, fd) summed over its one or two couplings:
+      //   W0(k) += E[k_fixed] fv(a),  W_c(k) += E[k_fixed] ((G n)_c fd)(a),  (G n) from the collapse chain
+      int s = 0;
       for_faces<0, NF>([&](auto Fc) {
         constexpr int f = decltype(Fc)::value;
-        constexpr int fx = fc(S, f, 0), hi = fc(S, f, 1) > 0 ? 1 : 0;
+        constexpr int fx = fc(S, f, 0), sd = fc(S, f, 1), hi = sd > 0 ? 1 : 0;
         constexpr bool onehot = gll_axis(S, fx);
         constexpr int kend = hi ? Q - 1 : 0;
-        if (!((fmask >> f) & 1)) return;
-        const double* Ff = FL + f * 4 * Q2;
+        constexpr double rs = sd < 0 ? 0.5 : 0.0, ps = 1.0 + sd;
+        if (!(s < ns && slot_hdr(hdr, s).face == f)) return;
+        const H3Slot& h = slot_hdr(hdr, s);
+        const double v0 = h.v[0], v1 = h.v[1], v2 = h.v[2];
+        const double* F0 = fbuf + s * 2 * Q2;
+        const bool two = C::NSMAX > NF && s + 1 < ns && slot_hdr(hdr, s + 1).face == f;   // tets: one coupling per face
+        const double* F1 = two ? F0 + 2 * Q2 : F0;
+        const double w2nd = two ? 1.0 : 0.0;
+        s += two ? 2 : 1;
         if constexpr (fx == 0) {
-          const double l0 = Ff[lt], l1 = Ff[Q2 + lt], l2 = Ff[2 * Q2 + lt], l3 = Ff[3 * Q2 + lt];
+          const double fv = F0[lt] + w2nd * F1[lt], fd = F0[Q2 + lt] + w2nd * F1[Q2 + lt];
+          const Chain ch = chain_t<S>(ps, tp1, tr1, tr2);
+          const double l1 = (ch.c00 * v0 + ch.c01 * v1 + ch.c02 * v2) * fd;
+          const double l2 = (ch.c11 * v1 + ch.c12 * v2) * fd, l3 = v2 * fd;
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
             if (onehot && k != kend) continue;
             const double ek = H3C_TX[XE + hi * Q + k];
-            ts.u[k] = fma(ek, l0, ts.u[k]);
+            ts.u[k] = fma(ek, fv, ts.u[k]);
             ts.d0[k] = fma(ek, l1, ts.d0[k]);
             ts.d1[k] = fma(ek, l2, ts.d1[k]);
             ts.d2[k] = fma(ek, l3, ts.d2[k]);
@@ -904,10 +803,14 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
             const int a = k * Q + ko;
-            ts.u[k] = fma(ek, Ff[a], ts.u[k]);
-            ts.d0[k] = fma(ek, Ff[Q2 + a], ts.d0[k]);
-            ts.d1[k] = fma(ek, Ff[2 * Q2 + a], ts.d1[k]);
-            ts.d2[k] = fma(ek, Ff[3 * Q2 + a], ts.d2[k]);
+            const double fv = F0[a] + w2nd * F1[a], fd = ek * (F0[Q2 + a] + w2nd * F1[Q2 + a]);
+            // the chain at face point (eta0 = point k, the other run axis at this thread's index)
+            const Chain ch = fx == 1 ? chain_t<S>(H3C_TX[XP0 + k], ps, rs, tr2)
+                                     : chain_t<S>(H3C_TX[XP0 + k], tp1, tr1, rs);
+            ts.u[k] = fma(ek, fv, ts.u[k]);
+            ts.d0[k] = fma(ch.c00 * v0 + ch.c01 * v1 + ch.c02 * v2, fd, ts.d0[k]);
+            ts.d1[k] = fma(ch.c11 * v1 + ch.c12 * v2, fd, ts.d1[k]);
+            ts.d2[k] = fma(v2, fd, ts.d2[k]);
           }
         }
       });
@@ -976,7 +879,10 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       });
     } else {
       par([&](int lt, TS&) {
-        for (int o = lt; o < C::NPM * Q; o += NT) {
+        H3C_ITEM_UNROLL
+        for (int rr = 0; rr < (C::NPM * Q + NT - 1) / NT; ++rr) {
+          const int o = lt + rr * NT;
+          if (o >= C::NPM * Q) break;
           const int k = o % Q, m = o / Q, g = gof[m];
           const double* Br = Bt + m * Q;
           double a = 0.0;
@@ -1002,7 +908,10 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
             for (int l = 0; l < N; ++l) y[dof + m * N + l] = out[l];
           }
         } else {
-          for (int r = lt; r < C::NC; r += NT) {
+          H3C_ITEM_UNROLL
+          for (int rr = 0; rr < (C::NC + NT - 1) / NT; ++rr) {
+            const int r = lt + rr * NT;
+            if (r >= C::NC) break;
             const int m = mofr[r];
             double a = 0.0;
 #pragma unroll
@@ -1015,14 +924,150 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   }
 }
 
-template <int Q>
-constexpr int h3c_minb() { return Q >= 8 ? SIPG_H3C_MINB8 : (Q == 7 ? 7 : (Q == 6 ? 8 : 16)); }
+// ---------------------------------------------------------------------------------------------
+// Flux kernel, one warp per coupling side (slot), any shape / order: the SIP flux at the trace points
+// (sipg.py:622-650, 663-677) from the published own and partner traces (boundary: jump 2u, average
+// g), then the transposed trace map onto the owning element's face grid (q x q):
+// fb[slot] = (fv, fd).  The reference's per-interface phase 2 (sipg.py:607-661).  A streaming
+// kernel: no element structure, few registers, full occupancy.
+#define H3C_FLUX_WPB 8     // warps (slots) per CTA
+template <typename Par, typename Sync>
+H3C_HD void flux_slot(const H3Plan& P, const int64_t i, double* tv, Par par, Sync sync) {
+  // the 64-byte record, four 16-byte loads (every lane the same address)
+  H3FluxRec h;
+  {
+    const int4* src = reinterpret_cast<const int4*>(P.frec + i);
+    int4* dst = reinterpret_cast<int4*>(&h);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) dst[r] = H3C_LDG(src + r);
+  }
+  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q, mkind = h.mk_kind & 255, kind = h.mk_kind >> 8;
+  double* fb = P.fb + (h.fb_q >> 4);
+  const double* tab = P.tab;
+  const bool ident = mkind == MAP_ID;
+  par([&](int lane) {
+    double2 own[2], nbv[2];
+    double wv[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = lane + 32 * r;
+      own[r] = nbv[r] = make_double2(0.0, 0.0);
+      wv[r] = 0.0;
+      if (p < h.nt) {
+        own[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+        if (kind) nbv[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+        wv[r] = H3C_LDG(tab + h.wtoff + p);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = lane + 32 * r;
+      if (p < h.nt) {
+        const double ut = own[r].x, gt = own[r].y;
+        const double un = kind ? nbv[r].x : -ut, gn = kind ? nbv[r].y : -gt;
+        const double j = ut - un, cc = 0.5 * (gt - gn);
+        const double w = h.sJ * wv[r];
+        const double fv = (h.tau * j - cc) * w, fd = -0.5 * j * w;
+        if (ident) {          // trace grid = own face grid
+          fb[p] = fv;
+          fb[Q2 + p] = fd;
+        } else {
+          tv[p] = fv;
+          tv[TMAX + p] = fd;
+        }
+      }
+    }
+  });
+  if (ident) return;
+  sync();
+  const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
+  // transposed map, stage 1: tensor / row first contraction, dense complete -> tv[2], tv[3]
+  par([&](int lane) {
+    const int tot = mkind == MAP_ROW ? n2 * Q : (mkind == MAP_TENSOR ? n1 * Q : Q2);
+    for (int it = lane; it < tot; it += 32) {
+      double a0 = 0.0, a1 = 0.0;
+      const int r1 = it / Q, ib = it - r1 * Q;
+      if (mkind == MAP_ROW) {   // tmp[pb][i_par] = sum_pa X[pb][pa][i_par] g[pa, pb]
+        H3C_MAPLOOP(pa, n1) {
+          const double m = H3C_LDG(tab + h.moff + (r1 * n1 + pa) * Q + ib);
+          a0 = fma(m, tv[pa * n2 + r1], a0);
+          a1 = fma(m, tv[TMAX + pa * n2 + r1], a1);
+        }
+      } else if (mkind == MAP_TENSOR) {
+        const double* Yc = tab + h.moff2 + ib;
+        const int pst = sw ? n1 : 1;
+        const int p0 = sw ? r1 : r1 * n2;
+        H3C_MAPLOOP(r2, n2) {
+          const double m = H3C_LDG(Yc + r2 * Q);
+          a0 = fma(m, tv[p0 + r2 * pst], a0);
+          a1 = fma(m, tv[TMAX + p0 + r2 * pst], a1);
+        }
+      } else {                    // dense: F(a) = sum_p M[p][a] g[p]
+        for (int p = 0; p < h.nt; ++p) {
+          const double m = H3C_LDG(tab + h.moff + (int64_t)p * Q2 + it);
+          a0 = fma(m, tv[p], a0);
+          a1 = fma(m, tv[TMAX + p], a1);
+        }
+      }
+      tv[2 * TMAX + it] = a0;
+      tv[3 * TMAX + it] = a1;
+    }
+  });
+  sync();
+  // stage 2: second contraction onto the own face grid -> fb
+  par([&](int lane) {
+    for (int a = lane; a < Q2; a += 32) {
+      double a0 = 0.0, a1 = 0.0;
+      const int ia = a / Q, ib = a - ia * Q;
+      if (mkind == MAP_ROW) {   // F(i_par, i_perp) = sum_pb Y[pb][i_perp] tmp[pb][i_par]
+        const int ipar = sw ? ia : ib, iperp = sw ? ib : ia;   // sw: the perp flag of a row map
+        H3C_MAPLOOP(pb, n2) {
+          const double m = H3C_LDG(tab + h.moff2 + pb * Q + iperp);
+          a0 = fma(m, tv[2 * TMAX + pb * Q + ipar], a0);
+          a1 = fma(m, tv[3 * TMAX + pb * Q + ipar], a1);
+        }
+      } else if (mkind == MAP_TENSOR) {
+        const double* Xc = tab + h.moff + ia;
+        const double* t0 = tv + 2 * TMAX + ib;
+        H3C_MAPLOOP(r1, n1) {
+          const double m = H3C_LDG(Xc + r1 * Q);
+          a0 = fma(m, t0[r1 * Q], a0);
+          a1 = fma(m, t0[TMAX + r1 * Q], a1);
+        }
+      } else {
+        a0 = tv[2 * TMAX + a];
+        a1 = tv[3 * TMAX + a];
+      }
+      fb[a] = a0;
+      fb[Q2 + a] = a1;
+    }
+  });
+}
 
-template <int S, int N, bool PUB>
-__global__ void __launch_bounds__((N + 1) * (N + 1), h3c_minb<N + 1>())
+// work-list records [first, first + count)
+__global__ void __launch_bounds__(32 * H3C_FLUX_WPB, 6) k_h3c_flux(const H3Plan P, const int64_t first, const int64_t count) {
+  __shared__ double scr[H3C_FLUX_WPB][4 * TMAX];
+  const int w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * H3C_FLUX_WPB + w;
+  if (i >= count) return;
+  flux_slot(P, first + i, scr[w], [&](auto&& f) { f((int)(threadIdx.x & 31)); }, [&]() { __syncwarp(); });
+}
+
+// resident CTAs per SM the register allocation must allow, per q (apply | publish)
+#ifndef H3C_MINB_A
+#define H3C_MINB_A(Q) ((Q) >= 8 ? 8 : ((Q) == 7 ? 8 : ((Q) == 6 ? 10 : 20)))
+#endif
+#ifndef H3C_MINB_P
+#define H3C_MINB_P(Q) ((Q) >= 8 ? 10 : ((Q) == 7 ? 10 : ((Q) == 6 ? 12 : 24)))
+#endif
+template <int Q, int MODE>
+constexpr int h3c_minb() { return MODE == 1 ? H3C_MINB_P(Q) : H3C_MINB_A(Q); }
+
+template <int S, int N, int MODE>
+__global__ void __launch_bounds__((N + 1) * (N + 1), h3c_minb<N + 1, MODE>())
 k_h3c(const H3Plan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(16) double h3c_sm[];
-  body<S, N, PUB>(P, cls, x, y, (int)blockIdx.x, (int)gridDim.x, h3c_sm);
+  body<S, N, MODE>(P, cls, x, y, (int)blockIdx.x, (int)gridDim.x, h3c_sm);
 }
 
 // __constant__ tables of one (shape, n) instantiation: the h3 tables (D, A, psi, even-odd blocks)

@@ -51,12 +51,13 @@ void run_class(const H3Plan& P, const sipg_h3_desc* d, int cls, const double* x,
   }
   const int G = 3;   // a few "CTAs": exercises the double-buffered element pipeline
   for (int b = 0; b < G; ++b) {
+    // shared memory exactly as large as the kernel's (NaN-filled: reads of unwritten words show up)
     if (phases == 0) {
-      std::vector<double> sm(C::smem_bytes(true) / 8 + 8, NAN);
-      h3c::body<S, N, true>(P, cls, x, y, b, G, sm.data());
+      std::vector<double> sm(C::smem_bytes(1) / 8 + 1, NAN);
+      h3c::body<S, N, 1>(P, cls, x, y, b, G, sm.data());
     } else {
-      std::vector<double> sm(C::smem_bytes(false) / 8 + 8, NAN);
-      h3c::body<S, N, false>(P, cls, x, y, b, G, sm.data());
+      std::vector<double> sm(C::smem_bytes(0) / 8 + 1, NAN);
+      h3c::body<S, N, 0>(P, cls, x, y, b, G, sm.data());
     }
   }
 }
@@ -75,10 +76,48 @@ bool dispatch_n(const H3Plan& P, const sipg_h3_desc* d, int cls, int n, const do
 }
 }  // namespace
 
-// phase 0: publish every class into pub; phase 1: apply every class (reads pub) into y
-extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, double* pub, int phase) {
+// own-grid flux buffer layout (as sipg_h3_plan_create): fb_off[n_elements + 1], returns the total
+extern "C" int64_t h3c_emu_fb_layout(const sipg_h3_desc* d, int64_t* fb_off) {
+  std::vector<int32_t> q2(d->n_elements, 0);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    for (int i = 0; i < cd[CD3_COUNT]; ++i) q2[d->class_elems[cd[CD3_ELEM_OFF] + i]] = cd[CD3_Q] * cd[CD3_Q];
+  }
+  fb_off[0] = 0;
+  for (int64_t e = 0; e < d->n_elements; ++e)
+    fb_off[e + 1] = fb_off[e] + 2ll * q2[e] * (d->slot_off[e + 1] - d->slot_off[e]);
+  return fb_off[d->n_elements];
+}
+
+// phase 0: publish every class into pub; phase 2: the fluxes of every class (reads pub) into fb;
+// phase 1: apply every class (reads fb) into y
+extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, double* pub, double* fb,
+                           const int64_t* fb_off, int phase) {
+  // the flux kernel's work list, as sipg_h3_plan_create builds it
+  std::vector<int32_t> qe(d->n_elements, 0);
+  std::vector<H3FluxRec> fr;
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    for (int i = 0; i < cd[CD3_COUNT]; ++i) qe[d->class_elems[cd[CD3_ELEM_OFF] + i]] = cd[CD3_Q];
+  }
+  const H3Slot* sl = (const H3Slot*)d->slots;
+  for (int64_t i = 0; i < d->n_elements; ++i) {
+    const int32_t e = d->class_elems[i];
+    for (int64_t q = d->slot_off[e]; q < d->slot_off[e + 1]; ++q) {
+      const H3Slot& s0 = sl[q];
+      fr.push_back(H3FluxRec{s0.pub_self, s0.pub_other, (fb_off[e] + 2ll * qe[e] * qe[e] * (q - d->slot_off[e])) * 16 + qe[e],
+                             s0.tau, s0.sJ, s0.nt, s0.mkind | (s0.kind << 8), s0.nab, s0.moff, s0.moff2, s0.wtoff});
+    }
+  }
   H3Plan P{d->class_desc, d->class_elems, d->dof_off, d->elem_geom, d->slot_off, (const H3Slot*)d->slots,
-           d->tables, pub, d->lambda};
+           d->tables, pub, d->lambda, fb, fb_off, fr.data()};
+  if (phase == 2) {   // the flux kernel: one "warp" per slot, lanes one after the other between the barriers
+    for (size_t i = 0; i < fr.size(); ++i) {
+      std::vector<double> scr(4 * h3::TMAX, NAN);
+      h3c::flux_slot(P, (int64_t)i, scr.data(), [&](auto&& f) { for (int lane = 0; lane < 32; ++lane) f(lane); }, [] {});
+    }
+    return 0;
+  }
   for (int c = 0; c < d->n_classes; ++c) {
     const int32_t* cd = d->class_desc + c * CD3_WORDS;
     if (cd[CD3_COUNT] <= 0) continue;
