@@ -126,9 +126,10 @@ struct H3State {
   double* fb = nullptr;
   int64_t* fb_off_d = nullptr;
   H3FluxRec* frec_d = nullptr;
-  std::vector<int64_t> cslot_off;
+  std::vector<int64_t> cs_id, cs_mp;   // per class-list position: first identity-map / mapped record
+  int64_t n_id = 0;                    // records: [identity-map slots | mapped slots], each in class-list order
   // streamed host apply (see build_stream_schedule_h3): per stage, publish rows and apply rows
-  struct Launch { int row, grid; const H3Entry* k; int64_t flux_first, flux_count; };
+  struct Launch { int row, grid; const H3Entry* k; int pos0, pos1; };   // pos: class-list positions of the row
   std::vector<std::vector<Launch>> st_pub, st_comp;
   int32_t* rows_d = nullptr;
   H3Plan hps{};
@@ -679,6 +680,20 @@ const NcclApi& nccl() {
     if (_r != ncclSuccess) return fail(SIPG_ERR_COMM, std::string(#call) + ": " + nccl().errorString(_r)); \
   } while (0)
 
+// the slot kernels (pass 2 flux, 3 trace maps) over the class-list positions [a, b): identity-map and
+// mapped slots are separate work lists (uniform warps per launch)
+static void h3_slot_launch(sipg_plan* p, const H3Plan& hp, int pass, int a, int b, cudaStream_t s) {
+  H3State* h = p->h3;
+  const int64_t i0 = h->cs_id[a], i1 = h->cs_id[b], m0 = h->n_id + h->cs_mp[a], m1 = h->n_id + h->cs_mp[b];
+  if (pass == 2) {
+    if (i1 > i0) { sipg_h3c_flux_launch(hp, i0, i1 - i0, false, p->sms, s); ++p->launches; }
+    if (m1 > m0) { sipg_h3c_flux_launch(hp, m0, m1 - m0, true, p->sms, s); ++p->launches; }
+  } else if (m1 > m0) {
+    sipg_h3c_map_launch(hp, m0, m1 - m0, p->sms, s);
+    ++p->launches;
+  }
+}
+
 // launch the classes of one pass (0 publish, 1 apply, 2 flux: the slots of those classes, adjacent
 // classes merged into one launch) whose role is selected by `want` (-1: all)
 int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_dev, cudaStream_t s) {
@@ -688,23 +703,18 @@ int h3_launch(sipg_plan* p, int pass, int want, const double* x_dev, double* y_d
     const int crole = h->cd[c * CD3_WORDS + CD3_ROLE];
     return count > 0 && (want < 0 || crole == want);
   };
-  if (pass == 2) {
+  if (pass >= 2) {   // 2 flux, 3 trace maps: the slots of the selected classes, adjacent classes merged
     if (!h->flux) return 0;
-    int64_t first = -1, last = -1;
+    int c0 = -1;
     for (int c = 0; c <= p->n_cls; ++c) {
       const bool on = c < p->n_cls && go(c);
-      const int64_t a = on ? h->cslot_off[h->cd[c * CD3_WORDS + CD3_ELEM_OFF]] : 0;
-      const int64_t b = on ? h->cslot_off[h->cd[c * CD3_WORDS + CD3_ELEM_OFF] + h->cd[c * CD3_WORDS + CD3_COUNT]] : 0;
-      if (on && first >= 0 && a == last) {
-        last = b;
-        continue;
+      if (on && c0 < 0) c0 = c;
+      if (!on && c0 >= 0) {
+        const int a = h->cd[c0 * CD3_WORDS + CD3_ELEM_OFF];
+        const int b = h->cd[(c - 1) * CD3_WORDS + CD3_ELEM_OFF] + h->cd[(c - 1) * CD3_WORDS + CD3_COUNT];
+        h3_slot_launch(p, h->hp, pass, a, b, s);
+        c0 = -1;
       }
-      if (first >= 0 && last > first) {
-        sipg_h3c_flux_launch(h->hp, first, last - first, s);
-        ++p->launches;
-      }
-      first = on ? a : -1;
-      last = on ? b : -1;
     }
     return 0;
   }
@@ -754,7 +764,7 @@ int h3_exchange(sipg_plan* p) {
 int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
   int rc = 0;
-  // pass 0 publish, 2 flux (register-column kernels; a no-op for the first generation), 1 apply
+  // pass 0 publish, 3 trace maps, 2 flux (register-column kernels; no-ops for the first generation), 1 apply
   if (role == 1) {
     if ((rc = h3_launch(p, 2, 1, x_dev, y_dev, s))) return rc;
     if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
@@ -766,6 +776,7 @@ int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStr
     return fail(SIPG_ERR_ARG, "partitioned plan without a communicator: call sipg_comm_init, or drive the "
                               "exchange with sipg_apply_role 0 / 1");
   if ((rc = h3_launch(p, 0, 1, x_dev, y_dev, s))) return rc;     // boundary layer publishes first
+  if ((rc = h3_launch(p, 3, 1, x_dev, y_dev, s))) return rc;
   if (role < 0 && halo) {
     ncclResult_t ae = ncclSuccess;
     if (nccl().commGetAsyncError(h->comm, &ae) != ncclSuccess || ae != ncclSuccess)
@@ -776,6 +787,7 @@ int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStr
     CK(cudaEventRecord(h->ev_comm, h->s_comm));
   }
   if ((rc = h3_launch(p, 0, 0, x_dev, y_dev, s))) return rc;
+  if ((rc = h3_launch(p, 3, 0, x_dev, y_dev, s))) return rc;
   if ((rc = h3_launch(p, 2, 0, x_dev, y_dev, s))) return rc;
   if ((rc = h3_launch(p, 1, 0, x_dev, y_dev, s))) return rc;
   if (role < 0) {
@@ -864,8 +876,7 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
         rows[(int64_t)r * CD3_WORDS + CD3_ELEM_OFF] += i0;
         const int cap = pass == 0 ? h->cap_pub[c] : h->cap_apply[c];
         const int g = (i1 - i0) < cap ? (i1 - i0) : cap;
-        const int64_t f0 = h->cslot_off[cd[CD3_ELEM_OFF] + i0], f1 = h->cslot_off[cd[CD3_ELEM_OFF] + i1];
-        (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c], f0, f1 - f0});
+        (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c], cd[CD3_ELEM_OFF] + i0, cd[CD3_ELEM_OFF] + i1});
         i0 = i1;
       }
     }
@@ -891,8 +902,7 @@ int sipg_h3_apply_traces(sipg_plan* p, const double* x_dev, const double* traces
     if (count == 0 || h->cd[c * CD3_WORDS + CD3_ROLE] == 2) continue;
     if (h->flux) {
       const int eo = h->cd[c * CD3_WORDS + CD3_ELEM_OFF];
-      sipg_h3c_flux_launch(hp, h->cslot_off[eo], h->cslot_off[eo + count] - h->cslot_off[eo], (cudaStream_t)stream);
-      ++p->launches;
+      h3_slot_launch(p, hp, 2, eo, eo + count, (cudaStream_t)stream);
     }
   }
   for (int c = 0; c < p->n_cls; ++c) {
@@ -1059,7 +1069,8 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     std::vector<int64_t> fbo((size_t)d->n_elements + 1, 0);
     std::vector<int32_t> qe(d->n_elements, 0);
     std::vector<H3FluxRec> fr((size_t)d->n_slots);
-    h->cslot_off.assign((size_t)d->n_elements + 1, 0);
+    h->cs_id.assign((size_t)d->n_elements + 1, 0);
+    h->cs_mp.assign((size_t)d->n_elements + 1, 0);
     for (int c = 0; c < d->n_classes; ++c) {
       const int32_t* cd = d->class_desc + c * CD3_WORDS;
       for (int i = 0; i < cd[CD3_COUNT]; ++i) qe[d->class_elems[cd[CD3_ELEM_OFF] + i]] = cd[CD3_Q];
@@ -1067,17 +1078,21 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     for (int64_t e = 0; e < d->n_elements; ++e)
       fbo[e + 1] = fbo[e] + 2ll * qe[e] * qe[e] * (d->slot_off[e + 1] - d->slot_off[e]);
     const H3Slot* sl = (const H3Slot*)d->slots;
-    int64_t k = 0;
+    for (int64_t q = 0; q < d->n_slots; ++q) h->n_id += sl[q].mkind == MAP_ID;
+    int64_t ki = 0, km = 0;
     for (int64_t i = 0; i < d->n_elements; ++i) {   // class-list order
       const int32_t e = d->class_elems[i];
-      h->cslot_off[i] = k;
-      for (int64_t q = d->slot_off[e]; q < d->slot_off[e + 1]; ++q, ++k) {
+      h->cs_id[i] = ki;
+      h->cs_mp[i] = km;
+      for (int64_t q = d->slot_off[e]; q < d->slot_off[e + 1]; ++q) {
         const H3Slot& s0 = sl[q];
-        fr[k] = H3FluxRec{s0.pub_self, s0.pub_other, (fbo[e] + 2ll * qe[e] * qe[e] * (q - d->slot_off[e])) * 16 + qe[e],
-                          s0.tau, s0.sJ, s0.nt, s0.mkind | (s0.kind << 8), s0.nab, s0.moff, s0.moff2, s0.wtoff};
+        fr[s0.mkind == MAP_ID ? ki++ : h->n_id + km++] =
+            H3FluxRec{s0.pub_self, s0.pub_other, (fbo[e] + 2ll * qe[e] * qe[e] * (q - d->slot_off[e])) * 16 + qe[e],
+                      s0.tau, s0.sJ, s0.nt, s0.mkind | (s0.kind << 8), s0.nab, s0.moff, s0.moff2, s0.wtoff};
       }
     }
-    h->cslot_off[d->n_elements] = k;
+    h->cs_id[d->n_elements] = ki;
+    h->cs_mp[d->n_elements] = km;
     h->flux = gen == 1;
     if ((rc = upload(fbo.data(), d->n_elements + 1, &h->fb_off_d)) || (rc = upload(fr.data(), d->n_slots, &h->frec_d))) {
       sipg_plan_destroy(p);
@@ -1246,13 +1261,17 @@ int sipg_apply_class(sipg_plan* p, int32_t cls, const double* x_dev, double* y_d
     const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
     const H3Entry* k = h->kern[c];
     if (count == 0 || (cls >= 2 * p->n_cls && !h->flux)) return 0;
-    if (cls < p->n_cls)
+    if (cls < p->n_cls) {
       k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
-    else if (cls < 2 * p->n_cls)
+      if (h->flux) {
+        const int eo = h->cd[c * CD3_WORDS + CD3_ELEM_OFF];
+        h3_slot_launch(p, h->hp, 3, eo, eo + count, (cudaStream_t)stream);
+      }
+    } else if (cls < 2 * p->n_cls)
       k->apply<<<h->grid_apply[c], k->threads, k->smem_apply, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
     else {
       const int eo = h->cd[c * CD3_WORDS + CD3_ELEM_OFF];
-      sipg_h3c_flux_launch(h->hp, h->cslot_off[eo], h->cslot_off[eo + count] - h->cslot_off[eo], (cudaStream_t)stream);
+      h3_slot_launch(p, h->hp, 2, eo, eo + count, (cudaStream_t)stream);
     }
     ++p->launches;
     CK(cudaGetLastError());
@@ -1422,17 +1441,16 @@ static int enqueue_streamed(sipg_plan* p, const double* x_host, double* y_host, 
       int rc = group_begin(p, s, (int)h->st_pub[k].size(), (int)h->st_pub[k].size());
       if (rc) return rc;
       for (const auto& L : h->st_pub[k]) {
-        L.k->pub<<<L.grid, L.k->threads, L.k->smem_pub, group_stream(p)>>>(h->hps, L.row, p->x_stage, p->y_stage);
+        cudaStream_t st = group_stream(p);
+        L.k->pub<<<L.grid, L.k->threads, L.k->smem_pub, st>>>(h->hps, L.row, p->x_stage, p->y_stage);
         ++p->launches;
+        if (h->flux) h3_slot_launch(p, h->hps, 3, L.pos0, L.pos1, st);
       }
       if ((rc = group_end(p))) return rc;
       if ((rc = group_begin(p, s, (int)h->st_comp[k].size(), (int)h->st_comp[k].size()))) return rc;
       for (const auto& L : h->st_comp[k]) {   // a stage row's flux kernel, then its apply kernel, on one stream
         cudaStream_t st = group_stream(p);
-        if (h->flux) {
-          sipg_h3c_flux_launch(h->hps, L.flux_first, L.flux_count, st);
-          ++p->launches;
-        }
+        if (h->flux) h3_slot_launch(p, h->hps, 2, L.pos0, L.pos1, st);
         L.k->apply<<<L.grid, L.k->threads, L.k->smem_apply, st>>>(h->hps, L.row, p->x_stage, p->y_stage);
         ++p->launches;
       }
@@ -1492,7 +1510,7 @@ int sipg_plan_kernels_per_apply(const sipg_plan* p) {
       const int32_t* cd = p->h3->cd.data() + c * CD3_WORDS;
       if (cd[CD3_COUNT] > 0) k += cd[CD3_ROLE] == 2 ? 1 : 2;
     }
-    return k + (p->h3->flux ? 1 : 0);   // + the flux kernel (one launch over every slot)
+    return k + (p->h3->flux ? 2 : 0);   // + the trace-map and flux kernels (one launch each over every slot)
   }
   for (int c = 0; c < p->n_cls; ++c) {
     if (p->cd_host[c * CD_WORDS + CD_COUNT] > 0 && p->cd_host[c * CD_WORDS + CD_ROLE] != 2) ++k;
@@ -1511,8 +1529,7 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
   int k = 0;
   if (p->h3) {
     for (int i = 0; i < p->n_chunks; ++i) {
-      k += (int)p->h3->st_pub[i].size();
-      k += (int)p->h3->st_comp[i].size() * (p->h3->flux ? 2 : 1);
+      k += (int)(p->h3->st_pub[i].size() + p->h3->st_comp[i].size()) * (p->h3->flux ? 2 : 1);
     }
     return k;
   }

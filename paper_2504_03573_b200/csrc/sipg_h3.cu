@@ -46,8 +46,26 @@ void sipg_register_h3(std::vector<H3Entry>& v) {
   add<H3_TET>(v);
 }
 
-void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, cudaStream_t stream) {
+// persistent grid of the mapped-slot kernels: resident CTAs per SM x SMs (capped by the work)
+template <bool FLUX>
+static unsigned slot_grid(int64_t count, int sms) {
+  static int occ = 0;
+  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h3c::k_h3c_slot<FLUX>, 32 * H3C_SLOT_WPB, 0) !=
+                   cudaSuccess || occ <= 0))
+    occ = 4;
+  const int64_t need = (count + H3C_SLOT_WPB - 1) / H3C_SLOT_WPB, cap = (int64_t)occ * sms;
+  return (unsigned)(need < cap ? need : cap);
+}
+
+void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, bool mapped, int sms, cudaStream_t stream) {
   if (count <= 0) return;
-  const int64_t ctas = (count + H3C_FLUX_WPB - 1) / H3C_FLUX_WPB;
-  h3c::k_h3c_flux<<<(unsigned)ctas, 32 * H3C_FLUX_WPB, 0, stream>>>(P, first, count);
+  if (mapped)
+    h3c::k_h3c_slot<true><<<slot_grid<true>(count, sms), 32 * H3C_SLOT_WPB, 0, stream>>>(P, first, count);
+  else
+    h3c::k_h3c_flux_id<<<(unsigned)((count + 7) / 8), 256, 0, stream>>>(P, first, count);
+}
+
+void sipg_h3c_map_launch(const H3Plan& P, int64_t first, int64_t count, int sms, cudaStream_t stream) {
+  if (count <= 0) return;
+  h3c::k_h3c_slot<false><<<slot_grid<false>(count, sms), 32 * H3C_SLOT_WPB, 0, stream>>>(P, first, count);
 }

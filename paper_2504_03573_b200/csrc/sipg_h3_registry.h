@@ -18,4 +18,6 @@ struct H3Entry {
 };
 void sipg_register_h3(std::vector<H3Entry>& v);
 // generation 1: the flux kernel (one warp per slot) over cslots[first, first + count), between publish and apply
-void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, cudaStream_t stream);
+void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, bool mapped, int sms, cudaStream_t stream);
+// generation 1: the trace-map kernel over the same work list, right after the publish kernels of those slots
+void sipg_h3c_map_launch(const H3Plan& P, int64_t first, int64_t count, int sms, cudaStream_t stream);

@@ -228,7 +228,7 @@ struct CfgC {
   static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
   static constexpr int TABD = (3 * Q + 3 * Q + Q2 + 6 * Q + TB + 1) & ~1;     // pts R W12 E B
   static constexpr int imax(int a, int b) { return a > b ? a : b; }
-  static constexpr int SCR_P = (imax(BUF + S1, SB * 4 * TMAX) + 1) & ~1;      // publish: u, s1 | map scratch
+  static constexpr int SCR_P = (BUF + S1 + 1) & ~1;                            // publish: u, s1
   static constexpr int FBN = NSMAX * 2 * Q2;                                   // own-grid fluxes of an element
   static constexpr int NI = 4 * NPM + 4 + NC + 16;
   // kernel modes: 0 apply, 1 publish
@@ -363,7 +363,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         r[1] = H3C_LDG(P.slot_off + e + 1) - sb;
         r[2] = H3C_LDG(P.dof_off + e);
         r[3] = sb;
-        r[4] = APP ? H3C_LDG(P.fb_off + e) : 0;
+        r[4] = H3C_LDG(P.fb_off + e);
       }
     });
   };
@@ -478,34 +478,31 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
       sync();
-      // stage 2: group sums with the B rows; thread (g, ko) produces the whole kb line
-      // (prism: kb = k2, ko = k1; tet: kb = k1, ko = k2)
-      par([&](int lt, TS&) {
-        const int g = lt / Q, ko = lt % Q;     // NG * Q = NT
-        double out[Q];
-#pragma unroll
-        for (int k = 0; k < Q; ++k) out[k] = 0.0;
-        const int q0 = gstart[g], cntg = gstart[g + 1] - q0;
-        for (int qq = 0; qq < cntg; ++qq) {
-          const int m = gmem[q0 + qq];
-          const double sv = s1[m * Q + ko];
-          const double* Br = Bt + m * Q;
-#pragma unroll
-          for (int k = 0; k < Q; ++k) out[k] = fma(Br[k], sv, out[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          if (S == H3_PRISM) s2[g * SI + ko * SJ + k] = out[k];
-          else s2[g * SI + k * SJ + ko] = out[k];
-        }
-      });
-      sync();
     }
+    // last stages, in registers: thread (k1, k2) sums every triangle mode's B x s1 product into its
+    // group's accumulator (compile-time mode -> group map, no shared-memory s2) and applies A along eta0
     par([&](int lt, TS& ts) {
       const int ta = lt / Q, tb_ = lt % Q;
       double col[NA];
+      if (S == H3_HEX) {
 #pragma unroll
-      for (int g = 0; g < NA; ++g) col[g] = s2[g * SI + ta * SJ + tb_];
+        for (int g = 0; g < NA; ++g) col[g] = s2[g * SI + ta * SJ + tb_];
+      } else {
+        // prism: B on eta2, s1 over eta1; tet: B on eta1, s1 over eta2
+        const double* Bk = Bt + (S == H3_PRISM ? tb_ : ta);
+        const double* sk = s1 + (S == H3_PRISM ? ta : tb_);
+#pragma unroll
+        for (int g = 0; g < NA; ++g) col[g] = 0.0;
+        int m = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j < N - i; ++j, ++m) {
+            const int g = i == 0 ? (j == 1 ? 1 : 0) : (i == 1 ? 2 : i + 1);
+            col[g] = fma(Bk[m * Q], sk[m * Q], col[g]);
+          }
+        if (S == H3_TET) col[1] = fma(Bk[C::NTRI * Q], sk[C::NTRI * Q], col[1]);   // apex pseudo-mode
+      }
       cmat<Q, NA>(H3C_TA, 0, col, ts.u);
     });
 
@@ -577,6 +574,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       });
       sync();
       // n.grad u at own face point a = lt of every face; identity-map couplings publish directly
+      double* fbe = P.fb + fbo;
       par([&](int lt, TS&) {
         int s = 0;
         for_faces<0, NF>([&](auto Fc) {
@@ -597,112 +595,16 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
             Ff[Q2 + lt] = gv;
             for (; s < ns && slot_hdr(hdr, s).face == f; ++s) {
               const H3Slot& hs = slot_hdr(hdr, s);
-              if (hs.mkind == MAP_ID) reinterpret_cast<double2*>(P.pub + hs.pub_self)[lt] = make_double2(uf, gv);
+              if (hs.mkind == MAP_ID) {
+                reinterpret_cast<double2*>(P.pub + hs.pub_self)[lt] = make_double2(uf, gv);
+              } else {   // staged on the own face grid for the trace-map kernel (fb is free until the flux kernel)
+                fbe[s * 2 * Q2 + lt] = uf;
+                fbe[s * 2 * Q2 + Q2 + lt] = gv;
+              }
             }
           }
         });
       });
-      bool mapped = false;
-      for (int j = 0; j < ns; ++j) mapped |= slot_hdr(hdr, j).mkind != MAP_ID;
-      if (mapped) {
-        sync();
-        for (int b0 = 0; b0 < ns; b0 += SB) {
-          const int nb = ns - b0 < SB ? ns - b0 : SB;
-          bool bm = false;
-          for (int j = 0; j < nb; ++j) bm |= slot_hdr(hdr, b0 + j).mkind != MAP_ID;
-          if (!bm) continue;
-          // forward maps, stage 1: tensor X / row Y contraction; dense complete
-          par([&](int lt, TS&) {
-            auto c1 = [&](int s) -> int {
-              const H3Slot& h = slot_hdr(hdr, s);
-              if (h.mkind == MAP_TENSOR) return (h.nab & 255) * Q;
-              if (h.mkind == MAP_ROW) return ((h.nab >> 8) & 255) * Q;
-              return h.mkind == MAP_DENSE ? h.nt : 0;
-            };
-            const Batch B1_(b0, nb, c1);
-            for (int it0 = lt; it0 < B1_.tot; it0 += NT) {
-              int it = it0;
-              const int s = B1_.slot(it);
-              const H3Slot& h = slot_hdr(hdr, s);
-              const double* fu = FL + h.face * 4 * Q2;
-              const double* fg = fu + Q2;
-              double* tu = tb + (s - b0) * 4 * TMAX;
-              double a0 = 0.0, a1 = 0.0;
-              if (h.mkind == MAP_ROW) {
-                const int pb = it / Q, ipar = it % Q, perp = (h.nab >> 16) & 1;
-                const double* Yr = tab + h.moff2 + pb * Q;
-#pragma unroll
-                for (int ip = 0; ip < Q; ++ip) {
-                  const double m = H3C_LDG(Yr + ip);
-                  const int o = perp ? ipar * Q + ip : ip * Q + ipar;
-                  a0 = fma(m, fu[o], a0);
-                  a1 = fma(m, fg[o], a1);
-                }
-                tu[2 * TMAX + it] = a0;
-                tu[3 * TMAX + it] = a1;
-              } else if (h.mkind == MAP_TENSOR) {
-                const int r1 = it / Q, ib = it % Q;
-                const double* X = tab + h.moff + r1 * Q;
-#pragma unroll
-                for (int ia = 0; ia < Q; ++ia) {
-                  const double m = H3C_LDG(X + ia);
-                  a0 = fma(m, fu[ia * Q + ib], a0);
-                  a1 = fma(m, fg[ia * Q + ib], a1);
-                }
-                tu[2 * TMAX + it] = a0;
-                tu[3 * TMAX + it] = a1;
-              } else {
-                const double* M = tab + h.moff + (int64_t)it * Q2;
-                for (int a = 0; a < Q2; ++a) {
-                  const double m = H3C_LDG(M + a);
-                  a0 = fma(m, fu[a], a0);
-                  a1 = fma(m, fg[a], a1);
-                }
-                reinterpret_cast<double2*>(P.pub + h.pub_self)[it] = make_double2(a0, a1);
-              }
-            }
-          });
-          sync();
-          par([&](int lt, TS&) {
-            auto c2 = [&](int s) -> int {
-              const H3Slot& h = slot_hdr(hdr, s);
-              return (h.mkind == MAP_TENSOR || h.mkind == MAP_ROW) ? h.nt : 0;
-            };
-            const Batch B2(b0, nb, c2);
-            for (int it0 = lt; it0 < B2.tot; it0 += NT) {
-              int it = it0;
-              const int s = B2.slot(it);
-              const H3Slot& h = slot_hdr(hdr, s);
-              const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
-              const double* tu = tb + (s - b0) * 4 * TMAX;
-              int p;
-              const double *Y, *m0, *m1;
-              if (h.mkind == MAP_ROW) {   // t[pa, pb] = sum_i_par X[pb][pa][i_par] tmp[pb][i_par]
-                const int pa = it / n2, pb = it % n2;
-                p = it;
-                Y = tab + h.moff + (pb * n1 + pa) * Q;
-                m0 = tu + 2 * TMAX + pb * Q;
-                m1 = tu + 3 * TMAX + pb * Q;
-              } else {
-                const int r1 = it / n2, r2 = it % n2;
-                p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
-                Y = tab + h.moff2 + r2 * Q;
-                m0 = tu + 2 * TMAX + r1 * Q;
-                m1 = tu + 3 * TMAX + r1 * Q;
-              }
-              double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-              for (int ib = 0; ib < Q; ++ib) {
-                const double m = H3C_LDG(Y + ib);
-                a0 = fma(m, m0[ib], a0);
-                a1 = fma(m, m1[ib], a1);
-              }
-              reinterpret_cast<double2*>(P.pub + h.pub_self)[p] = make_double2(a0, a1);
-            }
-          });
-          sync();
-        }
-      }
       continue;
     }
 
@@ -925,68 +827,250 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 }
 
 // ---------------------------------------------------------------------------------------------
-// Flux kernel, one warp per coupling side (slot), any shape / order: the SIP flux at the trace points
-// (sipg.py:622-650, 663-677) from the published own and partner traces (boundary: jump 2u, average
-// g), then the transposed trace map onto the owning element's face grid (q x q):
-// fb[slot] = (fv, fd).  The reference's per-interface phase 2 (sipg.py:607-661).  A streaming
-// kernel: no element structure, few registers, full occupancy.
-#define H3C_FLUX_WPB 8     // warps (slots) per CTA
-template <typename Par, typename Sync>
-H3C_HD void flux_slot(const H3Plan& P, const int64_t i, double* tv, Par par, Sync sync) {
-  // the 64-byte record, four 16-byte loads (every lane the same address)
-  H3FluxRec h;
-  {
-    const int4* src = reinterpret_cast<const int4*>(P.frec + i);
-    int4* dst = reinterpret_cast<int4*>(&h);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) dst[r] = H3C_LDG(src + r);
-  }
-  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q, mkind = h.mk_kind & 255, kind = h.mk_kind >> 8;
-  double* fb = P.fb + (h.fb_q >> 4);
-  const double* tab = P.tab;
-  const bool ident = mkind == MAP_ID;
+// Slot kernels, one warp per coupling side (slot), any shape / order, over work lists of 64-byte
+// records (identity-map and mapped slots separately, so the warps of a launch do uniform work).
+//   trace maps (mapped slots): the own traces (u, n.grad u) the publish kernel staged on the own face
+//     grid (in fb), interpolated to the coupling's trace points (trace.py:172-199 transfers; tensor
+//     X (x) Y, row-structured for subface quads, or dense) -> published;
+//   flux: the SIP flux at the trace points (sipg.py:622-650, 663-677) from the published own and
+//     partner traces (boundary: jump 2u, average g), then the transposed trace map onto the owning
+//     element's face grid: fb[slot] = (fv, fd) -- the reference's per-interface phase 2
+//     (sipg.py:607-661).
+// Identity-map flux is a pure streaming kernel (one slot per warp).  The mapped kernels are
+// persistent: a warp walks its slots with the next slot's inputs (and the record after that) in
+// flight by cp.async while it computes -- the dependent record -> data -> store chain of a slot is
+// several DRAM latencies long, and without the prefetch these kernels ran at a fifth of the HBM rate.
+#define H3C_SLOT_WPB 4                       // warps per CTA
+H3C_HD int div_small(int it, unsigned rcp) { return (int)(((unsigned)it * rcp) >> 16); }   // it < 600, divisor <= 8
+
+#if defined(__CUDA_ARCH__)
+// fp64 tensor-core tile D(8x8) += A(8x4) B(4x8): lane l = 4 g + t holds A[g][t], B[t][g], D[g][2t], D[g][2t+1]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, const double a, const double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+#endif
+
+// staged inputs of a mapped slot (doubles): map: own-grid (u | g), 2 q^2;  flux: own traces (u, g)
+// interleaved [0, 2 TMAX), partner traces [2 TMAX, 4 TMAX), trace weights [4 TMAX, 5 TMAX)
+#define H3C_ST_MAP (2 * h3::TMAX)
+#define H3C_ST_FLUX (5 * h3::TMAX)
+template <bool FLUX, typename Par>
+H3C_HD void slot_stage(const H3Plan& P, const H3FluxRec& h, double* st, Par par) {
+  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q;
   par([&](int lane) {
-    double2 own[2], nbv[2];
-    double wv[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int p = lane + 32 * r;
-      own[r] = nbv[r] = make_double2(0.0, 0.0);
-      wv[r] = 0.0;
-      if (p < h.nt) {
-        own[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
-        if (kind) nbv[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
-        wv[r] = H3C_LDG(tab + h.wtoff + p);
+#if defined(__CUDA_ARCH__)
+    if (FLUX) {
+      const double* own = P.pub + h.pub_self;
+      const double* nbr = P.pub + h.pub_other;
+      for (int r = lane; r < h.nt; r += 32) {
+        __pipeline_memcpy_async(st + 2 * r, own + 2 * r, 16);
+        if (h.mk_kind >> 8) __pipeline_memcpy_async(st + 2 * TMAX + 2 * r, nbr + 2 * r, 16);
+        __pipeline_memcpy_async(st + 4 * TMAX + r, P.tab + h.wtoff + r, 8);
       }
+    } else {
+      const double* og = P.fb + (h.fb_q >> 4);
+      for (int r = lane; r < Q2; r += 32) __pipeline_memcpy_async(st + 2 * r, og + 2 * r, 16);
     }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int p = lane + 32 * r;
-      if (p < h.nt) {
-        const double ut = own[r].x, gt = own[r].y;
-        const double un = kind ? nbv[r].x : -ut, gn = kind ? nbv[r].y : -gt;
-        const double j = ut - un, cc = 0.5 * (gt - gn);
-        const double w = h.sJ * wv[r];
-        const double fv = (h.tau * j - cc) * w, fd = -0.5 * j * w;
-        if (ident) {          // trace grid = own face grid
-          fb[p] = fv;
-          fb[Q2 + p] = fd;
-        } else {
-          tv[p] = fv;
-          tv[TMAX + p] = fd;
+#else
+    if (FLUX) {
+      for (int r = lane; r < h.nt; r += 32) {
+        st[2 * r] = P.pub[h.pub_self + 2 * r];
+        st[2 * r + 1] = P.pub[h.pub_self + 2 * r + 1];
+        if (h.mk_kind >> 8) {
+          st[2 * TMAX + 2 * r] = P.pub[h.pub_other + 2 * r];
+          st[2 * TMAX + 2 * r + 1] = P.pub[h.pub_other + 2 * r + 1];
         }
+        st[4 * TMAX + r] = P.tab[h.wtoff + r];
+      }
+    } else {
+      for (int r = lane; r < 2 * Q2; r += 32) st[r] = P.fb[(h.fb_q >> 4) + r];
+    }
+#endif
+  });
+}
+
+// trace map of a staged slot: st = own-grid (u | g); tmp: 2 TMAX doubles
+template <typename Par, typename Sync>
+H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& h, const double* st, double* tmp, Par par, Sync sync) {
+  const int mkind = h.mk_kind & 255;
+  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q;
+  const unsigned rq = 65536u / Q + 1;
+  const double* tab = P.tab;
+  double2* dst = reinterpret_cast<double2*>(P.pub + h.pub_self);
+  const double* fu = st;
+  const double* fg = st + Q2;
+  const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_TENSOR) {
+    // t_f = X F_f Y^T (f = u, g) as two 8 x 8 x 8 tensor-core products per field, zero-padded:
+    // T_f = X F_f, then t_f = T_f Y^T with T_f passed from the accumulator to the A layout by shuffles
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* X = tab + h.moff;
+    const double* Y = tab + h.moff2;
+    double cu0 = 0.0, cu1 = 0.0, cg0 = 0.0, cg1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int ia = 4 * ks + t;
+      const bool ok = ia < Q && g < Q;
+      const double a = (g < n1 && ia < Q) ? __ldg(X + g * Q + ia) : 0.0;
+      const double bu = ok ? fu[ia * Q + g] : 0.0, bg = ok ? fg[ia * Q + g] : 0.0;
+      dmma884(cu0, cu1, a, bu);
+      dmma884(cg0, cg1, a, bg);
+    }
+    double tu0 = 0.0, tu1 = 0.0, tg0 = 0.0, tg1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int src = (lane & ~3) + 2 * ks + (t >> 1), ib = 4 * ks + t;
+      const double xu0 = __shfl_sync(0xffffffffu, cu0, src), xu1 = __shfl_sync(0xffffffffu, cu1, src);
+      const double xg0 = __shfl_sync(0xffffffffu, cg0, src), xg1 = __shfl_sync(0xffffffffu, cg1, src);
+      const double au = (t & 1) ? xu1 : xu0, ag = (t & 1) ? xg1 : xg0;
+      const double b = (g < n2 && ib < Q) ? __ldg(Y + g * Q + ib) : 0.0;
+      dmma884(tu0, tu1, au, b);
+      dmma884(tg0, tg1, ag, b);
+    }
+    if (g < n1) {
+      const int r2 = 2 * t;
+      if (r2 < n2) dst[sw ? r2 * n1 + g : g * n2 + r2] = make_double2(tu0, tg0);
+      if (r2 + 1 < n2) dst[sw ? (r2 + 1) * n1 + g : g * n2 + r2 + 1] = make_double2(tu1, tg1);
+    }
+    return;
+  }
+#endif
+  par([&](int lane) {
+    const int tot = mkind == MAP_TENSOR ? n1 * Q : (mkind == MAP_ROW ? n2 * Q : h.nt);
+    for (int it = lane; it < tot; it += 32) {
+      double a0 = 0.0, a1 = 0.0;
+      const int r1 = div_small(it, rq), ib = it - r1 * Q;
+      if (mkind == MAP_ROW) {          // tmp[pb][i_par] = sum_i_perp Y[pb][i_perp] f(i_par, i_perp)
+        const double* Yr = tab + h.moff2 + r1 * Q;
+        H3C_MAPLOOP(ip, Q) {
+          const double m = H3C_LDG(Yr + ip);
+          const int o = sw ? ib * Q + ip : ip * Q + ib;
+          a0 = fma(m, fu[o], a0);
+          a1 = fma(m, fg[o], a1);
+        }
+        tmp[it] = a0;
+        tmp[TMAX + it] = a1;
+      } else if (mkind == MAP_TENSOR) {
+        const double* X = tab + h.moff + r1 * Q;
+        H3C_MAPLOOP(ia, Q) {
+          const double m = H3C_LDG(X + ia);
+          a0 = fma(m, fu[ia * Q + ib], a0);
+          a1 = fma(m, fg[ia * Q + ib], a1);
+        }
+        tmp[it] = a0;
+        tmp[TMAX + it] = a1;
+      } else {                         // dense
+        const double* M = tab + h.moff + (int64_t)it * Q2;
+        for (int a = 0; a < Q2; ++a) {
+          const double m = H3C_LDG(M + a);
+          a0 = fma(m, fu[a], a0);
+          a1 = fma(m, fg[a], a1);
+        }
+        dst[it] = make_double2(a0, a1);
       }
     }
   });
-  if (ident) return;
+  if (mkind == MAP_DENSE) return;
+  sync();
+  const unsigned rn2 = 65536u / n2 + 1;
+  par([&](int lane) {
+    for (int it = lane; it < h.nt; it += 32) {
+      const int r1 = div_small(it, rn2), r2 = it - r1 * n2;
+      int p;
+      const double *Y, *m0, *m1;
+      if (mkind == MAP_ROW) {   // t[pa, pb] = sum_i_par X[pb][pa][i_par] tmp[pb][i_par]  (r1 = pa, r2 = pb)
+        p = it;
+        Y = tab + h.moff + (r2 * n1 + r1) * Q;
+        m0 = tmp + r2 * Q;
+        m1 = tmp + TMAX + r2 * Q;
+      } else {
+        p = sw ? r2 * n1 + r1 : r1 * n2 + r2;
+        Y = tab + h.moff2 + r2 * Q;
+        m0 = tmp + r1 * Q;
+        m1 = tmp + TMAX + r1 * Q;
+      }
+      double a0 = 0.0, a1 = 0.0;
+      H3C_MAPLOOP(ib, Q) {
+        const double m = H3C_LDG(Y + ib);
+        a0 = fma(m, m0[ib], a0);
+        a1 = fma(m, m1[ib], a1);
+      }
+      dst[p] = make_double2(a0, a1);
+    }
+  });
+}
+
+// flux + transposed map of a staged mapped slot (st as slot_stage<true>; its own-trace part is reused
+// for the first contraction); tv: 2 TMAX doubles
+template <typename Par, typename Sync>
+H3C_HD void flux_compute(const H3Plan& P, const H3FluxRec& h, double* st, double* tv, Par par, Sync sync) {
+  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q, mkind = h.mk_kind & 255, kind = h.mk_kind >> 8;
+  const unsigned rq = 65536u / Q + 1;
+  double* fb = P.fb + (h.fb_q >> 4);
+  const double* tab = P.tab;
+  double* tmp = st;                // first contraction (over the consumed own traces)
+  par([&](int lane) {              // flux at the trace points: tv[p], tv[TMAX + p]
+    for (int p = lane; p < h.nt; p += 32) {
+      const double ut = st[2 * p], gt = st[2 * p + 1];
+      const double un = kind ? st[2 * TMAX + 2 * p] : -ut, gn = kind ? st[2 * TMAX + 2 * p + 1] : -gt;
+      const double j = ut - un, cc = 0.5 * (gt - gn);
+      const double w = h.sJ * st[4 * TMAX + p];
+      tv[p] = (h.tau * j - cc) * w;
+      tv[TMAX + p] = -0.5 * j * w;
+    }
+  });
   sync();
   const int n1 = h.nab & 255, n2 = (h.nab >> 8) & 255, sw = (h.nab >> 16) & 1;
-  // transposed map, stage 1: tensor / row first contraction, dense complete -> tv[2], tv[3]
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_TENSOR) {
+    // F_f = X^T G_f Y (f = fv, fd; G_f the flux on the n1 x n2 trace grid): U_f = G_f Y, F_f = X^T U_f
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* X = tab + h.moff;
+    const double* Y = tab + h.moff2;
+    double uv0 = 0.0, uv1 = 0.0, ud0 = 0.0, ud1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int r2 = 4 * ks + t;
+      const bool ok = g < n1 && r2 < n2;
+      const int p = sw ? r2 * n1 + g : g * n2 + r2;
+      const double av = ok ? tv[p] : 0.0, ad = ok ? tv[TMAX + p] : 0.0;
+      const double b = (r2 < n2 && g < Q) ? __ldg(Y + r2 * Q + g) : 0.0;
+      dmma884(uv0, uv1, av, b);
+      dmma884(ud0, ud1, ad, b);
+    }
+    double fv0 = 0.0, fv1 = 0.0, fd0 = 0.0, fd1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int r1 = 4 * ks + t, src = r1 * 4 + (g >> 1);
+      const double xv0 = __shfl_sync(0xffffffffu, uv0, src), xv1 = __shfl_sync(0xffffffffu, uv1, src);
+      const double xd0 = __shfl_sync(0xffffffffu, ud0, src), xd1 = __shfl_sync(0xffffffffu, ud1, src);
+      const double bv = (g & 1) ? xv1 : xv0, bd = (g & 1) ? xd1 : xd0;
+      const double a = (r1 < n1 && g < Q) ? __ldg(X + r1 * Q + g) : 0.0;
+      dmma884(fv0, fv1, a, bv);
+      dmma884(fd0, fd1, a, bd);
+    }
+    if (g < Q) {
+      const int ib = 2 * t;
+      if (ib < Q) {
+        fb[g * Q + ib] = fv0;
+        fb[Q2 + g * Q + ib] = fd0;
+      }
+      if (ib + 1 < Q) {
+        fb[g * Q + ib + 1] = fv1;
+        fb[Q2 + g * Q + ib + 1] = fd1;
+      }
+    }
+    return;
+  }
+#endif
+  // transposed map, stage 1: tensor / row first contraction, dense complete -> tmp
   par([&](int lane) {
     const int tot = mkind == MAP_ROW ? n2 * Q : (mkind == MAP_TENSOR ? n1 * Q : Q2);
     for (int it = lane; it < tot; it += 32) {
       double a0 = 0.0, a1 = 0.0;
-      const int r1 = it / Q, ib = it - r1 * Q;
+      const int r1 = div_small(it, rq), ib = it - r1 * Q;
       if (mkind == MAP_ROW) {   // tmp[pb][i_par] = sum_pa X[pb][pa][i_par] g[pa, pb]
         H3C_MAPLOOP(pa, n1) {
           const double m = H3C_LDG(tab + h.moff + (r1 * n1 + pa) * Q + ib);
@@ -1009,8 +1093,8 @@ H3C_HD void flux_slot(const H3Plan& P, const int64_t i, double* tv, Par par, Syn
           a1 = fma(m, tv[TMAX + p], a1);
         }
       }
-      tv[2 * TMAX + it] = a0;
-      tv[3 * TMAX + it] = a1;
+      tmp[it] = a0;
+      tmp[TMAX + it] = a1;
     }
   });
   sync();
@@ -1018,25 +1102,25 @@ H3C_HD void flux_slot(const H3Plan& P, const int64_t i, double* tv, Par par, Syn
   par([&](int lane) {
     for (int a = lane; a < Q2; a += 32) {
       double a0 = 0.0, a1 = 0.0;
-      const int ia = a / Q, ib = a - ia * Q;
+      const int ia = div_small(a, rq), ib = a - ia * Q;
       if (mkind == MAP_ROW) {   // F(i_par, i_perp) = sum_pb Y[pb][i_perp] tmp[pb][i_par]
         const int ipar = sw ? ia : ib, iperp = sw ? ib : ia;   // sw: the perp flag of a row map
         H3C_MAPLOOP(pb, n2) {
           const double m = H3C_LDG(tab + h.moff2 + pb * Q + iperp);
-          a0 = fma(m, tv[2 * TMAX + pb * Q + ipar], a0);
-          a1 = fma(m, tv[3 * TMAX + pb * Q + ipar], a1);
+          a0 = fma(m, tmp[pb * Q + ipar], a0);
+          a1 = fma(m, tmp[TMAX + pb * Q + ipar], a1);
         }
       } else if (mkind == MAP_TENSOR) {
         const double* Xc = tab + h.moff + ia;
-        const double* t0 = tv + 2 * TMAX + ib;
+        const double* t0 = tmp + ib;
         H3C_MAPLOOP(r1, n1) {
           const double m = H3C_LDG(Xc + r1 * Q);
           a0 = fma(m, t0[r1 * Q], a0);
           a1 = fma(m, t0[TMAX + r1 * Q], a1);
         }
       } else {
-        a0 = tv[2 * TMAX + a];
-        a1 = tv[3 * TMAX + a];
+        a0 = tmp[a];
+        a1 = tmp[TMAX + a];
       }
       fb[a] = a0;
       fb[Q2 + a] = a1;
@@ -1044,13 +1128,87 @@ H3C_HD void flux_slot(const H3Plan& P, const int64_t i, double* tv, Par par, Syn
   });
 }
 
-// work-list records [first, first + count)
-__global__ void __launch_bounds__(32 * H3C_FLUX_WPB, 6) k_h3c_flux(const H3Plan P, const int64_t first, const int64_t count) {
-  __shared__ double scr[H3C_FLUX_WPB][4 * TMAX];
-  const int w = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * H3C_FLUX_WPB + w;
+// identity-map flux: trace grid = own face grid, straight from global to global
+template <typename Par>
+H3C_HD void flux_ident(const H3Plan& P, const int64_t i, Par par) {
+  const H3FluxRec h = P.frec[i];
+  const int Q = (int)(h.fb_q & 15), Q2 = Q * Q, kind = h.mk_kind >> 8;
+  double* fb = P.fb + (h.fb_q >> 4);
+  par([&](int lane) {
+    double2 own[2], nbv[2];
+    double wv[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = lane + 32 * r;
+      own[r] = nbv[r] = make_double2(0.0, 0.0);
+      wv[r] = 0.0;
+      if (p < h.nt) {
+        own[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_self) + p);
+        if (kind) nbv[r] = H3C_LDG(reinterpret_cast<const double2*>(P.pub + h.pub_other) + p);
+        wv[r] = H3C_LDG(P.tab + h.wtoff + p);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = lane + 32 * r;
+      if (p < h.nt) {
+        const double ut = own[r].x, gt = own[r].y;
+        const double un = kind ? nbv[r].x : -ut, gn = kind ? nbv[r].y : -gt;
+        const double j = ut - un, cc = 0.5 * (gt - gn);
+        const double w = h.sJ * wv[r];
+        fb[p] = (h.tau * j - cc) * w;
+        fb[Q2 + p] = -0.5 * j * w;
+      }
+    }
+  });
+}
+
+// identity-map records [first, first + count), one per warp
+__global__ void __launch_bounds__(256, 6) k_h3c_flux_id(const H3Plan P, const int64_t first, const int64_t count) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= count) return;
-  flux_slot(P, first + i, scr[w], [&](auto&& f) { f((int)(threadIdx.x & 31)); }, [&]() { __syncwarp(); });
+  flux_ident(P, first + i, [&](auto&& f) { f((int)(threadIdx.x & 31)); });
+}
+
+// mapped records [first, first + count): persistent warps, inputs of the next slot and the record
+// after it prefetched by cp.async
+template <bool FLUX>
+__global__ void __launch_bounds__(32 * H3C_SLOT_WPB) k_h3c_slot(const H3Plan P, const int64_t first, const int64_t count) {
+  constexpr int ST = FLUX ? H3C_ST_FLUX : H3C_ST_MAP;
+  constexpr int PW = 3 * 8 + 2 * ST + 2 * TMAX;   // per warp: record ring | staged inputs x 2 | flux values / map tmp
+  __shared__ __align__(16) double sm_[H3C_SLOT_WPB * PW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* my = sm_ + w * PW;
+  H3FluxRec* ring = reinterpret_cast<H3FluxRec*>(my);
+  double* st = my + 24;
+  double* tmp = st + 2 * ST;
+  const int64_t W = (int64_t)gridDim.x * H3C_SLOT_WPB;
+  int64_t i = (int64_t)blockIdx.x * H3C_SLOT_WPB + w;
+  auto par = [&](auto&& f) { f(lane); };
+  auto sync = [&]() { __syncwarp(); };
+  auto fetch_rec = [&](int64_t idx, int slot) {   // 64 bytes: lanes 0..3, 16 bytes each
+    if (lane < 4)
+      __pipeline_memcpy_async(reinterpret_cast<char*>(ring + slot) + 16 * lane,
+                              reinterpret_cast<const char*>(P.frec + first + idx) + 16 * lane, 16);
+  };
+  if (i >= count) return;
+  fetch_rec(i, 0);
+  if (i + W < count) fetch_rec(i + W, 1);
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
+  __syncwarp();
+  slot_stage<FLUX>(P, ring[0], st, par);
+  __pipeline_commit();
+  for (int k = 0; i < count; i += W, ++k) {
+    __pipeline_wait_prior(0);
+    __syncwarp();
+    if (i + W < count) slot_stage<FLUX>(P, ring[(k + 1) % 3], st + ((k + 1) & 1) * ST, par);
+    if (i + 2 * W < count) fetch_rec(i + 2 * W, (k + 2) % 3);
+    __pipeline_commit();
+    if (FLUX) flux_compute(P, ring[k % 3], st + (k & 1) * ST, tmp, par, sync);
+    else map_compute(P, ring[k % 3], st + (k & 1) * ST, tmp, par, sync);
+    __syncwarp();
+  }
 }
 
 // resident CTAs per SM the register allocation must allow, per q (apply | publish)

@@ -89,7 +89,7 @@ extern "C" int64_t h3c_emu_fb_layout(const sipg_h3_desc* d, int64_t* fb_off) {
   return fb_off[d->n_elements];
 }
 
-// phase 0: publish every class into pub; phase 2: the fluxes of every class (reads pub) into fb;
+// phase 0: publish every class into pub; phase 3: the trace maps of the staged slots; phase 2: the fluxes of every class (reads pub) into fb;
 // phase 1: apply every class (reads fb) into y
 extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, double* pub, double* fb,
                            const int64_t* fb_off, int phase) {
@@ -111,10 +111,25 @@ extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, do
   }
   H3Plan P{d->class_desc, d->class_elems, d->dof_off, d->elem_geom, d->slot_off, (const H3Slot*)d->slots,
            d->tables, pub, d->lambda, fb, fb_off, fr.data()};
-  if (phase == 2) {   // the flux kernel: one "warp" per slot, lanes one after the other between the barriers
+  auto lanes = [&](auto&& f) { for (int lane = 0; lane < 32; ++lane) f(lane); };
+  if (phase == 3) {   // the trace-map kernel, after the publish kernels (mapped slots)
     for (size_t i = 0; i < fr.size(); ++i) {
-      std::vector<double> scr(4 * h3::TMAX, NAN);
-      h3c::flux_slot(P, (int64_t)i, scr.data(), [&](auto&& f) { for (int lane = 0; lane < 32; ++lane) f(lane); }, [] {});
+      if ((fr[i].mk_kind & 255) == MAP_ID) continue;
+      std::vector<double> st(H3C_ST_MAP, NAN), tmp(2 * h3::TMAX, NAN);
+      h3c::slot_stage<false>(P, fr[i], st.data(), lanes);
+      h3c::map_compute(P, fr[i], st.data(), tmp.data(), lanes, [] {});
+    }
+    return 0;
+  }
+  if (phase == 2) {   // the flux kernels: identity-map slots streaming, mapped slots staged
+    for (size_t i = 0; i < fr.size(); ++i) {
+      if ((fr[i].mk_kind & 255) == MAP_ID) {
+        h3c::flux_ident(P, (int64_t)i, lanes);
+      } else {
+        std::vector<double> st(H3C_ST_FLUX, NAN), tv(2 * h3::TMAX, NAN);
+        h3c::slot_stage<true>(P, fr[i], st.data(), lanes);
+        h3c::flux_compute(P, fr[i], st.data(), tv.data(), lanes, [] {});
+      }
     }
     return 0;
   }

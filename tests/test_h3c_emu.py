@@ -54,7 +54,7 @@ def run_emu(L, pb, x):
     pub = np.full(max(pb.n_pub, 1), np.nan)
     fb = np.full(max(nfb, 1), np.nan)
     y = np.full(pb.n_dofs, np.nan)
-    for phase in (0, 2, 1):
+    for phase in (0, 3, 2, 1):
         rc = L.h3c_emu_run(ctypes.byref(d), x.ctypes.data, y.ctypes.data, pub.ctypes.data, fb.ctypes.data,
                            fb_off.ctypes.data, phase)
         assert rc == 0
