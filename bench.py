@@ -39,7 +39,8 @@ OP_KW = dict(basis_kind="modified_modal", tau_rule="baseline", shared_rule="patc
 
 
 KERNEL_NAMES = {0: "k_apply", 2: "k_hex(generic faces)", 4: "k_hex", 5: "k_apply_w",
-                6: "k_hexp", 7: "k_hexp", 8: "k_h3_publish", 9: "k_h3_apply"}
+                6: "k_hexp", 7: "k_hexp", 8: "k_h3c publish (+ k_h3c_slot trace maps)", 9: "k_h3c apply",
+                10: "k_h3c_flux_id + k_h3c_slot flux"}
 
 
 def kernel_label(info, rd):

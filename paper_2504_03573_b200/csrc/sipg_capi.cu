@@ -317,33 +317,34 @@ int publish_grid(const int32_t* cd, int count, int sms) {
 // the last one; host apply 9.0 -> 8.1 ms with the graduated chunks and graph replay).
 // SIPG_STREAM_UNIFORM=1 keeps uniform chunks.  Returns K (0: too small to stream).
 int make_chunks(sipg_plan* p, int64_t ndof, int64_t chunk_bytes) {
-  std::vector<double> w;
   const double units = (double)ndof * 8 / (chunk_bytes > 0 ? chunk_bytes : 1) * 4.0;
-  if (getenv("SIPG_STREAM_UNIFORM") || units < 16) {
-    const int Ku = (int)(units / 4);
-    for (int k = 0; k < Ku; ++k) w.push_back(1.0);
-  } else {
+  auto place = [&](std::vector<double> w) -> int {
+    int K = (int)w.size();
+    if (K > 64) K = 64;
+    if (K < 2) return 0;
+    w.resize(K);
+    p->chunk_dof.assign(K + 1, 0);
+    double tot = 0.0, acc = 0.0;
+    for (double v : w) tot += v;
+    for (int k = 1; k < K; ++k) {
+      acc += w[k - 1];
+      p->chunk_dof[k] = (int64_t)((double)ndof * acc / tot) & ~(int64_t)511;
+    }
+    p->chunk_dof[K] = ndof;
+    for (int k = 0; k < K; ++k)
+      if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return 0;
+    return K;
+  };
+  if (!getenv("SIPG_STREAM_UNIFORM") && units >= 16) {   // graduated: short first copy, short tail
+    std::vector<double> w = {1, 2};
     const int mid = (int)((units - 6) / 4 + 0.5);
-    w = {1, 2};
     for (int k = 0; k < mid; ++k) w.push_back(4);
     w.push_back(2);
     w.push_back(1);
+    const int K = place(w);
+    if (K) return K;   // else (4 KB alignment leaves a short chunk empty on small meshes): uniform chunks
   }
-  int K = (int)w.size();
-  if (K > 64) K = 64;
-  if (K < 2) return 0;
-  w.resize(K);
-  p->chunk_dof.assign(K + 1, 0);
-  double tot = 0.0, acc = 0.0;
-  for (double v : w) tot += v;
-  for (int k = 1; k < K; ++k) {
-    acc += w[k - 1];
-    p->chunk_dof[k] = (int64_t)((double)ndof * acc / tot) & ~(int64_t)511;
-  }
-  p->chunk_dof[K] = ndof;
-  for (int k = 0; k < K; ++k)
-    if (p->chunk_dof[k + 1] <= p->chunk_dof[k]) return 0;
-  return K;
+  return place(std::vector<double>((size_t)(units / 4 > 0 ? units / 4 : 0), 1.0));
 }
 
 // Build the streamed-apply schedule (see sipg_plan).  Returns false when the mesh ordering does not

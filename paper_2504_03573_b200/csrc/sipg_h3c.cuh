@@ -45,6 +45,9 @@
 #ifndef H3C_ITEM_U
 #define H3C_ITEM_U 0        // ragged tet stages: item loops unrolled (measured slower: spills)
 #endif
+#ifndef H3C_TET_FUSE1
+#define H3C_TET_FUSE1 1     // tets: the ragged eta2 stage recomputed per thread inside the fused register stage
+#endif
 #if H3C_MAP_U8
 #define H3C_MAPLOOP(i, n) _Pragma("unroll") for (int i = 0; i < 8; ++i) if (i < (n))
 #else
@@ -226,11 +229,12 @@ struct CfgC {
   static constexpr int SLOTD = 12;
   static constexpr int SB = 4;                                  // slots per map batch
   static constexpr int TB = S == H3_HEX ? 0 : NPM * Q;
-  static constexpr int TABD = (3 * Q + 3 * Q + Q2 + 6 * Q + TB + 1) & ~1;     // pts R W12 E B
+  static constexpr int NCD = S == H3_TET ? N * (N - 1) / 2 + 1 : 0;            // distinct eta2 rows of a tet class
+  static constexpr int TABD = (3 * Q + 3 * Q + Q2 + 6 * Q + TB + NCD * Q + 1) & ~1;   // pts R W12 E B Cd
   static constexpr int imax(int a, int b) { return a > b ? a : b; }
   static constexpr int SCR_P = (BUF + S1 + 1) & ~1;                            // publish: u, s1
   static constexpr int FBN = NSMAX * 2 * Q2;                                   // own-grid fluxes of an element
-  static constexpr int NI = 4 * NPM + 4 + NC + 16;
+  static constexpr int NI = 2 * NPM + 2 + NC + NCD + 8;   // gof, minfo, rinfo, cdrep
   // kernel modes: 0 apply, 1 publish
   static constexpr int doubles(int mode) {
     return mode == 1 ? 16 + TABD + 2 * NCP + 2 * NSMAX * SLOTD + NF * 4 * Q2 + SCR_P
@@ -239,39 +243,36 @@ struct CfgC {
   static constexpr size_t smem_bytes(int mode) { return sizeof(double) * doubles(mode) + sizeof(int) * NI; }
 };
 
-// triangle-mode groups and tet mode offsets (h3::build_int_tables), by one thread
+// triangle pseudo-mode -> group (row 0 -> 0 except (0,1) -> 1, row 1 -> 2, row i >= 2 -> i + 1; the tet apex
+// pseudo-mode -> 1), and for tets the packed tables of the ragged eta2 stage.  The eta2 functions of a
+// tet mode (i, j, k) depend on the triangle mode's degree d = max(i + j, 1) and on k only
+// (plan3d.collapse_rows), so the class's C table (n_c x q) is kept as its n (n - 1) / 2 + 1 distinct
+// rows: cdrep[row] = a row of the plan's table holding it, minfo[m] = first mode | count << 8 | first
+// distinct row << 16, rinfo[r] = triangle pseudo-mode | distinct row << 8.  By one thread.
 template <int S, int N>
-H3C_HD void build_int_tables(int* gstart, int* gmem, int* gof, int* coff, int* mofr) {
+H3C_HD void build_int_tables(int* gof, int* minfo, int* rinfo, int* cdrep) {
   using C = CfgC<S, N>;
-  int cnt[C::NG + 1];
-  for (int g = 0; g <= C::NG; ++g) cnt[g] = 0;
   int m = 0;
   for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N - i; ++j, ++m) {
-      const int g = i == 0 ? (j == 1 ? 1 : 0) : (i == 1 ? 2 : i + 1);
-      gof[m] = g;
-      ++cnt[g];
-    }
+    for (int j = 0; j < N - i; ++j, ++m) gof[m] = i == 0 ? (j == 1 ? 1 : 0) : (i == 1 ? 2 : i + 1);
   if (S == H3_TET) {
     gof[C::NTRI] = 1;
-    ++cnt[1];
-  }
-  gstart[0] = 0;
-  for (int g = 0; g < C::NG; ++g) gstart[g + 1] = gstart[g] + cnt[g];
-  int fill[C::NG];
-  for (int g = 0; g < C::NG; ++g) fill[g] = gstart[g];
-  for (int mm = 0; mm < C::NPM; ++mm) gmem[fill[gof[mm]]++] = mm;
-  if (S == H3_TET) {
+    int doff[N + 1];
+    doff[1] = 0;
+    for (int d = 1; d < N; ++d) doff[d + 1] = doff[d] + (N - d);
     int r = 0, mm = 0;
     for (int i = 0; i < N; ++i)
       for (int j = 0; j < N - i; ++j, ++mm) {
         const int d = (i + j) > 1 ? i + j : 1;
-        coff[mm] = r;
-        for (int k = 0; k < N - d; ++k) mofr[r++] = mm;
+        minfo[mm] = r | ((N - d) << 8) | (doff[d] << 16);
+        for (int k = 0; k < N - d; ++k) {
+          cdrep[doff[d] + k] = r;
+          rinfo[r++] = mm | ((doff[d] + k) << 8);
+        }
       }
-    coff[C::NTRI] = r;
-    mofr[r++] = C::NTRI;
-    coff[C::NTRI + 1] = r;
+    minfo[C::NTRI] = r | (1 << 8) | (doff[N] << 16);   // apex: one mode, the last distinct row
+    cdrep[doff[N]] = r;
+    rinfo[r] = C::NTRI | (doff[N] << 8);
   }
 }
 
@@ -323,11 +324,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   double* s2 = B0;
   double* s1 = B0 + BUF;
   double* tb = B0;                                                  // publish / flux: [SB][4][TMAX]
-  int* gstart = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : 2 * BUF + (BUF & 1)));
-  int* gmem = gstart + C::NPM + 2;
-  int* gof = gmem + C::NPM;
-  int* coff = gof + C::NPM;
-  int* mofr = coff + C::NPM + 2;
+  double* Cd = Bt + C::TB;                                          // tets: distinct eta2 rows [NCD][Q]
+  int* gof = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : 2 * BUF + (BUF & 1)));
+  int* minfo = gof + C::NPM + 1;
+  int* rinfo = minfo + C::NPM + 1;
+  int* cdrep = rinfo + C::NC + 1;
 
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
@@ -343,8 +344,14 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       cp(W12, tab + cd[CD3_T_W] + Q, Q2);
       cp(Et, tab + cd[CD3_T_E], 6 * Q);
       if (S != H3_HEX) cp(Bt, tab + cd[CD3_T_B], C::TB);
-      if (S != H3_HEX && lt == 0) build_int_tables<S, N>(gstart, gmem, gof, coff, mofr);
+      if (S != H3_HEX && lt == 0) build_int_tables<S, N>(gof, minfo, rinfo, cdrep);
     });
+    if (S == H3_TET) {
+      sync();
+      par([&](int lt, TS&) {
+        for (int r = lt; r < C::NCD * Q; r += NT) Cd[r] = H3C_LDG(Ct + cdrep[r / Q] * Q + r % Q);
+      });
+    }
   }
 
   // ---- element pipeline: scalars two elements ahead; coefficients + slot headers + geometry one
@@ -449,7 +456,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
       sync();
-    } else {
+    } else if (S == H3_PRISM || !H3C_TET_FUSE1) {
       // stage 1: the innermost family (prism: psi on eta1 per triangle mode; tet: C rows on eta2)
       par([&](int lt, TS&) {
         if (S == H3_PRISM) {
@@ -468,10 +475,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
             if (o < C::NPM * Q) {
               const int k = o % Q, m = o / Q;
               double a = 0.0;
-              const int r0 = coff[m], cn = coff[m + 1] - r0;
+              const int inf = minfo[m], r0 = inf & 255, cn = (inf >> 8) & 255;
+              const double* Cr = Cd + (inf >> 16) * Q + k;
 #pragma unroll
               for (int kk = 0; kk < (N - 1 > 1 ? N - 1 : 1); ++kk)
-                if (kk < cn) a = fma(H3C_LDG(Ct + (r0 + kk) * Q + k), c[r0 + kk], a);
+                if (kk < cn) a = fma(Cr[kk * Q], c[r0 + kk], a);
               s1[o] = a;
             }
           }
@@ -493,15 +501,29 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         const double* sk = s1 + (S == H3_PRISM ? ta : tb_);
 #pragma unroll
         for (int g = 0; g < NA; ++g) col[g] = 0.0;
-        int m = 0;
+        int m = 0, r = 0;
 #pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
           for (int j = 0; j < N - i; ++j, ++m) {
             const int g = i == 0 ? (j == 1 ? 1 : 0) : (i == 1 ? 2 : i + 1);
-            col[g] = fma(Bk[m * Q], sk[m * Q], col[g]);
+            if (S == H3_TET && H3C_TET_FUSE1) {
+              // s1[m][k2] = sum_k Cd[d][k][k2] c[r + k] on the fly (every index a compile-time constant;
+              // c is a broadcast read): no ragged item loop, no barrier, q-fold redundant but short
+              const int d = (i + j) > 1 ? i + j : 1, cn = N - d, row = (d - 1) * (2 * N - d) / 2;
+              double sv = 0.0;
+#pragma unroll
+              for (int k = 0; k < cn; ++k) sv = fma(Cd[(row + k) * Q + tb_], c[r + k], sv);
+              r += cn;
+              col[g] = fma(Bk[m * Q], sv, col[g]);
+            } else {
+              col[g] = fma(Bk[m * Q], sk[m * Q], col[g]);
+            }
           }
-        if (S == H3_TET) col[1] = fma(Bk[C::NTRI * Q], sk[C::NTRI * Q], col[1]);   // apex pseudo-mode
+        if (S == H3_TET) {   // apex pseudo-mode
+          const double sv = H3C_TET_FUSE1 ? Cd[(C::NCD - 1) * Q + tb_] * c[r] : sk[C::NTRI * Q];
+          col[1] = fma(Bk[C::NTRI * Q], sv, col[1]);
+        }
       }
       cmat<Q, NA>(H3C_TA, 0, col, ts.u);
     });
@@ -814,10 +836,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
           for (int rr = 0; rr < (C::NC + NT - 1) / NT; ++rr) {
             const int r = lt + rr * NT;
             if (r >= C::NC) break;
-            const int m = mofr[r];
+            const int inf = rinfo[r], m = inf & 255;
+            const double* Cr = Cd + (inf >> 8) * Q;
             double a = 0.0;
 #pragma unroll
-            for (int k2 = 0; k2 < Q; ++k2) a = fma(H3C_LDG(Ct + r * Q + k2), s1[m * Q + k2], a);
+            for (int k2 = 0; k2 < Q; ++k2) a = fma(Cr[k2], s1[m * Q + k2], a);
             y[dof + r] = a;
           }
         }
@@ -936,6 +959,35 @@ H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& h, const double* st, d
     }
     return;
   }
+#endif
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_ROW) {
+    // tmp[pb][i_par] = sum_i_perp Y[pb][i_perp] f(i_par, i_perp) as one 8 x 8 x 8 tensor-core product per field
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* Y = tab + h.moff2;
+    double cu0 = 0.0, cu1 = 0.0, cg0 = 0.0, cg1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int ip = 4 * ks + t;
+      const bool ok = ip < Q && g < Q;
+      const int o = sw ? g * Q + ip : ip * Q + g;
+      const double a = (g < n2 && ip < Q) ? __ldg(Y + g * Q + ip) : 0.0;
+      const double bu = ok ? fu[o] : 0.0, bg = ok ? fg[o] : 0.0;
+      dmma884(cu0, cu1, a, bu);
+      dmma884(cg0, cg1, a, bg);
+    }
+    if (g < n2) {
+      const int ib = 2 * t;
+      if (ib < Q) {
+        tmp[g * Q + ib] = cu0;
+        tmp[TMAX + g * Q + ib] = cg0;
+      }
+      if (ib + 1 < Q) {
+        tmp[g * Q + ib + 1] = cu1;
+        tmp[TMAX + g * Q + ib + 1] = cg1;
+      }
+    }
+  } else
 #endif
   par([&](int lane) {
     const int tot = mkind == MAP_TENSOR ? n1 * Q : (mkind == MAP_ROW ? n2 * Q : h.nt);
@@ -1098,6 +1150,35 @@ H3C_HD void flux_compute(const H3Plan& P, const H3FluxRec& h, double* st, double
     }
   });
   sync();
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_ROW) {
+    // F(i_par, i_perp) = sum_pb tmp[pb][i_par] Y[pb][i_perp]: one 8 x 8 x 8 tensor-core product per field
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* Y = tab + h.moff2;
+    double fv0 = 0.0, fv1 = 0.0, fd0 = 0.0, fd1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int pb = 4 * ks + t;
+      const bool ok = pb < n2 && g < Q;
+      const double av = ok ? tmp[pb * Q + g] : 0.0, ad = ok ? tmp[TMAX + pb * Q + g] : 0.0;   // A[i_par = g][pb]
+      const double b = ok ? __ldg(Y + pb * Q + g) : 0.0;                                      // B[pb][i_perp = g]
+      dmma884(fv0, fv1, av, b);
+      dmma884(fd0, fd1, ad, b);
+    }
+    if (g < Q) {   // C[i_par = g][i_perp = 2 t, 2 t + 1]
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int iperp = 2 * t + e;
+        if (iperp < Q) {
+          const int a = sw ? g * Q + iperp : iperp * Q + g;
+          fb[a] = e ? fv1 : fv0;
+          fb[Q2 + a] = e ? fd1 : fd0;
+        }
+      }
+    }
+    return;
+  }
+#endif
   // stage 2: second contraction onto the own face grid -> fb
   par([&](int lane) {
     for (int a = lane; a < Q2; a += 32) {

@@ -17,15 +17,16 @@ from . import layout as L
 
 def _per_class_h3(pb):
     """Hybrid 3-D plans (plan3d.py): one row per launch unit — the publish kernels (recomputed
-    BwdTrans / PhysDeriv / traces: not part of the algorithmic count, 0 bytes / flops) followed by
-    the apply kernels, which carry the element's whole algorithmic count.  BwdTrans of the
+    BwdTrans / traces: not part of the algorithmic count, 0 bytes / flops), the apply kernels, which
+    carry the element's whole algorithmic count, then the per-class flux slot launches (face work,
+    not part of the volume count either).  BwdTrans of the
     collapsed shapes, stage by stage: prism n_tri n q + n_tri q^2 + (n+1) q^3, tet
     n_c q + (n_tri+1) q^2 + (n+1) q^3."""
     from .plan3d import CD3_COUNT, CD3_N, CD3_NC, CD3_Q, CD3_SHAPE
     names = {0: "hex", 1: "prism", 2: "tet"}
     nfaces = {0: 6, 1: 5, 2: 4}
     rows = []
-    for unit in ("pub", "apply"):
+    for unit in ("pub", "apply", "flux"):
         for ci, cd in enumerate(pb.class_desc):
             s, n, q, nc, cnt = int(cd[CD3_SHAPE]), int(cd[CD3_N]), int(cd[CD3_Q]), int(cd[CD3_NC]), int(cd[CD3_COUNT])
             ntri = n * (n + 1) // 2
