@@ -1302,8 +1302,22 @@ __global__ void __launch_bounds__(32 * H3C_SLOT_WPB) k_h3c_slot(const H3Plan P, 
 template <int Q, int MODE>
 constexpr int h3c_minb() { return MODE == 1 ? H3C_MINB_P(Q) : H3C_MINB_A(Q); }
 
+// registers per thread for that many resident CTAs (__maxnreg__: ptxas otherwise stops at 128 for the
+// 64-thread classes even where the bound allows 144)
+template <int Q, int MODE>
+constexpr int h3c_regs() {
+  const int warps = (Q * Q + 31) / 32, r = 65536 / (h3c_minb<Q, MODE>() * warps * 32) / 8 * 8;
+  return r > 255 ? 255 : r;
+}
+#ifndef H3C_USE_MAXNREG
+#define H3C_USE_MAXNREG 0
+#endif
 template <int S, int N, int MODE>
+#if H3C_USE_MAXNREG
+__global__ void __launch_bounds__((N + 1) * (N + 1)) __maxnreg__((h3c_regs<N + 1, MODE>()))
+#else
 __global__ void __launch_bounds__((N + 1) * (N + 1), h3c_minb<N + 1, MODE>())
+#endif
 k_h3c(const H3Plan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(16) double h3c_sm[];
   body<S, N, MODE>(P, cls, x, y, (int)blockIdx.x, (int)gridDim.x, h3c_sm);
