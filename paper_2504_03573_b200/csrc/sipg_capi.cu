@@ -876,7 +876,8 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
         rows[(int64_t)r * CD3_WORDS + CD3_COUNT] = i1 - i0;
         rows[(int64_t)r * CD3_WORDS + CD3_ELEM_OFF] += i0;
         const int cap = pass == 0 ? h->cap_pub[c] : h->cap_apply[c];
-        const int g = (i1 - i0) < cap ? (i1 - i0) : cap;
+        const int groups = (i1 - i0 + h->kern[c]->epc - 1) / h->kern[c]->epc;
+        const int g = groups < cap ? groups : cap;
         (pass == 0 ? h->st_pub : h->st_comp)[k].push_back({r, g, h->kern[c], cd[CD3_ELEM_OFF] + i0, cd[CD3_ELEM_OFF] + i1});
         i0 = i1;
       }
@@ -1140,8 +1141,9 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       sipg_plan_destroy(p);
       return fail(SIPG_ERR_CUDA, "occupancy query failed for a hybrid kernel");
     }
-    h->grid_pub.push_back(count < occ_p * sms ? count : occ_p * sms);
-    h->grid_apply.push_back(count < occ_a * sms ? count : occ_a * sms);
+    const int groups = (count + k->epc - 1) / k->epc;   // CTAs work on groups of epc elements
+    h->grid_pub.push_back(groups < occ_p * sms ? groups : occ_p * sms);
+    h->grid_apply.push_back(groups < occ_a * sms ? groups : occ_a * sms);
     h->cap_pub.push_back(occ_p * sms);
     h->cap_apply.push_back(occ_a * sms);
   }

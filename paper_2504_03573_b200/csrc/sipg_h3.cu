@@ -14,13 +14,13 @@ cudaError_t upload0(const double* D, const double* A, const double* psi, const d
 template <int S, int N>
 H3Entry entry0() {
   using C = h3::Cfg<S, N>;
-  return H3Entry{S, N, 0, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), C::smem_bytes(true),
+  return H3Entry{S, N, 0, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), 1, C::smem_bytes(true),
                  C::smem_bytes(false), &upload0<S, N>};
 }
 template <int S, int N>
 H3Entry entry1() {
   using C = h3c::CfgC<S, N>;
-  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, 1>, &h3c::k_h3c<S, N, 0>, C::NT, C::smem_bytes(1),
+  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, 1>, &h3c::k_h3c<S, N, 0>, C::NTC, C::E, C::smem_bytes(1),
                  C::smem_bytes(0), &h3c::h3c_upload<S, N>};
 }
 template <int S>

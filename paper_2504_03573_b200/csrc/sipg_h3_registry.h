@@ -13,6 +13,7 @@ struct H3Entry {
   int gen;             // 1: register-column kernels (sipg_h3c.cuh); 0: first generation (sipg_h3.cuh)
   H3Fn pub, apply;
   int threads;
+  int epc;             // elements per CTA (generation 1 packs several q^2-thread teams into a CTA)
   size_t smem_pub, smem_apply;
   H3UploadFn upload;
 };

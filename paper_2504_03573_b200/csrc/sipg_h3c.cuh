@@ -45,6 +45,9 @@
 #ifndef H3C_ITEM_U
 #define H3C_ITEM_U 0        // ragged tet stages: item loops unrolled (measured slower: spills)
 #endif
+#ifndef H3C_PACK
+#define H3C_PACK 1          // several elements per CTA (teams of q^2 threads) so that the warps are full
+#endif
 #ifndef H3C_TET_FUSE1
 #define H3C_TET_FUSE1 1     // tets: the ragged eta2 stage recomputed per thread inside the fused register stage
 #endif
@@ -216,7 +219,11 @@ H3C_HD void cmatT(const Tab& M, const int off, const double (&in)[K], double (&o
 
 template <int S, int N>
 struct CfgC {
-  static constexpr int Q = N + 1, Q2 = Q * Q, NT = Q2;
+  static constexpr int Q = N + 1, Q2 = Q * Q, NT = Q2;   // NT: threads of one element (its team)
+  // elements (teams) per CTA: q^2 threads each, packed without padding so the warps are full
+  // (q = 6: 36 threads would leave a 4-lane second warp; seven elements fill 252 of 256 lanes)
+  static constexpr int E = H3C_PACK ? (Q <= 3 ? 3 : (Q == 4 ? 2 : (Q == 5 ? 5 : (Q == 6 ? 7 : (Q == 7 ? 5 : 1))))) : 1;
+  static constexpr int NTC = E * NT;                     // CTA threads
   static constexpr int SJ = (Q & 1) ? Q : Q + 1, SI = Q * SJ, BUF = Q * SI;   // odd row stride
   static constexpr int NF = S == H3_HEX ? 6 : (S == H3_PRISM ? 5 : 4);
   static constexpr int NTRI = N * (N + 1) / 2, NG = N + 1;
@@ -235,11 +242,13 @@ struct CfgC {
   static constexpr int SCR_P = (BUF + S1 + 1) & ~1;                            // publish: u, s1
   static constexpr int FBN = NSMAX * 2 * Q2;                                   // own-grid fluxes of an element
   static constexpr int NI = 2 * NPM + 2 + NC + NCD + 8;   // gof, minfo, rinfo, cdrep
-  // kernel modes: 0 apply, 1 publish
-  static constexpr int doubles(int mode) {
-    return mode == 1 ? 16 + TABD + 2 * NCP + 2 * NSMAX * SLOTD + NF * 4 * Q2 + SCR_P
-                     : 16 + TABD + 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + FBN + 2 * BUF + (BUF & 1);
+  // kernel modes: 0 apply, 1 publish.  Shared memory: ring | class tables | one block per team | int tables
+  static constexpr int RING = (3 * E * 5 + 1) & ~1;
+  static constexpr int teamd(int mode) {
+    return mode == 1 ? 2 * NCP + 2 * NSMAX * SLOTD + NF * 4 * Q2 + SCR_P
+                     : 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + FBN + 2 * BUF;   // every term even: 16-byte cp.async
   }
+  static constexpr int doubles(int mode) { return RING + TABD + E * teamd(mode); }
   static constexpr size_t smem_bytes(int mode) { return sizeof(double) * doubles(mode) + sizeof(int) * NI; }
 };
 
@@ -301,34 +310,48 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   auto par = [&](auto&& f) { f((int)threadIdx.x, ts_); };
   auto sync = [&]() { __syncthreads(); };
 #else
-  static thread_local TS tsa[NT];
+  static thread_local TS tsa[C::NTC];
   auto par = [&](auto&& f) {
-    for (int lt = 0; lt < NT; ++lt) f(lt, tsa[lt]);
+    for (int lt = 0; lt < C::NTC; ++lt) f(lt, tsa[lt]);
   };
   auto sync = [&]() {};
 #endif
-  // ---- shared memory (CfgC::doubles)
-  long long* ring = reinterpret_cast<long long*>(sm);                  // [3][5] element scalars (e, ns, dof, sb, fbo)
-  double* pts = sm + 16;
+  // ---- shared memory (CfgC::doubles): ring | class tables | team blocks | int tables
+  constexpr int E = C::E, NTC = C::NTC, TEAMD = C::teamd(MODE);
+  long long* ring = reinterpret_cast<long long*>(sm);                  // [3][E][5] element scalars (e, ns, dof, sb, fbo)
+  double* pts = sm + C::RING;
   double* Rt = pts + 3 * Q;
   double* W12 = Rt + 3 * Q;
   double* Et = W12 + Q2;
   double* Bt = Et + 6 * Q;
-  double* cbuf = sm + 16 + C::TABD;                          // [2][NCP] coefficients
-  double* hbuf = cbuf + 2 * C::NCP;                     // [2][NSMAX][12] slot headers
-  double* ebuf = hbuf + 2 * C::NSMAX * C::SLOTD;                    // apply: [2][8] element geometry
-  double* fbuf = ebuf + 2 * H3_EGEO;                                // apply: [ns][2][Q2] own-grid fluxes
-  double* FL = hbuf + 2 * C::NSMAX * C::SLOTD;                      // publish: [NF][4][Q2] face arrays
-  double* B0 = APP ? fbuf + C::FBN : FL + NF * 4 * Q2;        // q^3 buffer (padded); s2; map scratch
-  double* B1 = B0 + BUF;                                            // q^3 buffer (apply); s1
-  double* s2 = B0;
-  double* s1 = B0 + BUF;
-  double* tb = B0;                                                  // publish / flux: [SB][4][TMAX]
   double* Cd = Bt + C::TB;                                          // tets: distinct eta2 rows [NCD][Q]
-  int* gof = reinterpret_cast<int*>(B0 + (PUB ? C::SCR_P : 2 * BUF + (BUF & 1)));
+  double* teams = sm + C::RING + C::TABD;
+  // per team (element): coefficients [2][NCP] | slot headers [2][NSMAX][12] | apply: geometry [2][8], own-grid
+  // fluxes [ns][2][Q2], B0, B1 (padded q^3 buffers; BwdTrans s2, s1) | publish: face arrays [NF][4][Q2], u, s1
+  constexpr int O_H = 2 * C::NCP, O_E = O_H + 2 * C::NSMAX * C::SLOTD, O_F = O_E + 2 * H3_EGEO;
+  constexpr int O_B0 = APP ? O_F + C::FBN : O_E + NF * 4 * Q2;
+  int* gof = reinterpret_cast<int*>(teams + E * TEAMD);
   int* minfo = gof + C::NPM + 1;
   int* rinfo = minfo + C::NPM + 1;
   int* cdrep = rinfo + C::NC + 1;
+  // a thread's team (element) and its buffers: the first statement of every element-work phase
+#define H3C_TEAM(ltc)                                                                  \
+  const int tm = (ltc) / NT, lt = (ltc) - tm * NT;                                     \
+  const long long* rg_ = ring + 5 * (slot * E + tm);                                   \
+  const int ns = (int)rg_[1];                                                          \
+  if (ns < 0) return;                                                                  \
+  const int64_t dof = rg_[2], fbo = rg_[4];                                            \
+  double* tmb_ = teams + tm * TEAMD;                                                    \
+  const double* c = tmb_ + bsel * C::NCP;                                               \
+  const double* hdr = tmb_ + O_H + bsel * C::NSMAX * C::SLOTD;                          \
+  const double* eg = tmb_ + O_E + bsel * H3_EGEO;                                       \
+  double* fbuf = tmb_ + O_F;                                                            \
+  double* FL = tmb_ + O_E;                                                              \
+  double* B0 = tmb_ + O_B0;                                                             \
+  double* B1 = B0 + BUF;                                                               \
+  double* s2 = B0;                                                                     \
+  double* s1 = B0 + BUF;                                                               \
+  (void)dof; (void)fbo; (void)c; (void)hdr; (void)eg; (void)fbuf; (void)FL; (void)B1; (void)s2; (void)s1; (void)lt
 
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
@@ -337,7 +360,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   {
     par([&](int lt, TS&) {
       auto cp = [&](double* dst, const double* src, int n) {
-        for (int r = lt; r < n; r += NT) dst[r] = H3C_LDG(src + r);
+        for (int r = lt; r < n; r += NTC) dst[r] = H3C_LDG(src + r);
       };
       cp(pts, tab + cd[CD3_T_PTS], 3 * Q);
       cp(Rt, tab + cd[CD3_T_R], 3 * Q);
@@ -349,7 +372,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     if (S == H3_TET) {
       sync();
       par([&](int lt, TS&) {
-        for (int r = lt; r < C::NCD * Q; r += NT) Cd[r] = H3C_LDG(Ct + cdrep[r / Q] * Q + r % Q);
+        for (int r = lt; r < C::NCD * Q; r += NTC) Cd[r] = H3C_LDG(Ct + cdrep[r / Q] * Q + r % Q);
       });
     }
   }
@@ -360,80 +383,92 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   const int32_t* ce = P.class_elems + cd[CD3_ELEM_OFF];
   // element scalars through a 3-deep ring in shared memory (one thread loads them two elements ahead;
   // nothing of the pipeline is carried in registers)
-  auto scalars = [&](int i, int slot) {
+  // group gi of the class list = elements gi E .. gi E + E - 1, one per team (ns = -1: none)
+  auto scalars = [&](int gi, int slot) {
     par([&](int lt, TS&) {
-      if (lt == 0 && i < count) {
-        const int e = H3C_LDG(ce + i);
-        const long long sb = H3C_LDG(P.slot_off + e);
-        long long* r = ring + 5 * slot;
-        r[0] = e;
-        r[1] = H3C_LDG(P.slot_off + e + 1) - sb;
-        r[2] = H3C_LDG(P.dof_off + e);
-        r[3] = sb;
-        r[4] = H3C_LDG(P.fb_off + e);
+      if (lt < E) {
+        const int i = gi * E + lt;
+        long long* r = ring + 5 * (slot * E + lt);
+        r[1] = -1;
+        if (i < count) {
+          const int e = H3C_LDG(ce + i);
+          const long long sb = H3C_LDG(P.slot_off + e);
+          r[0] = e;
+          r[1] = H3C_LDG(P.slot_off + e + 1) - sb;
+          r[2] = H3C_LDG(P.dof_off + e);
+          r[3] = sb;
+          r[4] = H3C_LDG(P.fb_off + e);
+        }
       }
     });
   };
   auto issue = [&](int buf, int slot) {
-    const long long* r = ring + 5 * slot;
-    const int e = (int)r[0], ns = (int)r[1];
-    const int64_t dof = r[2], sb = r[3];
-    double* cd_ = cbuf + buf * C::NCP;
-    double* hd_ = hbuf + buf * C::NSMAX * C::SLOTD;
-    const double* src = reinterpret_cast<const double*>(P.slots + sb);
-    par([&](int lt, TS&) {
+    par([&](int ltc, TS&) {
+      const int tm = ltc / NT, lt = ltc - tm * NT;
+      const long long* r = ring + 5 * (slot * E + tm);
+      const int e = (int)r[0], ns = (int)r[1];
+      const int64_t dof = r[2], sb = r[3];
+      double* tb_ = teams + tm * TEAMD;
+      double* cd_ = tb_ + buf * C::NCP;
+      double* hd_ = tb_ + O_H + buf * C::NSMAX * C::SLOTD;
+      double* eb_ = tb_ + O_E + buf * H3_EGEO;
+      const double* src = reinterpret_cast<const double*>(P.slots + sb);
 #if defined(__CUDA_ARCH__)
-      for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
-      for (int r = lt; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
-      if (APP && lt < H3_EGEO / 2)
-        __pipeline_memcpy_async(ebuf + buf * H3_EGEO + 2 * lt, P.egeo + (int64_t)e * H3_EGEO + 2 * lt,
-                                2 * sizeof(double));
+      if (ns >= 0) {
+        for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
+        for (int r = lt; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
+        if (APP && lt < H3_EGEO / 2)
+          __pipeline_memcpy_async(eb_ + 2 * lt, P.egeo + (int64_t)e * H3_EGEO + 2 * lt, 2 * sizeof(double));
+      }
       __pipeline_commit();
 #else
-      for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
-      for (int r = lt; r < ns * C::SLOTD; r += NT) hd_[r] = src[r];
-      if (APP && lt < H3_EGEO / 2) {
-        ebuf[buf * H3_EGEO + 2 * lt] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt];
-        ebuf[buf * H3_EGEO + 2 * lt + 1] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt + 1];
+      if (ns >= 0) {
+        for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
+        for (int r = lt; r < ns * C::SLOTD; r += NT) hd_[r] = src[r];
+        if (APP && lt < H3_EGEO / 2) {
+          eb_[2 * lt] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt];
+          eb_[2 * lt + 1] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt + 1];
+        }
       }
 #endif
     });
   };
-  auto issue_fb = [&](int64_t fbo, int ns) {   // ns * 2 * Q2 doubles, 16-byte pieces (fb_off is even)
-    const double* src = P.fb + fbo;
-    par([&](int lt, TS&) {
+  auto issue_fb = [&](int slot) {   // ns * 2 * Q2 doubles per team, 16-byte pieces (fb_off is even)
+    par([&](int ltc, TS&) {
+      const int tm = ltc / NT, lt = ltc - tm * NT;
+      const long long* r = ring + 5 * (slot * E + tm);
+      const int ns = (int)r[1];
+      const double* src = P.fb + r[4];
+      double* fbuf = teams + tm * TEAMD + O_F;
 #if defined(__CUDA_ARCH__)
-      for (int r = lt; r < ns * Q2; r += NT) __pipeline_memcpy_async(fbuf + 2 * r, src + 2 * r, 2 * sizeof(double));
+      for (int q = lt; q < ns * Q2; q += NT) __pipeline_memcpy_async(fbuf + 2 * q, src + 2 * q, 2 * sizeof(double));
       __pipeline_commit();
 #else
-      for (int r = lt; r < ns * 2 * Q2; r += NT) fbuf[r] = src[r];
+      for (int q = lt; q < ns * 2 * Q2; q += NT) fbuf[q] = src[q];
 #endif
     });
   };
+  const int ngroups = (count + E - 1) / E;
   scalars(bid, 0);
   scalars(bid + G, 1);
   sync();
-  if (bid < count) issue(0, 0);
+  if (bid < ngroups) issue(0, 0);
   int it_el = 0;
-  for (int i = bid; i < count; i += G, ++it_el) {
+  for (int gi = bid; gi < ngroups; gi += G, ++it_el) {
     const int bsel = it_el & 1;
     const int slot = it_el % 3, slot_n = (it_el + 1) % 3, slot_nn = (it_el + 2) % 3;
 #if defined(__CUDA_ARCH__)
     __pipeline_wait_prior(0);
 #endif
     sync();
-    const double* c = cbuf + bsel * C::NCP;
-    const double* hdr = hbuf + bsel * C::NSMAX * C::SLOTD;
-    const double* eg = ebuf + bsel * H3_EGEO;
-    const int ns = (int)ring[5 * slot + 1];
-    const int64_t dof = ring[5 * slot + 2], fbo = ring[5 * slot + 4];
-    if (i + G < count) issue(bsel ^ 1, slot_n);
-    scalars(i + 2 * G, slot_nn);
-    if (APP) issue_fb(fbo, ns);
+    if (gi + G < ngroups) issue(bsel ^ 1, slot_n);
+    scalars(gi + 2 * G, slot_nn);
+    if (APP) issue_fb(slot);
 
     // ================= BwdTrans (stdregions.py:575-597): u column in registers ====================
     if (S == H3_HEX) {
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (lt < N * N) {                      // (i0, i1): i2 -> k2
           double col[N], out[Q];
 #pragma unroll
@@ -444,7 +479,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
       sync();
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (lt < N * Q) {                      // (i0, k2): i1 -> k1
           const int i0 = lt / Q, k2 = lt % Q;
           double col[N], out[Q];
@@ -458,7 +494,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       sync();
     } else if (S == H3_PRISM || !H3C_TET_FUSE1) {
       // stage 1: the innermost family (prism: psi on eta1 per triangle mode; tet: C rows on eta2)
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (S == H3_PRISM) {
           for (int m = lt; m < C::NPM; m += NT) {
             double col[N], out[Q];
@@ -489,7 +526,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     }
     // last stages, in registers: thread (k1, k2) sums every triangle mode's B x s1 product into its
     // group's accumulator (compile-time mode -> group map, no shared-memory s2) and applies A along eta0
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
       double col[NA];
       if (S == H3_HEX) {
@@ -531,7 +569,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     if (PUB) {
       // ================= publish: own traces (u, n.grad u) of every coupling =====================
       // FL[f] = (u, d u / d eta_fixed, d u / d eta_ra, d u / d eta_rb) on the own face grid
-      par([&](int lt, TS& ts) {
+      par([&](int ltc, TS& ts) {
+        H3C_TEAM(ltc);
         const int ta = lt / Q, tb_ = lt % Q;
         for_faces<0, NF>([&](auto Fc) {
           constexpr int f = decltype(Fc)::value;
@@ -551,7 +590,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
       });
       sync();
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         const int ta = lt / Q, tb_ = lt % Q;
         double v[Q], w[Q];
 #pragma unroll
@@ -578,7 +618,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       });
       sync();
       // tangential derivatives: one face-grid line per task (face, direction, line)
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         for (int task = lt; task < NF * 2 * Q; task += NT) {
           const int f = task / (2 * Q), dir = (task / Q) & 1, line = task % Q;
           const int base = dir ? line * Q : line, st = dir ? 1 : Q;
@@ -596,8 +637,9 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       });
       sync();
       // n.grad u at own face point a = lt of every face; identity-map couplings publish directly
-      double* fbe = P.fb + fbo;
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
+        double* fbe = P.fb + fbo;
         int s = 0;
         for_faces<0, NF>([&](auto Fc) {
           constexpr int f = decltype(Fc)::value;
@@ -632,14 +674,16 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 
     // ================= apply: PhysDeriv (stdregions.py:658-674) ==================================
     // eta0 in registers; eta1 / eta2 one line per thread through B0 / B1
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
       for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
       eo_full<Q>(H3C_TE, 0 * EOS, ts.u, ts.d0);
     });
     sync();
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
       double v[Q], w[Q];
 #pragma unroll
@@ -653,7 +697,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       for (int r = 0; r < Q; ++r) B1[ta * SI + r * SJ + tb_] = ts.d1[r];
     });
     sync();   // every line of B0 read
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
       for (int r = 0; r < Q; ++r) B0[ta * SI + tb_ * SJ + r] = ts.d2[r];
@@ -663,7 +708,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     __pipeline_wait_prior(0);   // this element's own-grid fluxes (and the next element's prefetch)
 #endif
     sync();
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
@@ -750,7 +796,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       for (int k = 0; k < Q; ++k) ts.u[k] += r[k];
     });
     sync();
-    par([&](int lt, TS&) {
+    par([&](int ltc, TS&) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
       double v[Q], w[Q], r1[Q], r2[Q];
 #pragma unroll
@@ -768,7 +815,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     });
     sync();
     // ================= IProduct (stdregions.py:599-618): y = Phi^T T ==============================
-    par([&](int lt, TS& ts) {
+    par([&](int ltc, TS& ts) {
+      H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
       for (int k = 0; k < Q; ++k) ts.u[k] += B0[k * SI + ta * SJ + tb_] + B1[k * SI + ta * SJ + tb_];
@@ -779,7 +827,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     });
     sync();
     if (S == H3_HEX) {
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (lt < N * Q) {                      // (i0, k2): k1 -> i1
           const int i0 = lt / Q, k2 = lt % Q;
           double col[Q], out[N];
@@ -791,7 +840,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
       sync();
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (lt < N * N) {                      // (i0, i1): k2 -> i2
           double col[Q], out[N];
 #pragma unroll
@@ -802,7 +852,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
     } else {
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         H3C_ITEM_UNROLL
         for (int rr = 0; rr < (C::NPM * Q + NT - 1) / NT; ++rr) {
           const int o = lt + rr * NT;
@@ -821,7 +872,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         }
       });
       sync();
-      par([&](int lt, TS&) {
+      par([&](int ltc, TS&) {
+        H3C_TEAM(ltc);
         if (S == H3_PRISM) {
           for (int m = lt; m < C::NPM; m += NT) {
             double col[Q], out[N];
@@ -1293,11 +1345,20 @@ __global__ void __launch_bounds__(32 * H3C_SLOT_WPB) k_h3c_slot(const H3Plan P, 
 }
 
 // resident CTAs per SM the register allocation must allow, per q (apply | publish)
+#if H3C_PACK   // CTAs of 64 (q = 8), 245, 252, 125 (q = 7, 6, 5) threads
+#ifndef H3C_MINB_A
+#define H3C_MINB_A(Q) ((Q) >= 8 ? 8 : ((Q) == 7 ? 2 : ((Q) == 6 ? 2 : ((Q) == 5 ? 5 : 8))))
+#endif
+#ifndef H3C_MINB_P
+#define H3C_MINB_P(Q) ((Q) >= 8 ? 10 : ((Q) == 7 ? 2 : ((Q) == 6 ? 3 : ((Q) == 5 ? 6 : 8))))
+#endif
+#else
 #ifndef H3C_MINB_A
 #define H3C_MINB_A(Q) ((Q) >= 8 ? 8 : ((Q) == 7 ? 8 : ((Q) == 6 ? 10 : 20)))
 #endif
 #ifndef H3C_MINB_P
 #define H3C_MINB_P(Q) ((Q) >= 8 ? 10 : ((Q) == 7 ? 10 : ((Q) == 6 ? 12 : 24)))
+#endif
 #endif
 template <int Q, int MODE>
 constexpr int h3c_minb() { return MODE == 1 ? H3C_MINB_P(Q) : H3C_MINB_A(Q); }
@@ -1314,9 +1375,9 @@ constexpr int h3c_regs() {
 #endif
 template <int S, int N, int MODE>
 #if H3C_USE_MAXNREG
-__global__ void __launch_bounds__((N + 1) * (N + 1)) __maxnreg__((h3c_regs<N + 1, MODE>()))
+__global__ void __launch_bounds__(CfgC<S, N>::NTC) __maxnreg__((h3c_regs<N + 1, MODE>()))
 #else
-__global__ void __launch_bounds__((N + 1) * (N + 1), h3c_minb<N + 1, MODE>())
+__global__ void __launch_bounds__(CfgC<S, N>::NTC, h3c_minb<N + 1, MODE>())
 #endif
 k_h3c(const H3Plan P, const int cls, const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(16) double h3c_sm[];
