@@ -48,6 +48,18 @@
 #ifndef H3C_PACK
 #define H3C_PACK 1          // several elements per CTA (teams of q^2 threads) so that the warps are full
 #endif
+#ifndef H3C_E5
+#define H3C_E5 5
+#endif
+#ifndef H3C_E6
+#define H3C_E6 7
+#endif
+#ifndef H3C_E7
+#define H3C_E7 5
+#endif
+#ifndef H3C_E8
+#define H3C_E8 1
+#endif
 #ifndef H3C_TET_FUSE1
 #define H3C_TET_FUSE1 1     // tets: the ragged eta2 stage recomputed per thread inside the fused register stage
 #endif
@@ -222,7 +234,7 @@ struct CfgC {
   static constexpr int Q = N + 1, Q2 = Q * Q, NT = Q2;   // NT: threads of one element (its team)
   // elements (teams) per CTA: q^2 threads each, packed without padding so the warps are full
   // (q = 6: 36 threads would leave a 4-lane second warp; seven elements fill 252 of 256 lanes)
-  static constexpr int E = H3C_PACK ? (Q <= 3 ? 3 : (Q == 4 ? 2 : (Q == 5 ? 5 : (Q == 6 ? 7 : (Q == 7 ? 5 : 1))))) : 1;
+  static constexpr int E = H3C_PACK ? (Q <= 3 ? 3 : (Q == 4 ? 2 : (Q == 5 ? H3C_E5 : (Q == 6 ? H3C_E6 : (Q == 7 ? H3C_E7 : H3C_E8))))) : 1;
   static constexpr int NTC = E * NT;                     // CTA threads
   static constexpr int SJ = (Q & 1) ? Q : Q + 1, SI = Q * SJ, BUF = Q * SI;   // odd row stride
   static constexpr int NF = S == H3_HEX ? 6 : (S == H3_PRISM ? 5 : 4);
@@ -931,7 +943,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, const double a, 
 #define H3C_ST_MAP (2 * h3::TMAX)
 #define H3C_ST_FLUX (5 * h3::TMAX)
 template <bool FLUX, typename Par>
-H3C_HD void slot_stage(const H3Plan& P, const H3FluxRec& h, double* st, Par par) {
+H3C_HD void slot_stage(const H3Plan& P, const H3FluxRec& hr, double* st, Par par) {
+  const H3FluxRec h = hr;   // the record (shared-memory ring) in registers
   const int Q = (int)(h.fb_q & 15), Q2 = Q * Q;
   par([&](int lane) {
 #if defined(__CUDA_ARCH__)
@@ -967,7 +980,8 @@ H3C_HD void slot_stage(const H3Plan& P, const H3FluxRec& h, double* st, Par par)
 
 // trace map of a staged slot: st = own-grid (u | g); tmp: 2 TMAX doubles
 template <typename Par, typename Sync>
-H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& h, const double* st, double* tmp, Par par, Sync sync) {
+H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& hr, const double* st, double* tmp, Par par, Sync sync) {
+  const H3FluxRec h = hr;
   const int mkind = h.mk_kind & 255;
   const int Q = (int)(h.fb_q & 15), Q2 = Q * Q;
   const unsigned rq = 65536u / Q + 1;
@@ -1078,6 +1092,26 @@ H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& h, const double* st, d
   });
   if (mkind == MAP_DENSE) return;
   sync();
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_ROW) {
+    // t_f[pa, pb] = sum_i_par X[pb][pa][i_par] tmp_f[pb][i_par]: per trace row pb one 8 x 8 x 8 tensor-core
+    // product whose B operand holds the two fields (u, n.grad u) in its first two columns
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* X = tab + h.moff;
+    for (int pb = 0; pb < n2; ++pb) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int ip = 4 * ks + t;
+        const double a = (g < n1 && ip < Q) ? __ldg(X + (pb * n1 + g) * Q + ip) : 0.0;
+        const double b = (g < 2 && ip < Q) ? tmp[g * TMAX + pb * Q + ip] : 0.0;
+        dmma884(c0, c1, a, b);
+      }
+      if (t == 0 && g < n1) dst[g * n2 + pb] = make_double2(c0, c1);   // C[pa = g][field 0, 1]
+    }
+    return;
+  }
+#endif
   const unsigned rn2 = 65536u / n2 + 1;
   par([&](int lane) {
     for (int it = lane; it < h.nt; it += 32) {
@@ -1109,7 +1143,8 @@ H3C_HD void map_compute(const H3Plan& P, const H3FluxRec& h, const double* st, d
 // flux + transposed map of a staged mapped slot (st as slot_stage<true>; its own-trace part is reused
 // for the first contraction); tv: 2 TMAX doubles
 template <typename Par, typename Sync>
-H3C_HD void flux_compute(const H3Plan& P, const H3FluxRec& h, double* st, double* tv, Par par, Sync sync) {
+H3C_HD void flux_compute(const H3Plan& P, const H3FluxRec& hr, double* st, double* tv, Par par, Sync sync) {
+  const H3FluxRec h = hr;
   const int Q = (int)(h.fb_q & 15), Q2 = Q * Q, mkind = h.mk_kind & 255, kind = h.mk_kind >> 8;
   const unsigned rq = 65536u / Q + 1;
   double* fb = P.fb + (h.fb_q >> 4);
@@ -1168,6 +1203,28 @@ H3C_HD void flux_compute(const H3Plan& P, const H3FluxRec& h, double* st, double
     }
     return;
   }
+#endif
+#if defined(__CUDA_ARCH__)
+  if (mkind == MAP_ROW) {
+    // tmp_f[pb][i_par] = sum_pa X[pb][pa][i_par] g_f[pa, pb]: per trace row pb one tensor-core product,
+    // the two fields (fv, fd) in the first two columns of B
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const double* X = tab + h.moff;
+    for (int pb = 0; pb < n2; ++pb) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int pa = 4 * ks + t;
+        const double a = (g < Q && pa < n1) ? __ldg(X + (pb * n1 + pa) * Q + g) : 0.0;   // A[i_par = g][pa]
+        const double b = (g < 2 && pa < n1) ? tv[g * TMAX + pa * n2 + pb] : 0.0;          // B[pa][field g]
+        dmma884(c0, c1, a, b);
+      }
+      if (t == 0 && g < Q) {
+        tmp[pb * Q + g] = c0;
+        tmp[TMAX + pb * Q + g] = c1;
+      }
+    }
+  } else
 #endif
   // transposed map, stage 1: tensor / row first contraction, dense complete -> tmp
   par([&](int lane) {
