@@ -765,7 +765,7 @@ int h3_exchange(sipg_plan* p) {
 int h3_apply(sipg_plan* p, int role, const double* x_dev, double* y_dev, cudaStream_t s) {
   H3State* h = p->h3;
   int rc = 0;
-  // pass 0 publish, 3 trace maps, 2 flux (register-column kernels; no-ops for the first generation), 1 apply
+  // pass 0 publish, 3 trace maps, 2 flux, 1 apply
   if (role == 1) {
     if ((rc = h3_launch(p, 2, 1, x_dev, y_dev, s))) return rc;
     if ((rc = h3_launch(p, 1, 1, x_dev, y_dev, s))) return rc;
@@ -1022,13 +1022,11 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
   p->n_cls = d->n_classes;
   p->n_dofs = d->n_dofs;
   h->cd.assign(d->class_desc, d->class_desc + (int64_t)d->n_classes * CD3_WORDS);
-  // SIPG_H3_GEN=0: the first-generation kernels (same results to rounding; kept for A/B timing)
-  const int gen = getenv("SIPG_H3_GEN") ? atoi(getenv("SIPG_H3_GEN")) : 1;
   for (int c = 0; c < d->n_classes; ++c) {
     const int32_t* cd = d->class_desc + c * CD3_WORDS;
     const H3Entry* k = nullptr;
     for (const auto& e : table)
-      if (e.gen == gen && e.shape == cd[CD3_SHAPE] && e.n == cd[CD3_N] && cd[CD3_Q] == e.n + 1) k = &e;
+      if (e.shape == cd[CD3_SHAPE] && e.n == cd[CD3_N] && cd[CD3_Q] == e.n + 1) k = &e;
     if (!k) {
       sipg_plan_destroy(p);
       return fail(SIPG_ERR_UNSUPPORTED, "no sm_100a hybrid kernel for shape=" + std::to_string(cd[CD3_SHAPE]) +
@@ -1095,7 +1093,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     }
     h->cs_id[d->n_elements] = ki;
     h->cs_mp[d->n_elements] = km;
-    h->flux = gen == 1;
+    h->flux = true;
     if ((rc = upload(fbo.data(), d->n_elements + 1, &h->fb_off_d)) || (rc = upload(fr.data(), d->n_slots, &h->frec_d))) {
       sipg_plan_destroy(p);
       return rc;

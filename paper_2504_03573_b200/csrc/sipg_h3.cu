@@ -1,42 +1,35 @@
-// Instantiations of the config-4 hybrid hex / prism / tet kernels, n_modes 2..7: the register-column
-// kernels (sipg_h3c.cuh, generation 1, default) and the first-generation kernels (sipg_h3.cuh,
-// generation 0).
+// Instantiations of the config-4 hybrid hex / prism / tet kernels (sipg_h3c.cuh), n_modes 2..7, and
+// the launchers of the slot kernels (trace maps, flux).
 #include <vector>
 #include "sipg_h3c.cuh"
 #include "sipg_h3_registry.h"
 
 namespace {
 template <int S, int N>
-cudaError_t upload0(const double* D, const double* A, const double* psi, const double*, const double*, const double*,
-                    const double*) {
-  return h3::h3_upload<S, N>(D, A, psi);
-}
-template <int S, int N>
-H3Entry entry0() {
-  using C = h3::Cfg<S, N>;
-  return H3Entry{S, N, 0, &h3::k_h3<S, N, true>, &h3::k_h3<S, N, false>, h3::nthreads<N + 1>(), 1, C::smem_bytes(true),
-                 C::smem_bytes(false), &upload0<S, N>};
-}
-template <int S, int N>
-H3Entry entry1() {
+H3Entry entry() {
   using C = h3c::CfgC<S, N>;
-  return H3Entry{S, N, 1, &h3c::k_h3c<S, N, 1>, &h3c::k_h3c<S, N, 0>, C::NTC, C::E, C::smem_bytes(1),
+  return H3Entry{S, N, &h3c::k_h3c<S, N, 1>, &h3c::k_h3c<S, N, 0>, C::NTC, C::E, C::smem_bytes(1),
                  C::smem_bytes(0), &h3c::h3c_upload<S, N>};
 }
 template <int S>
 void add(std::vector<H3Entry>& v) {
-  v.push_back(entry0<S, 2>());
-  v.push_back(entry0<S, 3>());
-  v.push_back(entry0<S, 4>());
-  v.push_back(entry0<S, 5>());
-  v.push_back(entry0<S, 6>());
-  v.push_back(entry0<S, 7>());
-  v.push_back(entry1<S, 2>());
-  v.push_back(entry1<S, 3>());
-  v.push_back(entry1<S, 4>());
-  v.push_back(entry1<S, 5>());
-  v.push_back(entry1<S, 6>());
-  v.push_back(entry1<S, 7>());
+  v.push_back(entry<S, 2>());
+  v.push_back(entry<S, 3>());
+  v.push_back(entry<S, 4>());
+  v.push_back(entry<S, 5>());
+  v.push_back(entry<S, 6>());
+  v.push_back(entry<S, 7>());
+}
+
+// persistent grid of the mapped-slot kernels: resident CTAs per SM x SMs (capped by the work)
+template <bool FLUX>
+unsigned slot_grid(int64_t count, int sms) {
+  static int occ = 0;
+  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h3c::k_h3c_slot<FLUX>, 32 * H3C_SLOT_WPB, 0) !=
+                   cudaSuccess || occ <= 0))
+    occ = 4;
+  const int64_t need = (count + H3C_SLOT_WPB - 1) / H3C_SLOT_WPB, cap = (int64_t)occ * sms;
+  return (unsigned)(need < cap ? need : cap);
 }
 }  // namespace
 
@@ -44,17 +37,6 @@ void sipg_register_h3(std::vector<H3Entry>& v) {
   add<H3_HEX>(v);
   add<H3_PRISM>(v);
   add<H3_TET>(v);
-}
-
-// persistent grid of the mapped-slot kernels: resident CTAs per SM x SMs (capped by the work)
-template <bool FLUX>
-static unsigned slot_grid(int64_t count, int sms) {
-  static int occ = 0;
-  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h3c::k_h3c_slot<FLUX>, 32 * H3C_SLOT_WPB, 0) !=
-                   cudaSuccess || occ <= 0))
-    occ = 4;
-  const int64_t need = (count + H3C_SLOT_WPB - 1) / H3C_SLOT_WPB, cap = (int64_t)occ * sms;
-  return (unsigned)(need < cap ? need : cap);
 }
 
 void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, bool mapped, int sms, cudaStream_t stream) {

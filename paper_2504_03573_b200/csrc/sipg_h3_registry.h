@@ -10,15 +10,14 @@ using H3UploadFn = cudaError_t (*)(const double* D, const double* A, const doubl
                                    const double* ED, const double* pts, const double* W);
 struct H3Entry {
   int shape, n;
-  int gen;             // 1: register-column kernels (sipg_h3c.cuh); 0: first generation (sipg_h3.cuh)
   H3Fn pub, apply;
-  int threads;
-  int epc;             // elements per CTA (generation 1 packs several q^2-thread teams into a CTA)
+  int threads;         // CTA threads: epc teams of q^2 threads
+  int epc;             // elements per CTA
   size_t smem_pub, smem_apply;
   H3UploadFn upload;
 };
 void sipg_register_h3(std::vector<H3Entry>& v);
-// generation 1: the flux kernel (one warp per slot) over cslots[first, first + count), between publish and apply
+// the slot kernels over the work-list records [first, first + count): the flux kernel (identity-map
+// or mapped list) between publish and apply, the trace-map kernel (mapped list) right after publish
 void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, bool mapped, int sms, cudaStream_t stream);
-// generation 1: the trace-map kernel over the same work list, right after the publish kernels of those slots
 void sipg_h3c_map_launch(const H3Plan& P, int64_t first, int64_t count, int sms, cudaStream_t stream);

@@ -1,10 +1,9 @@
-// Config 4, register-column kernels: the SIP-Helmholtz apply on 3-D hybrid hex / prism / tet meshes
-// (sm_100a, fp64).  Same algorithm, plan layout and published-trace format as sipg_h3.cuh (the
-// reference's two-phase apply, pkg/src/dgsipg/sipg.py:558-602, on the shared-trace route
-// sipg.py:513-554, 653-677, extended to prisms and tets as restated in oracle/hybrid3d.py); what
-// changes is the mapping onto the machine.  ncu showed the first-generation kernels bound by the
-// shared-memory data pipe (85 % of its wavefront peak; every pointwise phase went through four q^3
-// arrays in shared memory), so here
+// Config 4: the SIP-Helmholtz apply on 3-D hybrid hex / prism / tet meshes (sm_100a, fp64) -- the
+// reference's two-phase apply (pkg/src/dgsipg/sipg.py:558-602) on the shared-trace route
+// (sipg.py:513-554, 653-677), extended to prisms and tets as restated in oracle/hybrid3d.py; plan
+// layout: paper_2504_03573_b200/plan3d.py, shared definitions: sipg_h3.cuh.  The first generation of
+// these kernels (round 1) kept four q^3 arrays per element in shared memory and ran at 85 % of the
+// shared-memory data pipe's wavefront peak (ncu); this generation is organised around registers:
 //   * one CTA of q^2 threads per element; thread (k1, k2) owns the q points (., k1, k2) along eta0 in
 //     REGISTERS: the last BwdTrans stage, PhysDeriv along eta0, the volume terms, every face lift,
 //     D0^T and the first IProduct stage never touch shared memory;
