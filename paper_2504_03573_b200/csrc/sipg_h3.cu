@@ -25,9 +25,13 @@ void add(std::vector<H3Entry>& v) {
 template <bool FLUX>
 unsigned slot_grid(int64_t count, int sms) {
   static int occ = 0;
-  if (!occ && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h3c::k_h3c_slot<FLUX>, 32 * H3C_SLOT_WPB, 0) !=
-                   cudaSuccess || occ <= 0))
-    occ = 4;
+  if (!occ) {
+    cudaFuncSetAttribute(h3c::k_h3c_slot<FLUX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)h3c::h3c_slot_smem<FLUX>());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h3c::k_h3c_slot<FLUX>, 32 * H3C_SLOT_WPB,
+                                                      h3c::h3c_slot_smem<FLUX>()) != cudaSuccess || occ <= 0)
+      occ = 4;
+  }
   const int64_t need = (count + H3C_SLOT_WPB - 1) / H3C_SLOT_WPB, cap = (int64_t)occ * sms;
   return (unsigned)(need < cap ? need : cap);
 }
@@ -42,12 +46,12 @@ void sipg_register_h3(std::vector<H3Entry>& v) {
 void sipg_h3c_flux_launch(const H3Plan& P, int64_t first, int64_t count, bool mapped, int sms, cudaStream_t stream) {
   if (count <= 0) return;
   if (mapped)
-    h3c::k_h3c_slot<true><<<slot_grid<true>(count, sms), 32 * H3C_SLOT_WPB, 0, stream>>>(P, first, count);
+    h3c::k_h3c_slot<true><<<slot_grid<true>(count, sms), 32 * H3C_SLOT_WPB, h3c::h3c_slot_smem<true>(), stream>>>(P, first, count);
   else
     h3c::k_h3c_flux_id<<<(unsigned)((count + 7) / 8), 256, 0, stream>>>(P, first, count);
 }
 
 void sipg_h3c_map_launch(const H3Plan& P, int64_t first, int64_t count, int sms, cudaStream_t stream) {
   if (count <= 0) return;
-  h3c::k_h3c_slot<false><<<slot_grid<false>(count, sms), 32 * H3C_SLOT_WPB, 0, stream>>>(P, first, count);
+  h3c::k_h3c_slot<false><<<slot_grid<false>(count, sms), 32 * H3C_SLOT_WPB, h3c::h3c_slot_smem<false>(), stream>>>(P, first, count);
 }

@@ -1359,45 +1359,56 @@ __global__ void __launch_bounds__(256, 6) k_h3c_flux_id(const H3Plan P, const in
   flux_ident(P, first + i, [&](auto&& f) { f((int)(threadIdx.x & 31)); });
 }
 
-// mapped records [first, first + count): persistent warps, inputs of the next slot and the record
-// after it prefetched by cp.async
+// mapped records [first, first + count): persistent warps; the inputs of the next H3C_SLOT_DEPTH slots
+// (and the records after them) are in flight by cp.async while a slot computes
+#ifndef H3C_SLOT_DEPTH
+#define H3C_SLOT_DEPTH 1
+#endif
 template <bool FLUX>
 __global__ void __launch_bounds__(32 * H3C_SLOT_WPB) k_h3c_slot(const H3Plan P, const int64_t first, const int64_t count) {
   constexpr int ST = FLUX ? H3C_ST_FLUX : H3C_ST_MAP;
-  constexpr int PW = 3 * 8 + 2 * ST + 2 * TMAX;   // per warp: record ring | staged inputs x 2 | flux values / map tmp
-  __shared__ __align__(16) double sm_[H3C_SLOT_WPB * PW];
+  constexpr int D = H3C_SLOT_DEPTH, NB = D + 1, NR = 2 * D + 1;   // staging buffers, record ring
+  constexpr int PW = NR * 8 + NB * ST + 2 * TMAX;   // per warp: record ring | staged inputs | flux values / map tmp
+  extern __shared__ __align__(16) double sm_[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* my = sm_ + w * PW;
   H3FluxRec* ring = reinterpret_cast<H3FluxRec*>(my);
-  double* st = my + 24;
-  double* tmp = st + 2 * ST;
+  double* st = my + NR * 8;
+  double* tmp = st + NB * ST;
   const int64_t W = (int64_t)gridDim.x * H3C_SLOT_WPB;
-  int64_t i = (int64_t)blockIdx.x * H3C_SLOT_WPB + w;
+  const int64_t i0 = (int64_t)blockIdx.x * H3C_SLOT_WPB + w;
   auto par = [&](auto&& f) { f(lane); };
   auto sync = [&]() { __syncwarp(); };
-  auto fetch_rec = [&](int64_t idx, int slot) {   // 64 bytes: lanes 0..3, 16 bytes each
-    if (lane < 4)
-      __pipeline_memcpy_async(reinterpret_cast<char*>(ring + slot) + 16 * lane,
-                              reinterpret_cast<const char*>(P.frec + first + idx) + 16 * lane, 16);
+  if (i0 >= count) return;
+  const int n = (int)((count - i0 + W - 1) / W);   // this warp's slots: i0, i0 + W, ...
+  auto fetch_rec = [&](int j) {                    // 64 bytes: lanes 0..3, 16 bytes each
+    if (j < n && lane < 4)
+      __pipeline_memcpy_async(reinterpret_cast<char*>(ring + j % NR) + 16 * lane,
+                              reinterpret_cast<const char*>(P.frec + first + i0 + j * W) + 16 * lane, 16);
   };
-  if (i >= count) return;
-  fetch_rec(i, 0);
-  if (i + W < count) fetch_rec(i + W, 1);
+  // record j is issued 2 D groups before its slot computes and D groups before its inputs are staged
+  for (int j = 0; j < 2 * D; ++j) fetch_rec(j);
   __pipeline_commit();
   __pipeline_wait_prior(0);
   __syncwarp();
-  slot_stage<FLUX>(P, ring[0], st, par);
-  __pipeline_commit();
-  for (int k = 0; i < count; i += W, ++k) {
-    __pipeline_wait_prior(0);
-    __syncwarp();
-    if (i + W < count) slot_stage<FLUX>(P, ring[(k + 1) % 3], st + ((k + 1) & 1) * ST, par);
-    if (i + 2 * W < count) fetch_rec(i + 2 * W, (k + 2) % 3);
+  for (int j = 0; j < D; ++j) {
+    if (j < n) slot_stage<FLUX>(P, ring[j % NR], st + (j % NB) * ST, par);
     __pipeline_commit();
-    if (FLUX) flux_compute(P, ring[k % 3], st + (k & 1) * ST, tmp, par, sync);
-    else map_compute(P, ring[k % 3], st + (k & 1) * ST, tmp, par, sync);
+  }
+  for (int j = 0; j < n; ++j) {
+    __pipeline_wait_prior(D - 1);   // the inputs of slot j (and every older group) have landed
+    __syncwarp();
+    if (j + D < n) slot_stage<FLUX>(P, ring[(j + D) % NR], st + ((j + D) % NB) * ST, par);
+    fetch_rec(j + 2 * D);
+    __pipeline_commit();
+    if (FLUX) flux_compute(P, ring[j % NR], st + (j % NB) * ST, tmp, par, sync);
+    else map_compute(P, ring[j % NR], st + (j % NB) * ST, tmp, par, sync);
     __syncwarp();
   }
+}
+template <bool FLUX>
+constexpr size_t h3c_slot_smem() {
+  return sizeof(double) * H3C_SLOT_WPB * ((2 * H3C_SLOT_DEPTH + 1) * 8 + (H3C_SLOT_DEPTH + 1) * (FLUX ? H3C_ST_FLUX : H3C_ST_MAP) + 2 * TMAX);
 }
 
 // resident CTAs per SM the register allocation must allow, per q (apply | publish)
