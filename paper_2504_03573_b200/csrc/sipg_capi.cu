@@ -133,6 +133,11 @@ struct H3State {
   std::vector<std::vector<Launch>> st_pub, st_comp;
   int32_t* rows_d = nullptr;
   H3Plan hps{};
+  // streamed host apply: the slot records once more, ordered by stage (one trace-map launch and two flux
+  // launches per stage instead of three per class row): per stage k the ranges [st_mp[k], st_mp[k+1]) etc.
+  H3FluxRec* frec_stage_d = nullptr;
+  std::vector<int64_t> st_mp, st_fi, st_fm;
+  std::vector<H3FluxRec> frec_host;   // kept until the stream schedule is built
   void* bufs[7] = {};
   double* pub = nullptr;
   int64_t n_pub = 0;
@@ -886,6 +891,27 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
   if (upload(rows.data(), (int64_t)rows.size(), &h->rows_d)) return false;
   h->hps = h->hp;
   h->hps.cd = h->rows_d;
+  if (h->flux) {   // stage-ordered slot records: [mapped by publish stage | identity by compute stage | mapped by compute stage]
+    std::vector<H3FluxRec> sr;
+    sr.reserve(h->frec_host.size() * 2);
+    auto gather = [&](const std::vector<std::vector<H3State::Launch>>& rows_of, bool mapped, std::vector<int64_t>& off) {
+      off.assign(K + 1, 0);
+      for (int k = 0; k < K; ++k) {
+        off[k] = (int64_t)sr.size();
+        for (const auto& L : rows_of[k]) {
+          const std::vector<int64_t>& cs = mapped ? h->cs_mp : h->cs_id;
+          const int64_t base = mapped ? h->n_id : 0;
+          sr.insert(sr.end(), h->frec_host.begin() + base + cs[L.pos0], h->frec_host.begin() + base + cs[L.pos1]);
+        }
+      }
+      off[K] = (int64_t)sr.size();
+    };
+    gather(h->st_pub, true, h->st_mp);
+    gather(h->st_comp, false, h->st_fi);
+    gather(h->st_comp, true, h->st_fm);
+    if (upload(sr.data(), (int64_t)sr.size(), &h->frec_stage_d)) return false;
+    h->hps.frec = h->frec_stage_d;
+  }
   p->n_chunks = K;
   return true;
 }
@@ -1093,6 +1119,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     }
     h->cs_id[d->n_elements] = ki;
     h->cs_mp[d->n_elements] = km;
+    h->frec_host = fr;
     h->flux = true;
     if ((rc = upload(fbo.data(), d->n_elements + 1, &h->fb_off_d)) || (rc = upload(fr.data(), d->n_slots, &h->frec_d))) {
       sipg_plan_destroy(p);
@@ -1146,6 +1173,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
     h->cap_apply.push_back(occ_a * sms);
   }
   p->streamed = !getenv("SIPG_NO_STREAM") && build_stream_schedule_h3(p, d);
+  std::vector<H3FluxRec>().swap(h->frec_host);
   *out = p;
   return 0;
 }
@@ -1445,13 +1473,25 @@ static int enqueue_streamed(sipg_plan* p, const double* x_host, double* y_host, 
         cudaStream_t st = group_stream(p);
         L.k->pub<<<L.grid, L.k->threads, L.k->smem_pub, st>>>(h->hps, L.row, p->x_stage, p->y_stage);
         ++p->launches;
-        if (h->flux) h3_slot_launch(p, h->hps, 3, L.pos0, L.pos1, st);
       }
       if ((rc = group_end(p))) return rc;
+      if (h->flux) {   // the stage's slot kernels, one launch each over its stage-ordered records
+        if (h->st_mp[k + 1] > h->st_mp[k]) {
+          sipg_h3c_map_launch(h->hps, h->st_mp[k], h->st_mp[k + 1] - h->st_mp[k], p->sms, s);
+          ++p->launches;
+        }
+        if (h->st_fi[k + 1] > h->st_fi[k]) {
+          sipg_h3c_flux_launch(h->hps, h->st_fi[k], h->st_fi[k + 1] - h->st_fi[k], false, p->sms, s);
+          ++p->launches;
+        }
+        if (h->st_fm[k + 1] > h->st_fm[k]) {
+          sipg_h3c_flux_launch(h->hps, h->st_fm[k], h->st_fm[k + 1] - h->st_fm[k], true, p->sms, s);
+          ++p->launches;
+        }
+      }
       if ((rc = group_begin(p, s, (int)h->st_comp[k].size(), (int)h->st_comp[k].size()))) return rc;
-      for (const auto& L : h->st_comp[k]) {   // a stage row's flux kernel, then its apply kernel, on one stream
+      for (const auto& L : h->st_comp[k]) {
         cudaStream_t st = group_stream(p);
-        if (h->flux) h3_slot_launch(p, h->hps, 2, L.pos0, L.pos1, st);
         L.k->apply<<<L.grid, L.k->threads, L.k->smem_apply, st>>>(h->hps, L.row, p->x_stage, p->y_stage);
         ++p->launches;
       }
@@ -1530,7 +1570,7 @@ int sipg_plan_host_launches_per_apply(const sipg_plan* p) {
   int k = 0;
   if (p->h3) {
     for (int i = 0; i < p->n_chunks; ++i) {
-      k += (int)(p->h3->st_pub[i].size() + p->h3->st_comp[i].size()) * (p->h3->flux ? 2 : 1);
+      k += (int)(p->h3->st_pub[i].size() + p->h3->st_comp[i].size()) + (p->h3->flux ? 3 : 0);
     }
     return k;
   }
@@ -1559,6 +1599,7 @@ int sipg_plan_destroy(sipg_plan* p) {
     if (p->h3->fb) cudaFree(p->h3->fb);
     if (p->h3->fb_off_d) cudaFree(p->h3->fb_off_d);
     if (p->h3->frec_d) cudaFree(p->h3->frec_d);
+    if (p->h3->frec_stage_d) cudaFree(p->h3->frec_stage_d);
     if (p->h3->rows_d) cudaFree(p->h3->rows_d);
     delete p->h3;
     p->h3 = nullptr;
