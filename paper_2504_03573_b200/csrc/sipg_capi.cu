@@ -126,6 +126,8 @@ struct H3State {
   double* fb = nullptr;
   int64_t* fb_off_d = nullptr;
   H3FluxRec* frec_d = nullptr;
+  double* ug = nullptr;          // u on the q^3 grids, publish -> apply
+  int64_t* ug_off_d = nullptr;
   std::vector<int64_t> cs_id, cs_mp;   // per class-list position: first identity-map / mapped record
   int64_t n_id = 0;                    // records: [identity-map slots | mapped slots], each in class-list order
   // streamed host apply (see build_stream_schedule_h3): per stage, publish rows and apply rows
@@ -923,6 +925,15 @@ bool build_stream_schedule_h3(sipg_plan* p, const sipg_h3_desc* d) {
 int sipg_h3_apply_traces(sipg_plan* p, const double* x_dev, const double* traces_dev, double* y_dev, void* stream) {
   if (!p || !p->h3 || !x_dev || !traces_dev || !y_dev) return fail(SIPG_ERR_ARG, "bad argument");
   H3State* h = p->h3;
+  // (u hand-over builds) the apply kernels take u from the publish kernels: run those first, publishing into the plan's own
+  // trace buffer (scratch here; the caller's traces are what the flux kernels read)
+  for (int c = 0; H3C_UHAND && c < p->n_cls; ++c) {
+    const int count = h->cd[c * CD3_WORDS + CD3_COUNT];
+    if (count == 0 || h->cd[c * CD3_WORDS + CD3_ROLE] == 2) continue;
+    const H3Entry* k = h->kern[c];
+    k->pub<<<h->grid_pub[c], k->threads, k->smem_pub, (cudaStream_t)stream>>>(h->hp, c, x_dev, y_dev);
+    ++p->launches;
+  }
   H3Plan hp = h->hp;
   hp.pub = const_cast<double*>(traces_dev);
   for (int c = 0; c < p->n_cls; ++c) {
@@ -1125,6 +1136,20 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       sipg_plan_destroy(p);
       return rc;
     }
+    {   // u hand-over buffer: q^3 doubles per element (offsets even: 16-byte cp.async)
+      std::vector<int64_t> ugo((size_t)d->n_elements + 1, 0);
+      for (int64_t e = 0; e < d->n_elements; ++e) ugo[e + 1] = ugo[e] + (((int64_t)qe[e] * qe[e] * qe[e] + 1) & ~1ll);
+      if ((rc = upload(ugo.data(), d->n_elements + 1, &h->ug_off_d))) {
+        sipg_plan_destroy(p);
+        return rc;
+      }
+      cudaError_t e = H3C_UHAND ? cudaMalloc((void**)&h->ug, sizeof(double) * (ugo[d->n_elements] > 0 ? ugo[d->n_elements] : 2))
+                                : cudaSuccess;
+      if (e != cudaSuccess) {
+        sipg_plan_destroy(p);
+        return fail(SIPG_ERR_CUDA, std::string("u hand-over buffer: ") + cudaGetErrorString(e));
+      }
+    }
     if (h->flux && fbo[d->n_elements] > 0) {
       cudaError_t e = cudaMalloc((void**)&h->fb, sizeof(double) * fbo[d->n_elements]);
       if (e != cudaSuccess) {
@@ -1133,7 +1158,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       }
     }
   }
-  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda, h->fb, h->fb_off_d, h->frec_d};
+  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda, h->fb, h->fb_off_d, h->frec_d, h->ug, h->ug_off_d};
   h->fork_all = getenv("SIPG_H3_FORK") && atoi(getenv("SIPG_H3_FORK")) != 0;
   for (const H3Entry* k : h->kern) {
     cudaError_t e1 = cudaFuncSetAttribute((const void*)k->pub, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1600,6 +1625,8 @@ int sipg_plan_destroy(sipg_plan* p) {
     if (p->h3->fb_off_d) cudaFree(p->h3->fb_off_d);
     if (p->h3->frec_d) cudaFree(p->h3->frec_d);
     if (p->h3->frec_stage_d) cudaFree(p->h3->frec_stage_d);
+    if (p->h3->ug) cudaFree(p->h3->ug);
+    if (p->h3->ug_off_d) cudaFree(p->h3->ug_off_d);
     if (p->h3->rows_d) cudaFree(p->h3->rows_d);
     delete p->h3;
     p->h3 = nullptr;

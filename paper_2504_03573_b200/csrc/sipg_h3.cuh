@@ -13,6 +13,13 @@
 #include <stdint.h>
 
 #define SIPG_H3_ABI_VERSION 1
+// build knob: the publish kernels hand u (q^3 grid, 0.74 GB at 48^3) to the apply kernels, which then skip
+// their BwdTrans.  Measured on cfg4: 3.87 -> 3.78 ms (tet n = 7 apply 0.395 -> 0.346 ms, the publish kernels
+// 4 % slower), for 1.5 GB more DRAM traffic per apply and an apply kernel that moves 6 x its algorithmic
+// bytes; left off.
+#ifndef H3C_UHAND
+#define H3C_UHAND 0
+#endif
 
 enum { H3_HEX = 0, H3_PRISM = 1, H3_TET = 2 };
 #define CD3_WORDS 16
@@ -45,6 +52,9 @@ struct H3Plan {
   double* fb;
   const int64_t* fb_off;
   const struct H3FluxRec* frec;   // the flux kernel's work list: one record per slot, class-list order
+  // u on the q^3 grid, handed from the publish kernels to the apply kernels (element e from ug_off[e])
+  double* ug;
+  const int64_t* ug_off;
 };
 // what the flux kernel needs of a slot, 64 bytes, in work-list order (built by sipg_h3_plan_create)
 struct H3FluxRec {

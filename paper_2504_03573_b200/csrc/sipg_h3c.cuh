@@ -254,10 +254,11 @@ struct CfgC {
   static constexpr int FBN = NSMAX * 2 * Q2;                                   // own-grid fluxes of an element
   static constexpr int NI = 2 * NPM + 2 + NC + NCD + 8;   // gof, minfo, rinfo, cdrep
   // kernel modes: 0 apply, 1 publish.  Shared memory: ring | class tables | one block per team | int tables
-  static constexpr int RING = (3 * E * 5 + 1) & ~1;
+  static constexpr int RING = (3 * E * 6 + 1) & ~1;
+  static constexpr int UBP = (Q2 * Q + 1) & ~1;                                // apply: the element's u, q^3 (unpadded)
   static constexpr int teamd(int mode) {
     return mode == 1 ? 2 * NCP + 2 * NSMAX * SLOTD + NF * 4 * Q2 + SCR_P
-                     : 2 * NCP + 2 * NSMAX * SLOTD + 2 * H3_EGEO + FBN + 2 * BUF;   // every term even: 16-byte cp.async
+                     : (H3C_UHAND ? UBP : 2 * NCP) + 2 * NSMAX * SLOTD + 2 * H3_EGEO + FBN + 2 * BUF;   // every term even
   }
   static constexpr int doubles(int mode) { return RING + TABD + E * teamd(mode); }
   static constexpr size_t smem_bytes(int mode) { return sizeof(double) * doubles(mode) + sizeof(int) * NI; }
@@ -329,7 +330,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 #endif
   // ---- shared memory (CfgC::doubles): ring | class tables | team blocks | int tables
   constexpr int E = C::E, NTC = C::NTC, TEAMD = C::teamd(MODE);
-  long long* ring = reinterpret_cast<long long*>(sm);                  // [3][E][5] element scalars (e, ns, dof, sb, fbo)
+  long long* ring = reinterpret_cast<long long*>(sm);                  // [3][E][6] element scalars (e, ns, dof, sb, fbo, ugo)
   double* pts = sm + C::RING;
   double* Rt = pts + 3 * Q;
   double* W12 = Rt + 3 * Q;
@@ -339,7 +340,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   double* teams = sm + C::RING + C::TABD;
   // per team (element): coefficients [2][NCP] | slot headers [2][NSMAX][12] | apply: geometry [2][8], own-grid
   // fluxes [ns][2][Q2], B0, B1 (padded q^3 buffers; BwdTrans s2, s1) | publish: face arrays [NF][4][Q2], u, s1
-  constexpr int O_H = 2 * C::NCP, O_E = O_H + 2 * C::NSMAX * C::SLOTD, O_F = O_E + 2 * H3_EGEO;
+  constexpr bool UH = APP && H3C_UHAND;   // apply: u arrives from the publish kernel (one q^3 buffer, no coefficients)
+  constexpr int O_H = UH ? C::UBP : 2 * C::NCP, O_E = O_H + 2 * C::NSMAX * C::SLOTD, O_F = O_E + 2 * H3_EGEO;
   constexpr int O_B0 = APP ? O_F + C::FBN : O_E + NF * 4 * Q2;
   int* gof = reinterpret_cast<int*>(teams + E * TEAMD);
   int* minfo = gof + C::NPM + 1;
@@ -348,10 +350,10 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   // a thread's team (element) and its buffers: the first statement of every element-work phase
 #define H3C_TEAM(ltc)                                                                  \
   const int tm = (ltc) / NT, lt = (ltc) - tm * NT;                                     \
-  const long long* rg_ = ring + 5 * (slot * E + tm);                                   \
+  const long long* rg_ = ring + 6 * (slot * E + tm);                                   \
   const int ns = (int)rg_[1];                                                          \
   if (ns < 0) return;                                                                  \
-  const int64_t dof = rg_[2], fbo = rg_[4];                                            \
+  const int64_t dof = rg_[2], fbo = rg_[4], ugo = rg_[5];                              \
   double* tmb_ = teams + tm * TEAMD;                                                    \
   const double* c = tmb_ + bsel * C::NCP;                                               \
   const double* hdr = tmb_ + O_H + bsel * C::NSMAX * C::SLOTD;                          \
@@ -362,7 +364,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   double* B1 = B0 + BUF;                                                               \
   double* s2 = B0;                                                                     \
   double* s1 = B0 + BUF;                                                               \
-  (void)dof; (void)fbo; (void)c; (void)hdr; (void)eg; (void)fbuf; (void)FL; (void)B1; (void)s2; (void)s1; (void)lt
+  (void)dof; (void)fbo; (void)ugo; (void)c; (void)hdr; (void)eg; (void)fbuf; (void)FL; (void)B1; (void)s2; (void)s1; (void)lt
 
   const int32_t* cd = P.cd + cls * CD3_WORDS;
   const int count = cd[CD3_COUNT];
@@ -399,7 +401,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     par([&](int lt, TS&) {
       if (lt < E) {
         const int i = gi * E + lt;
-        long long* r = ring + 5 * (slot * E + lt);
+        long long* r = ring + 6 * (slot * E + lt);
         r[1] = -1;
         if (i < count) {
           const int e = H3C_LDG(ce + i);
@@ -409,15 +411,16 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
           r[2] = H3C_LDG(P.dof_off + e);
           r[3] = sb;
           r[4] = H3C_LDG(P.fb_off + e);
+          r[5] = H3C_LDG(P.ug_off + e);
         }
       }
     });
   };
-  auto issue = [&](int buf, int slot) {
+  auto issue = [&](int buf, int slot, bool on) {   // coefficients (not with the u hand-over), slot headers, geometry
     par([&](int ltc, TS&) {
       const int tm = ltc / NT, lt = ltc - tm * NT;
-      const long long* r = ring + 5 * (slot * E + tm);
-      const int e = (int)r[0], ns = (int)r[1];
+      const long long* r = ring + 6 * (slot * E + tm);
+      const int e = (int)r[0], ns = on ? (int)r[1] : -1;
       const int64_t dof = r[2], sb = r[3];
       double* tb_ = teams + tm * TEAMD;
       double* cd_ = tb_ + buf * C::NCP;
@@ -426,7 +429,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       const double* src = reinterpret_cast<const double*>(P.slots + sb);
 #if defined(__CUDA_ARCH__)
       if (ns >= 0) {
-        for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
+        if (!UH)
+          for (int r = lt; r < C::NC; r += NT) __pipeline_memcpy_async(cd_ + r, x + dof + r, sizeof(double));
         for (int r = lt; r < ns * C::SLOTD; r += NT) __pipeline_memcpy_async(hd_ + r, src + r, sizeof(double));
         if (APP && lt < H3_EGEO / 2)
           __pipeline_memcpy_async(eb_ + 2 * lt, P.egeo + (int64_t)e * H3_EGEO + 2 * lt, 2 * sizeof(double));
@@ -434,7 +438,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       __pipeline_commit();
 #else
       if (ns >= 0) {
-        for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
+        if (!UH)
+          for (int r = lt; r < C::NC; r += NT) cd_[r] = x[dof + r];
         for (int r = lt; r < ns * C::SLOTD; r += NT) hd_[r] = src[r];
         if (APP && lt < H3_EGEO / 2) {
           eb_[2 * lt] = P.egeo[(int64_t)e * H3_EGEO + 2 * lt];
@@ -444,10 +449,30 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 #endif
     });
   };
+  auto issue_u = [&](int slot, bool on) {   // the element's u (q^3 doubles, ug_off even: 16-byte pieces; odd tail 8)
+    par([&](int ltc, TS&) {
+      const int tm = ltc / NT, lt = ltc - tm * NT;
+      const long long* r = ring + 6 * (slot * E + tm);
+      const int ns = on ? (int)r[1] : -1;
+      const double* src = P.ug + r[5];
+      double* ub = teams + tm * TEAMD;
+      constexpr int Q3 = Q2 * Q;
+#if defined(__CUDA_ARCH__)
+      if (ns >= 0) {
+        for (int q = lt; q < Q3 / 2; q += NT) __pipeline_memcpy_async(ub + 2 * q, src + 2 * q, 2 * sizeof(double));
+        if ((Q3 & 1) && lt == 0) __pipeline_memcpy_async(ub + Q3 - 1, src + Q3 - 1, sizeof(double));
+      }
+      __pipeline_commit();
+#else
+      if (ns >= 0)
+        for (int q = lt; q < Q3; q += NT) ub[q] = src[q];
+#endif
+    });
+  };
   auto issue_fb = [&](int slot) {   // ns * 2 * Q2 doubles per team, 16-byte pieces (fb_off is even)
     par([&](int ltc, TS&) {
       const int tm = ltc / NT, lt = ltc - tm * NT;
-      const long long* r = ring + 5 * (slot * E + tm);
+      const long long* r = ring + 6 * (slot * E + tm);
       const int ns = (int)r[1];
       const double* src = P.fb + r[4];
       double* fbuf = teams + tm * TEAMD + O_F;
@@ -463,7 +488,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   scalars(bid, 0);
   scalars(bid + G, 1);
   sync();
-  if (bid < ngroups) issue(0, 0);
+  issue(0, 0, bid < ngroups);
+  if (UH) issue_u(0, bid < ngroups);
   int it_el = 0;
   for (int gi = bid; gi < ngroups; gi += G, ++it_el) {
     const int bsel = it_el & 1;
@@ -472,10 +498,26 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     __pipeline_wait_prior(0);
 #endif
     sync();
-    if (gi + G < ngroups) issue(bsel ^ 1, slot_n);
+    issue(bsel ^ 1, slot_n, gi + G < ngroups);
     scalars(gi + 2 * G, slot_nn);
     if (APP) issue_fb(slot);
 
+    if (UH) {
+      // ================= apply with the u hand-over: the column from the publish kernel's u ==========
+      par([&](int ltc, TS& ts) {
+        H3C_TEAM(ltc);
+        const int ta = lt / Q, tb_ = lt % Q;
+        const double* ub = tmb_;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          ts.u[k] = ub[k * Q2 + lt];
+          B0[k * SI + ta * SJ + tb_] = ts.u[k];
+        }
+        eo_full<Q>(H3C_TE, 0 * EOS, ts.u, ts.d0);
+      });
+      sync();
+      issue_u(slot_n, gi + G < ngroups);   // the u buffer is free again: the next element's u, a whole element ahead
+    } else {
     // ================= BwdTrans (stdregions.py:575-597): u column in registers ====================
     if (S == H3_HEX) {
       par([&](int ltc, TS&) {
@@ -577,6 +619,8 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       cmat<Q, NA>(H3C_TA, 0, col, ts.u);
     });
 
+    }   // BwdTrans (not with the u hand-over)
+
     if (PUB) {
       // ================= publish: own traces (u, n.grad u) of every coupling =====================
       // FL[f] = (u, d u / d eta_fixed, d u / d eta_ra, d u / d eta_rb) on the own face grid
@@ -599,6 +643,11 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         });
 #pragma unroll
         for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
+        if (H3C_UHAND) {   // u for the apply kernel (coalesced: consecutive threads, consecutive points)
+          double* ue = P.ug + ugo;
+#pragma unroll
+          for (int k = 0; k < Q; ++k) ue[k * Q2 + lt] = ts.u[k];
+        }
       });
       sync();
       par([&](int ltc, TS&) {
@@ -685,14 +734,16 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
 
     // ================= apply: PhysDeriv (stdregions.py:658-674) ==================================
     // eta0 in registers; eta1 / eta2 one line per thread through B0 / B1
-    par([&](int ltc, TS& ts) {
-      H3C_TEAM(ltc);
-      const int ta = lt / Q, tb_ = lt % Q;
+    if (!UH) {
+      par([&](int ltc, TS& ts) {
+        H3C_TEAM(ltc);
+        const int ta = lt / Q, tb_ = lt % Q;
 #pragma unroll
-      for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
-      eo_full<Q>(H3C_TE, 0 * EOS, ts.u, ts.d0);
-    });
-    sync();
+        for (int k = 0; k < Q; ++k) B0[k * SI + ta * SJ + tb_] = ts.u[k];
+        eo_full<Q>(H3C_TE, 0 * EOS, ts.u, ts.d0);
+      });
+      sync();
+    }
     par([&](int ltc, TS& ts) {
       H3C_TEAM(ltc);
       const int ta = lt / Q, tb_ = lt % Q;
@@ -716,7 +767,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
     });
     // ================= volume terms (sipg.py:575-582) + face lifts, in registers ==================
 #if defined(__CUDA_ARCH__)
-    __pipeline_wait_prior(0);   // this element's own-grid fluxes (and the next element's prefetch)
+    __pipeline_wait_prior(UH ? 1 : 0);   // this element's own-grid fluxes (the next element's u may still be in flight)
 #endif
     sync();
     par([&](int ltc, TS& ts) {

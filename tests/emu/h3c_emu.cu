@@ -91,8 +91,20 @@ extern "C" int64_t h3c_emu_fb_layout(const sipg_h3_desc* d, int64_t* fb_off) {
 
 // phase 0: publish every class into pub; phase 3: the trace maps of the staged slots; phase 2: the fluxes of every class (reads pub) into fb;
 // phase 1: apply every class (reads fb) into y
+// u hand-over buffer layout (as sipg_h3_plan_create): ug_off[n_elements + 1], returns the total
+extern "C" int64_t h3c_emu_ug_layout(const sipg_h3_desc* d, int64_t* ug_off) {
+  std::vector<int64_t> q(d->n_elements, 0);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int32_t* cd = d->class_desc + c * CD3_WORDS;
+    for (int i = 0; i < cd[CD3_COUNT]; ++i) q[d->class_elems[cd[CD3_ELEM_OFF] + i]] = cd[CD3_Q];
+  }
+  ug_off[0] = 0;
+  for (int64_t e = 0; e < d->n_elements; ++e) ug_off[e + 1] = ug_off[e] + ((q[e] * q[e] * q[e] + 1) & ~1ll);
+  return ug_off[d->n_elements];
+}
+
 extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, double* pub, double* fb,
-                           const int64_t* fb_off, int phase) {
+                           const int64_t* fb_off, double* ug, const int64_t* ug_off, int phase) {
   // the flux kernel's work list, as sipg_h3_plan_create builds it
   std::vector<int32_t> qe(d->n_elements, 0);
   std::vector<H3FluxRec> fr;
@@ -110,7 +122,7 @@ extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, do
     }
   }
   H3Plan P{d->class_desc, d->class_elems, d->dof_off, d->elem_geom, d->slot_off, (const H3Slot*)d->slots,
-           d->tables, pub, d->lambda, fb, fb_off, fr.data()};
+           d->tables, pub, d->lambda, fb, fb_off, fr.data(), ug, ug_off};
   auto lanes = [&](auto&& f) { for (int lane = 0; lane < 32; ++lane) f(lane); };
   if (phase == 3) {   // the trace-map kernel, after the publish kernels (mapped slots)
     for (size_t i = 0; i < fr.size(); ++i) {

@@ -28,7 +28,9 @@ def emu():
     L = ctypes.CDLL(str(lib))
     L.h3c_emu_fb_layout.argtypes = [ctypes.POINTER(H3Desc), ctypes.c_void_p]
     L.h3c_emu_fb_layout.restype = ctypes.c_int64
-    L.h3c_emu_run.argtypes = [ctypes.POINTER(H3Desc)] + [ctypes.c_void_p] * 5 + [ctypes.c_int]
+    L.h3c_emu_ug_layout.argtypes = [ctypes.POINTER(H3Desc), ctypes.c_void_p]
+    L.h3c_emu_ug_layout.restype = ctypes.c_int64
+    L.h3c_emu_run.argtypes = [ctypes.POINTER(H3Desc)] + [ctypes.c_void_p] * 7 + [ctypes.c_int]
     return L
 
 
@@ -51,12 +53,15 @@ def run_emu(L, pb, x):
     d, keep = _desc(pb)
     fb_off = np.zeros(len(pb.shapes) + 1, dtype=np.int64)
     nfb = L.h3c_emu_fb_layout(ctypes.byref(d), fb_off.ctypes.data)
+    ug_off = np.zeros(len(pb.shapes) + 1, dtype=np.int64)
+    nug = L.h3c_emu_ug_layout(ctypes.byref(d), ug_off.ctypes.data)
+    ug = np.full(max(nug, 1), np.nan)
     pub = np.full(max(pb.n_pub, 1), np.nan)
     fb = np.full(max(nfb, 1), np.nan)
     y = np.full(pb.n_dofs, np.nan)
     for phase in (0, 3, 2, 1):
         rc = L.h3c_emu_run(ctypes.byref(d), x.ctypes.data, y.ctypes.data, pub.ctypes.data, fb.ctypes.data,
-                           fb_off.ctypes.data, phase)
+                           fb_off.ctypes.data, ug.ctypes.data, ug_off.ctypes.data, phase)
         assert rc == 0
     return y, pub
 
