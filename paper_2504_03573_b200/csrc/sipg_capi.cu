@@ -128,6 +128,7 @@ struct H3State {
   H3FluxRec* frec_d = nullptr;
   double* ug = nullptr;          // u on the q^3 grids, publish -> apply
   int64_t* ug_off_d = nullptr;
+  long long* escal_d = nullptr;  // per class-list position: element scalars (H3Plan::escal)
   std::vector<int64_t> cs_id, cs_mp;   // per class-list position: first identity-map / mapped record
   int64_t n_id = 0;                    // records: [identity-map slots | mapped slots], each in class-list order
   // streamed host apply (see build_stream_schedule_h3): per stage, publish rows and apply rows
@@ -1143,6 +1144,21 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
         sipg_plan_destroy(p);
         return rc;
       }
+      std::vector<long long> es((size_t)d->n_elements * 6);
+      for (int64_t i = 0; i < d->n_elements; ++i) {
+        const int32_t e = d->class_elems[i];
+        long long* r = es.data() + 6 * i;
+        r[0] = e;
+        r[1] = d->slot_off[e + 1] - d->slot_off[e];
+        r[2] = d->dof_off[e];
+        r[3] = d->slot_off[e];
+        r[4] = fbo[e];
+        r[5] = ugo[e];
+      }
+      if ((rc = upload(es.data(), (int64_t)es.size(), &h->escal_d))) {
+        sipg_plan_destroy(p);
+        return rc;
+      }
       cudaError_t e = H3C_UHAND ? cudaMalloc((void**)&h->ug, sizeof(double) * (ugo[d->n_elements] > 0 ? ugo[d->n_elements] : 2))
                                 : cudaSuccess;
       if (e != cudaSuccess) {
@@ -1158,7 +1174,7 @@ int sipg_h3_plan_create(const sipg_h3_desc* d, sipg_plan** out) {
       }
     }
   }
-  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda, h->fb, h->fb_off_d, h->frec_d, h->ug, h->ug_off_d};
+  h->hp = H3Plan{cd_d, ce_d, dof_d, eg_d, so_d, sl_d, tab_d, h->pub, d->lambda, h->fb, h->fb_off_d, h->frec_d, h->ug, h->ug_off_d, h->escal_d};
   h->fork_all = getenv("SIPG_H3_FORK") && atoi(getenv("SIPG_H3_FORK")) != 0;
   for (const H3Entry* k : h->kern) {
     cudaError_t e1 = cudaFuncSetAttribute((const void*)k->pub, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1627,6 +1643,7 @@ int sipg_plan_destroy(sipg_plan* p) {
     if (p->h3->frec_stage_d) cudaFree(p->h3->frec_stage_d);
     if (p->h3->ug) cudaFree(p->h3->ug);
     if (p->h3->ug_off_d) cudaFree(p->h3->ug_off_d);
+    if (p->h3->escal_d) cudaFree(p->h3->escal_d);
     if (p->h3->rows_d) cudaFree(p->h3->rows_d);
     delete p->h3;
     p->h3 = nullptr;

@@ -55,6 +55,9 @@ struct H3Plan {
   // u on the q^3 grid, handed from the publish kernels to the apply kernels (element e from ug_off[e])
   double* ug;
   const int64_t* ug_off;
+  // per class-list position: (element, n_slots, dof offset, first slot, fb offset, ug offset), 48 bytes -- what a
+  // CTA needs to start an element, fetched by cp.async (no dependent global loads in the element loop)
+  const long long* escal;
 };
 // what the flux kernel needs of a slot, 64 bytes, in work-list order (built by sipg_h3_plan_create)
 struct H3FluxRec {

@@ -402,18 +402,22 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       if (lt < E) {
         const int i = gi * E + lt;
         long long* r = ring + 6 * (slot * E + lt);
-        r[1] = -1;
         if (i < count) {
-          const int e = H3C_LDG(ce + i);
-          const long long sb = H3C_LDG(P.slot_off + e);
-          r[0] = e;
-          r[1] = H3C_LDG(P.slot_off + e + 1) - sb;
-          r[2] = H3C_LDG(P.dof_off + e);
-          r[3] = sb;
-          r[4] = H3C_LDG(P.fb_off + e);
-          r[5] = H3C_LDG(P.ug_off + e);
+          const long long* src = P.escal + 6 * (long long)(cd[CD3_ELEM_OFF] + i);
+#if defined(__CUDA_ARCH__)
+          __pipeline_memcpy_async(r, src, 16);
+          __pipeline_memcpy_async(r + 2, src + 2, 16);
+          __pipeline_memcpy_async(r + 4, src + 4, 16);
+#else
+          for (int q = 0; q < 6; ++q) r[q] = src[q];
+#endif
+        } else {
+          r[1] = -1;
         }
       }
+#if defined(__CUDA_ARCH__)
+      __pipeline_commit();
+#endif
     });
   };
   auto issue = [&](int buf, int slot, bool on) {   // coefficients (not with the u hand-over), slot headers, geometry
@@ -487,6 +491,9 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
   const int ngroups = (count + E - 1) / E;
   scalars(bid, 0);
   scalars(bid + G, 1);
+#if defined(__CUDA_ARCH__)
+  __pipeline_wait_prior(0);
+#endif
   sync();
   issue(0, 0, bid < ngroups);
   if (UH) issue_u(0, bid < ngroups);

@@ -121,8 +121,15 @@ extern "C" int h3c_emu_run(const sipg_h3_desc* d, const double* x, double* y, do
                              s0.tau, s0.sJ, s0.nt, s0.mkind | (s0.kind << 8), s0.nab, s0.moff, s0.moff2, s0.wtoff});
     }
   }
+  std::vector<long long> es((size_t)d->n_elements * 6);
+  for (int64_t i = 0; i < d->n_elements; ++i) {
+    const int32_t e = d->class_elems[i];
+    long long* r = es.data() + 6 * i;
+    r[0] = e; r[1] = d->slot_off[e + 1] - d->slot_off[e]; r[2] = d->dof_off[e]; r[3] = d->slot_off[e];
+    r[4] = fb_off[e]; r[5] = ug_off[e];
+  }
   H3Plan P{d->class_desc, d->class_elems, d->dof_off, d->elem_geom, d->slot_off, (const H3Slot*)d->slots,
-           d->tables, pub, d->lambda, fb, fb_off, fr.data(), ug, ug_off};
+           d->tables, pub, d->lambda, fb, fb_off, fr.data(), ug, ug_off, es.data()};
   auto lanes = [&](auto&& f) { for (int lane = 0; lane < 32; ++lane) f(lane); };
   if (phase == 3) {   // the trace-map kernel, after the publish kernels (mapped slots)
     for (size_t i = 0; i < fr.size(); ++i) {
