@@ -708,10 +708,14 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
         H3C_TEAM(ltc);
         double* fbe = P.fb + fbo;
         int s = 0;
+        // one coupling per face and every face coupled (always so for tets): slot f is face f, and the
+        // header reads below are at compile-time offsets instead of a dependent search through the slots
+        const bool onefc = C::NSMAX == NF && ns == NF;
         for_faces<0, NF>([&](auto Fc) {
           constexpr int f = decltype(Fc)::value;
           constexpr int fx = fc(S, f, 0), sd = fc(S, f, 1), ra = fc(S, f, 2), rb = fc(S, f, 3);
-          if (s < ns && slot_hdr(hdr, s).face == f) {
+          if (onefc) s = f;
+          if (onefc || (s < ns && slot_hdr(hdr, s).face == f)) {
             const H3Slot& h = slot_hdr(hdr, s);
             double* Ff = FL + f * 4 * Q2;
             const Chain ch = face_chain<S>(pts, Rt, Q, fx, sd, ra, rb, lt / Q, lt % Q);
@@ -724,7 +728,7 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
             const double uf = Ff[lt];
             const double gv = gf * Ff[Q2 + lt] + ga * Ff[2 * Q2 + lt] + gb * Ff[3 * Q2 + lt];
             Ff[Q2 + lt] = gv;
-            for (; s < ns && slot_hdr(hdr, s).face == f; ++s) {
+            for (const int s1_ = onefc ? s + 1 : ns; s < s1_ && (onefc || slot_hdr(hdr, s).face == f); ++s) {
               const H3Slot& hs = slot_hdr(hdr, s);
               if (hs.mkind == MAP_ID) {
                 reinterpret_cast<double2*>(P.pub + hs.pub_self)[lt] = make_double2(uf, gv);
@@ -807,13 +811,15 @@ H3C_HD void body(const H3Plan& P, const int cls, const double* __restrict__ x, d
       // fluxes (fv, fd) summed over its one or two couplings:
       //   W0(k) += E[k_fixed] fv(a),  W_c(k) += E[k_fixed] ((G n)_c fd)(a),  (G n) from the collapse chain
       int s = 0;
+      const bool onefc = C::NSMAX == NF && ns == NF;   // tets: slot f is face f (compile-time header offsets)
       for_faces<0, NF>([&](auto Fc) {
         constexpr int f = decltype(Fc)::value;
         constexpr int fx = fc(S, f, 0), sd = fc(S, f, 1), hi = sd > 0 ? 1 : 0;
         constexpr bool onehot = gll_axis(S, fx);
         constexpr int kend = hi ? Q - 1 : 0;
         constexpr double rs = sd < 0 ? 0.5 : 0.0, ps = 1.0 + sd;
-        if (!(s < ns && slot_hdr(hdr, s).face == f)) return;
+        if (onefc) s = f;
+        else if (!(s < ns && slot_hdr(hdr, s).face == f)) return;
         const H3Slot& h = slot_hdr(hdr, s);
         const double v0 = h.v[0], v1 = h.v[1], v2 = h.v[2];
         const double* F0 = fbuf + s * 2 * Q2;
