@@ -49,6 +49,29 @@ def _desc(pb):
     return d, keep
 
 
+class EmuRun:
+    """The kernel phases of one plan (global or one rank's partition), pub / fb / y kept between them."""
+
+    def __init__(self, L, pb, x):
+        self.L, self.x = L, np.ascontiguousarray(x)
+        self.d, self.keep = _desc(pb)
+        nel = self.keep[1].size
+        self.fb_off = np.zeros(nel + 1, dtype=np.int64)
+        nfb = L.h3c_emu_fb_layout(ctypes.byref(self.d), self.fb_off.ctypes.data)
+        self.ug_off = np.zeros(nel + 1, dtype=np.int64)
+        nug = L.h3c_emu_ug_layout(ctypes.byref(self.d), self.ug_off.ctypes.data)
+        self.ug = np.full(max(nug, 1), np.nan)
+        self.pub = np.full(max(pb.n_pub, 1), np.nan)
+        self.fb = np.full(max(nfb, 1), np.nan)
+        self.y = np.full(pb.n_dofs, np.nan)
+
+    def phase(self, ph):
+        rc = self.L.h3c_emu_run(ctypes.byref(self.d), self.x.ctypes.data, self.y.ctypes.data, self.pub.ctypes.data,
+                                self.fb.ctypes.data, self.fb_off.ctypes.data, self.ug.ctypes.data,
+                                self.ug_off.ctypes.data, ph)
+        assert rc == 0
+
+
 def run_emu(L, pb, x):
     d, keep = _desc(pb)
     fb_off = np.zeros(len(pb.shapes) + 1, dtype=np.int64)
@@ -87,3 +110,31 @@ def test_h3c_body_matches_oracle(emu, nx, seed):
     # in the numpy emulation): agreement to the conditioning of the collapsed chain
     assert np.abs(pub[0::2] - pub_ref[0::2]).max() <= 1e-13 * np.abs(pub_ref[0::2]).max()
     assert np.abs(pub[1::2] - pub_ref[1::2]).max() <= 1e-10 * np.abs(pub_ref[1::2]).max()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_h3c_body_on_partitioned_plans(emu, world):
+    """The kernels on the x-slab partition's local plans (halo3d: receive ranges, roles), the trace halo
+    moved by hand between the ranks' published buffers: every rank's owned y is bitwise the global run's."""
+    from paper_2504_03573_b200.distributed3d import partition_ranks
+    from paper_2504_03573_b200.halo3d import partition_plan
+    case = configs.build_case("cfg4", 3, seed=3)
+    pb = Plan3DBuilder(case.mesh, case.order_map).build()
+    x = case.draw_x(pb.n_dofs)
+    y_glob, _ = run_emu(emu, pb, x)
+    ranges = partition_ranks(pb, world)
+    parts = [partition_plan(pb, ranges, r) for r in range(world)]
+    runs = [EmuRun(emu, p, x[p.dof_lo:p.dof_hi]) for p in parts]
+    for r in runs:          # publish + trace maps on every rank
+        r.phase(0)
+        r.phase(3)
+    for p, r in zip(parts, runs):   # the halo: each send range into the neighbour's receive range
+        for i, nb in enumerate(p.nbr):
+            q = parts[int(nb)]
+            j = int(np.flatnonzero(q.nbr == p.rank)[0])
+            runs[int(nb)].pub[q.recv_off[j]:q.recv_off[j] + q.recv_cnt[j]] = \
+                r.pub[p.send_off[i]:p.send_off[i] + p.send_cnt[i]]
+    for p, r in zip(parts, runs):
+        r.phase(2)
+        r.phase(1)
+        assert np.array_equal(r.y, y_glob[p.dof_lo:p.dof_hi])
