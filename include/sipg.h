@@ -79,7 +79,7 @@ typedef struct sipg_h3_desc {
   const double* tables;        /* basis tables, trace weights, trace maps */
 } sipg_h3_desc;
 int sipg_h3_plan_create(const sipg_h3_desc* desc, sipg_plan** plan);
-/* The apply kernels of a hybrid plan reading `traces` (device, sipg_h3_trace_len doubles, the
+/* The flux and apply kernels of a hybrid plan reading `traces` (device, sipg_h3_trace_len doubles, the
  * published-trace layout: per slot (u, n.grad u) per trace point) instead of publishing: with
  * x = 0 and the Dirichlet data as the boundary slots' traces this is the boundary lift of the
  * reference's rhs_assemble (sipg.py:707-717). */
@@ -125,8 +125,10 @@ int sipg_apply_role(sipg_plan* plan, int32_t role, const double* x_dev, double* 
 
 /* One element class only (instrumentation: per-kernel timing).  Classes are
  * independent, so applying every class once equals sipg_apply.  Hybrid 3-D plans
- * (sipg_h3_plan_create) have 2 n_classes launch units: the publish kernels
- * (0..n-1) must run before the apply kernels (n..2n-1). */
+ * (sipg_h3_plan_create) have 3 n_classes launch units, run in this order for a whole apply:
+ * every class's publish kernel with the trace maps of its slots (0..n-1), every class's
+ * flux launches (2n..3n-1: the per-interface phase 2 of its slots), then every class's
+ * apply kernel (n..2n-1). */
 int sipg_apply_class(sipg_plan* plan, int32_t cls, const double* x_dev, double* y_dev, void* stream);
 /* (shape, n_modes, n_quad, geometry mode, element count, kernel kind) of a class. */
 int sipg_plan_class_info(const sipg_plan* plan, int32_t cls, int32_t* out6);
